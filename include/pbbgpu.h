@@ -1,0 +1,123 @@
+/* pbbgpu.h — C-ABI of the B200-native PFSP Branch-and-Bound explorer pool.
+ *
+ * Drop-in boundary for the reference solver's solve/explore path. Each entry point names
+ * the reference interface it replaces (paths under /root/reference/proj):
+ *
+ *   pbbgpu_create / pbbgpu_destroy  <- ExplorerPool::ExplorerPool(const Instance&, PoolConfig)
+ *                                      (include/pbb/explorer.hpp:68, src/explorer.cpp:87-106)
+ *   pbbgpu_K                        <- ExplorerPool::K()                (explorer.hpp:70)
+ *   pbbgpu_set_initial_bound        <- ExplorerPool::set_initial_bound  (explorer.hpp:73)
+ *   pbbgpu_assign                   <- ExplorerPool::assign_fresh       (explorer.hpp:76)
+ *   pbbgpu_assign_split             <- assign_fresh of [0,n!) cut into K equal ranges
+ *                                      (pool_run's default interval, explorer.cpp:479)
+ *   pbbgpu_run_round                <- ExplorerPool::run_round          (explorer.hpp:85)
+ *   pbbgpu_active_count             <- ExplorerPool::active_count       (explorer.hpp:87)
+ *   pbbgpu_snapshot                 <- ExplorerPool::snapshot_intervals (explorer.hpp:88)
+ *   pbbgpu_best                     <- best_value / best_schedule       (explorer.hpp:90-91)
+ *   pbbgpu_offer_bound              <- ExplorerPool::offer_bound        (explorer.hpp:92)
+ *   pbbgpu_stats                    <- ExplorerPool::stats              (explorer.hpp:101)
+ *   pbbgpu_histogram                <- (new) decomposed nodes by free-job count (roofline)
+ *   pbbgpu_decompose_batch          <- decompose(inst, sub, incumbent, ...) (bound.hpp:78-79)
+ *   pbbgpu_solve                    <- pool_run(inst, ub, intervals, cfg) (explorer.hpp:145-146)
+ *   pbbgpu_taillard / pbbgpu_makespan / pbbgpu_neh
+ *                                   <- generate_taillard / taillard_named / makespan / neh
+ *                                      (instance.hpp:42-48, heuristic.hpp:21)
+ *
+ * Conventions: int status, 0 = OK, negative = error class (no exceptions cross the ABI);
+ * pbbgpu_last_error() returns the message of the last failure on the calling thread.
+ * Factoradic vectors are MSD first, digit l in [0, n-1-l] (factoradic.hpp:12-26); an
+ * interval end equal to n! is passed with b_is_nfact = 1. Bounds are int64 makespans;
+ * kNoIncumbent = INT64_MAX. The product path has no CPU fallback: every compute entry
+ * fails with PBBGPU_ERR_CUDA when no sm_100 device is present.
+ */
+#ifndef PBBGPU_H
+#define PBBGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBBGPU_OK 0
+#define PBBGPU_ERR_ARG -1      /* std::invalid_argument in the reference */
+#define PBBGPU_ERR_STATE -2    /* std::logic_error */
+#define PBBGPU_ERR_CUDA -3     /* device / driver failure, no GPU */
+#define PBBGPU_ERR_CAPACITY -4 /* std::runtime_error (capacity) */
+
+#define PBBGPU_LB1 1
+#define PBBGPU_LB2 2
+
+typedef struct pbbgpu_pool pbbgpu_pool;
+
+typedef struct {
+  int explorers;         /* K; 0 = fill the GPU (occupancy) */
+  int group;             /* lanes per explorer (4, 8, 16, 32); 0 = auto */
+  int steps_per_round;   /* explore steps per explorer per round; 0 = auto */
+  int disable_pruning;   /* PoolConfig.disable_pruning (explorer.hpp:37) */
+  int pinned;            /* prune >= initial ub, never improve (explore_step(ub, 0)) */
+  double time_limit_s;   /* pbbgpu_solve only; 0 = none */
+  double min_steal_log2; /* log2 of the minimal stolen interval length; 0 = log2(8!) */
+  int device;            /* CUDA device ordinal */
+} pbbgpu_config_t;
+
+typedef struct {
+  uint64_t decomposed;          /* raw, PoolStats.decomposed semantics */
+  uint64_t unique;              /* decomposed - replay duplicates (partition invariant) */
+  uint64_t replay_dups;
+  uint64_t leaves;
+  uint64_t improvements;
+  uint64_t local_steals;
+  uint64_t steal_phases;
+  uint64_t intervals_initialized;
+  uint64_t rounds;
+  uint64_t steps;
+  double wall_s;                /* pbbgpu_solve only */
+  double kernel_ms;             /* device time of explore kernels (CUDA events) */
+  int completed;                /* pbbgpu_solve only */
+  int K;
+  int group;
+  int steps_per_round;
+} pbbgpu_stats_t;
+
+const char* pbbgpu_last_error(void);
+int pbbgpu_device_count(void);
+
+/* instance helpers (host) */
+int pbbgpu_taillard(int n, int m, int32_t seed, int32_t* p_out);
+int pbbgpu_taillard_named(const char* name, int* n, int* m, int32_t* p_out /* n*m */);
+int64_t pbbgpu_makespan(int n, int m, const int32_t* p, const int32_t* perm);
+int64_t pbbgpu_neh(int n, int m, const int32_t* p, int32_t* perm_out);
+
+/* pool */
+int pbbgpu_create(int n, int m, const int32_t* p_jobmajor, int bound_kind,
+                  const pbbgpu_config_t* cfg, pbbgpu_pool** out);
+void pbbgpu_destroy(pbbgpu_pool* pool);
+int pbbgpu_K(const pbbgpu_pool* pool);
+int pbbgpu_set_initial_bound(pbbgpu_pool* pool, int64_t ub, const int32_t* sched, int len);
+int pbbgpu_assign(pbbgpu_pool* pool, const uint16_t* a_digits, const uint16_t* b_digits,
+                  const uint8_t* b_is_nfact, int count);
+int pbbgpu_assign_split(pbbgpu_pool* pool, int pieces);
+int pbbgpu_run_round(pbbgpu_pool* pool, int* active_out);
+int pbbgpu_active_count(pbbgpu_pool* pool, int* active_out);
+int pbbgpu_snapshot(pbbgpu_pool* pool, uint16_t* pos_digits, uint16_t* end_digits,
+                    uint8_t* end_is_nfact, int cap, int* count);
+int pbbgpu_best(pbbgpu_pool* pool, int64_t* value, int32_t* perm_or_null, int* has_perm);
+int pbbgpu_offer_bound(pbbgpu_pool* pool, int64_t value);
+int pbbgpu_stats(pbbgpu_pool* pool, pbbgpu_stats_t* out);
+int pbbgpu_histogram(pbbgpu_pool* pool, uint64_t* hist_out, int len);
+int pbbgpu_decompose_batch(pbbgpu_pool* pool, const int32_t* perms, const int32_t* d1,
+                           const int32_t* d2, int count, int64_t incumbent, int64_t* child_lb,
+                           uint8_t* direction, uint8_t* pruned, int64_t* lb_fwd_or_null,
+                           int64_t* lb_bwd_or_null);
+
+/* pool_run: assign [0,n!) (or the given intervals), run rounds to exhaustion or time limit */
+int pbbgpu_solve(pbbgpu_pool* pool, int64_t initial_ub, const uint16_t* a_digits,
+                 const uint16_t* b_digits, const uint8_t* b_is_nfact, int count,
+                 int64_t* best_value, int32_t* best_perm, int* has_perm, pbbgpu_stats_t* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,16 @@
+"""paper_2012_09511_b200 — B200-native PFSP Branch-and-Bound (GPU IVM explorers, LB1/LB2).
+
+Drop-in for the reference solver's solve/explore path (ExplorerPool / pool_run / decompose,
+/root/reference/proj/include/pbb/explorer.hpp, bound.hpp). Compute runs only in
+libpbbgpu.so (hand-written sm_100a kernels); see DESIGN.md.
+"""
+from .factoradic import compare, from_decimal, midpoint, to_decimal
+from .instance import Instance, Schedule, generate_taillard, makespan, neh, parse_instance, taillard_named
+from .pool import (BACKWARD, FORWARD, NO_INCUMBENT, Decomposition, GpuPool, PoolConfig, PoolResult,
+                   PoolStats, Subproblem, normalize, pool_run)
+
+__all__ = [
+    "Instance", "Schedule", "generate_taillard", "taillard_named", "makespan", "neh", "parse_instance",
+    "GpuPool", "PoolConfig", "PoolStats", "PoolResult", "Subproblem", "Decomposition", "pool_run",
+    "normalize", "to_decimal", "from_decimal", "compare", "midpoint", "FORWARD", "BACKWARD", "NO_INCUMBENT",
+]

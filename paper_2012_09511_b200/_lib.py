@@ -1,0 +1,137 @@
+"""ctypes binding of the C-ABI in include/pbbgpu.h (libpbbgpu.so, built in-tree).
+
+The shared library is the product: there is no Python or CPU fallback for any compute
+entry point. If the library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpbbgpu.so")
+
+PBBGPU_OK = 0
+PBBGPU_ERR_ARG = -1
+PBBGPU_ERR_STATE = -2
+PBBGPU_ERR_CUDA = -3
+PBBGPU_ERR_CAPACITY = -4
+LB1 = 1
+LB2 = 2
+
+# every symbol include/pbbgpu.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "pbbgpu_last_error", "pbbgpu_device_count", "pbbgpu_taillard", "pbbgpu_taillard_named",
+    "pbbgpu_makespan", "pbbgpu_neh", "pbbgpu_create", "pbbgpu_destroy", "pbbgpu_K",
+    "pbbgpu_set_initial_bound", "pbbgpu_assign", "pbbgpu_assign_split", "pbbgpu_run_round",
+    "pbbgpu_active_count", "pbbgpu_snapshot", "pbbgpu_best", "pbbgpu_offer_bound",
+    "pbbgpu_stats", "pbbgpu_histogram", "pbbgpu_decompose_batch", "pbbgpu_solve",
+)
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("explorers", ctypes.c_int),
+        ("group", ctypes.c_int),
+        ("steps_per_round", ctypes.c_int),
+        ("disable_pruning", ctypes.c_int),
+        ("pinned", ctypes.c_int),
+        ("time_limit_s", ctypes.c_double),
+        ("min_steal_log2", ctypes.c_double),
+        ("device", ctypes.c_int),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("decomposed", ctypes.c_uint64),
+        ("unique", ctypes.c_uint64),
+        ("replay_dups", ctypes.c_uint64),
+        ("leaves", ctypes.c_uint64),
+        ("improvements", ctypes.c_uint64),
+        ("local_steals", ctypes.c_uint64),
+        ("steal_phases", ctypes.c_uint64),
+        ("intervals_initialized", ctypes.c_uint64),
+        ("rounds", ctypes.c_uint64),
+        ("steps", ctypes.c_uint64),
+        ("wall_s", ctypes.c_double),
+        ("kernel_ms", ctypes.c_double),
+        ("completed", ctypes.c_int),
+        ("K", ctypes.c_int),
+        ("group", ctypes.c_int),
+        ("steps_per_round", ctypes.c_int),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libpbbgpu.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the product has no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    u16p = ctypes.POINTER(ctypes.c_uint16)
+    u8p = ctypes.POINTER(ctypes.c_uint8)
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    ip = ctypes.POINTER(ctypes.c_int)
+    sig = {
+        "pbbgpu_last_error": (ctypes.c_char_p, []),
+        "pbbgpu_device_count": (ctypes.c_int, []),
+        "pbbgpu_taillard": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int32, i32p]),
+        "pbbgpu_taillard_named": (ctypes.c_int, [ctypes.c_char_p, ip, ip, i32p]),
+        "pbbgpu_makespan": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, i32p, i32p]),
+        "pbbgpu_neh": (ctypes.c_int64, [ctypes.c_int, ctypes.c_int, i32p, i32p]),
+        "pbbgpu_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, i32p, ctypes.c_int,
+                                         ctypes.POINTER(Config), ctypes.POINTER(P)]),
+        "pbbgpu_destroy": (None, [P]),
+        "pbbgpu_K": (ctypes.c_int, [P]),
+        "pbbgpu_set_initial_bound": (ctypes.c_int, [P, ctypes.c_int64, i32p, ctypes.c_int]),
+        "pbbgpu_assign": (ctypes.c_int, [P, u16p, u16p, u8p, ctypes.c_int]),
+        "pbbgpu_assign_split": (ctypes.c_int, [P, ctypes.c_int]),
+        "pbbgpu_run_round": (ctypes.c_int, [P, ip]),
+        "pbbgpu_active_count": (ctypes.c_int, [P, ip]),
+        "pbbgpu_snapshot": (ctypes.c_int, [P, u16p, u16p, u8p, ctypes.c_int, ip]),
+        "pbbgpu_best": (ctypes.c_int, [P, i64p, i32p, ip]),
+        "pbbgpu_offer_bound": (ctypes.c_int, [P, ctypes.c_int64]),
+        "pbbgpu_stats": (ctypes.c_int, [P, ctypes.POINTER(Stats)]),
+        "pbbgpu_histogram": (ctypes.c_int, [P, u64p, ctypes.c_int]),
+        "pbbgpu_decompose_batch": (ctypes.c_int, [P, i32p, i32p, i32p, ctypes.c_int, ctypes.c_int64,
+                                                  i64p, u8p, u8p, i64p, i64p]),
+        "pbbgpu_solve": (ctypes.c_int, [P, ctypes.c_int64, u16p, u16p, u8p, ctypes.c_int, i64p, i32p,
+                                        ip, ctypes.POINTER(Stats)]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class PbbError(RuntimeError):
+    """Error returned through the C-ABI (status code + pbbgpu_last_error())."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"pbbgpu error {code}: {msg}")
+        self.code = code
+
+
+def check(rc: int) -> None:
+    if rc != PBBGPU_OK:
+        msg = load().pbbgpu_last_error()
+        msg = msg.decode() if msg else ""
+        if rc == PBBGPU_ERR_ARG:
+            raise ValueError(msg)
+        raise PbbError(rc, msg)

@@ -1,0 +1,856 @@
+// B200-native PFSP Branch-and-Bound device code (sm_100a).
+//
+// One explorer (IVM: Integer-Vector-Matrix, §2.5 / src/ivm.cpp) per group of G
+// lanes; a 128-thread CTA holds 128/G explorers whose whole state lives in shared memory
+// for the duration of a persistent launch ("round"). Each group loops
+//     select (or replay) -> [leaf: makespan | internal: bound children -> MinMin -> prune
+//     -> branch]
+// entirely out of shared memory; the only global traffic per step is the incumbent read.
+//
+// Semantics follow the reference bit-for-bit (paths under /root/reference/proj):
+//   select_next + end test      src/ivm.cpp:90-122
+//   decode (free jobs in row order minus the selected cell)  src/ivm.cpp:152-172
+//   LB1 children, fwd/bwd       src/bound.cpp:61-88
+//   MinMin + prune (>=)         src/bound.cpp:109-138
+//   branch                      src/ivm.cpp:124-145
+//   leaf = one free job, improve iff mk < improve bound   src/explorer.cpp:42-57
+//   init_at replay              src/ivm.cpp:48-88
+// LB2 follows SURVEY.md §8 row a22 (no reference implementation exists).
+//
+// Incremental node tables (B200 design, not in the reference): instead of re-scanning the
+// prefix/suffix of every node (bound_tables, src/bound.cpp:20-46), the explorer keeps
+//   FS[d] = front of the first d forward jobs, TS[d] = tail of the first d backward jobs
+// in one (n+1)*m uint16 stack (FS grows from slot 0, TS from slot n; d1+d2 <= n-1 keeps
+// them disjoint) and R = per-machine sum over the jobs of the current row, updated by
+// +-p on descend/backtrack. A node's tables then cost one O(m) extension.
+#pragma once
+
+#include <climits>
+#include <cstdint>
+
+#include "pbb_layout.h"
+
+namespace pbbgpu {
+
+__host__ __device__ inline int tri_off(int l, int n) { return l * n - (l * (l - 1)) / 2; }
+__host__ __device__ inline int round_up(int x, int a) { return (x + a - 1) / a * a; }
+
+// Per-CTA shared instance region (identical computation on host and device).
+struct InstLayout {
+  int o_p32, o_pk, o_pl, o_ord, o_lag, o_cnt, o_hist, o_dhist, bytes;
+};
+
+__host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs) {
+  InstLayout s;
+  int o = 0;
+  s.o_p32 = o;
+  o += n * mp * 4;
+  s.o_lag = o;
+  o += round_up(npairs * n * 2, 16);
+  s.o_pk = o;
+  o += round_up(npairs, 16);
+  s.o_pl = o;
+  o += round_up(npairs, 16);
+  s.o_ord = o;
+  o += round_up(npairs * n, 16);
+  s.o_cnt = o;
+  o += 64;
+  s.o_hist = o;
+  o += round_up((n + 1) * 4, 16);
+  s.o_dhist = o;
+  o += round_up((n + 1) * 4, 16);
+  s.bytes = round_up(o, 128);
+  return s;
+}
+
+__host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound) {
+  IvmLayout L;
+  L.n = n;
+  L.m = m;
+  L.mp = round_up(m, 4);
+  int o = 8;  // IvmHdr
+  L.o_cells = o;
+  o += n * (n + 1) / 2;
+  L.o_v = o;
+  o += n;
+  L.o_dir = o;
+  o += n;
+  L.o_end = o;
+  o += n;
+  L.o_tgt = o;
+  o += n;
+  o = round_up(o, 4);
+  L.o_ft = o;
+  o += (n + 1) * m * 2;
+  L.o_r = o;
+  o += m * 2;
+  L.gstride = round_up(o, 16);
+  o = L.gstride;
+  L.o_fr = o;
+  o += L.mp * 4;
+  L.o_tl = o;
+  o += L.mp * 4;
+  L.o_rm = o;
+  o += L.mp * 4;
+  L.o_rt = o;
+  o += L.mp * 4;
+  L.o_frm = o;
+  o += L.mp * 4;
+  // lbf / lbb live right after frm: two int32 [n] arrays
+  o += round_up(2 * n * 4, 16);
+  L.o_free = o;
+  o += round_up(n, 16);
+  if (bound == kLB2) {
+    L.o_heads = o;
+    o += round_up(n * m * 2, 16);
+    L.o_tails = o;
+    o += round_up(n * m * 2, 16);
+    L.o_lst = o;
+    o += n * 16;
+    L.o_pos = o;
+    o += round_up(n, 16);
+  } else {
+    L.o_heads = L.o_tails = L.o_lst = L.o_pos = 0;
+  }
+  o = round_up(o, 16);
+  // stride == 16 (mod 128): the groups of one warp hit distinct bank quads on LDS.128
+  L.sstride = o + ((16 - (o % 128)) + 128) % 128;
+  return L;
+}
+
+#ifdef __CUDACC__
+
+template <int G>
+struct Group {
+  unsigned mask;
+  int g;
+  int base;
+  __device__ __forceinline__ Group() {
+    const int lane = threadIdx.x & 31;
+    g = lane & (G - 1);
+    base = lane & ~(G - 1);
+    mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << base);
+  }
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    const unsigned b = __ballot_sync(mask, p);
+    return G == 32 ? b : ((b >> base) & ((1u << G) - 1u));
+  }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  __device__ __forceinline__ int bcast(int v, int src) const { return __shfl_sync(mask, v, src, G); }
+  __device__ __forceinline__ int rmin(int v) const {
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1) v = min(v, __shfl_xor_sync(mask, v, o, G));
+    return v;
+  }
+  __device__ __forceinline__ int rmax(int v) const {
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1) v = max(v, __shfl_xor_sync(mask, v, o, G));
+    return v;
+  }
+  __device__ __forceinline__ int rsum(int v) const {
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1) v += __shfl_xor_sync(mask, v, o, G);
+    return v;
+  }
+  __device__ __forceinline__ unsigned long long ror64(unsigned long long v) const {
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1) v |= __shfl_xor_sync(mask, v, o, G);
+    return v;
+  }
+};
+
+// Shared-memory view of one explorer.
+struct IvmView {
+  IvmHdr* hdr;
+  int8_t* cells;
+  int8_t* V;
+  uint8_t* dir;
+  int8_t* endd;
+  int8_t* tgt;
+  uint16_t* ft;
+  uint16_t* R;
+  int* fr;
+  int* tl;
+  int* rm;
+  int* rt;
+  int* frm;
+  int* lbf;
+  int* lbb;
+  uint8_t* freej;
+  uint16_t* heads;
+  uint16_t* tails;
+  int4* lst;
+  uint8_t* pos;
+  __device__ __forceinline__ IvmView(unsigned char* b, const IvmLayout& L) {
+    hdr = reinterpret_cast<IvmHdr*>(b);
+    cells = reinterpret_cast<int8_t*>(b + L.o_cells);
+    V = reinterpret_cast<int8_t*>(b + L.o_v);
+    dir = b + L.o_dir;
+    endd = reinterpret_cast<int8_t*>(b + L.o_end);
+    tgt = reinterpret_cast<int8_t*>(b + L.o_tgt);
+    ft = reinterpret_cast<uint16_t*>(b + L.o_ft);
+    R = reinterpret_cast<uint16_t*>(b + L.o_r);
+    fr = reinterpret_cast<int*>(b + L.o_fr);
+    tl = reinterpret_cast<int*>(b + L.o_tl);
+    rm = reinterpret_cast<int*>(b + L.o_rm);
+    rt = reinterpret_cast<int*>(b + L.o_rt);
+    frm = reinterpret_cast<int*>(b + L.o_frm);
+    lbf = reinterpret_cast<int*>(b + L.o_frm + L.mp * 4);
+    lbb = lbf + L.n;
+    freej = b + L.o_free;
+    heads = reinterpret_cast<uint16_t*>(b + L.o_heads);
+    tails = reinterpret_cast<uint16_t*>(b + L.o_tails);
+    lst = reinterpret_cast<int4*>(b + L.o_lst);
+    pos = b + L.o_pos;
+  }
+};
+
+struct InstView {
+  const int* p32;  // [n][mp]
+  const uint8_t* pk;
+  const uint8_t* pl;
+  const uint8_t* ord;
+  const uint16_t* lag;
+  int npairs;
+};
+
+// ------------------------------------------------------------------ bounding
+//
+// Input (shared, per explorer): fr/tl/rm/rt/frm tables of the node, freej[0..f-1].
+// Output: lbf[c], lbb[c] = bound of the forward child sigma1.j and of the backward child
+// j.sigma2 for free job j = freej[c].
+
+// LB1 (src/bound.cpp:61-88), rewritten so each machine costs 4 integer ops per direction:
+//   fwd: t = max(prev, front[k]); best = max(best, t + remain[k] + tail[k]); prev = t + p
+//   bwd: t = max(prev, tail[k]);  best = max(best, t + front[k] + remain[k]); prev = t + p
+// (prev + remain - p + tail with prev = t + p is exactly t + remain + tail).
+template <int M, int G>
+__device__ __forceinline__ void children_lb1(const Group<G>& grp, const IvmView& iv,
+                                             const InstView& in, int mp, int f) {
+  for (int c = grp.g; c < f; c += G) {
+    const int j = iv.freej[c];
+    const int* pr = in.p32 + j * mp;
+    int p[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) p[k] = pr[k];
+    int prev = 0, best = 0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const int t = max(prev, iv.fr[k]);
+      best = max(best, t + iv.rt[k]);
+      prev = t + p[k];
+    }
+    iv.lbf[c] = best;
+    prev = 0;
+    best = 0;
+#pragma unroll
+    for (int k = M - 1; k >= 0; --k) {
+      const int t = max(prev, iv.tl[k]);
+      best = max(best, t + iv.frm[k]);
+      prev = t + p[k];
+    }
+    iv.lbb[c] = best;
+  }
+}
+
+// LB2: for every machine pair (k<l) the free jobs are taken in that pair's Johnson/Mitten
+// order (precomputed per instance); each child c evaluates
+//   t0 = r[k], t1 = r[l]; for j in order, j free, j != job(c):
+//       t0 += p[j][k]; t1 = max(t1, t0 + lag_j) + p[j][l]
+//   lb_kl = max(t0 + q[k], t1 + q[l])
+// with (r, q) = (extended head, node tail) for forward children and (node head, extended
+// tail) for backward children; LB2 = max over pairs.
+// Per pair the group first compacts the node's free jobs in pair order (ballot), then the
+// lanes run the 2f child chains over the compacted sequence (broadcast LDS.128 reads).
+template <int M, int G>
+__device__ __forceinline__ void children_lb2(const Group<G>& grp, const IvmView& iv,
+                                             const InstView& in, int n, int mp, int f,
+                                             unsigned long long fmask) {
+  // child heads / tails
+  for (int c = grp.g; c < f; c += G) {
+    const int j = iv.freej[c];
+    const int* pr = in.p32 + j * mp;
+    int prev = 0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      prev = max(prev, iv.fr[k]) + pr[k];
+      iv.heads[c * M + k] = static_cast<uint16_t>(prev);
+    }
+    prev = 0;
+#pragma unroll
+    for (int k = M - 1; k >= 0; --k) {
+      prev = max(prev, iv.tl[k]) + pr[k];
+      iv.tails[c * M + k] = static_cast<uint16_t>(prev);
+    }
+    iv.lbf[c] = 0;
+    iv.lbb[c] = 0;
+  }
+  grp.sync();
+  for (int q = 0; q < in.npairs; ++q) {
+    const int k = in.pk[q], l = in.pl[q];
+    const uint8_t* ord = in.ord + q * n;
+    const uint16_t* lag = in.lag + q * n;
+    int cnt = 0;
+    for (int b0 = 0; b0 < n; b0 += G) {
+      const int t = b0 + grp.g;
+      const int j = t < n ? ord[t] : 0;
+      const bool isf = t < n && ((fmask >> j) & 1ull);
+      const unsigned bal = grp.ballot(isf);
+      if (isf) {
+        const int idx = cnt + __popc(bal & ((1u << grp.g) - 1u));
+        iv.lst[idx] = make_int4(in.p32[j * mp + k], in.p32[j * mp + l], lag[j], 0);
+        iv.pos[j] = static_cast<uint8_t>(idx);
+      }
+      cnt += __popc(bal);
+    }
+    grp.sync();
+    const int qk = iv.tl[k], ql = iv.tl[l], rk = iv.fr[k], rl = iv.fr[l];
+    for (int cc = grp.g; cc < 2 * f; cc += G) {
+      const bool fwd = cc < f;
+      const int c = fwd ? cc : cc - f;
+      const int s = iv.pos[iv.freej[c]];
+      int t0, t1, q0, q1;
+      if (fwd) {
+        t0 = iv.heads[c * M + k];
+        t1 = iv.heads[c * M + l];
+        q0 = qk;
+        q1 = ql;
+      } else {
+        t0 = rk;
+        t1 = rl;
+        q0 = iv.tails[c * M + k];
+        q1 = iv.tails[c * M + l];
+      }
+      for (int i = 0; i < f; ++i) {
+        const int4 e = iv.lst[i];
+        if (i != s) {
+          t0 += e.x;
+          t1 = max(t1, t0 + e.z) + e.y;
+        }
+      }
+      const int v = max(t0 + q0, t1 + q1);
+      int* dst = fwd ? &iv.lbf[c] : &iv.lbb[c];
+      *dst = max(*dst, v);
+    }
+    grp.sync();
+  }
+}
+
+// MinMin (src/bound.cpp:109-131): lo over the union, fewer occurrences of lo wins, then the
+// larger sum, then Forward.
+template <int G>
+__device__ __forceinline__ int minmin(const Group<G>& grp, const IvmView& iv, int f) {
+  int lo = INT_MAX;
+  for (int c = grp.g; c < f; c += G) lo = min(lo, min(iv.lbf[c], iv.lbb[c]));
+  lo = grp.rmin(lo);
+  int cnt = 0, sf = 0, sb = 0;
+  for (int c = grp.g; c < f; c += G) {
+    const int a = iv.lbf[c], b = iv.lbb[c];
+    cnt += (a == lo) + ((b == lo) << 16);
+    sf += a;
+    sb += b;
+  }
+  cnt = grp.rsum(cnt);
+  sf = grp.rsum(sf);
+  sb = grp.rsum(sb);
+  const int cf = cnt & 0xffff, cb = cnt >> 16;
+  if (cf != cb) return cf < cb ? kFwd : kBwd;
+  if (sf != sb) return sf > sb ? kFwd : kBwd;
+  return kFwd;
+}
+
+// Node tables from the incremental stacks: node at `level` with selected job `job` placed
+// by dir[level]; d1/d2 include it.
+template <int M, int G>
+__device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& iv,
+                                            const InstView& in, int n, int mp, int job, int dI,
+                                            int d1, int d2) {
+  const uint16_t* fsrc = iv.ft + (dI == kFwd ? d1 - 1 : d1) * M;
+  const uint16_t* tsrc = iv.ft + (n - (dI == kBwd ? d2 - 1 : d2)) * M;
+  const int* pr = in.p32 + job * mp;
+  for (int k = grp.g; k < M; k += G) {
+    iv.rm[k] = static_cast<int>(iv.R[k]) - pr[k];
+    if (dI != kFwd) iv.fr[k] = fsrc[k];
+    if (dI != kBwd) iv.tl[k] = tsrc[k];
+  }
+  if (grp.g == G - 1) {
+    int prev = 0;
+    if (dI == kFwd) {
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        prev = max(prev, static_cast<int>(fsrc[k])) + pr[k];
+        iv.fr[k] = prev;
+      }
+    } else {
+#pragma unroll
+      for (int k = M - 1; k >= 0; --k) {
+        prev = max(prev, static_cast<int>(tsrc[k])) + pr[k];
+        iv.tl[k] = prev;
+      }
+    }
+  }
+  grp.sync();
+  for (int k = grp.g; k < M; k += G) {
+    iv.rt[k] = iv.rm[k] + iv.tl[k];
+    iv.frm[k] = iv.fr[k] + iv.rm[k];
+  }
+}
+
+// Free jobs of the node (row minus the selected cell, row order, src/ivm.cpp:164-169).
+template <int G>
+__device__ __forceinline__ unsigned long long gather_free(const Group<G>& grp, const IvmView& iv,
+                                                          const int8_t* row, int sel, int f) {
+  unsigned long long m = 0;
+  for (int c = grp.g; c < f; c += G) {
+    const int x = row[c < sel ? c : c + 1];
+    const int j = (x < 0 ? -x : x) - 1;
+    iv.freej[c] = static_cast<uint8_t>(j);
+    m |= 1ull << j;
+  }
+  return m;
+}
+
+// ------------------------------------------------------------------ explorer steps
+
+// position_reached_end (src/ivm.cpp:90-97): padded V >= end.
+template <int G>
+__device__ __forceinline__ bool reached_end(const Group<G>& grp, const IvmView& iv, int n,
+                                            int level) {
+  for (int b0 = 0; b0 < n; b0 += G) {
+    const int l = b0 + grp.g;
+    int pv = 0, ev = 0;
+    if (l < n) {
+      pv = l <= level ? iv.V[l] : 0;
+      ev = iv.endd[l];
+    }
+    const unsigned b = grp.ballot(pv != ev);
+    if (b) {
+      const int src = __ffs(b) - 1;
+      return grp.bcast(pv, src) > grp.bcast(ev, src);
+    }
+  }
+  return true;
+}
+
+// select_next (src/ivm.cpp:99-122) with the incremental R / d1 / d2 bookkeeping.
+// Returns the selected cell, or -1 when the explorer is exhausted.
+template <int M, int G>
+__device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& iv,
+                                           const InstView& in, int n, int mp, bool has_end,
+                                           int& level, int& d1, int& d2) {
+  for (;;) {
+    if (level < 0) return -1;
+    const int len = n - level;
+    const int8_t* row = iv.cells + tri_off(level, n);
+    const int c0 = iv.V[level];
+    int found = -1;
+    for (int b0 = c0; b0 < len; b0 += G) {
+      const int c = b0 + grp.g;
+      const unsigned b = grp.ballot(c < len && row[c] > 0);
+      if (b) {
+        found = b0 + __ffs(b) - 1;
+        break;
+      }
+    }
+    if (found < 0) {  // row exhausted: backtrack
+      const int dl = iv.dir[level];
+      d1 -= dl == kFwd;
+      d2 -= dl == kBwd;
+      grp.sync();
+      if (grp.g == 0) iv.V[level] = 0;
+      --level;
+      if (level >= 0) {
+        const int psel = iv.V[level];
+        const int x = iv.cells[tri_off(level, n) + psel];
+        const int job = (x < 0 ? -x : x) - 1;
+        const int* pr = in.p32 + job * mp;
+        for (int k = grp.g; k < M; k += G) iv.R[k] = static_cast<uint16_t>(iv.R[k] + pr[k]);
+        grp.sync();
+        if (grp.g == 0) iv.V[level] = static_cast<int8_t>(psel + 1);
+      }
+      grp.sync();
+      continue;
+    }
+    grp.sync();
+    if (grp.g == 0) iv.V[level] = static_cast<int8_t>(found);
+    grp.sync();
+    if (has_end && reached_end(grp, iv, n, level)) return -1;
+    return found;
+  }
+}
+
+struct StepCounters {
+  unsigned int decomposed, leaves, dups, improvements, steps;
+};
+
+// Decompose the node at (level, sel) and branch (bound.cpp:98-139 + ivm.cpp:124-145).
+template <int M, int G, int BOUND>
+__device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmView& iv,
+                                                 const InstView& in, int n, int mp, int sel,
+                                                 int prune, int& level, int& d1, int& d2,
+                                                 unsigned* shist) {
+  const int I = level;
+  const int f = n - 1 - I;
+  int8_t* row = iv.cells + tri_off(I, n);
+  const int x = row[sel];
+  const int job = (x < 0 ? -x : x) - 1;
+  const int dI = iv.dir[I];
+  node_tables<M, G>(grp, iv, in, n, mp, job, dI, d1, d2);
+  const unsigned long long fm = grp.ror64(gather_free<G>(grp, iv, row, sel, f));
+  grp.sync();
+  if (BOUND == kLB1) {
+    children_lb1<M, G>(grp, iv, in, mp, f);
+  } else {
+    children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
+  }
+  grp.sync();
+  const int dir = minmin<G>(grp, iv, f);
+  int8_t* nrow = iv.cells + tri_off(I + 1, n);
+  for (int c = grp.g; c < f; c += G) {
+    const int lb = dir == kFwd ? iv.lbf[c] : iv.lbb[c];
+    const int j1 = iv.freej[c] + 1;
+    nrow[c] = static_cast<int8_t>(lb >= prune ? -j1 : j1);
+  }
+  for (int k = grp.g; k < M; k += G) {
+    if (dI == kFwd) iv.ft[d1 * M + k] = static_cast<uint16_t>(iv.fr[k]);
+    else iv.ft[(n - d2) * M + k] = static_cast<uint16_t>(iv.tl[k]);
+    iv.R[k] = static_cast<uint16_t>(iv.rm[k]);
+  }
+  if (grp.g == 0) {
+    iv.dir[I + 1] = static_cast<uint8_t>(dir);
+    iv.V[I + 1] = 0;
+    atomicAdd(&shist[f], 1u);
+  }
+  grp.sync();
+  level = I + 1;
+  d1 += dir == kFwd;
+  d2 += dir == kBwd;
+}
+
+// Leaf: one free job (explorer.cpp:42-57). Makespan of sigma1.j.sigma2 from the node
+// tables: C = max_k (front_{sigma1.j}[k] + tail_{sigma2}[k]).
+template <int M, int G>
+__device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, const InstView& in,
+                                     int n, int mp, int sel, int level, int d1, int d2,
+                                     int improve, DevCounters* ctr, ImpRecord* imp,
+                                     StepCounters& sc) {
+  int8_t* row = iv.cells + tri_off(level, n);
+  const int x = row[sel];
+  const int job = (x < 0 ? -x : x) - 1;
+  const int dI = iv.dir[level];
+  node_tables<M, G>(grp, iv, in, n, mp, job, dI, d1, d2);
+  grp.sync();
+  if (grp.g == 0) {
+    const int len = n - level;
+    int jf = -1;
+    for (int c = 0; c < len; ++c) {
+      if (c == sel) continue;
+      const int y = row[c];
+      jf = (y < 0 ? -y : y) - 1;
+    }
+    int mk = 0;
+    if (jf >= 0) {
+      const int* pr = in.p32 + jf * mp;
+      int prev = 0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        prev = max(prev, iv.fr[k]) + pr[k];
+        mk = max(mk, prev + iv.tl[k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < M; ++k) mk = max(mk, iv.fr[k] + iv.tl[k]);
+    }
+    row[sel] = static_cast<int8_t>(x < 0 ? x : -x);  // prune_current
+    ++sc.leaves;
+    if (mk < improve) {
+      const int old = atomicMin(&ctr->best, mk);
+      if (mk < old) {
+        ++sc.improvements;
+        const int slot = atomicAdd(&ctr->imp_count, 1);
+        if (slot < kImpCap) {
+          ImpRecord* r = imp + slot;
+          int a = 0, b = 0;
+          for (int l = 0; l <= level; ++l) {
+            const int y = iv.cells[tri_off(l, n) + iv.V[l]];
+            const int jj = (y < 0 ? -y : y) - 1;
+            if (iv.dir[l] == kFwd) r->perm[a++] = static_cast<int8_t>(jj);
+            else r->perm[n - 1 - b++] = static_cast<int8_t>(jj);
+          }
+          if (jf >= 0) r->perm[a] = static_cast<int8_t>(jf);
+          r->mk = mk;
+        }
+      }
+    }
+  }
+  grp.sync();
+}
+
+template <int M, int G, int BOUND>
+__global__ void __launch_bounds__(128) explore_kernel(const ExploreParams P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const IvmLayout& L = P.L;
+  const int n = L.n, mp = L.mp;
+  constexpr int NG = 128 / G;
+  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? P.npairs : 0);
+
+  // ---- stage the instance (and LB2 pair tables) into shared memory
+  {
+    int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
+    for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = P.p32[i];
+    if (BOUND == kLB2) {
+      uint16_t* sl = reinterpret_cast<uint16_t*>(smem + IL.o_lag);
+      for (int i = threadIdx.x; i < P.npairs * n; i += blockDim.x) {
+        sl[i] = P.lag[i];
+        smem[IL.o_ord + i] = P.order[i];
+      }
+      for (int i = threadIdx.x; i < P.npairs; i += blockDim.x) {
+        smem[IL.o_pk + i] = P.pk[i];
+        smem[IL.o_pl + i] = P.pl[i];
+      }
+    }
+    unsigned* h = reinterpret_cast<unsigned*>(smem + IL.o_hist);
+    unsigned* dh = reinterpret_cast<unsigned*>(smem + IL.o_dhist);
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) h[i] = dh[i] = 0;
+    unsigned* cnt = reinterpret_cast<unsigned*>(smem + IL.o_cnt);
+    if (threadIdx.x < 16) cnt[threadIdx.x] = 0;
+  }
+  // ---- stage this CTA's explorers
+  const int first = blockIdx.x * NG;
+  unsigned char* ivbase = smem + IL.bytes;
+  {
+    const int words = L.gstride / 16;
+    for (int idx = threadIdx.x; idx < NG * words; idx += blockDim.x) {
+      const int i = idx / words, w = idx % words;
+      if (first + i < P.K) {
+        reinterpret_cast<uint4*>(ivbase + i * L.sstride)[w] =
+            reinterpret_cast<const uint4*>(P.state + static_cast<size_t>(first + i) * L.gstride)[w];
+      }
+    }
+  }
+  __syncthreads();
+
+  InstView in;
+  in.p32 = reinterpret_cast<const int*>(smem + IL.o_p32);
+  in.pk = smem + IL.o_pk;
+  in.pl = smem + IL.o_pl;
+  in.ord = smem + IL.o_ord;
+  in.lag = reinterpret_cast<const uint16_t*>(smem + IL.o_lag);
+  in.npairs = P.npairs;
+  unsigned* shist = reinterpret_cast<unsigned*>(smem + IL.o_hist);
+  unsigned* sdhist = reinterpret_cast<unsigned*>(smem + IL.o_dhist);
+
+  Group<G> grp;
+  const int gi = threadIdx.x / G;
+  StepCounters sc = {0, 0, 0, 0, 0};
+  if (first + gi < P.K) {
+    IvmView iv(ivbase + gi * L.sstride, L);
+    int level = iv.hdr->level, state = iv.hdr->state, d1 = iv.hdr->d1, d2 = iv.hdr->d2;
+    int rlev = iv.hdr->rlev, nrep = iv.hdr->nrep;
+    const bool has_end = iv.hdr->has_end != 0;
+    int best = *reinterpret_cast<volatile int*>(&P.ctr->best);
+    for (int step = 0; step < P.steps && state != kEmpty; ++step) {
+      if ((step & 15) == 15) best = *reinterpret_cast<volatile int*>(&P.ctr->best);
+      const int prune = P.prune_mode == 0 ? best : (P.prune_mode == 1 ? P.pinned_ub : INT_MAX);
+      const int improve = P.prune_mode == 1 ? 0 : best;
+      ++sc.steps;
+      if (state == kInit) {
+        // one replay level of init_at (src/ivm.cpp:70-86)
+        const int l = rlev;
+        const int digit = iv.tgt[l];
+        int8_t* row = iv.cells + tri_off(l, n);
+        level = l;
+        for (int c = grp.g; c < digit; c += G) {
+          const int x = row[c];
+          if (x > 0) row[c] = static_cast<int8_t>(-x);
+        }
+        grp.sync();
+        if (grp.g == 0) iv.V[l] = static_cast<int8_t>(digit);
+        grp.sync();
+        if (row[digit] < 0 || l >= n - 2) {
+          // positioned: duplicates = min(L, lnz(a)) (SURVEY.md §7 hard part 1)
+          int lz = 0;
+          for (int t = grp.g; t < n; t += G)
+            if (iv.tgt[t] != 0) lz = max(lz, t);
+          lz = grp.rmax(lz);
+          const int dup = min(nrep, lz);
+          if (grp.g == 0) {
+            sc.dups += dup;
+            for (int t = 0; t < dup; ++t) atomicAdd(&sdhist[n - 1 - t], 1u);
+          }
+          state = kActive;
+          continue;
+        }
+        decompose_branch<M, G, BOUND>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist);
+        ++sc.decomposed;
+        ++nrep;
+        rlev = level;
+        continue;
+      }
+      const int sel = select_next<M, G>(grp, iv, in, n, mp, has_end, level, d1, d2);
+      if (sel < 0) {
+        state = kEmpty;
+        break;
+      }
+      if (n - 1 - level <= 1) {
+        leaf<M, G>(grp, iv, in, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc);
+        continue;
+      }
+      decompose_branch<M, G, BOUND>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist);
+      ++sc.decomposed;
+    }
+    if (grp.g == 0) {
+      iv.hdr->level = static_cast<int16_t>(level);
+      iv.hdr->state = static_cast<uint8_t>(state);
+      iv.hdr->d1 = static_cast<uint8_t>(d1);
+      iv.hdr->d2 = static_cast<uint8_t>(d2);
+      iv.hdr->rlev = static_cast<uint8_t>(rlev);
+      iv.hdr->nrep = static_cast<uint8_t>(nrep);
+      unsigned* cnt = reinterpret_cast<unsigned*>(smem + IL.o_cnt);
+      atomicAdd(&cnt[0], sc.decomposed);
+      atomicAdd(&cnt[1], sc.leaves);
+      atomicAdd(&cnt[2], sc.dups);
+      atomicAdd(&cnt[3], sc.improvements);
+      atomicAdd(&cnt[4], sc.steps);
+    }
+  }
+  __syncthreads();
+  // ---- write back explorers and counters
+  {
+    const int words = L.gstride / 16;
+    for (int idx = threadIdx.x; idx < NG * words; idx += blockDim.x) {
+      const int i = idx / words, w = idx % words;
+      if (first + i < P.K) {
+        reinterpret_cast<uint4*>(P.state + static_cast<size_t>(first + i) * L.gstride)[w] =
+            reinterpret_cast<const uint4*>(ivbase + i * L.sstride)[w];
+      }
+    }
+    const unsigned* cnt = reinterpret_cast<const unsigned*>(smem + IL.o_cnt);
+    if (threadIdx.x == 0) {
+      if (cnt[0]) atomicAdd(&P.ctr->decomposed, static_cast<unsigned long long>(cnt[0]));
+      if (cnt[1]) atomicAdd(&P.ctr->leaves, static_cast<unsigned long long>(cnt[1]));
+      if (cnt[2]) atomicAdd(&P.ctr->dups, static_cast<unsigned long long>(cnt[2]));
+      if (cnt[3]) atomicAdd(&P.ctr->improvements, static_cast<unsigned long long>(cnt[3]));
+      if (cnt[4]) atomicAdd(&P.ctr->steps, static_cast<unsigned long long>(cnt[4]));
+    }
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+      if (shist[i]) atomicAdd(&P.hist[i], static_cast<unsigned long long>(shist[i]));
+      if (sdhist[i]) atomicAdd(&P.dhist[i], static_cast<unsigned long long>(sdhist[i]));
+    }
+  }
+}
+
+// Batched decompose of explicit nodes (the per-node parity hook, bound.hpp:78-79):
+// node i = perm[i*n .. i*n+n-1], d1[i], d2[i]. Tables are rebuilt from scratch
+// (bound_tables, src/bound.cpp:20-46); outputs are the chosen-direction bounds.
+struct BatchParams {
+  IvmLayout L;
+  const int* perms;
+  const int* d1;
+  const int* d2;
+  int count;
+  int incumbent;
+  const int* p32;
+  int npairs;
+  const uint8_t* pk;
+  const uint8_t* pl;
+  const uint8_t* order;
+  const uint16_t* lag;
+  int* child_lb;   // [count*n]
+  int* lb_fwd;     // [count*n] both sets (before MinMin), for the parity tests
+  int* lb_bwd;
+  uint8_t* dir;    // [count]
+  uint8_t* pruned; // [count*n]
+};
+
+template <int M, int G, int BOUND>
+__global__ void __launch_bounds__(128) decompose_batch_kernel(const BatchParams B) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const IvmLayout& L = B.L;
+  const int n = L.n, mp = L.mp;
+  constexpr int NG = 128 / G;
+  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? B.npairs : 0);
+  {
+    int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
+    for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
+    if (BOUND == kLB2) {
+      uint16_t* sl = reinterpret_cast<uint16_t*>(smem + IL.o_lag);
+      for (int i = threadIdx.x; i < B.npairs * n; i += blockDim.x) {
+        sl[i] = B.lag[i];
+        smem[IL.o_ord + i] = B.order[i];
+      }
+      for (int i = threadIdx.x; i < B.npairs; i += blockDim.x) {
+        smem[IL.o_pk + i] = B.pk[i];
+        smem[IL.o_pl + i] = B.pl[i];
+      }
+    }
+  }
+  __syncthreads();
+  InstView in;
+  in.p32 = reinterpret_cast<const int*>(smem + IL.o_p32);
+  in.pk = smem + IL.o_pk;
+  in.pl = smem + IL.o_pl;
+  in.ord = smem + IL.o_ord;
+  in.lag = reinterpret_cast<const uint16_t*>(smem + IL.o_lag);
+  in.npairs = B.npairs;
+  Group<G> grp;
+  const int gi = threadIdx.x / G;
+  IvmView iv(smem + IL.bytes + gi * L.sstride, L);
+  for (int node = blockIdx.x * NG + gi; node < B.count; node += gridDim.x * NG) {
+    const int* perm = B.perms + static_cast<size_t>(node) * n;
+    const int d1 = B.d1[node], d2 = B.d2[node];
+    const int f = n - d1 - d2;
+    if (grp.g == 0) {
+      for (int k = 0; k < M; ++k) iv.fr[k] = iv.tl[k] = iv.rm[k] = 0;
+      for (int i = 0; i < d1; ++i) {  // front (bound.cpp:25-30)
+        const int* pr = in.p32 + perm[i] * mp;
+        int prev = 0;
+        for (int k = 0; k < M; ++k) {
+          prev = max(prev, iv.fr[k]) + pr[k];
+          iv.fr[k] = prev;
+        }
+      }
+      for (int i = n - 1; i >= n - d2; --i) {  // tail (bound.cpp:35-39)
+        const int* pr = in.p32 + perm[i] * mp;
+        int prev = 0;
+        for (int k = M - 1; k >= 0; --k) {
+          prev = max(prev, iv.tl[k]) + pr[k];
+          iv.tl[k] = prev;
+        }
+      }
+      for (int i = d1; i < n - d2; ++i) {
+        const int* pr = in.p32 + perm[i] * mp;
+        for (int k = 0; k < M; ++k) iv.rm[k] += pr[k];
+      }
+      for (int k = 0; k < M; ++k) {
+        iv.rt[k] = iv.rm[k] + iv.tl[k];
+        iv.frm[k] = iv.fr[k] + iv.rm[k];
+      }
+    }
+    unsigned long long fm = 0;
+    for (int c = grp.g; c < f; c += G) {
+      const int j = perm[d1 + c];
+      iv.freej[c] = static_cast<uint8_t>(j);
+      fm |= 1ull << j;
+    }
+    fm = grp.ror64(fm);
+    grp.sync();
+    if (BOUND == kLB1) children_lb1<M, G>(grp, iv, in, mp, f);
+    else children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
+    grp.sync();
+    const int dir = minmin<G>(grp, iv, f);
+    for (int c = grp.g; c < f; c += G) {
+      const int lb = dir == kFwd ? iv.lbf[c] : iv.lbb[c];
+      B.child_lb[static_cast<size_t>(node) * n + c] = lb;
+      B.lb_fwd[static_cast<size_t>(node) * n + c] = iv.lbf[c];
+      B.lb_bwd[static_cast<size_t>(node) * n + c] = iv.lbb[c];
+      B.pruned[static_cast<size_t>(node) * n + c] = lb >= B.incumbent;
+    }
+    if (grp.g == 0) B.dir[node] = static_cast<uint8_t>(dir);
+    grp.sync();
+  }
+}
+
+#endif  // __CUDACC__
+
+}  // namespace pbbgpu

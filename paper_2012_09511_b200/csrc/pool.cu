@@ -1,0 +1,1135 @@
+// Host driver of the B200 explorer pool + C-ABI (include/pbbgpu.h).
+//
+// Round structure (replaces ExplorerPool::run_round, src/explorer.cpp:224-257):
+//   explore_kernel  persistent, all explorers resident, `steps` select/bound/branch cycles
+//   steal_kernel    one CTA: activity count, steal-right-half pairing of idle explorers with
+//                   the longest remaining intervals, factoradic midpoints, thief re-seating
+//                   (src/explorer.cpp:265-340); thieves replay init_at inside the next
+//                   explore launch
+//   8-byte counter readback (the only per-round host<->device traffic)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pbbgpu.h"
+#include "explore.cuh"
+
+using namespace pbbgpu;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateError : std::logic_error {
+  using std::logic_error::logic_error;
+};
+struct CapacityError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ instance (host)
+
+// Minimal-standard LCG (16807, 2^31-1) via Schrage, machine-major fill: reproduces the
+// published Taillard matrices (generate_taillard, src/instance.cpp:80-114).
+void taillard(int n, int m, int32_t seed, int32_t* p) {
+  if (n < 1 || m < 1) throw std::invalid_argument("generate_taillard needs n >= 1 and m >= 1");
+  if (seed < 1 || seed > 2147483645) throw std::invalid_argument("generator seed must be in [1, 2^31-3]");
+  int64_t s = seed;
+  for (int k = 0; k < m; ++k) {
+    for (int j = 0; j < n; ++j) {
+      const int64_t q = s / 127773, r = s % 127773;
+      s = 16807 * r - 2836 * q;
+      if (s < 0) s += 2147483647;
+      p[static_cast<size_t>(j) * m + k] = static_cast<int32_t>(1 + s * 99 / 2147483647);
+    }
+  }
+}
+
+struct TaClass {
+  int n, m;
+  int32_t seeds[10];
+};
+// Taillard (1993) time seeds, classes ta001-010 ... ta111-120 (src/instance.cpp:125-138).
+const TaClass kTa[12] = {
+    {20, 5, {873654221, 379008056, 1866992158, 216771124, 495070989, 402959317, 1369363414, 2021925980, 573109518, 88325120}},
+    {20, 10, {587595453, 1401007982, 873136276, 268827376, 1634173168, 691823909, 73807235, 1273398721, 2065119309, 1672900551}},
+    {20, 20, {479340445, 268827376, 1958948863, 918272953, 555010963, 2010851491, 1519833303, 1748670931, 1923497586, 1829909967}},
+    {50, 5, {1328042058, 200382020, 496319842, 1203030903, 1730708564, 450926852, 1303135678, 1273398721, 587288402, 248421594}},
+    {50, 10, {1958948863, 575633267, 655816003, 1977864101, 93805469, 1803345551, 49612559, 1899802599, 2013025619, 578962478}},
+    {50, 20, {1539989115, 691823909, 655816003, 1315102446, 1949668355, 1923497586, 1805594913, 1861070898, 715643788, 464843328}},
+    {100, 5, {896678084, 1179439976, 1122278347, 416756875, 267829958, 1835213917, 1328833962, 1418570761, 161033112, 304212574}},
+    {100, 10, {1539989115, 655816003, 960914243, 1915696806, 2013025619, 1168140026, 1923497586, 167698528, 1528387973, 993794175}},
+    {100, 20, {450926852, 1462772409, 1021685265, 83696007, 508154254, 1861070898, 26482542, 444956424, 2115448041, 118254244}},
+    {200, 10, {471503978, 1215892992, 135346136, 1602504050, 160037322, 551454346, 519485142, 383947510, 1968171878, 540872513}},
+    {200, 20, {2013025619, 475051709, 914834335, 810642687, 1019331795, 2056065863, 1342855162, 1325809384, 1988803007, 765656702}},
+    {500, 20, {1368624604, 450181436, 1927888393, 1759567256, 606425239, 19268348, 1298201670, 2041736264, 379756761, 28837162}},
+};
+
+int64_t makespan_host(int n, int m, const int32_t* p, const int32_t* perm) {
+  std::vector<int64_t> c(static_cast<size_t>(m), 0);
+  std::vector<char> seen(static_cast<size_t>(n), 0);
+  for (int i = 0; i < n; ++i) {
+    const int j = perm[i];
+    if (j < 0 || j >= n || seen[static_cast<size_t>(j)]) throw std::invalid_argument("schedule is not a permutation of 0..n-1");
+    seen[static_cast<size_t>(j)] = 1;
+    const int32_t* row = p + static_cast<size_t>(j) * m;
+    c[0] += row[0];
+    for (int k = 1; k < m; ++k) c[k] = std::max(c[k], c[k - 1]) + row[k];
+  }
+  return c[static_cast<size_t>(m) - 1];
+}
+
+// NEH (src/heuristic.cpp:73-103) with Taillard's O(nm) insertion scan: e = prefix heads,
+// q = suffix tails, best position = first minimum.
+int64_t neh_host(int n, int m, const int32_t* p, int32_t* out) {
+  std::vector<int> order(static_cast<size_t>(n));
+  std::iota(order.begin(), order.end(), 0);
+  std::vector<int64_t> load(static_cast<size_t>(n), 0);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < m; ++k) load[static_cast<size_t>(j)] += p[static_cast<size_t>(j) * m + k];
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return load[static_cast<size_t>(a)] > load[static_cast<size_t>(b)]; });
+  std::vector<int> seq;
+  std::vector<int64_t> e, q, f(static_cast<size_t>(m));
+  int64_t last = 0;
+  for (int s = 0; s < n; ++s) {
+    const int job = order[static_cast<size_t>(s)];
+    const int len = static_cast<int>(seq.size());
+    e.assign(static_cast<size_t>(len + 1) * m, 0);
+    q.assign(static_cast<size_t>(len + 2) * m, 0);
+    for (int i = 1; i <= len; ++i) {
+      const int32_t* row = p + static_cast<size_t>(seq[static_cast<size_t>(i - 1)]) * m;
+      for (int k = 0; k < m; ++k) {
+        const int64_t up = k ? e[static_cast<size_t>(i) * m + k - 1] : 0;
+        e[static_cast<size_t>(i) * m + k] = std::max(up, e[static_cast<size_t>(i - 1) * m + k]) + row[k];
+      }
+    }
+    for (int i = len; i >= 1; --i) {
+      const int32_t* row = p + static_cast<size_t>(seq[static_cast<size_t>(i - 1)]) * m;
+      for (int k = m - 1; k >= 0; --k) {
+        const int64_t dn = k < m - 1 ? q[static_cast<size_t>(i) * m + k + 1] : 0;
+        q[static_cast<size_t>(i) * m + k] = std::max(dn, q[static_cast<size_t>(i + 1) * m + k]) + row[k];
+      }
+    }
+    const int32_t* jr = p + static_cast<size_t>(job) * m;
+    int bp = 0;
+    int64_t bv = INT64_MAX;
+    for (int pos = 0; pos <= len; ++pos) {
+      int64_t v = 0;
+      for (int k = 0; k < m; ++k) {
+        f[static_cast<size_t>(k)] = std::max(k ? f[static_cast<size_t>(k - 1)] : 0, e[static_cast<size_t>(pos) * m + k]) + jr[k];
+        v = std::max(v, f[static_cast<size_t>(k)] + q[static_cast<size_t>(pos + 1) * m + k]);
+      }
+      if (v < bv) {
+        bv = v;
+        bp = pos;
+      }
+    }
+    seq.insert(seq.begin() + bp, job);
+    last = bv;
+  }
+  for (int i = 0; i < n; ++i) out[i] = seq[static_cast<size_t>(i)];
+  return last;
+}
+
+// Johnson/Mitten order per machine pair for LB2: pairs (k<l)
+// lexicographic; lag_j = sum_{k<i<l} p[j][i]; J1 = {a<b} ascending a+lag, then J2
+// descending b+lag, ties by ascending job.
+void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::vector<uint8_t>& pl,
+                std::vector<uint8_t>& ord, std::vector<uint16_t>& lag) {
+  const int P = m * (m - 1) / 2;
+  pk.resize(static_cast<size_t>(P));
+  pl.resize(static_cast<size_t>(P));
+  ord.resize(static_cast<size_t>(P) * n);
+  lag.resize(static_cast<size_t>(P) * n);
+  int q = 0;
+  std::vector<int> idx(static_cast<size_t>(n));
+  std::vector<int> key(static_cast<size_t>(n));
+  std::vector<char> first(static_cast<size_t>(n));
+  for (int k = 0; k < m; ++k) {
+    for (int l = k + 1; l < m; ++l, ++q) {
+      pk[static_cast<size_t>(q)] = static_cast<uint8_t>(k);
+      pl[static_cast<size_t>(q)] = static_cast<uint8_t>(l);
+      for (int j = 0; j < n; ++j) {
+        int lg = 0;
+        for (int i = k + 1; i < l; ++i) lg += p[static_cast<size_t>(j) * m + i];
+        if (lg > 65535) throw std::invalid_argument("LB2 lag exceeds 16 bits");
+        lag[static_cast<size_t>(q) * n + j] = static_cast<uint16_t>(lg);
+        const int a = p[static_cast<size_t>(j) * m + k], b = p[static_cast<size_t>(j) * m + l];
+        first[static_cast<size_t>(j)] = a < b;
+        key[static_cast<size_t>(j)] = (a < b ? a : b) + lg;
+        idx[static_cast<size_t>(j)] = j;
+      }
+      std::sort(idx.begin(), idx.end(), [&](int x, int y) {
+        if (first[static_cast<size_t>(x)] != first[static_cast<size_t>(y)]) return first[static_cast<size_t>(x)] > first[static_cast<size_t>(y)];
+        const int kx = key[static_cast<size_t>(x)], ky = key[static_cast<size_t>(y)];
+        if (kx != ky) return first[static_cast<size_t>(x)] ? kx < ky : kx > ky;
+        return x < y;
+      });
+      for (int t = 0; t < n; ++t) ord[static_cast<size_t>(q) * n + t] = static_cast<uint8_t>(idx[static_cast<size_t>(t)]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ small device kernels
+
+__device__ void seat_explorer(unsigned char* blk, const IvmLayout& L, const int* ptot,
+                              const int* a, const int* b, bool has_end) {
+  const int n = L.n, m = L.m;
+  IvmHdr* h = reinterpret_cast<IvmHdr*>(blk);
+  int8_t* cells = reinterpret_cast<int8_t*>(blk + L.o_cells);
+  int8_t* V = reinterpret_cast<int8_t*>(blk + L.o_v);
+  uint8_t* dir = blk + L.o_dir;
+  int8_t* endd = reinterpret_cast<int8_t*>(blk + L.o_end);
+  int8_t* tgt = reinterpret_cast<int8_t*>(blk + L.o_tgt);
+  uint16_t* ft = reinterpret_cast<uint16_t*>(blk + L.o_ft);
+  uint16_t* R = reinterpret_cast<uint16_t*>(blk + L.o_r);
+  bool empty = false;
+  if (has_end) {  // to_decimal(a) >= b -> Empty (src/ivm.cpp:61-64)
+    int cmp = 0;
+    for (int l = 0; l < n && !cmp; ++l) cmp = a[l] < b[l] ? -1 : (a[l] > b[l] ? 1 : 0);
+    empty = cmp >= 0;
+  }
+  for (int c = 0; c < n; ++c) cells[c] = static_cast<int8_t>(c + 1);  // init_root (ivm.cpp:38-46)
+  for (int l = 0; l < n; ++l) {
+    V[l] = 0;
+    dir[l] = kFwd;
+    tgt[l] = static_cast<int8_t>(a[l]);
+    endd[l] = static_cast<int8_t>(has_end ? b[l] : 0);
+  }
+  for (int k = 0; k < m; ++k) {
+    ft[k] = 0;                 // FS[0]
+    ft[n * m + k] = 0;         // TS[0]
+    R[k] = static_cast<uint16_t>(ptot[k]);
+  }
+  h->level = 0;
+  h->state = empty ? kEmpty : kInit;
+  h->has_end = has_end ? 1 : 0;
+  h->d1 = 1;
+  h->d2 = 0;
+  h->rlev = 0;
+  h->nrep = 0;
+}
+
+__global__ void init_kernel(IvmLayout L, unsigned char* state, const int* ptot, const int* a,
+                            const int* b, const uint8_t* b_nfact, const int* slots, int count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  unsigned char* blk = state + static_cast<size_t>(slots[i]) * L.gstride;
+  seat_explorer(blk, L, ptot, a + static_cast<size_t>(i) * L.n, b + static_cast<size_t>(i) * L.n, !b_nfact[i]);
+}
+
+__global__ void clear_kernel(IvmLayout L, unsigned char* state, int K) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  IvmHdr* h = reinterpret_cast<IvmHdr*>(state + static_cast<size_t>(i) * L.gstride);
+  h->state = kEmpty;
+  h->level = -1;
+}
+
+struct StealParams {
+  IvmLayout L;
+  unsigned char* state;
+  int K;
+  const int* ptot;
+  DevCounters* ctr;
+  int* thief;   // [K]
+  int* victim;  // [K]
+  float min_log2;
+  const float* lgfact;  // [n+1] log2(k!)
+};
+
+constexpr int kStealThreads = 1024;
+constexpr int kBins = 2048;
+
+__device__ float remaining_log2(const unsigned char* blk, const IvmLayout& L, const float* lgfact) {
+  const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
+  const int n = L.n;
+  const int8_t* V = reinterpret_cast<const int8_t*>(blk + L.o_v);
+  const int8_t* E = reinterpret_cast<const int8_t*>(blk + L.o_end);
+  if (h->state != kActive || h->level < 0) return -1.f;
+  const int level = h->level;
+  if (!h->has_end) {  // n! - pos
+    const float d = static_cast<float>(n - V[0]) - (n > 1 && level >= 1 ? static_cast<float>(V[1]) / (n - 1) : 0.f);
+    return lgfact[n - 1] + log2f(fmaxf(d, 1e-3f));
+  }
+  for (int l = 0; l < n; ++l) {
+    const int pv = l <= level ? V[l] : 0;
+    if (pv == E[l]) continue;
+    if (pv > E[l]) return -1.f;
+    float d = static_cast<float>(E[l] - pv);
+    if (l + 1 < n) {
+      const int pv1 = l + 1 <= level ? V[l + 1] : 0;
+      d += static_cast<float>(E[l + 1] - pv1) / static_cast<float>(n - 1 - l);
+    }
+    return lgfact[n - 1 - l] + log2f(fmaxf(d, 1e-3f));
+  }
+  return -1.f;
+}
+
+// Steal phase (src/explorer.cpp:283-340, B200 form): triggered when fewer than 0.8 K
+// explorers are active; idle explorers (thieves, in index order) are paired with active
+// explorers in decreasing order of remaining interval length (log2 buckets); the victim
+// keeps [pos, mid), the thief replays init_at(mid) with the victim's old end.
+__global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
+  __shared__ int s_idle[kStealThreads];
+  __shared__ int bins[kBins];
+  __shared__ int s_tot[4];
+  const int t = threadIdx.x;
+  const int K = S.K;
+  const int CH = (K + kStealThreads - 1) / kStealThreads;
+  const int lo = t * CH, hi = min(K, lo + CH);
+  int idle = 0, active = 0;
+  for (int i = lo; i < hi; ++i) {
+    const IvmHdr* h = reinterpret_cast<const IvmHdr*>(S.state + static_cast<size_t>(i) * S.L.gstride);
+    if (h->state == kEmpty) ++idle;
+    else ++active;
+  }
+  s_idle[t] = idle;
+  for (int b = t; b < kBins; b += kStealThreads) bins[b] = 0;
+  if (t < 4) s_tot[t] = 0;
+  __syncthreads();
+  atomicAdd(&s_tot[0], active);
+  // inclusive scan of idle counts (Hillis-Steele)
+  for (int off = 1; off < kStealThreads; off <<= 1) {
+    const int v = t >= off ? s_idle[t - off] : 0;
+    __syncthreads();
+    s_idle[t] += v;
+    __syncthreads();
+  }
+  const int total_idle = s_idle[kStealThreads - 1];
+  const int total_active = s_tot[0];
+  if (total_active * 5 >= K * 4 || total_idle == 0 || total_active == 0) {
+    if (t == 0) S.ctr->active = total_active;
+    return;
+  }
+  // thieves in index order
+  int r = s_idle[t] - idle;
+  for (int i = lo; i < hi; ++i) {
+    const IvmHdr* h = reinterpret_cast<const IvmHdr*>(S.state + static_cast<size_t>(i) * S.L.gstride);
+    if (h->state == kEmpty) S.thief[r++] = i;
+  }
+  // victim buckets
+  for (int i = lo; i < hi; ++i) {
+    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact);
+    if (lg >= S.min_log2 && lg >= 1.f) {
+      const int b = min(kBins - 1, static_cast<int>(lg * 4.f));
+      atomicAdd(&bins[b], 1);
+    }
+  }
+  __syncthreads();
+  if (t == 0) {  // descending exclusive offsets
+    int acc = 0;
+    for (int b = kBins - 1; b >= 0; --b) {
+      const int c = bins[b];
+      bins[b] = acc;
+      acc += c;
+    }
+    s_tot[1] = acc;
+  }
+  __syncthreads();
+  const int nvict = s_tot[1];
+  const int npairs = min(nvict, total_idle);
+  for (int i = lo; i < hi; ++i) {
+    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact);
+    if (lg >= S.min_log2 && lg >= 1.f) {
+      const int b = min(kBins - 1, static_cast<int>(lg * 4.f));
+      const int rank = atomicAdd(&bins[b], 1);
+      if (rank < npairs) S.victim[rank] = i;
+    }
+  }
+  __syncthreads();
+  int ok = 0;
+  const int n = S.L.n;
+  for (int pidx = t; pidx < npairs; pidx += kStealThreads) {
+    unsigned char* vb = S.state + static_cast<size_t>(S.victim[pidx]) * S.L.gstride;
+    unsigned char* tb = S.state + static_cast<size_t>(S.thief[pidx]) * S.L.gstride;
+    IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
+    const int8_t* V = reinterpret_cast<const int8_t*>(vb + S.L.o_v);
+    int8_t* E = reinterpret_cast<int8_t*>(vb + S.L.o_end);
+    int pos[kMaxN], mid[kMaxN], sum[kMaxN], oend[kMaxN];
+    for (int l = 0; l < n; ++l) {
+      pos[l] = l <= vh->level ? V[l] : 0;
+      oend[l] = E[l];
+    }
+    // midpoint (src/factoradic.cpp:59-93)
+    int carry = 0;
+    if (vh->has_end) {
+      for (int l = n - 1; l >= 0; --l) {
+        const int s = pos[l] + oend[l] + carry, radix = n - l;
+        sum[l] = s % radix;
+        carry = s / radix;
+      }
+    } else {
+      for (int l = 0; l < n; ++l) sum[l] = pos[l];
+      carry = 1;
+    }
+    int rem = carry;
+    for (int l = 0; l < n; ++l) {
+      const int cur = rem * (n - l) + sum[l];
+      mid[l] = cur / 2;
+      rem = cur % 2;
+    }
+    int cmp = 0;
+    for (int l = 0; l < n && !cmp; ++l) cmp = mid[l] < pos[l] ? -1 : (mid[l] > pos[l] ? 1 : 0);
+    if (cmp <= 0) continue;  // end < pos + 2 (explorer.cpp:270)
+    const bool had_end = vh->has_end != 0;
+    seat_explorer(tb, S.L, S.ptot, mid, oend, had_end);
+    for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(mid[l]);
+    vh->has_end = 1;
+    ++ok;
+  }
+  atomicAdd(&s_tot[2], ok);
+  __syncthreads();
+  if (t == 0) {
+    S.ctr->active = total_active + s_tot[2];
+    S.ctr->steals += static_cast<unsigned long long>(s_tot[2]);
+    S.ctr->inits += static_cast<unsigned long long>(s_tot[2]);
+    S.ctr->steal_phases += 1ull;
+  }
+}
+
+// ------------------------------------------------------------------ kernel tables
+
+using ExploreFn = void (*)(ExploreParams);
+using BatchFn = void (*)(BatchParams);
+
+template <int M, int B>
+ExploreFn explore_for_group(int G) {
+  switch (G) {
+    case 4: return explore_kernel<M, 4, B>;
+    case 8: return explore_kernel<M, 8, B>;
+    case 16: return explore_kernel<M, 16, B>;
+    case 32: return explore_kernel<M, 32, B>;
+  }
+  return nullptr;
+}
+template <int M, int B>
+BatchFn batch_for_group(int G) {
+  switch (G) {
+    case 4: return decompose_batch_kernel<M, 4, B>;
+    case 8: return decompose_batch_kernel<M, 8, B>;
+    case 16: return decompose_batch_kernel<M, 16, B>;
+    case 32: return decompose_batch_kernel<M, 32, B>;
+  }
+  return nullptr;
+}
+
+ExploreFn explore_fn(int m, int bound, int G) {
+  if (bound == kLB1) {
+    switch (m) {
+      case 5: return explore_for_group<5, kLB1>(G);
+      case 10: return explore_for_group<10, kLB1>(G);
+      case 20: return explore_for_group<20, kLB1>(G);
+    }
+  } else {
+    switch (m) {
+      case 5: return explore_for_group<5, kLB2>(G);
+      case 10: return explore_for_group<10, kLB2>(G);
+      case 20: return explore_for_group<20, kLB2>(G);
+    }
+  }
+  return nullptr;
+}
+
+BatchFn batch_fn(int m, int bound, int G) {
+  if (bound == kLB1) {
+    switch (m) {
+      case 5: return batch_for_group<5, kLB1>(G);
+      case 10: return batch_for_group<10, kLB1>(G);
+      case 20: return batch_for_group<20, kLB1>(G);
+    }
+  } else {
+    switch (m) {
+      case 5: return batch_for_group<5, kLB2>(G);
+      case 10: return batch_for_group<10, kLB2>(G);
+      case 20: return batch_for_group<20, kLB2>(G);
+    }
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ pool
+
+struct pbbgpu_pool {
+  int n = 0, m = 0, mp = 0, bound = 0;
+  pbbgpu_config_t cfg{};
+  std::vector<int32_t> p;
+  int K = 0, G = 0, steps = 0, grid = 0;
+  size_t smem = 0;
+  IvmLayout L{};
+  InstLayout IL{};
+  int npairs = 0;
+  ExploreFn efn = nullptr;
+  BatchFn bfn = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  unsigned char* d_state = nullptr;
+  int *d_p32 = nullptr, *d_ptot = nullptr, *d_wrk = nullptr;
+  uint8_t *d_pk = nullptr, *d_pl = nullptr, *d_ord = nullptr;
+  uint16_t* d_lag = nullptr;
+  float* d_lgfact = nullptr;
+  DevCounters* d_ctr = nullptr;
+  DevCounters* h_ctr = nullptr;  // pinned
+  unsigned long long *d_hist = nullptr, *d_dhist = nullptr;
+  ImpRecord* d_imp = nullptr;
+  std::mutex best_mu;
+  std::atomic<int64_t> pending_offer{INT64_MAX};
+  int64_t best_value = INT64_MAX;
+  int64_t best_sched_value = INT64_MAX;
+  int64_t pinned_ub = INT64_MAX;
+  std::vector<int32_t> best_sched;
+  uint64_t rounds = 0;
+  double kernel_ms = 0;
+  int last_active = 0;
+
+  void release() {
+    if (stream) cudaStreamSynchronize(stream);
+    cudaFree(d_state);
+    cudaFree(d_p32);
+    cudaFree(d_ptot);
+    cudaFree(d_wrk);
+    cudaFree(d_pk);
+    cudaFree(d_pl);
+    cudaFree(d_ord);
+    cudaFree(d_lag);
+    cudaFree(d_lgfact);
+    cudaFree(d_ctr);
+    cudaFree(d_hist);
+    cudaFree(d_dhist);
+    cudaFree(d_imp);
+    if (h_ctr) cudaFreeHost(h_ctr);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+int pick_group(int n, int bound) {
+  if (bound == kLB1) return n <= 24 ? 4 : 8;
+  return n <= 24 ? 8 : 16;
+}
+
+void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const pbbgpu_config_t* cfg) {
+  if (n < 2 || n > kMaxN) throw std::invalid_argument("pbbgpu: n must be in [2, 64] for the shared-memory IVM store");
+  if (m != 5 && m != 10 && m != 20) throw std::invalid_argument("pbbgpu: m must be 5, 10 or 20 (compiled machine counts)");
+  if (bound != kLB1 && bound != kLB2) throw std::invalid_argument("pbbgpu: bound must be PBBGPU_LB1 or PBBGPU_LB2");
+  int pmax = 0;
+  for (int i = 0; i < n * m; ++i) {
+    if (p[i] < 0) throw std::invalid_argument("negative processing time");
+    pmax = std::max(pmax, p[i]);
+  }
+  if (static_cast<int64_t>(n + m) * pmax >= 65536) throw std::invalid_argument("pbbgpu: (n+m)*max(p) must stay below 2^16");
+  P->n = n;
+  P->m = m;
+  P->bound = bound;
+  P->p.assign(p, p + static_cast<size_t>(n) * m);
+  if (cfg) P->cfg = *cfg;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw CudaError("pbbgpu: no CUDA device (the product path has no CPU fallback)");
+  ck(cudaSetDevice(P->cfg.device), "cudaSetDevice");
+  cudaDeviceProp prop;
+  ck(cudaGetDeviceProperties(&prop, P->cfg.device), "cudaGetDeviceProperties");
+  if (prop.major < 10) throw CudaError("pbbgpu: kernels are built for sm_100a only");
+  ck(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking), "stream");
+  ck(cudaEventCreate(&P->ev0), "event");
+  ck(cudaEventCreate(&P->ev1), "event");
+
+  P->L = ivm_layout(n, m, bound);
+  P->mp = P->L.mp;
+  std::vector<uint8_t> pk, pl, ord;
+  std::vector<uint16_t> lag;
+  if (bound == kLB2) {
+    lb2_tables(n, m, p, pk, pl, ord, lag);
+    P->npairs = m * (m - 1) / 2;
+  }
+  P->IL = inst_layout(n, P->mp, P->npairs);
+  P->G = P->cfg.group > 0 ? P->cfg.group : pick_group(n, bound);
+  if (P->G != 4 && P->G != 8 && P->G != 16 && P->G != 32) throw std::invalid_argument("pbbgpu: group must be 4, 8, 16 or 32");
+  const int NG = 128 / P->G;
+  P->smem = static_cast<size_t>(P->IL.bytes) + static_cast<size_t>(NG) * P->L.sstride;
+  while (P->smem > 227 * 1024 && P->G < 32) {
+    P->G *= 2;
+    P->smem = static_cast<size_t>(P->IL.bytes) + static_cast<size_t>(128 / P->G) * P->L.sstride;
+  }
+  if (P->smem > 227 * 1024) throw CapacityError("pbbgpu: explorer state exceeds shared memory");
+  P->efn = explore_fn(m, bound, P->G);
+  P->bfn = batch_fn(m, bound, P->G);
+  ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->efn), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
+  ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->bfn), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
+  int per_sm = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(P->efn), 128, P->smem), "occupancy");
+  if (per_sm < 1) throw CapacityError("pbbgpu: explore kernel cannot be resident");
+  const int NGb = 128 / P->G;
+  if (P->cfg.explorers > 0) {
+    P->K = P->cfg.explorers;
+  } else {
+    P->K = per_sm * prop.multiProcessorCount * NGb;
+  }
+  P->grid = (P->K + NGb - 1) / NGb;
+  P->steps = P->cfg.steps_per_round > 0 ? P->cfg.steps_per_round : (bound == kLB1 ? 4096 : 256);
+
+  // device buffers
+  const int mp = P->mp;
+  std::vector<int> p32(static_cast<size_t>(n) * mp, 0), ptot(static_cast<size_t>(m), 0);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < m; ++k) {
+      p32[static_cast<size_t>(j) * mp + k] = p[static_cast<size_t>(j) * m + k];
+      ptot[static_cast<size_t>(k)] += p[static_cast<size_t>(j) * m + k];
+    }
+  std::vector<float> lgf(static_cast<size_t>(n) + 1, 0.f);
+  for (int k = 2; k <= n; ++k) lgf[static_cast<size_t>(k)] = lgf[static_cast<size_t>(k - 1)] + std::log2(static_cast<float>(k));
+  ck(cudaMalloc(&P->d_state, static_cast<size_t>(P->K) * P->L.gstride), "malloc state");
+  ck(cudaMalloc(&P->d_p32, p32.size() * sizeof(int)), "malloc");
+  ck(cudaMalloc(&P->d_ptot, ptot.size() * sizeof(int)), "malloc");
+  ck(cudaMalloc(&P->d_wrk, static_cast<size_t>(P->K) * 2 * sizeof(int)), "malloc");
+  ck(cudaMalloc(&P->d_lgfact, lgf.size() * sizeof(float)), "malloc");
+  ck(cudaMalloc(&P->d_ctr, sizeof(DevCounters)), "malloc");
+  ck(cudaMallocHost(&P->h_ctr, sizeof(DevCounters)), "malloc host");
+  ck(cudaMalloc(&P->d_hist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
+  ck(cudaMalloc(&P->d_dhist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
+  ck(cudaMalloc(&P->d_imp, kImpCap * sizeof(ImpRecord)), "malloc");
+  ck(cudaMemcpy(P->d_p32, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
+  ck(cudaMemcpy(P->d_ptot, ptot.data(), ptot.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
+  ck(cudaMemcpy(P->d_lgfact, lgf.data(), lgf.size() * sizeof(float), cudaMemcpyHostToDevice), "copy");
+  if (bound == kLB2) {
+    ck(cudaMalloc(&P->d_pk, pk.size()), "malloc");
+    ck(cudaMalloc(&P->d_pl, pl.size()), "malloc");
+    ck(cudaMalloc(&P->d_ord, ord.size()), "malloc");
+    ck(cudaMalloc(&P->d_lag, lag.size() * sizeof(uint16_t)), "malloc");
+    ck(cudaMemcpy(P->d_pk, pk.data(), pk.size(), cudaMemcpyHostToDevice), "copy");
+    ck(cudaMemcpy(P->d_pl, pl.data(), pl.size(), cudaMemcpyHostToDevice), "copy");
+    ck(cudaMemcpy(P->d_ord, ord.data(), ord.size(), cudaMemcpyHostToDevice), "copy");
+    ck(cudaMemcpy(P->d_lag, lag.data(), lag.size() * sizeof(uint16_t), cudaMemcpyHostToDevice), "copy");
+  }
+  DevCounters z{};
+  z.best = INT_MAX;
+  ck(cudaMemcpy(P->d_ctr, &z, sizeof(z), cudaMemcpyHostToDevice), "copy");
+  ck(cudaMemset(P->d_hist, 0, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "memset");
+  ck(cudaMemset(P->d_dhist, 0, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "memset");
+  clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
+  ck(cudaGetLastError(), "clear_kernel");
+  ck(cudaStreamSynchronize(P->stream), "sync");
+}
+
+void read_counters(pbbgpu_pool* P) {
+  ck(cudaMemcpyAsync(P->h_ctr, P->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, P->stream), "ctr copy");
+  ck(cudaStreamSynchronize(P->stream), "sync");
+}
+
+void set_device_best(pbbgpu_pool* P, int64_t v) {
+  const int b = v >= INT_MAX ? INT_MAX : static_cast<int>(std::max<int64_t>(v, 0));
+  ck(cudaMemcpyAsync(reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, best), &b, sizeof(int), cudaMemcpyHostToDevice, P->stream), "best copy");
+  ck(cudaStreamSynchronize(P->stream), "sync");
+}
+
+// Harvest leaf improvements recorded by the last round(s).
+void harvest(pbbgpu_pool* P) {
+  const int cnt = std::min(P->h_ctr->imp_count, kImpCap);
+  if (cnt > 0) {
+    std::vector<ImpRecord> recs(static_cast<size_t>(cnt));
+    ck(cudaMemcpy(recs.data(), P->d_imp, recs.size() * sizeof(ImpRecord), cudaMemcpyDeviceToHost), "imp copy");
+    std::scoped_lock lk(P->best_mu);
+    for (const ImpRecord& r : recs) {
+      if (r.mk < P->best_sched_value) {
+        P->best_sched_value = r.mk;
+        P->best_sched.assign(r.perm, r.perm + P->n);
+      }
+      P->best_value = std::min<int64_t>(P->best_value, r.mk);
+    }
+    const int zero = 0;
+    ck(cudaMemcpy(reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, imp_count), &zero, sizeof(int), cudaMemcpyHostToDevice), "imp reset");
+  }
+  std::scoped_lock lk(P->best_mu);
+  P->best_value = std::min<int64_t>(P->best_value, P->h_ctr->best);
+}
+
+ExploreParams explore_params(pbbgpu_pool* P) {
+  ExploreParams E{};
+  E.L = P->L;
+  E.state = P->d_state;
+  E.K = P->K;
+  E.steps = P->steps;
+  E.prune_mode = P->cfg.disable_pruning ? 2 : (P->cfg.pinned ? 1 : 0);
+  E.pinned_ub = static_cast<int>(std::min<int64_t>(P->best_value, INT_MAX));
+  E.p32 = P->d_p32;
+  E.ptot = P->d_ptot;
+  E.npairs = P->npairs;
+  E.pk = P->d_pk;
+  E.pl = P->d_pl;
+  E.order = P->d_ord;
+  E.lag = P->d_lag;
+  E.ctr = P->d_ctr;
+  E.hist = P->d_hist;
+  E.dhist = P->d_dhist;
+  E.imp = P->d_imp;
+  E.smem_inst_bytes = P->IL.bytes;
+  return E;
+}
+
+void assign_digits(pbbgpu_pool* P, const std::vector<int>& a, const std::vector<int>& b, const std::vector<uint8_t>& nf, const std::vector<int>& slots) {
+  const int cnt = static_cast<int>(slots.size());
+  if (cnt == 0) return;
+  int *da = nullptr, *db = nullptr, *ds = nullptr;
+  uint8_t* dn = nullptr;
+  ck(cudaMalloc(&da, a.size() * sizeof(int)), "malloc");
+  ck(cudaMalloc(&db, b.size() * sizeof(int)), "malloc");
+  ck(cudaMalloc(&ds, slots.size() * sizeof(int)), "malloc");
+  ck(cudaMalloc(&dn, nf.size()), "malloc");
+  ck(cudaMemcpy(da, a.data(), a.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
+  ck(cudaMemcpy(db, b.data(), b.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
+  ck(cudaMemcpy(ds, slots.data(), slots.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
+  ck(cudaMemcpy(dn, nf.data(), nf.size(), cudaMemcpyHostToDevice), "copy");
+  init_kernel<<<(cnt + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, da, db, dn, ds, cnt);
+  ck(cudaGetLastError(), "init_kernel");
+  ck(cudaStreamSynchronize(P->stream), "sync");
+  cudaFree(da);
+  cudaFree(db);
+  cudaFree(ds);
+  cudaFree(dn);
+  read_counters(P);
+  // inits counter
+  unsigned long long inits = P->h_ctr->inits + static_cast<unsigned long long>(cnt);
+  ck(cudaMemcpy(reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, inits), &inits, sizeof(inits), cudaMemcpyHostToDevice), "copy");
+}
+
+int count_active_host(pbbgpu_pool* P) {
+  std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
+  ck(cudaMemcpy(st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost), "state copy");
+  int a = 0;
+  for (int i = 0; i < P->K; ++i) a += reinterpret_cast<const IvmHdr*>(st.data() + static_cast<size_t>(i) * P->L.gstride)->state != kEmpty;
+  return a;
+}
+
+int run_round(pbbgpu_pool* P) {
+  const int64_t offer = P->pending_offer.exchange(INT64_MAX);
+  if (offer < P->best_value) {
+    {
+      std::scoped_lock lk(P->best_mu);
+      P->best_value = offer;
+    }
+    if (!P->cfg.pinned) set_device_best(P, offer);
+  }
+  ExploreParams E = explore_params(P);
+  if (P->cfg.pinned) E.pinned_ub = static_cast<int>(std::min<int64_t>(P->pinned_ub, INT_MAX));
+  ck(cudaEventRecord(P->ev0, P->stream), "event");
+  P->efn<<<P->grid, 128, P->smem, P->stream>>>(E);
+  ck(cudaGetLastError(), "explore_kernel launch");
+  ck(cudaEventRecord(P->ev1, P->stream), "event");
+  StealParams S{};
+  S.L = P->L;
+  S.state = P->d_state;
+  S.K = P->K;
+  S.ptot = P->d_ptot;
+  S.ctr = P->d_ctr;
+  S.thief = P->d_wrk;
+  S.victim = P->d_wrk + P->K;
+  S.min_log2 = static_cast<float>(P->cfg.min_steal_log2 > 0 ? P->cfg.min_steal_log2 : std::log2(40320.0));
+  S.lgfact = P->d_lgfact;
+  steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
+  ck(cudaGetLastError(), "steal_kernel launch");
+  read_counters(P);
+  float ms = 0;
+  ck(cudaEventElapsedTime(&ms, P->ev0, P->ev1), "elapsed");
+  P->kernel_ms += ms;
+  ++P->rounds;
+  harvest(P);
+  P->last_active = P->h_ctr->active;
+  return P->h_ctr->active;
+}
+
+int set_err(const std::exception& e) {
+  g_last_error = e.what();
+  if (dynamic_cast<const CudaError*>(&e)) return PBBGPU_ERR_CUDA;
+  if (dynamic_cast<const CapacityError*>(&e)) return PBBGPU_ERR_CAPACITY;
+  if (dynamic_cast<const StateError*>(&e)) return PBBGPU_ERR_STATE;
+  if (dynamic_cast<const std::logic_error*>(&e)) return PBBGPU_ERR_ARG;
+  return PBBGPU_ERR_CUDA;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PBBGPU_OK;
+  } catch (const std::exception& e) {
+    return set_err(e);
+  }
+}
+
+void check_digits(int n, const uint16_t* d) {
+  for (int l = 0; l < n; ++l)
+    if (d[l] > n - 1 - l) throw std::invalid_argument("factoradic digit out of radix at level " + std::to_string(l));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C-ABI
+
+extern "C" {
+
+const char* pbbgpu_last_error(void) { return g_last_error.c_str(); }
+
+int pbbgpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int pbbgpu_taillard(int n, int m, int32_t seed, int32_t* p_out) {
+  return guarded([&] { taillard(n, m, seed, p_out); });
+}
+
+int pbbgpu_taillard_named(const char* name, int* n, int* m, int32_t* p_out) {
+  return guarded([&] {
+    const std::string s = name ? name : "";
+    if (s.size() != 5 || (s.rfind("ta", 0) != 0 && s.rfind("Ta", 0) != 0)) throw std::invalid_argument("expected instance name of the form ta001..ta120");
+    const int idx = std::atoi(s.c_str() + 2);
+    if (idx < 1 || idx > 120) throw std::invalid_argument("instance number out of range 1..120");
+    const TaClass& c = kTa[(idx - 1) / 10];
+    *n = c.n;
+    *m = c.m;
+    if (p_out) taillard(c.n, c.m, c.seeds[(idx - 1) % 10], p_out);
+  });
+}
+
+int64_t pbbgpu_makespan(int n, int m, const int32_t* p, const int32_t* perm) {
+  try {
+    return makespan_host(n, m, p, perm);
+  } catch (const std::exception& e) {
+    set_err(e);
+    return -1;
+  }
+}
+
+int64_t pbbgpu_neh(int n, int m, const int32_t* p, int32_t* perm_out) {
+  try {
+    return neh_host(n, m, p, perm_out);
+  } catch (const std::exception& e) {
+    set_err(e);
+    return -1;
+  }
+}
+
+int pbbgpu_create(int n, int m, const int32_t* p, int bound_kind, const pbbgpu_config_t* cfg, pbbgpu_pool** out) {
+  *out = nullptr;
+  pbbgpu_pool* P = new pbbgpu_pool();
+  const int rc = guarded([&] { pool_init(P, n, m, p, bound_kind, cfg); });
+  if (rc != PBBGPU_OK) {
+    P->release();
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return PBBGPU_OK;
+}
+
+void pbbgpu_destroy(pbbgpu_pool* P) {
+  if (!P) return;
+  P->release();
+  delete P;
+}
+
+int pbbgpu_K(const pbbgpu_pool* P) { return P ? P->K : 0; }
+
+int pbbgpu_set_initial_bound(pbbgpu_pool* P, int64_t ub, const int32_t* sched, int len) {
+  return guarded([&] {
+    if (ub <= 0) throw std::invalid_argument("incumbent must be positive");
+    {
+      std::scoped_lock lk(P->best_mu);
+      P->best_value = ub;
+      if (sched && len == P->n) {
+        P->best_sched.assign(sched, sched + len);
+        P->best_sched_value = ub;
+      } else {
+        P->best_sched.clear();
+        P->best_sched_value = INT64_MAX;
+      }
+      P->pinned_ub = ub;
+    }
+    set_device_best(P, ub);
+  });
+}
+
+int pbbgpu_assign(pbbgpu_pool* P, const uint16_t* a, const uint16_t* b, const uint8_t* nf, int count) {
+  return guarded([&] {
+    if (count < 0 || count > P->K) throw std::invalid_argument("more intervals than explorers");
+    if (count == 0) return;
+    const int n = P->n;
+    std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
+    ck(cudaMemcpy(st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost), "state copy");
+    std::vector<int> idle;
+    for (int i = 0; i < P->K; ++i)
+      if (reinterpret_cast<const IvmHdr*>(st.data() + static_cast<size_t>(i) * P->L.gstride)->state == kEmpty) idle.push_back(i);
+    if (static_cast<int>(idle.size()) < count) throw CapacityError("not enough idle explorers for the assignment");
+    std::vector<int> da(static_cast<size_t>(count) * n), db(static_cast<size_t>(count) * n, 0), slots(static_cast<size_t>(count));
+    std::vector<uint8_t> dn(static_cast<size_t>(count));
+    for (int i = 0; i < count; ++i) {
+      check_digits(n, a + static_cast<size_t>(i) * n);
+      const bool inf = nf && nf[i];
+      if (!inf) check_digits(n, b + static_cast<size_t>(i) * n);
+      for (int l = 0; l < n; ++l) {
+        da[static_cast<size_t>(i) * n + l] = a[static_cast<size_t>(i) * n + l];
+        if (!inf) db[static_cast<size_t>(i) * n + l] = b[static_cast<size_t>(i) * n + l];
+      }
+      dn[static_cast<size_t>(i)] = inf ? 1 : 0;
+      slots[static_cast<size_t>(i)] = idle[static_cast<size_t>(i)];
+    }
+    assign_digits(P, da, db, dn, slots);
+  });
+}
+
+int pbbgpu_assign_split(pbbgpu_pool* P, int pieces) {
+  return guarded([&] {
+    if (pieces <= 0) pieces = P->K;
+    if (pieces > P->K) throw std::invalid_argument("more pieces than explorers");
+    const int n = P->n;
+    // floor(i * n! / pieces) in factoradic, digit by digit: d_l = floor(r (n-l) / C),
+    // r <- r (n-l) mod C (exact rational expansion, no big integers needed)
+    auto digits_of = [&](int64_t i, int* out) {
+      int64_t r = i;
+      for (int l = 0; l < n; ++l) {
+        r *= (n - l);
+        out[l] = static_cast<int>(r / pieces);
+        r %= pieces;
+      }
+    };
+    std::vector<int> a(static_cast<size_t>(pieces) * n), b(static_cast<size_t>(pieces) * n, 0), slots(static_cast<size_t>(pieces));
+    std::vector<uint8_t> nf(static_cast<size_t>(pieces), 0);
+    for (int i = 0; i < pieces; ++i) {
+      digits_of(i, &a[static_cast<size_t>(i) * n]);
+      if (i + 1 < pieces) digits_of(i + 1, &b[static_cast<size_t>(i) * n]);
+      else nf[static_cast<size_t>(i)] = 1;
+      slots[static_cast<size_t>(i)] = i;
+    }
+    clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
+    ck(cudaGetLastError(), "clear_kernel");
+    assign_digits(P, a, b, nf, slots);
+  });
+}
+
+int pbbgpu_run_round(pbbgpu_pool* P, int* active_out) {
+  return guarded([&] {
+    const int a = run_round(P);
+    if (active_out) *active_out = a;
+  });
+}
+
+int pbbgpu_active_count(pbbgpu_pool* P, int* active_out) {
+  return guarded([&] { *active_out = count_active_host(P); });
+}
+
+int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_nf, int cap, int* count) {
+  return guarded([&] {
+    const int n = P->n;
+    std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
+    ck(cudaMemcpy(st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost), "state copy");
+    int c = 0;
+    for (int i = 0; i < P->K; ++i) {
+      const unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
+      const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
+      if (h->state == kEmpty) continue;
+      if (c >= cap) throw CapacityError("snapshot buffer too small");
+      const int8_t* V = reinterpret_cast<const int8_t*>(blk + P->L.o_v);
+      const int8_t* E = reinterpret_cast<const int8_t*>(blk + P->L.o_end);
+      const int8_t* T = reinterpret_cast<const int8_t*>(blk + P->L.o_tgt);
+      for (int l = 0; l < n; ++l) {
+        int pv;
+        if (h->state == kInit) pv = T[l];  // not yet positioned: [target, end)
+        else pv = l <= h->level ? V[l] : 0;
+        pos[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(pv);
+        end[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(h->has_end ? E[l] : 0);
+      }
+      end_nf[c] = h->has_end ? 0 : 1;
+      ++c;
+    }
+    *count = c;
+  });
+}
+
+int pbbgpu_best(pbbgpu_pool* P, int64_t* value, int32_t* perm, int* has_perm) {
+  return guarded([&] {
+    std::scoped_lock lk(P->best_mu);
+    *value = P->best_value;
+    if (has_perm) *has_perm = P->best_sched.empty() ? 0 : 1;
+    if (perm && !P->best_sched.empty()) std::copy(P->best_sched.begin(), P->best_sched.end(), perm);
+  });
+}
+
+int pbbgpu_offer_bound(pbbgpu_pool* P, int64_t v) {
+  return guarded([&] {
+    int64_t cur = P->pending_offer.load();
+    while (v < cur && !P->pending_offer.compare_exchange_weak(cur, v)) {
+    }
+  });
+}
+
+int pbbgpu_stats(pbbgpu_pool* P, pbbgpu_stats_t* out) {
+  return guarded([&] {
+    read_counters(P);
+    const DevCounters& c = *P->h_ctr;
+    std::memset(out, 0, sizeof(*out));
+    out->decomposed = c.decomposed;
+    out->replay_dups = c.dups;
+    out->unique = c.decomposed - c.dups;
+    out->leaves = c.leaves;
+    out->improvements = c.improvements;
+    out->local_steals = c.steals;
+    out->steal_phases = c.steal_phases;
+    out->intervals_initialized = c.inits;
+    out->rounds = P->rounds;
+    out->steps = c.steps;
+    out->kernel_ms = P->kernel_ms;
+    out->completed = P->last_active == 0;
+    out->K = P->K;
+    out->group = P->G;
+    out->steps_per_round = P->steps;
+  });
+}
+
+int pbbgpu_histogram(pbbgpu_pool* P, uint64_t* hist, int len) {
+  return guarded([&] {
+    const int n = P->n;
+    std::vector<unsigned long long> h(static_cast<size_t>(n) + 1), d(static_cast<size_t>(n) + 1);
+    ck(cudaMemcpy(h.data(), P->d_hist, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "hist copy");
+    ck(cudaMemcpy(d.data(), P->d_dhist, d.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "hist copy");
+    for (int f = 0; f < len; ++f) hist[f] = f <= n ? h[static_cast<size_t>(f)] - d[static_cast<size_t>(f)] : 0;
+  });
+}
+
+int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* d1, const int32_t* d2, int count,
+                           int64_t incumbent, int64_t* child_lb, uint8_t* direction, uint8_t* pruned,
+                           int64_t* lb_fwd, int64_t* lb_bwd) {
+  return guarded([&] {
+    if (count <= 0) return;
+    if (incumbent <= 0) throw std::invalid_argument("decompose: incumbent must be positive");
+    const int n = P->n;
+    for (int i = 0; i < count; ++i) {
+      const int a = d1[i], b = d2[i];
+      if (a < 0 || b < 0 || a + b > n - 1) throw std::invalid_argument("decompose: no free jobs / bad depths");
+      std::vector<char> seen(static_cast<size_t>(n), 0);
+      for (int t = 0; t < n; ++t) {
+        const int j = perms[static_cast<size_t>(i) * n + t];
+        if (j < 0 || j >= n || seen[static_cast<size_t>(j)]) throw std::invalid_argument("subproblem perm is not a permutation");
+        seen[static_cast<size_t>(j)] = 1;
+      }
+    }
+    int *dp = nullptr, *dd1 = nullptr, *dd2 = nullptr, *dlb = nullptr, *dlf = nullptr, *dlbw = nullptr;
+    uint8_t *ddir = nullptr, *dpr = nullptr;
+    const size_t cn = static_cast<size_t>(count) * n;
+    ck(cudaMalloc(&dp, cn * sizeof(int)), "malloc");
+    ck(cudaMalloc(&dd1, count * sizeof(int)), "malloc");
+    ck(cudaMalloc(&dd2, count * sizeof(int)), "malloc");
+    ck(cudaMalloc(&dlb, cn * sizeof(int)), "malloc");
+    ck(cudaMalloc(&dlf, cn * sizeof(int)), "malloc");
+    ck(cudaMalloc(&dlbw, cn * sizeof(int)), "malloc");
+    ck(cudaMalloc(&ddir, count), "malloc");
+    ck(cudaMalloc(&dpr, cn), "malloc");
+    ck(cudaMemcpy(dp, perms, cn * sizeof(int), cudaMemcpyHostToDevice), "copy");
+    ck(cudaMemcpy(dd1, d1, count * sizeof(int), cudaMemcpyHostToDevice), "copy");
+    ck(cudaMemcpy(dd2, d2, count * sizeof(int), cudaMemcpyHostToDevice), "copy");
+    BatchParams B{};
+    B.L = P->L;
+    B.perms = dp;
+    B.d1 = dd1;
+    B.d2 = dd2;
+    B.count = count;
+    B.incumbent = static_cast<int>(std::min<int64_t>(incumbent, INT_MAX));
+    B.p32 = P->d_p32;
+    B.npairs = P->npairs;
+    B.pk = P->d_pk;
+    B.pl = P->d_pl;
+    B.order = P->d_ord;
+    B.lag = P->d_lag;
+    B.child_lb = dlb;
+    B.lb_fwd = dlf;
+    B.lb_bwd = dlbw;
+    B.dir = ddir;
+    B.pruned = dpr;
+    const int NG = 128 / P->G;
+    const int grid = std::min((count + NG - 1) / NG, 148 * 8);
+    P->bfn<<<grid, 128, P->smem, P->stream>>>(B);
+    ck(cudaGetLastError(), "decompose_batch launch");
+    ck(cudaStreamSynchronize(P->stream), "sync");
+    std::vector<int> lb(cn), lf(cn), lbw(cn);
+    std::vector<uint8_t> pr(cn);
+    ck(cudaMemcpy(lb.data(), dlb, cn * sizeof(int), cudaMemcpyDeviceToHost), "copy");
+    ck(cudaMemcpy(lf.data(), dlf, cn * sizeof(int), cudaMemcpyDeviceToHost), "copy");
+    ck(cudaMemcpy(lbw.data(), dlbw, cn * sizeof(int), cudaMemcpyDeviceToHost), "copy");
+    ck(cudaMemcpy(pr.data(), dpr, cn, cudaMemcpyDeviceToHost), "copy");
+    ck(cudaMemcpy(direction, ddir, count, cudaMemcpyDeviceToHost), "copy");
+    for (int i = 0; i < count; ++i) {
+      const int f = n - d1[i] - d2[i];
+      for (int c = 0; c < f; ++c) {
+        const size_t s = static_cast<size_t>(i) * n + c;
+        child_lb[s] = lb[s];
+        pruned[s] = pr[s];
+        if (lb_fwd) lb_fwd[s] = lf[s];
+        if (lb_bwd) lb_bwd[s] = lbw[s];
+      }
+    }
+    cudaFree(dp);
+    cudaFree(dd1);
+    cudaFree(dd2);
+    cudaFree(dlb);
+    cudaFree(dlf);
+    cudaFree(dlbw);
+    cudaFree(ddir);
+    cudaFree(dpr);
+  });
+}
+
+int pbbgpu_solve(pbbgpu_pool* P, int64_t initial_ub, const uint16_t* a, const uint16_t* b, const uint8_t* nf,
+                 int count, int64_t* best_value, int32_t* best_perm, int* has_perm, pbbgpu_stats_t* stats) {
+  int rc = pbbgpu_set_initial_bound(P, initial_ub, nullptr, 0);
+  if (rc) return rc;
+  rc = count > 0 ? pbbgpu_assign(P, a, b, nf, count) : pbbgpu_assign_split(P, 0);
+  if (rc) return rc;
+  const auto t0 = std::chrono::steady_clock::now();
+  bool completed = true;
+  rc = guarded([&] {
+    for (;;) {
+      const int act = run_round(P);
+      if (act == 0) break;
+      if (P->cfg.time_limit_s > 0) {
+        const std::chrono::duration<double> el = std::chrono::steady_clock::now() - t0;
+        if (el.count() >= P->cfg.time_limit_s) {
+          completed = false;
+          break;
+        }
+      }
+    }
+  });
+  if (rc) return rc;
+  const std::chrono::duration<double> el = std::chrono::steady_clock::now() - t0;
+  rc = pbbgpu_best(P, best_value, best_perm, has_perm);
+  if (rc) return rc;
+  if (stats) {
+    rc = pbbgpu_stats(P, stats);
+    stats->wall_s = el.count();
+    stats->completed = completed ? 1 : 0;
+  }
+  return rc;
+}
+
+}  // extern "C"

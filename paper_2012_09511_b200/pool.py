@@ -1,0 +1,294 @@
+"""GPU explorer pool — host mirror of the reference's ExplorerPool / pool_run / decompose.
+
+Reference interfaces mirrored (paths under /root/reference/proj):
+  PoolConfig / PoolStats / PoolResult   include/pbb/explorer.hpp:34-61
+  ExplorerPool                           include/pbb/explorer.hpp:66-103
+  pool_run                               include/pbb/explorer.hpp:145-146, src/explorer.cpp:473-507
+  Subproblem / Decomposition / decompose include/pbb/bound.hpp:19-79
+Intervals are (a, b) pairs of Python integers over [0, n!) (BigCount); they cross the
+C-ABI as factoradic digit vectors.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from math import factorial
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from .factoradic import from_decimal, to_decimal
+from .instance import Instance, Schedule
+
+NO_INCUMBENT = (1 << 63) - 1
+FORWARD, BACKWARD = 0, 1
+Interval = Tuple[int, int]
+
+_u16p = ctypes.POINTER(ctypes.c_uint16)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+@dataclass
+class PoolConfig:
+    explorers: int = 0          # K; 0 = fill the GPU
+    group: int = 0              # lanes per explorer; 0 = auto
+    batch_steps: int = 0        # explore steps per explorer per round; 0 = auto
+    disable_pruning: bool = False
+    pinned: bool = False        # prune >= ub, never improve (explore_step(ub, 0))
+    time_limit_s: float = 0.0
+    min_steal_len: int = 0      # 0 = 8!
+    device: int = 0
+
+    def to_c(self) -> _lib.Config:
+        c = _lib.Config()
+        c.explorers = self.explorers
+        c.group = self.group
+        c.steps_per_round = self.batch_steps
+        c.disable_pruning = int(self.disable_pruning)
+        c.pinned = int(self.pinned)
+        c.time_limit_s = self.time_limit_s
+        c.min_steal_log2 = float(np.log2(self.min_steal_len)) if self.min_steal_len > 1 else 0.0
+        c.device = self.device
+        return c
+
+
+@dataclass
+class PoolStats:
+    decomposed: int = 0
+    unique: int = 0
+    replay_dups: int = 0
+    leaves: int = 0
+    improvements: int = 0
+    local_steals: int = 0
+    steal_phases: int = 0
+    intervals_initialized: int = 0
+    rounds: int = 0
+    steps: int = 0
+    wall_s: float = 0.0
+    kernel_ms: float = 0.0
+    completed: bool = True
+    K: int = 0
+    group: int = 0
+    steps_per_round: int = 0
+
+
+@dataclass
+class PoolResult:
+    best: Schedule
+    best_value: int
+    stats: PoolStats
+    hist: Dict[int, int] = field(default_factory=dict)
+
+
+@dataclass
+class Subproblem:
+    perm: List[int]
+    d1: int = 0
+    d2: int = 0
+
+    def free_count(self) -> int:
+        return len(self.perm) - self.d1 - self.d2
+
+
+@dataclass
+class Decomposition:
+    direction: int
+    child_lb: List[int]
+    pruned: List[int]
+
+
+def _bound_kind(bound) -> int:
+    if bound in (1, "lb1", "LB1"):
+        return _lib.LB1
+    if bound in (2, "lb2", "LB2"):
+        return _lib.LB2
+    raise ValueError(f"unknown bound {bound!r}")
+
+
+def _digits(intervals: Sequence[Interval], n: int):
+    nf = factorial(n)
+    a = np.zeros((len(intervals), n), dtype=np.uint16)
+    b = np.zeros((len(intervals), n), dtype=np.uint16)
+    inf = np.zeros(len(intervals), dtype=np.uint8)
+    for i, (lo, hi) in enumerate(intervals):
+        if lo < 0 or hi > nf or lo > hi:
+            raise ValueError("interval outside [0, n!)")
+        a[i] = from_decimal(min(lo, nf - 1), n) if lo < nf else from_decimal(nf - 1, n)
+        if hi >= nf:
+            inf[i] = 1
+        else:
+            b[i] = from_decimal(hi, n)
+    return a, b, inf
+
+
+def normalize(intervals: Sequence[Interval]) -> List[Interval]:
+    """src/workunit.cpp:8-27: drop empties, sort, merge overlaps (adjacent kept apart)."""
+    for a, b in intervals:
+        if a > b:
+            raise ValueError("interval with a > b")
+    ivs = sorted((a, b) for a, b in intervals if a < b)
+    out: List[Interval] = []
+    for a, b in ivs:
+        if out and a < out[-1][1]:
+            out[-1] = (out[-1][0], max(out[-1][1], b))
+        else:
+            out.append((a, b))
+    return out
+
+
+class GpuPool:
+    """ExplorerPool on one B200: K IVM explorers resident in shared memory."""
+
+    def __init__(self, inst: Instance, cfg: Optional[PoolConfig] = None, bound="lb1"):
+        self.inst = inst
+        self.cfg = cfg or PoolConfig()
+        self.bound = _bound_kind(bound)
+        self._lib = _lib.load()
+        h = ctypes.c_void_p()
+        c = self.cfg.to_c()
+        _lib.check(self._lib.pbbgpu_create(inst.n, inst.m, inst.ptr(), self.bound, ctypes.byref(c), ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.pbbgpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- ExplorerPool surface -------------------------------------------------------------
+    def K(self) -> int:
+        return self._lib.pbbgpu_K(self._h)
+
+    def set_initial_bound(self, ub: int, sched: Sequence[int] = ()) -> None:
+        arr = np.ascontiguousarray(np.asarray(list(sched), dtype=np.int32))
+        ptr = arr.ctypes.data_as(_i32p) if arr.size else None
+        _lib.check(self._lib.pbbgpu_set_initial_bound(self._h, int(min(ub, NO_INCUMBENT)), ptr, int(arr.size)))
+
+    def assign_fresh(self, intervals: Sequence[Interval]) -> None:
+        ivs = normalize(intervals)
+        if len(ivs) > self.K():
+            raise ValueError("more intervals than explorers")
+        a, b, inf = _digits(ivs, self.inst.n)
+        _lib.check(self._lib.pbbgpu_assign(self._h, a.ctypes.data_as(_u16p), b.ctypes.data_as(_u16p),
+                                           inf.ctypes.data_as(_u8p), len(ivs)))
+
+    def assign_split(self, pieces: int = 0) -> None:
+        _lib.check(self._lib.pbbgpu_assign_split(self._h, pieces))
+
+    def run_round(self) -> int:
+        act = ctypes.c_int()
+        _lib.check(self._lib.pbbgpu_run_round(self._h, ctypes.byref(act)))
+        return act.value
+
+    def active_count(self) -> int:
+        act = ctypes.c_int()
+        _lib.check(self._lib.pbbgpu_active_count(self._h, ctypes.byref(act)))
+        return act.value
+
+    def snapshot_intervals(self) -> List[Interval]:
+        K, n = self.K(), self.inst.n
+        pos = np.zeros((K, n), dtype=np.uint16)
+        end = np.zeros((K, n), dtype=np.uint16)
+        inf = np.zeros(K, dtype=np.uint8)
+        cnt = ctypes.c_int()
+        _lib.check(self._lib.pbbgpu_snapshot(self._h, pos.ctypes.data_as(_u16p), end.ctypes.data_as(_u16p),
+                                             inf.ctypes.data_as(_u8p), K, ctypes.byref(cnt)))
+        nf = factorial(n)
+        out = []
+        for i in range(cnt.value):
+            a = to_decimal([int(x) for x in pos[i]])
+            b = nf if inf[i] else to_decimal([int(x) for x in end[i]])
+            if a < b:
+                out.append((a, b))
+        return normalize(out)
+
+    def best_value(self) -> int:
+        v = ctypes.c_int64()
+        _lib.check(self._lib.pbbgpu_best(self._h, ctypes.byref(v), None, None))
+        return v.value
+
+    def best_schedule(self) -> Schedule:
+        v = ctypes.c_int64()
+        has = ctypes.c_int()
+        perm = np.zeros(self.inst.n, dtype=np.int32)
+        _lib.check(self._lib.pbbgpu_best(self._h, ctypes.byref(v), perm.ctypes.data_as(_i32p), ctypes.byref(has)))
+        if not has.value:
+            return Schedule([], -1)
+        return Schedule([int(x) for x in perm], int(v.value))
+
+    def offer_bound(self, value: int) -> None:
+        _lib.check(self._lib.pbbgpu_offer_bound(self._h, int(value)))
+
+    def stats(self) -> PoolStats:
+        s = _lib.Stats()
+        _lib.check(self._lib.pbbgpu_stats(self._h, ctypes.byref(s)))
+        d = s.as_dict()
+        d["completed"] = bool(d["completed"])
+        return PoolStats(**d)
+
+    def histogram(self) -> Dict[int, int]:
+        n = self.inst.n
+        h = np.zeros(n + 1, dtype=np.uint64)
+        _lib.check(self._lib.pbbgpu_histogram(self._h, h.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n + 1))
+        return {f: int(v) for f, v in enumerate(h) if v}
+
+    # -- per-node bounding operator (bound.hpp:78-79) -----------------------------------------
+    def decompose_batch(self, perms, d1, d2, incumbent: int):
+        perms = np.ascontiguousarray(np.asarray(perms, dtype=np.int32).reshape(-1, self.inst.n))
+        d1 = np.ascontiguousarray(np.asarray(d1, dtype=np.int32).reshape(-1))
+        d2 = np.ascontiguousarray(np.asarray(d2, dtype=np.int32).reshape(-1))
+        cnt = perms.shape[0]
+        lb = np.zeros((cnt, self.inst.n), dtype=np.int64)
+        lf = np.zeros((cnt, self.inst.n), dtype=np.int64)
+        lbw = np.zeros((cnt, self.inst.n), dtype=np.int64)
+        dr = np.zeros(cnt, dtype=np.uint8)
+        pr = np.zeros((cnt, self.inst.n), dtype=np.uint8)
+        _lib.check(self._lib.pbbgpu_decompose_batch(
+            self._h, perms.ctypes.data_as(_i32p), d1.ctypes.data_as(_i32p), d2.ctypes.data_as(_i32p), cnt,
+            int(min(incumbent, NO_INCUMBENT)), lb.ctypes.data_as(_i64p), dr.ctypes.data_as(_u8p),
+            pr.ctypes.data_as(_u8p), lf.ctypes.data_as(_i64p), lbw.ctypes.data_as(_i64p)))
+        return lb, dr, pr, lf, lbw
+
+    def decompose(self, sub: Subproblem, incumbent: int) -> Decomposition:
+        lb, dr, pr, _, _ = self.decompose_batch([sub.perm], [sub.d1], [sub.d2], incumbent)
+        f = sub.free_count()
+        return Decomposition(int(dr[0]), [int(x) for x in lb[0, :f]], [int(x) for x in pr[0, :f]])
+
+
+def pool_run(inst: Instance, initial_ub: int, intervals: Sequence[Interval] = (),
+             cfg: Optional[PoolConfig] = None, bound="lb1") -> PoolResult:
+    """pool_run (src/explorer.cpp:473-507) on one GPU: [0, n!) by default, cut evenly over K."""
+    cfg = cfg or PoolConfig()
+    with GpuPool(inst, cfg, bound) as pool:
+        lib = pool._lib
+        ivs = normalize(list(intervals))
+        a = b = inf = None
+        if ivs:
+            a, b, inf = _digits(ivs, inst.n)
+        best = ctypes.c_int64()
+        has = ctypes.c_int()
+        perm = np.zeros(inst.n, dtype=np.int32)
+        st = _lib.Stats()
+        _lib.check(lib.pbbgpu_solve(
+            pool._h, int(min(initial_ub, NO_INCUMBENT)),
+            a.ctypes.data_as(_u16p) if ivs else None, b.ctypes.data_as(_u16p) if ivs else None,
+            inf.ctypes.data_as(_u8p) if ivs else None, len(ivs), ctypes.byref(best),
+            perm.ctypes.data_as(_i32p), ctypes.byref(has), ctypes.byref(st)))
+        d = st.as_dict()
+        d["completed"] = bool(d["completed"])
+        sched = Schedule([int(x) for x in perm], int(best.value)) if has.value else Schedule([], -1)
+        return PoolResult(sched, int(best.value), PoolStats(**d), pool.histogram())
