@@ -1,0 +1,50 @@
+"""Regenerate the golden fixtures in tests/golden/ from the REFERENCE ITSELF.
+
+Runs oracle/_ref/ref_driver (the unmodified reference sources compiled by oracle/Makefile,
+`make -C oracle ref`) and stores its outputs. Needs /root/reference, i.e. runs in the build
+container only; the fixtures are committed so the GPU box never reads the reference.
+
+    python tests/golden/make_golden.py
+"""
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+
+
+def run(*args):
+    out = subprocess.run([DRIVER, *map(str, args)], check=True, capture_output=True, text=True)
+    return out.stdout
+
+
+def main():
+    if not os.path.exists(DRIVER):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref"], check=True)
+    counts = {}
+    # fixed trees (UB = optimum) and improving runs, K = 1 (pool_run semantics)
+    for name, ub in (("ta001", 1278), ("ta011", 1582), ("ta031", 2724), ("ta041", 2991)):
+        counts[f"{name}@{ub}"] = json.loads(run("hist", name, ub))
+    for name in ("ta001", "ta041"):
+        counts[f"{name}@neh"] = json.loads(run("solve", name, "neh", 1, 1))
+    for name in ("ta001", "ta011", "ta021", "ta031", "ta041", "ta056", "ta111"):
+        counts[f"neh:{name}"] = json.loads(run("neh", name))
+    with open(os.path.join(HERE, "ref_counts.json"), "w") as f:
+        json.dump(counts, f, indent=1, sort_keys=True)
+    # per-node decompose dumps (SURVEY.md §8(d) sampler): seed 42
+    for name, ub, starts, per in (("ta001", 1278, 40, 10), ("ta021", 2297, 40, 10),
+                                  ("ta041", 2991, 30, 10), ("ta056", 3679, 30, 10)):
+        with open(os.path.join(HERE, f"ref_nodes_{name}.txt"), "w") as f:
+            f.write(run("nodes", name, ub, 42, starts, per))
+    # instance matrices as the reference generates them
+    with open(os.path.join(HERE, "ref_instances.txt"), "w") as f:
+        for name in ("ta001", "ta021", "ta041", "ta056", "ta111"):
+            f.write(f"# {name}\n" + run("inst", name))
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,226 @@
+"""GPU parity tests: the sm_100a kernels (through the C-ABI) against the reference's golden
+outputs and the C oracle. Bit-exact integer parity everywhere.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import paper_2012_09511_b200 as pbb
+from oracle import oracle as orc
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+
+def _hist_str(h):
+    return {str(k): int(v) for k, v in h.items() if v}
+
+
+# ---------------------------------------------------------------- per-node bounding parity
+
+@pytest.mark.parametrize("name", ["ta001", "ta021", "ta041", "ta056"])
+def test_decompose_batch_matches_reference_nodes(name):
+    nodes, ub = golden_io.ref_nodes(name)
+    inst = pbb.taillard_named(name)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=512)) as pool:
+        perms = np.array([x[0] for x in nodes])
+        lb, dr, pr, _, _ = pool.decompose_batch(perms, [x[1] for x in nodes], [x[2] for x in nodes], ub)
+    for i, (perm, d1, d2, direction, lbs, pruned) in enumerate(nodes):
+        f = len(lbs)
+        assert int(dr[i]) == direction
+        assert [int(x) for x in lb[i, :f]] == lbs
+        assert [int(x) for x in pr[i, :f]] == pruned
+
+
+def _random_nodes(n, count, seed):
+    rng = np.random.default_rng(seed)
+    perms, d1s, d2s = [], [], []
+    for _ in range(count):
+        perms.append(rng.permutation(n))
+        f = int(rng.integers(1, n + 1))
+        d1 = int(rng.integers(0, n - f + 1))
+        d1s.append(d1)
+        d2s.append(n - f - d1)
+    return np.array(perms), d1s, d2s
+
+
+@pytest.mark.parametrize("bound", ["lb1", "lb2"])
+@pytest.mark.parametrize("name", ["ta001", "ta011", "ta021", "ta031", "ta041", "ta056"])
+@pytest.mark.parametrize("group", [4, 8, 32])
+def test_decompose_batch_matches_oracle(bound, name, group):
+    inst = pbb.taillard_named(name)
+    count = 400 if bound == "lb2" else 1500
+    perms, d1s, d2s = _random_nodes(inst.n, count, 17)
+    prob = orc.Problem(inst.p, orc.LB1 if bound == "lb1" else orc.LB2)
+    inc = int(pbb.neh(inst).cmax)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=256, group=group), bound=bound) as pool:
+        lb, dr, pr, lf, lbw = pool.decompose_batch(perms, d1s, d2s, inc)
+    for i in range(count):
+        f = inst.n - d1s[i] - d2s[i]
+        fw, bw = prob.children_bounds(perms[i], d1s[i], d2s[i])
+        d, clb, cpr = prob.decompose(perms[i], d1s[i], d2s[i], inc)
+        assert [int(x) for x in lf[i, :f]] == fw
+        assert [int(x) for x in lbw[i, :f]] == bw
+        assert int(dr[i]) == d
+        assert [int(x) for x in lb[i, :f]] == clb
+        assert [int(x) for x in pr[i, :f]] == cpr
+
+
+def test_decompose_errors():
+    inst = pbb.taillard_named("ta001")
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=64)) as pool:
+        with pytest.raises(ValueError):
+            pool.decompose(pbb.Subproblem(list(range(20)), 10, 10), 1278)   # no free jobs
+        with pytest.raises(ValueError):
+            pool.decompose(pbb.Subproblem(list(range(20)), 1, 1), 0)        # incumbent <= 0
+        with pytest.raises(ValueError):
+            pool.decompose(pbb.Subproblem([0] * 20, 1, 1), 1278)            # not a permutation
+
+
+# ---------------------------------------------------------------- fixed trees (UB = optimum)
+
+@pytest.mark.parametrize("key", ["ta001@1278", "ta011@1582", "ta031@2724", "ta041@2991"])
+@pytest.mark.parametrize("explorers", [0, 64, 1000])
+def test_fixed_tree_lb1_matches_reference(key, explorers):
+    ref = golden_io.ref_counts()[key]
+    name, ub = key.split("@")
+    res = pbb.pool_run(pbb.taillard_named(name), int(ub), cfg=pbb.PoolConfig(explorers=explorers))
+    assert res.stats.completed
+    assert res.stats.unique == ref["decomposed"]
+    assert res.stats.leaves == ref["leaves"]
+    assert res.best_value == ref["best_value"]
+    assert not res.best.perm              # no improvement below the optimum
+    assert _hist_str(res.hist) == ref["hist"]
+
+
+def test_fixed_tree_ta021_lb1_full_proof():
+    """462,443,491 decomposed nodes / 1,440 leaves: the reference's 534.8 s K=1 proof."""
+    res = pbb.pool_run(pbb.taillard_named("ta021"), 2297)
+    assert res.stats.completed
+    assert res.stats.unique == golden_io.TA021_LB1["decomposed"]
+    assert res.stats.leaves == golden_io.TA021_LB1["leaves"]
+    assert res.hist == golden_io.TA021_LB1["hist"]
+
+
+@pytest.mark.parametrize("key", ["ta001@1278", "ta011@1582", "ta031@2724", "ta041@2991", "ta021@2297"])
+def test_fixed_tree_lb2_matches_oracle(key):
+    gold = golden_io.lb2_counts()[key]
+    name, ub = key.split("@")
+    res = pbb.pool_run(pbb.taillard_named(name), int(ub), bound="lb2")
+    assert res.stats.completed
+    assert res.stats.unique == gold["unique"]
+    assert res.stats.leaves == gold["leaves"]
+    assert _hist_str(res.hist) == gold["hist"]
+
+
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("steps,explorers,min_steal", [(64, 200, 2), (31, 333, 24), (200, 4096, 40320)])
+def test_unique_count_invariant_under_stealing(steps, explorers, min_steal):
+    """Tiny rounds + many thieves: the unique-count rule must hold under heavy stealing."""
+    ref = golden_io.ref_counts()["ta011@1582"]
+    cfg = pbb.PoolConfig(explorers=explorers, batch_steps=steps, min_steal_len=min_steal)
+    res = pbb.pool_run(pbb.taillard_named("ta011"), 1582, cfg=cfg)
+    assert res.stats.unique == ref["decomposed"]
+    assert res.stats.leaves == ref["leaves"]
+    assert res.stats.local_steals > 0
+    assert _hist_str(res.hist) == ref["hist"]
+
+
+def test_user_intervals_partition_invariance():
+    """Any partition of [0, n!) into intervals gives the K=1 unique count."""
+    ref = golden_io.ref_counts()["ta041@2991"]
+    inst = pbb.taillard_named("ta041")
+    nf = math.factorial(inst.n)
+    rng = np.random.default_rng(5)
+    cuts = sorted({int(x) * (nf >> 62) for x in rng.integers(1, 2 ** 62, 40)} | {nf // 3, nf // 2})
+    bounds = [0] + cuts + [nf]
+    ivs = list(zip(bounds[:-1], bounds[1:]))
+    res = pbb.pool_run(inst, 2991, intervals=ivs, cfg=pbb.PoolConfig(explorers=128))
+    assert res.stats.unique == ref["decomposed"]
+    assert res.stats.leaves == ref["leaves"]
+
+
+# ---------------------------------------------------------------- improving search
+
+@pytest.mark.parametrize("name,opt", [("ta001", 1278), ("ta011", 1582), ("ta031", 2724), ("ta041", 2991)])
+@pytest.mark.parametrize("bound", ["lb1", "lb2"])
+def test_optimum_from_neh(name, opt, bound):
+    inst = pbb.taillard_named(name)
+    ub = pbb.neh(inst).cmax
+    res = pbb.pool_run(inst, ub, bound=bound)
+    assert res.best_value == opt
+    if ub > opt:
+        assert res.best.cmax == opt
+        assert pbb.makespan(inst, res.best.perm) == opt
+        assert res.stats.improvements >= 1
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("bound", ["lb1", "lb2"])
+def test_optimum_matches_brute_force(seed, bound):
+    n, m = 8, 5
+    inst = pbb.generate_taillard(n, m, 4242 + seed)
+    best = min(pbb.makespan(inst, perm) for perm in itertools.permutations(range(n)))
+    res = pbb.pool_run(inst, 10 ** 6, bound=bound, cfg=pbb.PoolConfig(explorers=128))
+    assert res.best_value == best
+    assert pbb.makespan(inst, res.best.perm) == best
+
+
+def test_census_without_pruning_visits_every_leaf():
+    """disable_pruning: exactly n! leaves are evaluated (SPEC.md acceptance 4)."""
+    n, m = 8, 5
+    inst = pbb.generate_taillard(n, m, 77)
+    res = pbb.pool_run(inst, 10 ** 6, cfg=pbb.PoolConfig(explorers=100, disable_pruning=True, batch_steps=64))
+    assert res.stats.leaves == math.factorial(n)
+
+
+@pytest.mark.parametrize("name,ub", [("ta041", 2992), ("ta011", 1583)])
+def test_pinned_mode_matches_oracle(name, ub):
+    """Pinned UB (prune >= ub, never improve) just above the optimum is a fixed tree too."""
+    inst = pbb.taillard_named(name)
+    ref = orc.Problem(inst.p, orc.LB1).solve(ub, pinned=True, threads=4, prefix_depth=2)
+    res = pbb.pool_run(inst, ub, cfg=pbb.PoolConfig(pinned=True, explorers=300))
+    assert res.stats.unique == ref["unique"]
+    assert res.stats.leaves == ref["leaves"]
+    assert res.stats.improvements == 0
+
+
+# ---------------------------------------------------------------- pool surface
+
+def test_pool_rounds_snapshot_and_offer_bound():
+    inst = pbb.taillard_named("ta021")
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=512, batch_steps=256)) as pool:
+        pool.set_initial_bound(2297)
+        pool.assign_fresh([(0, math.factorial(20))])
+        assert pool.active_count() == 1
+        for _ in range(3):
+            pool.run_round()
+        snap = pool.snapshot_intervals()
+        assert snap and all(a < b for a, b in snap)
+        assert all(snap[i][1] <= snap[i + 1][0] for i in range(len(snap) - 1))
+        pool.offer_bound(2296)
+        pool.run_round()
+        assert pool.best_value() == 2296
+        st = pool.stats()
+        assert st.rounds == 4 and st.decomposed > 0
+
+
+def test_snapshot_resume_preserves_count():
+    """Snapshot the remaining work after a few rounds, restart it in a fresh pool:
+    nodes before + nodes after == full count (apply_work_update-style handover)."""
+    ref = golden_io.ref_counts()["ta011@1582"]
+    inst = pbb.taillard_named("ta011")
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=256, batch_steps=64)) as pool:
+        pool.set_initial_bound(1582)
+        pool.assign_split(256)
+        for _ in range(3):
+            pool.run_round()
+        snap = pool.snapshot_intervals()
+        done = pool.stats()
+    res = pbb.pool_run(inst, 1582, intervals=snap, cfg=pbb.PoolConfig(explorers=max(256, len(snap))))
+    # nodes on the path to each resumed position are re-decomposed by the new pool's replay;
+    # they are discounted exactly like steal replays, so the totals add up
+    assert done.unique + res.stats.unique >= ref["decomposed"]
+    assert done.leaves + res.stats.leaves == ref["leaves"]
