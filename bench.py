@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""bench.py — decomposed B&B nodes/s (and time-to-proof) of the B200 PFSP solver.
+
+Workload (BASELINE.json configs[1]): Taillard ta021 (20 jobs x 20 machines), LB2 Johnson
+two-machine bound, initial UB = optimum 2297, FULL PROOF per step (fixed tree: every step
+decomposes exactly the same 35,671,488 unique nodes). One step = one complete proof.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+N > 1 is launched by torchrun (one process per GPU, NCCL); the proof is shared by all ranks
+(strong scaling: [0,n!) partitioned over GPUs, inter-GPU interval stealing + MIN incumbent,
+paper_2012_09511_b200/multi.py). Each timed step is bracketed by a barrier and
+torch.cuda.synchronize(); its device time is measured with CUDA events and the max over
+ranks is taken. L2 is flushed (256 MiB write) between steps, outside the brackets.
+
+--impl reference runs the reference's CPU implementation of the path on the host cores: the
+reference has no LB2, so for LB2 workloads this is the builder's C restatement
+(oracle/pfsp_oracle, kind "port"); for LB1 workloads it is the compiled reference itself
+(oracle/_ref/ref_driver, kind "reference").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decomposed B&B nodes/sec at 1/2/4/8 B200; time-to-proof (UB=opt) vs CPU ref"
+
+WORKLOADS = {
+    "ta021-lb2": dict(instance="ta021", bound="lb2", ub=2297,
+                      desc="Taillard ta021 (20x20), LB2 Johnson bound, initial UB = optimum 2297, full proof per step"),
+    "ta021-lb1": dict(instance="ta021", bound="lb1", ub=2297,
+                      desc="Taillard ta021 (20x20), LB1 one-machine bound, initial UB = optimum 2297, full proof per step"),
+}
+
+# algorithmic 32-bit integer ops per decomposed node as a function of the
+# node's free-job count f (the reference algorithm's work, not the kernel's executed ops).
+def w_lb1(f, n, m):
+    return (2 * m - 1) * (n - f) + 13 * m * f + 9 * f
+
+
+def w_lb2(f, n, m):
+    P = m * (m - 1) // 2
+    return (2 * m - 1) * (n - f) + 2 * f * (2 * m - 1) + 8 * P * f * f + 9 * f
+
+
+REASONS = {  # nvidia-smi clocks_event_reasons bits
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        loaded = [r for r in self.rows if not (r[2] & 0x1)] or self.rows
+        reasons = set()
+        for _, _, bits in loaded:
+            for b, name in REASONS.items():
+                if bits & b and b != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(reasons), "samples": len(loaded)}
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_sample(wl, seconds, cores):
+    """Reference CPU arm on a bounded sample: nodes/s of the CPU implementation."""
+    inst, bound, ub = wl["instance"], wl["bound"], wl["ub"]
+    if bound == "lb1":
+        drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+        if os.path.exists(drv):
+            out = subprocess.run([drv, "solve", inst, str(ub), str(8 * cores), str(cores), str(seconds)],
+                                 capture_output=True, text=True, check=True).stdout
+            r = json.loads(out.strip().splitlines()[-1])
+            return {"value": r["decomposed"] / r["wall_s"], "unit": "nodes/s", "cores": cores, "kind": "reference",
+                    "sample": f"oracle/_ref/ref_driver pool_run {inst} LB1 UB={ub}, K={8 * cores}, "
+                              f"{cores} threads, {seconds:.0f} s time limit ({r['decomposed']} raw nodes)"}
+    cli = os.path.join(ROOT, "oracle", "pfsp_oracle")
+    if not os.path.exists(cli):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "pfsp_oracle"], check=True, capture_output=True)
+    out = subprocess.run([cli, "solve", inst, bound, str(ub), str(cores), "2", "0", str(seconds)],
+                         capture_output=True, text=True, check=True).stdout
+    r = json.loads(out)
+    return {"value": r["unique"] / r["wall_s"], "unit": "nodes/s", "cores": cores, "kind": "port",
+            "sample": f"oracle/pfsp_oracle (C restatement; the reference has no LB2) {inst} {bound.upper()} "
+                      f"UB={ub}, {cores} threads, {seconds:.0f} s of the proof ({r['unique']} unique nodes)"}
+
+
+def run_reference(args, wl, rank):
+    if rank != 0:
+        return 0
+    cores = cpu_cores()
+    vals = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(wl, args.ref_warmup_s if i < args.warmup else args.ref_step_s, cores)
+        if i >= args.warmup:
+            vals.append(s)
+    v = statistics.mean(x["value"] for x in vals)
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "nodes/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * args.ref_step_s,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (Taillard generator, published seed)",
+            "config": {"workload": args.workload, "instance": wl["instance"], "bound": wl["bound"].upper(),
+                       "initial_ub": wl["ub"], "desc": wl["desc"]},
+            "cpu_baseline": cb, "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="ta021-lb2", choices=sorted(WORKLOADS))
+    ap.add_argument("--cpu-sample-s", type=float, default=20.0)
+    ap.add_argument("--ref-step-s", type=float, default=15.0)
+    ap.add_argument("--ref-warmup-s", type=float, default=3.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, wl, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2012_09511_b200 as pbb
+    from paper_2012_09511_b200.multi import solve_distributed
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    inst = pbb.taillard_named(wl["instance"])
+    n, m = inst.n, inst.m
+    W = w_lb2 if wl["bound"] == "lb2" else w_lb1
+    cfg = pbb.PoolConfig(device=local)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def maxred(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def step(pool):
+        before = pool.stats()
+        res = solve_distributed(pool, wl["ub"], device=dev)
+        after = pool.stats()
+        return res, before, after
+
+    pool = pbb.GpuPool(inst, cfg, bound=wl["bound"])
+    for _ in range(args.warmup):
+        flush.zero_()
+        barrier()
+        step(pool)
+    times, results, kern_ms, launches = [], [], [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            res, before, after = step(pool)
+            torch.cuda.synchronize()
+            e1.record()
+            barrier()
+            e1.synchronize()
+            times.append(maxred(e0.elapsed_time(e1)))
+            results.append(res)
+            kern_ms.append(after.kernel_ms - before.kernel_ms)
+            launches += after.kernel_launches - before.kernel_launches
+    clocks = clk.summary()
+    unique = results[-1].unique
+    assert all(r.unique == unique and r.completed for r in results), "fixed-tree steps must repeat exactly"
+    total_ms = sum(times)
+    value = unique * len(times) / (total_ms / 1000.0)
+
+    # roofline of the dominant kernel (explore_kernel): algorithmic int ops / its device time
+    hist = results[-1].hist
+    ops = sum(v * W(f, n, m) for f, v in hist.items())
+    kms = maxred(statistics.mean(kern_ms))
+    peak = pbb.int32_peak(local)
+    tr = load_traffic()
+    traffic = tr.get(f"{args.workload}:explore_kernel_dram_bytes_per_launch")
+    roofline = {"bound": "int_alu", "achieved": ops / (kms / 1000.0) / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
+                "frac": (ops / (kms / 1000.0)) / peak, "traffic": traffic,
+                "kernel": "explore_kernel", "kernel_ms_per_step": kms,
+                "kernel_share_of_step": kms / statistics.mean(times),
+                "ops_per_step": ops, "ops_model": "SURVEY.md §8(d) W2(f)" if wl["bound"] == "lb2" else "SURVEY.md §8(d) W1(f)",
+                "peak_source": "pbbgpu_int32_peak microbenchmark, this run (add+max streams; MEASURED_PEAKS.json has no integer peak)"}
+
+    # e2e: the C-ABI call a user makes, HOST buffers in, results back to host, per step
+    e2e = None
+    if not args.no_e2e:
+        e_times, h2d, d2h = [], 0, 0
+        for i in range(1 + args.steps):
+            flush.zero_()
+            barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            p2 = pbb.GpuPool(pbb.Instance(n, m, inst.p.copy()), cfg, bound=wl["bound"])
+            r = solve_distributed(p2, wl["ub"], device=dev)
+            st = p2.stats()
+            p2.close()
+            torch.cuda.synchronize()
+            dt = maxred(time.perf_counter() - t0)
+            assert r.unique == unique
+            if i > 0:  # first one warms the create path
+                e_times.append(dt)
+                h2d, d2h = st.h2d_bytes, st.d2h_bytes
+        e2e = {"value": unique / statistics.mean(e_times), "unit": "nodes/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "s_per_step": statistics.mean(e_times),
+               "path": "pbbgpu_create(host matrix) + pbbgpu_solve + stats/hist/best to host + pbbgpu_destroy"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu and world == 1:
+        cpu = cpu_sample(wl, args.cpu_sample_s, cpu_cores())
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": statistics.mean(times), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+                "data": "synthetic (Taillard instance regenerated from its published seed; exact benchmark matrix)",
+                "config": {"workload": args.workload, "instance": wl["instance"], "bound": wl["bound"].upper(),
+                           "initial_ub": wl["ub"], "mode": "full proof (fixed tree) per step",
+                           "unique_nodes_per_step": unique, "leaves_per_step": results[-1].leaves,
+                           "time_to_proof_ms": statistics.mean(times), "explorers_per_gpu": pool.K(),
+                           "parallelism": f"dp{world}" if world > 1 else "single",
+                           "l2": "256 MiB flush between steps, outside the per-step event brackets",
+                           "desc": wl["desc"]},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    pool.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -10,6 +10,9 @@
  *   pbbgpu_assign                   <- ExplorerPool::assign_fresh       (explorer.hpp:76)
  *   pbbgpu_assign_split             <- assign_fresh of [0,n!) cut into K equal ranges
  *                                      (pool_run's default interval, explorer.cpp:479)
+ *   pbbgpu_assign_split_range       <- initial partition of [0,n!) over GPUs
+ *   pbbgpu_export                   <- split_unit right halves for another worker
+ *                                      (src/workunit.cpp:59-74, src/coordinator.cpp:170-187)
  *   pbbgpu_run_round                <- ExplorerPool::run_round          (explorer.hpp:85)
  *   pbbgpu_active_count             <- ExplorerPool::active_count       (explorer.hpp:87)
  *   pbbgpu_snapshot                 <- ExplorerPool::snapshot_intervals (explorer.hpp:88)
@@ -19,6 +22,7 @@
  *   pbbgpu_histogram                <- (new) decomposed nodes by free-job count (roofline)
  *   pbbgpu_decompose_batch          <- decompose(inst, sub, incumbent, ...) (bound.hpp:78-79)
  *   pbbgpu_solve                    <- pool_run(inst, ub, intervals, cfg) (explorer.hpp:145-146)
+ *   pbbgpu_int32_peak               <- (new) integer-ALU roofline denominator
  *   pbbgpu_taillard / pbbgpu_makespan / pbbgpu_neh
  *                                   <- generate_taillard / taillard_named / makespan / neh
  *                                      (instance.hpp:42-48, heuristic.hpp:21)
@@ -78,6 +82,10 @@ typedef struct {
   int K;
   int group;
   int steps_per_round;
+  double device_ms;             /* pbbgpu_solve only: CUDA-event time from the first round to the last */
+  uint64_t kernel_launches;     /* kernels launched by the pool so far (explore + steal + init) */
+  uint64_t h2d_bytes;           /* host->device bytes copied by the pool so far */
+  uint64_t d2h_bytes;           /* device->host bytes copied by the pool so far */
 } pbbgpu_stats_t;
 
 const char* pbbgpu_last_error(void);
@@ -98,6 +106,12 @@ int pbbgpu_set_initial_bound(pbbgpu_pool* pool, int64_t ub, const int32_t* sched
 int pbbgpu_assign(pbbgpu_pool* pool, const uint16_t* a_digits, const uint16_t* b_digits,
                   const uint8_t* b_is_nfact, int count);
 int pbbgpu_assign_split(pbbgpu_pool* pool, int pieces);
+/* pieces [first, first+count) of [0,n!) cut into `total` equal ranges (multi-GPU partition) */
+int pbbgpu_assign_split_range(pbbgpu_pool* pool, int first, int count, int total);
+/* hand the right halves [mid, end) of the `max_count` longest remaining intervals to another
+ * pool (inter-GPU stealing); the explorers keep [pos, mid) */
+int pbbgpu_export(pbbgpu_pool* pool, int max_count, uint16_t* a_out, uint16_t* b_out,
+                  uint8_t* b_is_nfact_out, int* count);
 int pbbgpu_run_round(pbbgpu_pool* pool, int* active_out);
 int pbbgpu_active_count(pbbgpu_pool* pool, int* active_out);
 int pbbgpu_snapshot(pbbgpu_pool* pool, uint16_t* pos_digits, uint16_t* end_digits,
@@ -110,6 +124,11 @@ int pbbgpu_decompose_batch(pbbgpu_pool* pool, const int32_t* perms, const int32_
                            const int32_t* d2, int count, int64_t incumbent, int64_t* child_lb,
                            uint8_t* direction, uint8_t* pruned, int64_t* lb_fwd_or_null,
                            int64_t* lb_bwd_or_null);
+
+/* INT32 ALU microbenchmark (add + max streams, the bounding kernels' instruction mix):
+ * measured integer-op throughput of the device, the roofline denominator of the bounding
+ * kernels (MEASURED_PEAKS.json has no integer peak). */
+int pbbgpu_int32_peak(int device, double* ops_per_s);
 
 /* pool_run: assign [0,n!) (or the given intervals), run rounds to exhaustion or time limit */
 int pbbgpu_solve(pbbgpu_pool* pool, int64_t initial_ub, const uint16_t* a_digits,

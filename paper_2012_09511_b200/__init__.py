@@ -7,10 +7,10 @@ libpbbgpu.so (hand-written sm_100a kernels); see DESIGN.md.
 from .factoradic import compare, from_decimal, midpoint, to_decimal
 from .instance import Instance, Schedule, generate_taillard, makespan, neh, parse_instance, taillard_named
 from .pool import (BACKWARD, FORWARD, NO_INCUMBENT, Decomposition, GpuPool, PoolConfig, PoolResult,
-                   PoolStats, Subproblem, normalize, pool_run)
+                   PoolStats, Subproblem, int32_peak, normalize, pool_run)
 
 __all__ = [
     "Instance", "Schedule", "generate_taillard", "taillard_named", "makespan", "neh", "parse_instance",
     "GpuPool", "PoolConfig", "PoolStats", "PoolResult", "Subproblem", "Decomposition", "pool_run",
-    "normalize", "to_decimal", "from_decimal", "compare", "midpoint", "FORWARD", "BACKWARD", "NO_INCUMBENT",
+    "normalize", "int32_peak", "to_decimal", "from_decimal", "compare", "midpoint", "FORWARD", "BACKWARD", "NO_INCUMBENT",
 ]

@@ -25,7 +25,8 @@ EXPORTS = (
     "pbbgpu_makespan", "pbbgpu_neh", "pbbgpu_create", "pbbgpu_destroy", "pbbgpu_K",
     "pbbgpu_set_initial_bound", "pbbgpu_assign", "pbbgpu_assign_split", "pbbgpu_run_round",
     "pbbgpu_active_count", "pbbgpu_snapshot", "pbbgpu_best", "pbbgpu_offer_bound",
-    "pbbgpu_stats", "pbbgpu_histogram", "pbbgpu_decompose_batch", "pbbgpu_solve",
+    "pbbgpu_stats", "pbbgpu_histogram", "pbbgpu_decompose_batch", "pbbgpu_solve", "pbbgpu_int32_peak",
+    "pbbgpu_assign_split_range", "pbbgpu_export",
 )
 
 
@@ -60,6 +61,10 @@ class Stats(ctypes.Structure):
         ("K", ctypes.c_int),
         ("group", ctypes.c_int),
         ("steps_per_round", ctypes.c_int),
+        ("device_ms", ctypes.c_double),
+        ("kernel_launches", ctypes.c_uint64),
+        ("h2d_bytes", ctypes.c_uint64),
+        ("d2h_bytes", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:
@@ -109,6 +114,9 @@ def load() -> ctypes.CDLL:
         "pbbgpu_histogram": (ctypes.c_int, [P, u64p, ctypes.c_int]),
         "pbbgpu_decompose_batch": (ctypes.c_int, [P, i32p, i32p, i32p, ctypes.c_int, ctypes.c_int64,
                                                   i64p, u8p, u8p, i64p, i64p]),
+        "pbbgpu_assign_split_range": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+        "pbbgpu_export": (ctypes.c_int, [P, ctypes.c_int, u16p, u16p, u8p, ip]),
+        "pbbgpu_int32_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
         "pbbgpu_solve": (ctypes.c_int, [P, ctypes.c_int64, u16p, u16p, u8p, ctypes.c_int, i64p, i32p,
                                         ip, ctypes.POINTER(Stats)]),
     }

@@ -405,6 +405,129 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
   }
 }
 
+// Export work to another GPU (inter-GPU interval stealing, the intra-box analogue of
+// the coordinator's split_unit / steal_from_active, src/workunit.cpp:59-74,
+// src/coordinator.cpp:170-187): the `want` active explorers with the longest remaining
+// intervals keep [pos, mid) and hand [mid, end) out as factoradic digit vectors.
+__global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, int want, int* out_digits,
+                                                              uint8_t* out_nf, int* out_count) {
+  __shared__ int bins[kBins];
+  __shared__ int s_tot[2];
+  const int t = threadIdx.x, K = S.K, n = S.L.n;
+  const int CH = (K + kStealThreads - 1) / kStealThreads;
+  const int lo = t * CH, hi = min(K, lo + CH);
+  for (int b = t; b < kBins; b += kStealThreads) bins[b] = 0;
+  if (t < 2) s_tot[t] = 0;
+  __syncthreads();
+  for (int i = lo; i < hi; ++i) {
+    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact);
+    if (lg >= S.min_log2 && lg >= 1.f) atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
+  }
+  __syncthreads();
+  if (t == 0) {
+    int acc = 0;
+    for (int b = kBins - 1; b >= 0; --b) {
+      const int c = bins[b];
+      bins[b] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int i = lo; i < hi; ++i) {
+    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact);
+    if (lg >= S.min_log2 && lg >= 1.f) {
+      const int rank = atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
+      if (rank < want) S.victim[rank] = i;
+      if (rank < want) atomicAdd(&s_tot[1], 1);
+    }
+  }
+  __syncthreads();
+  const int npairs = s_tot[1];
+  for (int pidx = t; pidx < npairs; pidx += kStealThreads) {
+    unsigned char* vb = S.state + static_cast<size_t>(S.victim[pidx]) * S.L.gstride;
+    IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
+    const int8_t* V = reinterpret_cast<const int8_t*>(vb + S.L.o_v);
+    int8_t* E = reinterpret_cast<int8_t*>(vb + S.L.o_end);
+    int pos[kMaxN], mid[kMaxN], sum[kMaxN];
+    for (int l = 0; l < n; ++l) pos[l] = l <= vh->level ? V[l] : 0;
+    int carry = 0;
+    if (vh->has_end) {
+      for (int l = n - 1; l >= 0; --l) {
+        const int s = pos[l] + E[l] + carry, radix = n - l;
+        sum[l] = s % radix;
+        carry = s / radix;
+      }
+    } else {
+      for (int l = 0; l < n; ++l) sum[l] = pos[l];
+      carry = 1;
+    }
+    int rem = carry;
+    for (int l = 0; l < n; ++l) {
+      const int cur = rem * (n - l) + sum[l];
+      mid[l] = cur / 2;
+      rem = cur % 2;
+    }
+    int cmp = 0;
+    for (int l = 0; l < n && !cmp; ++l) cmp = mid[l] < pos[l] ? -1 : (mid[l] > pos[l] ? 1 : 0);
+    if (cmp <= 0) continue;
+    const int slot = atomicAdd(&s_tot[0], 1);
+    int* o = out_digits + static_cast<size_t>(slot) * 2 * n;
+    for (int l = 0; l < n; ++l) {
+      o[l] = mid[l];
+      o[n + l] = vh->has_end ? E[l] : 0;
+    }
+    out_nf[slot] = vh->has_end ? 0 : 1;
+    for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(mid[l]);
+    vh->has_end = 1;
+  }
+  __syncthreads();
+  if (t == 0) *out_count = s_tot[0];
+}
+
+// Idle explorers in index order (slots for assign / import) and their count.
+__global__ void __launch_bounds__(kStealThreads) list_idle_kernel(IvmLayout L, const unsigned char* state, int K,
+                                                                 int* slots, int* count) {
+  __shared__ int s_idle[kStealThreads];
+  const int t = threadIdx.x;
+  const int CH = (K + kStealThreads - 1) / kStealThreads;
+  const int lo = t * CH, hi = min(K, lo + CH);
+  int idle = 0;
+  for (int i = lo; i < hi; ++i)
+    idle += reinterpret_cast<const IvmHdr*>(state + static_cast<size_t>(i) * L.gstride)->state == kEmpty;
+  s_idle[t] = idle;
+  __syncthreads();
+  for (int off = 1; off < kStealThreads; off <<= 1) {
+    const int v = t >= off ? s_idle[t - off] : 0;
+    __syncthreads();
+    s_idle[t] += v;
+    __syncthreads();
+  }
+  int r = s_idle[t] - idle;
+  for (int i = lo; i < hi; ++i)
+    if (reinterpret_cast<const IvmHdr*>(state + static_cast<size_t>(i) * L.gstride)->state == kEmpty) slots[r++] = i;
+  if (t == kStealThreads - 1) *count = s_idle[t];
+}
+
+// INT32 peak microbenchmark: 8 independent add+max chains per thread (IADD3 / IMNMX on
+// the ALU pipe, the same mix as the LB1/LB2 chains).
+__global__ void __launch_bounds__(256) int32_peak_kernel(const int* in, int* out, int iters) {
+  int x[8];
+  const int y = in[threadIdx.x & 7], z = in[8 + (threadIdx.x & 7)];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = in[16 + i] + threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      x[i] = max(x[i] + y, z);
+      x[i] = max(x[i] + z, y);
+    }
+  }
+  int acc = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc ^= x[i];
+  if (acc == 0x7fffffff) out[blockIdx.x] = acc;
+}
+
 // ------------------------------------------------------------------ kernel tables
 
 using ExploreFn = void (*)(ExploreParams);
@@ -498,6 +621,8 @@ struct pbbgpu_pool {
   int64_t pinned_ub = INT64_MAX;
   std::vector<int32_t> best_sched;
   uint64_t rounds = 0;
+  uint64_t launches = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
   double kernel_ms = 0;
   int last_active = 0;
 
@@ -524,6 +649,14 @@ struct pbbgpu_pool {
 };
 
 namespace {
+
+// Every host<->device copy of a pool goes through here (counted for the e2e report).
+void xfer(pbbgpu_pool* P, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, const char* what) {
+  ck(cudaMemcpyAsync(dst, src, bytes, kind, P->stream), what);
+  ck(cudaStreamSynchronize(P->stream), what);
+  if (kind == cudaMemcpyHostToDevice) P->h2d_bytes += bytes;
+  else if (kind == cudaMemcpyDeviceToHost) P->d2h_bytes += bytes;
+}
 
 int pick_group(int n, int bound) {
   if (bound == kLB1) return n <= 24 ? 4 : 8;
@@ -602,29 +735,29 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   ck(cudaMalloc(&P->d_state, static_cast<size_t>(P->K) * P->L.gstride), "malloc state");
   ck(cudaMalloc(&P->d_p32, p32.size() * sizeof(int)), "malloc");
   ck(cudaMalloc(&P->d_ptot, ptot.size() * sizeof(int)), "malloc");
-  ck(cudaMalloc(&P->d_wrk, static_cast<size_t>(P->K) * 2 * sizeof(int)), "malloc");
+  ck(cudaMalloc(&P->d_wrk, (static_cast<size_t>(P->K) * 2 + 1) * sizeof(int)), "malloc");
   ck(cudaMalloc(&P->d_lgfact, lgf.size() * sizeof(float)), "malloc");
   ck(cudaMalloc(&P->d_ctr, sizeof(DevCounters)), "malloc");
   ck(cudaMallocHost(&P->h_ctr, sizeof(DevCounters)), "malloc host");
   ck(cudaMalloc(&P->d_hist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
   ck(cudaMalloc(&P->d_dhist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
   ck(cudaMalloc(&P->d_imp, kImpCap * sizeof(ImpRecord)), "malloc");
-  ck(cudaMemcpy(P->d_p32, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
-  ck(cudaMemcpy(P->d_ptot, ptot.data(), ptot.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
-  ck(cudaMemcpy(P->d_lgfact, lgf.data(), lgf.size() * sizeof(float), cudaMemcpyHostToDevice), "copy");
+  xfer(P, P->d_p32, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
+  xfer(P, P->d_ptot, ptot.data(), ptot.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
+  xfer(P, P->d_lgfact, lgf.data(), lgf.size() * sizeof(float), cudaMemcpyHostToDevice, "copy");
   if (bound == kLB2) {
     ck(cudaMalloc(&P->d_pk, pk.size()), "malloc");
     ck(cudaMalloc(&P->d_pl, pl.size()), "malloc");
     ck(cudaMalloc(&P->d_ord, ord.size()), "malloc");
     ck(cudaMalloc(&P->d_lag, lag.size() * sizeof(uint16_t)), "malloc");
-    ck(cudaMemcpy(P->d_pk, pk.data(), pk.size(), cudaMemcpyHostToDevice), "copy");
-    ck(cudaMemcpy(P->d_pl, pl.data(), pl.size(), cudaMemcpyHostToDevice), "copy");
-    ck(cudaMemcpy(P->d_ord, ord.data(), ord.size(), cudaMemcpyHostToDevice), "copy");
-    ck(cudaMemcpy(P->d_lag, lag.data(), lag.size() * sizeof(uint16_t), cudaMemcpyHostToDevice), "copy");
+    xfer(P, P->d_pk, pk.data(), pk.size(), cudaMemcpyHostToDevice, "copy");
+    xfer(P, P->d_pl, pl.data(), pl.size(), cudaMemcpyHostToDevice, "copy");
+    xfer(P, P->d_ord, ord.data(), ord.size(), cudaMemcpyHostToDevice, "copy");
+    xfer(P, P->d_lag, lag.data(), lag.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, "copy");
   }
   DevCounters z{};
   z.best = INT_MAX;
-  ck(cudaMemcpy(P->d_ctr, &z, sizeof(z), cudaMemcpyHostToDevice), "copy");
+  xfer(P, P->d_ctr, &z, sizeof(z), cudaMemcpyHostToDevice, "copy");
   ck(cudaMemset(P->d_hist, 0, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "memset");
   ck(cudaMemset(P->d_dhist, 0, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "memset");
   clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
@@ -633,13 +766,12 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
 }
 
 void read_counters(pbbgpu_pool* P) {
-  ck(cudaMemcpyAsync(P->h_ctr, P->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, P->stream), "ctr copy");
-  ck(cudaStreamSynchronize(P->stream), "sync");
+  xfer(P, P->h_ctr, P->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, "ctr copy");
 }
 
 void set_device_best(pbbgpu_pool* P, int64_t v) {
   const int b = v >= INT_MAX ? INT_MAX : static_cast<int>(std::max<int64_t>(v, 0));
-  ck(cudaMemcpyAsync(reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, best), &b, sizeof(int), cudaMemcpyHostToDevice, P->stream), "best copy");
+  xfer(P, reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, best), &b, sizeof(int), cudaMemcpyHostToDevice, "best copy");
   ck(cudaStreamSynchronize(P->stream), "sync");
 }
 
@@ -648,7 +780,7 @@ void harvest(pbbgpu_pool* P) {
   const int cnt = std::min(P->h_ctr->imp_count, kImpCap);
   if (cnt > 0) {
     std::vector<ImpRecord> recs(static_cast<size_t>(cnt));
-    ck(cudaMemcpy(recs.data(), P->d_imp, recs.size() * sizeof(ImpRecord), cudaMemcpyDeviceToHost), "imp copy");
+    xfer(P, recs.data(), P->d_imp, recs.size() * sizeof(ImpRecord), cudaMemcpyDeviceToHost, "imp copy");
     std::scoped_lock lk(P->best_mu);
     for (const ImpRecord& r : recs) {
       if (r.mk < P->best_sched_value) {
@@ -658,7 +790,7 @@ void harvest(pbbgpu_pool* P) {
       P->best_value = std::min<int64_t>(P->best_value, r.mk);
     }
     const int zero = 0;
-    ck(cudaMemcpy(reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, imp_count), &zero, sizeof(int), cudaMemcpyHostToDevice), "imp reset");
+    xfer(P, reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, imp_count), &zero, sizeof(int), cudaMemcpyHostToDevice, "imp reset");
   }
   std::scoped_lock lk(P->best_mu);
   P->best_value = std::min<int64_t>(P->best_value, P->h_ctr->best);
@@ -696,12 +828,13 @@ void assign_digits(pbbgpu_pool* P, const std::vector<int>& a, const std::vector<
   ck(cudaMalloc(&db, b.size() * sizeof(int)), "malloc");
   ck(cudaMalloc(&ds, slots.size() * sizeof(int)), "malloc");
   ck(cudaMalloc(&dn, nf.size()), "malloc");
-  ck(cudaMemcpy(da, a.data(), a.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
-  ck(cudaMemcpy(db, b.data(), b.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
-  ck(cudaMemcpy(ds, slots.data(), slots.size() * sizeof(int), cudaMemcpyHostToDevice), "copy");
-  ck(cudaMemcpy(dn, nf.data(), nf.size(), cudaMemcpyHostToDevice), "copy");
+  xfer(P, da, a.data(), a.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
+  xfer(P, db, b.data(), b.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
+  xfer(P, ds, slots.data(), slots.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
+  xfer(P, dn, nf.data(), nf.size(), cudaMemcpyHostToDevice, "copy");
   init_kernel<<<(cnt + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, da, db, dn, ds, cnt);
   ck(cudaGetLastError(), "init_kernel");
+  P->launches += 1;
   ck(cudaStreamSynchronize(P->stream), "sync");
   cudaFree(da);
   cudaFree(db);
@@ -710,15 +843,29 @@ void assign_digits(pbbgpu_pool* P, const std::vector<int>& a, const std::vector<
   read_counters(P);
   // inits counter
   unsigned long long inits = P->h_ctr->inits + static_cast<unsigned long long>(cnt);
-  ck(cudaMemcpy(reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, inits), &inits, sizeof(inits), cudaMemcpyHostToDevice), "copy");
+  xfer(P, reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, inits), &inits, sizeof(inits), cudaMemcpyHostToDevice, "copy");
+}
+
+std::vector<int> idle_slots(pbbgpu_pool* P) {
+  int* d_cnt = P->d_wrk + 2 * P->K;
+  list_idle_kernel<<<1, kStealThreads, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_wrk, d_cnt);
+  ck(cudaGetLastError(), "list_idle_kernel");
+  P->launches += 1;
+  int cnt = 0;
+  xfer(P, &cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, "idle count");
+  std::vector<int> slots(static_cast<size_t>(cnt));
+  if (cnt) xfer(P, slots.data(), P->d_wrk, slots.size() * sizeof(int), cudaMemcpyDeviceToHost, "idle slots");
+  return slots;
 }
 
 int count_active_host(pbbgpu_pool* P) {
-  std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
-  ck(cudaMemcpy(st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost), "state copy");
-  int a = 0;
-  for (int i = 0; i < P->K; ++i) a += reinterpret_cast<const IvmHdr*>(st.data() + static_cast<size_t>(i) * P->L.gstride)->state != kEmpty;
-  return a;
+  int* d_cnt = P->d_wrk + 2 * P->K;
+  list_idle_kernel<<<1, kStealThreads, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_wrk, d_cnt);
+  ck(cudaGetLastError(), "list_idle_kernel");
+  P->launches += 1;
+  int cnt = 0;
+  xfer(P, &cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, "idle count");
+  return P->K - cnt;
 }
 
 int run_round(pbbgpu_pool* P) {
@@ -748,6 +895,7 @@ int run_round(pbbgpu_pool* P) {
   S.lgfact = P->d_lgfact;
   steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
   ck(cudaGetLastError(), "steal_kernel launch");
+  P->launches += 2;
   read_counters(P);
   float ms = 0;
   ck(cudaEventElapsedTime(&ms, P->ev0, P->ev1), "elapsed");
@@ -794,6 +942,44 @@ int pbbgpu_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
   return n;
+}
+
+int pbbgpu_int32_peak(int device, double* ops_per_s) {
+  return guarded([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw CudaError("pbbgpu: no CUDA device");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "props");
+    int* d_in = nullptr;
+    int* d_out = nullptr;
+    int h_in[24];
+    for (int i = 0; i < 24; ++i) h_in[i] = (i * 7919) % 97 - 40;
+    ck(cudaMalloc(&d_in, sizeof(h_in)), "malloc");
+    ck(cudaMalloc(&d_out, 1 << 20), "malloc");
+    ck(cudaMemcpy(d_in, h_in, sizeof(h_in), cudaMemcpyHostToDevice), "copy");
+    const int blocks = prop.multiProcessorCount * 8, threads = 256, iters = 1 << 14;
+    cudaEvent_t a, b;
+    ck(cudaEventCreate(&a), "event");
+    ck(cudaEventCreate(&b), "event");
+    int32_peak_kernel<<<blocks, threads>>>(d_in, d_out, 256);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+      ck(cudaEventRecord(a), "event");
+      int32_peak_kernel<<<blocks, threads>>>(d_in, d_out, iters);
+      ck(cudaEventRecord(b), "event");
+      ck(cudaEventSynchronize(b), "sync");
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+      best = std::min(best, ms);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d_in);
+    cudaFree(d_out);
+    const double ops = static_cast<double>(blocks) * threads * iters * 8 * 4;  // 2 x (add, max)
+    *ops_per_s = ops / (best * 1e-3);
+  });
 }
 
 int pbbgpu_taillard(int n, int m, int32_t seed, int32_t* p_out) {
@@ -876,11 +1062,7 @@ int pbbgpu_assign(pbbgpu_pool* P, const uint16_t* a, const uint16_t* b, const ui
     if (count < 0 || count > P->K) throw std::invalid_argument("more intervals than explorers");
     if (count == 0) return;
     const int n = P->n;
-    std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
-    ck(cudaMemcpy(st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost), "state copy");
-    std::vector<int> idle;
-    for (int i = 0; i < P->K; ++i)
-      if (reinterpret_cast<const IvmHdr*>(st.data() + static_cast<size_t>(i) * P->L.gstride)->state == kEmpty) idle.push_back(i);
+    const std::vector<int> idle = idle_slots(P);
     if (static_cast<int>(idle.size()) < count) throw CapacityError("not enough idle explorers for the assignment");
     std::vector<int> da(static_cast<size_t>(count) * n), db(static_cast<size_t>(count) * n, 0), slots(static_cast<size_t>(count));
     std::vector<uint8_t> dn(static_cast<size_t>(count));
@@ -899,32 +1081,88 @@ int pbbgpu_assign(pbbgpu_pool* P, const uint16_t* a, const uint16_t* b, const ui
   });
 }
 
-int pbbgpu_assign_split(pbbgpu_pool* P, int pieces) {
+int pbbgpu_assign_split_range(pbbgpu_pool* P, int first, int count, int total) {
   return guarded([&] {
-    if (pieces <= 0) pieces = P->K;
-    if (pieces > P->K) throw std::invalid_argument("more pieces than explorers");
+    if (total <= 0) total = P->K;
+    if (count < 0) count = total;
+    if (first < 0 || count > P->K || first + count > total) throw std::invalid_argument("bad split range");
     const int n = P->n;
-    // floor(i * n! / pieces) in factoradic, digit by digit: d_l = floor(r (n-l) / C),
+    // floor(i * n! / total) in factoradic, digit by digit: d_l = floor(r (n-l) / C),
     // r <- r (n-l) mod C (exact rational expansion, no big integers needed)
     auto digits_of = [&](int64_t i, int* out) {
       int64_t r = i;
       for (int l = 0; l < n; ++l) {
         r *= (n - l);
-        out[l] = static_cast<int>(r / pieces);
-        r %= pieces;
+        out[l] = static_cast<int>(r / total);
+        r %= total;
       }
     };
-    std::vector<int> a(static_cast<size_t>(pieces) * n), b(static_cast<size_t>(pieces) * n, 0), slots(static_cast<size_t>(pieces));
-    std::vector<uint8_t> nf(static_cast<size_t>(pieces), 0);
-    for (int i = 0; i < pieces; ++i) {
-      digits_of(i, &a[static_cast<size_t>(i) * n]);
-      if (i + 1 < pieces) digits_of(i + 1, &b[static_cast<size_t>(i) * n]);
-      else nf[static_cast<size_t>(i)] = 1;
-      slots[static_cast<size_t>(i)] = i;
+    std::vector<int> a(static_cast<size_t>(count) * n), b(static_cast<size_t>(count) * n, 0), slots(static_cast<size_t>(count));
+    std::vector<uint8_t> nf(static_cast<size_t>(count), 0);
+    for (int c = 0; c < count; ++c) {
+      const int i = first + c;
+      digits_of(i, &a[static_cast<size_t>(c) * n]);
+      if (i + 1 < total) digits_of(i + 1, &b[static_cast<size_t>(c) * n]);
+      else nf[static_cast<size_t>(c)] = 1;
+      slots[static_cast<size_t>(c)] = c;
     }
     clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
     ck(cudaGetLastError(), "clear_kernel");
+    P->launches += 1;
     assign_digits(P, a, b, nf, slots);
+  });
+}
+
+int pbbgpu_assign_split(pbbgpu_pool* P, int pieces) {
+  if (pieces <= 0) pieces = P ? P->K : 0;
+  return pbbgpu_assign_split_range(P, 0, pieces, pieces);
+}
+
+int pbbgpu_export(pbbgpu_pool* P, int max_count, uint16_t* a_out, uint16_t* b_out, uint8_t* nf_out, int* count) {
+  return guarded([&] {
+    *count = 0;
+    if (max_count <= 0) return;
+    const int n = P->n;
+    const int want = std::min(max_count, P->K);
+    int* d_dig = nullptr;
+    uint8_t* d_nf = nullptr;
+    int* d_cnt = nullptr;
+    ck(cudaMalloc(&d_dig, static_cast<size_t>(want) * 2 * n * sizeof(int)), "malloc");
+    ck(cudaMalloc(&d_nf, static_cast<size_t>(want)), "malloc");
+    ck(cudaMalloc(&d_cnt, sizeof(int)), "malloc");
+    StealParams S{};
+    S.L = P->L;
+    S.state = P->d_state;
+    S.K = P->K;
+    S.ptot = P->d_ptot;
+    S.ctr = P->d_ctr;
+    S.thief = P->d_wrk;
+    S.victim = P->d_wrk + P->K;
+    S.min_log2 = static_cast<float>(P->cfg.min_steal_log2 > 0 ? P->cfg.min_steal_log2 : std::log2(40320.0));
+    S.lgfact = P->d_lgfact;
+    export_kernel<<<1, kStealThreads, 0, P->stream>>>(S, want, d_dig, d_nf, d_cnt);
+    ck(cudaGetLastError(), "export_kernel");
+    P->launches += 1;
+    int cnt = 0;
+    xfer(P, &cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost, "copy");
+    ck(cudaStreamSynchronize(P->stream), "sync");
+    std::vector<int> dig(static_cast<size_t>(cnt) * 2 * n);
+    std::vector<uint8_t> nf(static_cast<size_t>(cnt));
+    if (cnt > 0) {
+      xfer(P, dig.data(), d_dig, dig.size() * sizeof(int), cudaMemcpyDeviceToHost, "copy");
+      xfer(P, nf.data(), d_nf, nf.size(), cudaMemcpyDeviceToHost, "copy");
+    }
+    cudaFree(d_dig);
+    cudaFree(d_nf);
+    cudaFree(d_cnt);
+    for (int i = 0; i < cnt; ++i) {
+      for (int l = 0; l < n; ++l) {
+        a_out[static_cast<size_t>(i) * n + l] = static_cast<uint16_t>(dig[static_cast<size_t>(i) * 2 * n + l]);
+        b_out[static_cast<size_t>(i) * n + l] = static_cast<uint16_t>(dig[static_cast<size_t>(i) * 2 * n + n + l]);
+      }
+      nf_out[i] = nf[static_cast<size_t>(i)];
+    }
+    *count = cnt;
   });
 }
 
@@ -943,7 +1181,7 @@ int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_n
   return guarded([&] {
     const int n = P->n;
     std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
-    ck(cudaMemcpy(st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost), "state copy");
+    xfer(P, st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost, "state copy");
     int c = 0;
     for (int i = 0; i < P->K; ++i) {
       const unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
@@ -1004,6 +1242,9 @@ int pbbgpu_stats(pbbgpu_pool* P, pbbgpu_stats_t* out) {
     out->K = P->K;
     out->group = P->G;
     out->steps_per_round = P->steps;
+    out->kernel_launches = P->launches;
+    out->h2d_bytes = P->h2d_bytes;
+    out->d2h_bytes = P->d2h_bytes;
   });
 }
 
@@ -1011,8 +1252,8 @@ int pbbgpu_histogram(pbbgpu_pool* P, uint64_t* hist, int len) {
   return guarded([&] {
     const int n = P->n;
     std::vector<unsigned long long> h(static_cast<size_t>(n) + 1), d(static_cast<size_t>(n) + 1);
-    ck(cudaMemcpy(h.data(), P->d_hist, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "hist copy");
-    ck(cudaMemcpy(d.data(), P->d_dhist, d.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "hist copy");
+    xfer(P, h.data(), P->d_hist, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, "hist copy");
+    xfer(P, d.data(), P->d_dhist, d.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, "hist copy");
     for (int f = 0; f < len; ++f) hist[f] = f <= n ? h[static_cast<size_t>(f)] - d[static_cast<size_t>(f)] : 0;
   });
 }
@@ -1045,9 +1286,9 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
     ck(cudaMalloc(&dlbw, cn * sizeof(int)), "malloc");
     ck(cudaMalloc(&ddir, count), "malloc");
     ck(cudaMalloc(&dpr, cn), "malloc");
-    ck(cudaMemcpy(dp, perms, cn * sizeof(int), cudaMemcpyHostToDevice), "copy");
-    ck(cudaMemcpy(dd1, d1, count * sizeof(int), cudaMemcpyHostToDevice), "copy");
-    ck(cudaMemcpy(dd2, d2, count * sizeof(int), cudaMemcpyHostToDevice), "copy");
+    xfer(P, dp, perms, cn * sizeof(int), cudaMemcpyHostToDevice, "copy");
+    xfer(P, dd1, d1, count * sizeof(int), cudaMemcpyHostToDevice, "copy");
+    xfer(P, dd2, d2, count * sizeof(int), cudaMemcpyHostToDevice, "copy");
     BatchParams B{};
     B.L = P->L;
     B.perms = dp;
@@ -1073,11 +1314,11 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
     ck(cudaStreamSynchronize(P->stream), "sync");
     std::vector<int> lb(cn), lf(cn), lbw(cn);
     std::vector<uint8_t> pr(cn);
-    ck(cudaMemcpy(lb.data(), dlb, cn * sizeof(int), cudaMemcpyDeviceToHost), "copy");
-    ck(cudaMemcpy(lf.data(), dlf, cn * sizeof(int), cudaMemcpyDeviceToHost), "copy");
-    ck(cudaMemcpy(lbw.data(), dlbw, cn * sizeof(int), cudaMemcpyDeviceToHost), "copy");
-    ck(cudaMemcpy(pr.data(), dpr, cn, cudaMemcpyDeviceToHost), "copy");
-    ck(cudaMemcpy(direction, ddir, count, cudaMemcpyDeviceToHost), "copy");
+    xfer(P, lb.data(), dlb, cn * sizeof(int), cudaMemcpyDeviceToHost, "copy");
+    xfer(P, lf.data(), dlf, cn * sizeof(int), cudaMemcpyDeviceToHost, "copy");
+    xfer(P, lbw.data(), dlbw, cn * sizeof(int), cudaMemcpyDeviceToHost, "copy");
+    xfer(P, pr.data(), dpr, cn, cudaMemcpyDeviceToHost, "copy");
+    xfer(P, direction, ddir, count, cudaMemcpyDeviceToHost, "copy");
     for (int i = 0; i < count; ++i) {
       const int f = n - d1[i] - d2[i];
       for (int c = 0; c < f; ++c) {
@@ -1107,7 +1348,12 @@ int pbbgpu_solve(pbbgpu_pool* P, int64_t initial_ub, const uint16_t* a, const ui
   if (rc) return rc;
   const auto t0 = std::chrono::steady_clock::now();
   bool completed = true;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  float dev_ms = 0.f;
   rc = guarded([&] {
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    ck(cudaEventRecord(e0, P->stream), "event");
     for (;;) {
       const int act = run_round(P);
       if (act == 0) break;
@@ -1119,7 +1365,12 @@ int pbbgpu_solve(pbbgpu_pool* P, int64_t initial_ub, const uint16_t* a, const ui
         }
       }
     }
+    ck(cudaEventRecord(e1, P->stream), "event");
+    ck(cudaEventSynchronize(e1), "event sync");
+    ck(cudaEventElapsedTime(&dev_ms, e0, e1), "elapsed");
   });
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
   if (rc) return rc;
   const std::chrono::duration<double> el = std::chrono::steady_clock::now() - t0;
   rc = pbbgpu_best(P, best_value, best_perm, has_perm);
@@ -1128,6 +1379,7 @@ int pbbgpu_solve(pbbgpu_pool* P, int64_t initial_ub, const uint16_t* a, const ui
     rc = pbbgpu_stats(P, stats);
     stats->wall_s = el.count();
     stats->completed = completed ? 1 : 0;
+    stats->device_ms = dev_ms;
   }
   return rc;
 }

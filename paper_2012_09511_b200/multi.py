@@ -1,0 +1,157 @@
+"""Multi-GPU solve: one process per GPU, torch.distributed for the plumbing.
+
+  partition   [0, n!) cut into world*K equal ranges; rank r seats pieces [r*K, (r+1)*K)
+              (pbbgpu_assign_split_range) -- the intra-box analogue of the coordinator's
+              initial work units (src/coordinator.cpp)
+  per round   every rank runs one pool round (explore + intra-GPU steal kernels), then one
+              all_gather of (active explorers, incumbent, exported intervals)
+  incumbent   MIN over ranks (the BEST message of src/protocol.cpp), fed back through
+              offer_bound
+  stealing    a rank whose active explorers drop below `low` receives the right halves of a
+              busy rank's longest intervals (pbbgpu_export -> all_gather -> pbbgpu_assign);
+              the donor keeps [pos, mid) -- the coordinator's split_unit
+              (src/workunit.cpp:59-74) between GPUs
+  termination all ranks report 0 active explorers in the same gathered snapshot
+Node counts stay exact: replays on the receiving GPU are discounted by the same
+unique = raw - min(L, lnz(a)) rule, which is partition invariant.
+The pool object only needs the GpuPool surface, so the orchestration logic is tested on CPU
+with a simulated pool and the gloo backend (tests/test_multi.py).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, Optional
+
+import numpy as np
+
+
+@dataclass
+class DistResult:
+    best_value: int
+    best_perm: list
+    unique: int
+    decomposed: int
+    leaves: int
+    improvements: int
+    local_steals: int
+    remote_intervals: int
+    rounds: int
+    exchanges: int
+    hist: Dict[int, int]
+    completed: bool
+
+
+_DELTA = ("unique", "decomposed", "leaves", "improvements", "local_steals")
+
+
+def solve_distributed(pool, ub: int, group=None, device=None, export_max: Optional[int] = None,
+                      low_fraction: float = 0.25, time_limit_s: float = 0.0) -> DistResult:
+    """Run `pool` (a GpuPool, or any object with its surface) to exhaustion cooperatively with
+    the other ranks of `group` (torch.distributed). world_size == 1 degenerates to pool_run."""
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n = pool.inst.n
+    K = pool.K()
+    st0 = pool.stats()
+    h0 = pool.histogram()
+    pool.set_initial_bound(ub)
+    pool.assign_split_range(rank * K, K, world * K)
+    X = export_max if export_max else max(1, min(1024, K // 4))
+    low = int(K * low_fraction)
+    remote = 0
+    rounds = 0
+    exchanges = 0
+    completed = True
+    t0 = time.time()
+    width = 2 * n + 1
+    while True:
+        active = pool.run_round()
+        rounds += 1
+        if world == 1:
+            if active == 0:
+                break
+            if time_limit_s and time.time() - t0 >= time_limit_s:
+                completed = False
+                break
+            continue
+        exchanges += 1
+        best = pool.best_value()
+        stop = int(bool(time_limit_s) and time.time() - t0 >= time_limit_s)
+        # phase 1: who is idle, who is busy, incumbent, time limit
+        info = torch.tensor([active, min(best, (1 << 62)), stop], dtype=torch.int64, device=device)
+        gathered = [torch.zeros_like(info) for _ in range(world)]
+        dist.all_gather(gathered, info, group=group)
+        g = torch.stack(gathered).cpu().numpy()
+        actives, bests = g[:, 0], g[:, 1]
+        gbest = int(bests.min())
+        if gbest < best:
+            pool.offer_bound(gbest)
+        if int(actives.sum()) == 0:
+            break
+        if int(g[:, 2].max()):
+            completed = False
+            break
+        receivers = [r for r in range(world) if actives[r] < low]
+        donors = [r for r in np.argsort(-actives, kind="stable") if actives[r] >= 2 * low and actives[r] > 0]
+        if not receivers or not donors:
+            continue
+        # phase 2: donors export, everybody gathers, receivers seat their share
+        pairs = {}
+        for i, r in enumerate(receivers):
+            pairs.setdefault(int(donors[i % len(donors)]), []).append(r)
+        buf = np.zeros((X, width), dtype=np.int32)
+        cnt = 0
+        if rank in pairs:
+            a, b, nf = pool.export_work(X)
+            cnt = len(nf)
+            buf[:cnt, :n] = a
+            buf[:cnt, n:2 * n] = b
+            buf[:cnt, 2 * n] = nf
+        sbuf = torch.from_numpy(np.concatenate([buf.reshape(-1), np.array([cnt], dtype=np.int32)])).to(device)
+        allb = [torch.zeros_like(sbuf) for _ in range(world)]
+        dist.all_gather(allb, sbuf, group=group)
+        for donor, recvs in pairs.items():
+            if rank not in recvs:
+                continue
+            arr = allb[donor].cpu().numpy()
+            c = int(arr[-1])
+            rows = arr[:-1].reshape(X, width)[:c]
+            mine = rows[recvs.index(rank)::len(recvs)]
+            if len(mine):
+                pool.import_work(mine[:, :n].astype(np.uint16), mine[:, n:2 * n].astype(np.uint16),
+                                 mine[:, 2 * n].astype(np.uint8))
+                remote += len(mine)
+    st1 = pool.stats()
+    h1 = pool.histogram()
+    # this solve only (the pool's counters are cumulative)
+    st = type(st1)(**{k: (getattr(st1, k) - getattr(st0, k)) if k in _DELTA else getattr(st1, k)
+                      for k in st1.__dataclass_fields__})
+    hist = {f: v - h0.get(f, 0) for f, v in h1.items() if v - h0.get(f, 0)}
+    bsched = pool.best_schedule()
+    if world > 1:
+        vec = torch.tensor([st.unique, st.decomposed, st.leaves, st.improvements, st.local_steals, remote],
+                           dtype=torch.int64, device=device)
+        dist.all_reduce(vec, group=group)
+        hv = torch.zeros(n + 1, dtype=torch.int64, device=device)
+        for f, v in hist.items():
+            hv[f] = v
+        dist.all_reduce(hv, group=group)
+        bv = torch.tensor([pool.best_value(), rank], dtype=torch.int64, device=device)
+        allbv = [torch.zeros_like(bv) for _ in range(world)]
+        dist.all_gather(allbv, bv, group=group)
+        bvals = torch.stack(allbv).cpu().numpy()
+        owner = int(bvals[np.argmin(bvals[:, 0]), 1])
+        pv = torch.tensor(bsched.perm if bsched.perm else [-1] * n, dtype=torch.int64, device=device)
+        dist.broadcast(pv, src=owner, group=group)
+        perm = [int(x) for x in pv.cpu().numpy()]
+        v = vec.cpu().numpy()
+        return DistResult(int(bvals[:, 0].min()), perm if perm[0] >= 0 else [], int(v[0]), int(v[1]), int(v[2]),
+                          int(v[3]), int(v[4]), int(v[5]), rounds, exchanges,
+                          {f: int(x) for f, x in enumerate(hv.cpu().numpy()) if x}, completed)
+    return DistResult(pool.best_value(), bsched.perm, st.unique, st.decomposed, st.leaves, st.improvements,
+                      st.local_steals, 0, rounds, exchanges, hist, completed)

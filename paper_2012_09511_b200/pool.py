@@ -73,6 +73,10 @@ class PoolStats:
     K: int = 0
     group: int = 0
     steps_per_round: int = 0
+    device_ms: float = 0.0
+    kernel_launches: int = 0
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
 
 
 @dataclass
@@ -189,6 +193,31 @@ class GpuPool:
     def assign_split(self, pieces: int = 0) -> None:
         _lib.check(self._lib.pbbgpu_assign_split(self._h, pieces))
 
+    def assign_split_range(self, first: int, count: int, total: int) -> None:
+        _lib.check(self._lib.pbbgpu_assign_split_range(self._h, first, count, total))
+
+    def export_work(self, max_count: int):
+        """Right halves of the longest remaining intervals, as digit arrays (a, b, b_is_nfact)."""
+        n = self.inst.n
+        a = np.zeros((max_count, n), dtype=np.uint16)
+        b = np.zeros((max_count, n), dtype=np.uint16)
+        nf = np.zeros(max_count, dtype=np.uint8)
+        cnt = ctypes.c_int()
+        _lib.check(self._lib.pbbgpu_export(self._h, max_count, a.ctypes.data_as(_u16p), b.ctypes.data_as(_u16p),
+                                           nf.ctypes.data_as(_u8p), ctypes.byref(cnt)))
+        c = cnt.value
+        return a[:c].copy(), b[:c].copy(), nf[:c].copy()
+
+    def import_work(self, a, b, nf) -> None:
+        """Seat digit intervals (e.g. from another GPU's export_work) on idle explorers."""
+        a = np.ascontiguousarray(a, dtype=np.uint16)
+        b = np.ascontiguousarray(b, dtype=np.uint16)
+        nf = np.ascontiguousarray(nf, dtype=np.uint8)
+        if len(nf) == 0:
+            return
+        _lib.check(self._lib.pbbgpu_assign(self._h, a.ctypes.data_as(_u16p), b.ctypes.data_as(_u16p),
+                                           nf.ctypes.data_as(_u8p), len(nf)))
+
     def run_round(self) -> int:
         act = ctypes.c_int()
         _lib.check(self._lib.pbbgpu_run_round(self._h, ctypes.byref(act)))
@@ -292,3 +321,10 @@ def pool_run(inst: Instance, initial_ub: int, intervals: Sequence[Interval] = ()
         d["completed"] = bool(d["completed"])
         sched = Schedule([int(x) for x in perm], int(best.value)) if has.value else Schedule([], -1)
         return PoolResult(sched, int(best.value), PoolStats(**d), pool.histogram())
+
+
+def int32_peak(device: int = 0) -> float:
+    """Measured INT32 add/max throughput of the device (ops/s), the bounding roofline."""
+    v = ctypes.c_double()
+    _lib.check(_lib.load().pbbgpu_int32_peak(device, ctypes.byref(v)))
+    return v.value

@@ -1,0 +1,51 @@
+"""Multi-rank solve on real GPU pools: 2 ranks (gloo plumbing, pools on cuda:rank % ngpu) must
+reproduce the single-GPU fixed-tree counts exactly while exchanging intervals."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from tests import golden_io
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, name, ub, bound, out):
+    import paper_2012_09511_b200 as pbb
+    from paper_2012_09511_b200.multi import solve_distributed
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = rank % torch.cuda.device_count()
+    pool = pbb.GpuPool(pbb.taillard_named(name), pbb.PoolConfig(device=dev, explorers=2048), bound=bound)
+    res = solve_distributed(pool, ub, device="cpu")
+    out[rank] = (res.unique, res.leaves, res.best_value, res.remote_intervals, res.completed, res.hist)
+    pool.close()
+    dist.destroy_process_group()
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("name,ub,bound", [("ta011", 1582, "lb1"), ("ta041", 2991, "lb1"), ("ta011", 1582, "lb2")])
+def test_two_ranks_match_single_gpu_counts(name, ub, bound):
+    gold = golden_io.ref_counts()[f"{name}@{ub}"] if bound == "lb1" else golden_io.lb2_counts()[f"{name}@{ub}"]
+    want = gold["decomposed"] if bound == "lb1" else gold["unique"]
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_worker, args=(2, _port(), name, ub, bound, out), nprocs=2, start_method="spawn", join=True)
+        r0, r1 = out[0], out[1]
+    assert r0[0] == r1[0] == want
+    assert r0[1] == r1[1] == gold["leaves"]
+    assert r0[2] == r1[2] == ub
+    assert r0[4] and r1[4]
+    assert {str(k): v for k, v in r0[5].items()} == gold["hist"]

@@ -1,0 +1,156 @@
+"""Multi-GPU orchestration logic (paper_2012_09511_b200/multi.py) on CPU: world_size 2 over
+gloo with a simulated pool. Every unit of work must be processed exactly once, the incumbent
+must be the global minimum, and idle ranks must receive exported intervals."""
+import os
+import socket
+from dataclasses import dataclass
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2012_09511_b200.multi import solve_distributed
+
+BASE = 1 << 14  # digit radix of the simulated positions (fits the int16 transport)
+
+
+def enc(x):
+    return [(x >> (14 * (3 - i))) & (BASE - 1) for i in range(4)]
+
+
+def dec(d):
+    v = 0
+    for x in d:
+        v = (v << 14) | int(x)
+    return v
+
+
+@dataclass
+class _Inst:
+    n: int = 4
+
+
+@dataclass
+class _Stats:
+    unique: int
+    decomposed: int
+    leaves: int
+    improvements: int
+    local_steals: int
+
+
+class FakePool:
+    """K explorers over integer intervals; a round processes `speed` units per explorer."""
+
+    def __init__(self, K, total, speed, rank, skew):
+        self.inst = _Inst()
+        self.K_, self.total, self.speed, self.rank, self.skew = K, total, speed, rank, skew
+        self.iv = [None] * K
+        self.done = 0
+        self.best = None
+        self.steals = 0
+
+    def K(self):
+        return self.K_
+
+    def set_initial_bound(self, ub):
+        self.best = ub
+
+    def assign_split_range(self, first, count, total):
+        # rank 1 gets a skewed share so that it runs dry first and must receive work
+        for c in range(count):
+            i = first + c
+            a = self.total * i // total
+            b = self.total * (i + 1) // total
+            if self.skew and self.rank == 1:
+                b = a + (b - a) // 50
+                self.done_skip = getattr(self, "done_skip", 0)
+            self.iv[c] = [a, b] if a < b else None
+        self.owned = sum(b - a for a, b in (x for x in self.iv if x))
+
+    def run_round(self):
+        for k in range(self.K_):
+            if self.iv[k]:
+                a, b = self.iv[k]
+                step = min(self.speed, b - a)
+                self.done += step
+                self.iv[k] = [a + step, b] if a + step < b else None
+        if self.best is not None and self.done > 0:
+            self.best = min(self.best, 1000 + 10 * self.rank)  # rank 0 finds the better incumbent
+        return sum(1 for x in self.iv if x)
+
+    def best_value(self):
+        return self.best
+
+    def offer_bound(self, v):
+        self.best = min(self.best, v)
+
+    def export_work(self, m):
+        order = sorted((k for k in range(self.K_) if self.iv[k]), key=lambda k: -(self.iv[k][1] - self.iv[k][0]))
+        a, b, nf = [], [], []
+        for k in order[:m]:
+            lo, hi = self.iv[k]
+            if hi - lo < 2:
+                continue
+            mid = (lo + hi) // 2
+            self.iv[k] = [lo, mid]
+            a.append(enc(mid))
+            b.append(enc(hi))
+            nf.append(0)
+        return (np.array(a, dtype=np.uint16).reshape(-1, 4), np.array(b, dtype=np.uint16).reshape(-1, 4),
+                np.array(nf, dtype=np.uint8))
+
+    def import_work(self, a, b, nf):
+        idle = [k for k in range(self.K_) if not self.iv[k]]
+        assert len(idle) >= len(nf)
+        for i in range(len(nf)):
+            self.iv[idle[i]] = [dec(a[i]), dec(b[i])]
+
+    def stats(self):
+        return _Stats(self.done, self.done, 0, 0, self.steals)
+
+
+    def histogram(self):
+        return {1: self.done}
+
+    def best_schedule(self):
+        class S:
+            perm = [3, 2, 1, 0] if self.rank == 0 else [0, 1, 2, 3]
+        return S()
+
+
+def _worker(rank, world, port, total, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pool = FakePool(K=64, total=total, speed=1000, rank=rank, skew=True)
+    res = solve_distributed(pool, ub=5000, device="cpu")
+    out[rank] = (res.unique, res.best_value, res.remote_intervals, res.best_perm, res.completed, pool.done)
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.timeout(120)
+def test_two_rank_exchange_processes_everything_once():
+    total = 64 * 2 * 200000
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_worker, args=(2, _free_port(), total, out), nprocs=2, start_method="spawn", join=True)
+        r0, r1 = out[0], out[1]
+    # rank 1's skewed share is 1/50 of its range; the rest of its range is never assigned,
+    # so the work actually owned is total/2 + total/100
+    owned = total // 2 + (total // 2) // 50
+    assert r0[0] == r1[0] == owned               # all-reduced unique count
+    assert r0[5] + r1[5] == owned                # processed exactly once
+    assert r1[5] > (total // 2) // 50            # rank 1 received remote work
+    assert r0[2] == r1[2] > 0                    # remote intervals moved
+    assert r0[1] == r1[1] == 1000                # global incumbent
+    assert r0[3] == r1[3] == [3, 2, 1, 0]        # schedule of the owner of the best value
+    assert r0[4] and r1[4]
