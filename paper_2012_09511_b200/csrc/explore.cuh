@@ -37,22 +37,26 @@ __host__ __device__ inline int round_up(int x, int a) { return (x + a - 1) / a *
 
 // Per-CTA shared instance region (identical computation on host and device).
 struct InstLayout {
-  int o_p32, o_pk, o_pl, o_ord, o_lag, o_cnt, o_hist, o_dhist, bytes;
+  int o_p32, o_pk, o_pl, o_ord, o_lag, o_pk32, o_cnt, o_hist, o_dhist, bytes;
 };
 
-__host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs) {
+// packed = warp-per-explorer LB2 (children_lb2_w): one uint32 per (position, pair),
+// transposed [t][q]; otherwise the group LB2 tables (order [q][t], lag [q][j]).
+__host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs, bool packed = false) {
   InstLayout s;
   int o = 0;
   s.o_p32 = o;
   o += n * mp * 4;
   s.o_lag = o;
-  o += round_up(npairs * n * 2, 16);
+  o += packed ? 0 : round_up(npairs * n * 2, 16);
+  s.o_pk32 = o;
+  o += packed ? round_up(npairs * n * 4, 16) : 0;
   s.o_pk = o;
   o += round_up(npairs, 16);
   s.o_pl = o;
   o += round_up(npairs, 16);
   s.o_ord = o;
-  o += round_up(npairs * n, 16);
+  o += packed ? 0 : round_up(npairs * n, 16);
   s.o_cnt = o;
   o += 64;
   s.o_hist = o;
@@ -63,7 +67,7 @@ __host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs) {
   return s;
 }
 
-__host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound) {
+__host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound, int lanes) {
   IvmLayout L;
   L.n = n;
   L.m = m;
@@ -106,9 +110,14 @@ __host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound) {
     L.o_tails = o;
     o += round_up(n * m * 2, 16);
     L.o_lst = o;
-    o += n * 16;
-    L.o_pos = o;
-    o += round_up(n, 16);
+    if (lanes == 32) {
+      o += round_up(2 * n * 32 * 2, 16);  // int16 PM[j][lane], SM[j][lane]
+      L.o_pos = 0;
+    } else {
+      o += n * 16;
+      L.o_pos = o;
+      o += round_up(n, 16);
+    }
   } else {
     L.o_heads = L.o_tails = L.o_lst = L.o_pos = 0;
   }
@@ -181,6 +190,8 @@ struct IvmView {
   uint16_t* tails;
   int4* lst;
   uint8_t* pos;
+  int16_t* pm;
+  int16_t* sm;
   __device__ __forceinline__ IvmView(unsigned char* b, const IvmLayout& L) {
     hdr = reinterpret_cast<IvmHdr*>(b);
     cells = reinterpret_cast<int8_t*>(b + L.o_cells);
@@ -202,6 +213,8 @@ struct IvmView {
     tails = reinterpret_cast<uint16_t*>(b + L.o_tails);
     lst = reinterpret_cast<int4*>(b + L.o_lst);
     pos = b + L.o_pos;
+    pm = reinterpret_cast<int16_t*>(b + L.o_lst);
+    sm = pm + L.n * 32;
   }
 };
 
@@ -211,6 +224,7 @@ struct InstView {
   const uint8_t* pl;
   const uint8_t* ord;
   const uint16_t* lag;
+  const uint32_t* packed;  // [n][npairs]: job | a << 6 | b << 13 | lag << 20
   int npairs;
 };
 
@@ -333,6 +347,111 @@ __device__ __forceinline__ void children_lb2(const Group<G>& grp, const IvmView&
       *dst = max(*dst, v);
     }
     grp.sync();
+  }
+}
+
+// LB2, warp per explorer, lanes over machine pairs, exact max-plus prefix/suffix form.
+// For one pair (k,l) and the node's free jobs s_1..s_f in that pair's Johnson order the
+// chain of row a22 unrolls to
+//   t1 = max(r_l + B, r_k + max_i X_i),  X_i = A_{<=i} + lag_i + B_{>=i}
+// (A, B: sums of p[.][k], p[.][l]); a child that removes s_i = j keeps the X terms before
+// i reduced by b_j and those after i reduced by a_j, so with PM_j = max_{i'<i} X_i',
+// SM_j = max_{i'>i} X_i' (one forward and one backward pass per pair):
+//   t0 = r_k + A - a_j,  t1 = max(r_l + B - b_j, r_k + max(PM_j - b_j, SM_j - a_j))
+//   lb_kl(child) = max(t0 + q_k, t1 + q_l)
+// Integer-exact, identical values to the per-child chains, O(P (n + f)) per node instead of
+// O(P f^2). Each lane owns a pair (32 pairs per round); per child the 32 pair bounds are
+// combined with one REDUX.MAX (__reduce_max_sync).
+template <int M>
+__device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView& in, int n, int mp, int f,
+                                               unsigned long long fmask) {
+  constexpr unsigned FULL = 0xffffffffu;
+  constexpr int NEG = -30000;
+  const int lane = threadIdx.x & 31;
+  for (int c = lane; c < f; c += 32) {
+    const int j = iv.freej[c];
+    const int* pr = in.p32 + j * mp;
+    int prev = 0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      prev = max(prev, iv.fr[k]) + pr[k];
+      iv.heads[c * M + k] = static_cast<uint16_t>(prev);
+    }
+    prev = 0;
+#pragma unroll
+    for (int k = M - 1; k >= 0; --k) {
+      prev = max(prev, iv.tl[k]) + pr[k];
+      iv.tails[c * M + k] = static_cast<uint16_t>(prev);
+    }
+  }
+  __syncwarp();
+  int accF0 = 0, accF1 = 0, accB0 = 0, accB1 = 0;
+  const int P = in.npairs;
+  int16_t* PMl = iv.pm + lane;
+  int16_t* SMl = iv.sm + lane;
+  for (int q0 = 0; q0 < P; q0 += 32) {
+    const int q = q0 + lane;
+    const bool live = q < P;
+    const int k = live ? in.pk[q] : 0, l = live ? in.pl[q] : 0;
+    const int Atot = iv.rm[k], Btot = iv.rm[l];
+    if (live) {
+      int A = 0, Bp = 0, pm = NEG;
+      for (int t = 0; t < n; ++t) {
+        const unsigned e = in.packed[t * P + q];
+        const int j = e & 63;
+        if ((fmask >> j) & 1ull) {
+          A += (e >> 6) & 127;
+          const int X = A + static_cast<int>(e >> 20) - Bp;
+          PMl[j * 32] = static_cast<int16_t>(pm);
+          pm = max(pm, X);
+          Bp += (e >> 13) & 127;
+        }
+      }
+      int As = 0, Bs = Atot - Btot, sm = NEG;  // Bs = B_{>=i} + (A - B)
+      for (int t = n - 1; t >= 0; --t) {
+        const unsigned e = in.packed[t * P + q];
+        const int j = e & 63;
+        if ((fmask >> j) & 1ull) {
+          Bs += (e >> 13) & 127;
+          // X'_i = A_{<=i} + lag_i - B_{<i} = (Atot - As) + lag_i + (B_{>=i} - Btot)
+          const int X = static_cast<int>(e >> 20) + Bs - As;
+          SMl[j * 32] = static_cast<int16_t>(sm);
+          sm = max(sm, X);
+          As += (e >> 6) & 127;
+        }
+      }
+    }
+    const int qk = iv.tl[k], ql = iv.tl[l], rk = iv.fr[k], rl = iv.fr[l];
+    for (int c = 0; c < f; ++c) {
+      const int j = iv.freej[c];
+      int vF = 0, vB = 0;
+      if (live) {
+        const int a = in.p32[j * mp + k], b = in.p32[j * mp + l];
+        const int inner = max(PMl[j * 32] - b, SMl[j * 32] - a) + Btot;
+        const int hk = iv.heads[c * M + k], hl = iv.heads[c * M + l];
+        vF = max(hk + Atot - a + qk, max(hl + Btot - b, hk + inner) + ql);
+        vB = max(rk + Atot - a + iv.tails[c * M + k], max(rl + Btot - b, rk + inner) + iv.tails[c * M + l]);
+      }
+      vF = __reduce_max_sync(FULL, vF);
+      vB = __reduce_max_sync(FULL, vB);
+      if (lane == (c & 31)) {
+        if (c < 32) {
+          accF0 = max(accF0, vF);
+          accB0 = max(accB0, vB);
+        } else {
+          accF1 = max(accF1, vF);
+          accB1 = max(accB1, vB);
+        }
+      }
+    }
+  }
+  if (lane < f) {
+    iv.lbf[lane] = accF0;
+    iv.lbb[lane] = accB0;
+  }
+  if (lane + 32 < f) {
+    iv.lbf[lane + 32] = accF1;
+    iv.lbb[lane + 32] = accB1;
   }
 }
 
@@ -498,8 +617,10 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
   node_tables<M, G>(grp, iv, in, n, mp, job, dI, d1, d2);
   const unsigned long long fm = grp.ror64(gather_free<G>(grp, iv, row, sel, f));
   grp.sync();
-  if (BOUND == kLB1) {
+  if constexpr (BOUND == kLB1) {
     children_lb1<M, G>(grp, iv, in, mp, f);
+  } else if constexpr (G == 32) {
+    children_lb2_w<M>(iv, in, n, mp, f, fm);
   } else {
     children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
   }
@@ -592,13 +713,21 @@ __global__ void __launch_bounds__(128) explore_kernel(const ExploreParams P) {
   const IvmLayout& L = P.L;
   const int n = L.n, mp = L.mp;
   constexpr int NG = 128 / G;
-  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? P.npairs : 0);
+  constexpr bool PACKED = BOUND == kLB2 && G == 32;
+  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? P.npairs : 0, PACKED);
 
   // ---- stage the instance (and LB2 pair tables) into shared memory
   {
     int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = P.p32[i];
-    if (BOUND == kLB2) {
+    if (PACKED) {
+      uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
+      for (int i = threadIdx.x; i < P.npairs * n; i += blockDim.x) sk[i] = P.packed[i];
+      for (int i = threadIdx.x; i < P.npairs; i += blockDim.x) {
+        smem[IL.o_pk + i] = P.pk[i];
+        smem[IL.o_pl + i] = P.pl[i];
+      }
+    } else if (BOUND == kLB2) {
       uint16_t* sl = reinterpret_cast<uint16_t*>(smem + IL.o_lag);
       for (int i = threadIdx.x; i < P.npairs * n; i += blockDim.x) {
         sl[i] = P.lag[i];
@@ -636,6 +765,7 @@ __global__ void __launch_bounds__(128) explore_kernel(const ExploreParams P) {
   in.pl = smem + IL.o_pl;
   in.ord = smem + IL.o_ord;
   in.lag = reinterpret_cast<const uint16_t*>(smem + IL.o_lag);
+  in.packed = reinterpret_cast<const uint32_t*>(smem + IL.o_pk32);
   in.npairs = P.npairs;
   unsigned* shist = reinterpret_cast<unsigned*>(smem + IL.o_hist);
   unsigned* sdhist = reinterpret_cast<unsigned*>(smem + IL.o_dhist);
@@ -756,6 +886,7 @@ struct BatchParams {
   const uint8_t* pl;
   const uint8_t* order;
   const uint16_t* lag;
+  const uint32_t* packed;
   int* child_lb;   // [count*n]
   int* lb_fwd;     // [count*n] both sets (before MinMin), for the parity tests
   int* lb_bwd;
@@ -769,11 +900,19 @@ __global__ void __launch_bounds__(128) decompose_batch_kernel(const BatchParams 
   const IvmLayout& L = B.L;
   const int n = L.n, mp = L.mp;
   constexpr int NG = 128 / G;
-  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? B.npairs : 0);
+  constexpr bool PACKED = BOUND == kLB2 && G == 32;
+  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? B.npairs : 0, PACKED);
   {
     int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
-    if (BOUND == kLB2) {
+    if (PACKED) {
+      uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
+      for (int i = threadIdx.x; i < B.npairs * n; i += blockDim.x) sk[i] = B.packed[i];
+      for (int i = threadIdx.x; i < B.npairs; i += blockDim.x) {
+        smem[IL.o_pk + i] = B.pk[i];
+        smem[IL.o_pl + i] = B.pl[i];
+      }
+    } else if (BOUND == kLB2) {
       uint16_t* sl = reinterpret_cast<uint16_t*>(smem + IL.o_lag);
       for (int i = threadIdx.x; i < B.npairs * n; i += blockDim.x) {
         sl[i] = B.lag[i];
@@ -792,6 +931,7 @@ __global__ void __launch_bounds__(128) decompose_batch_kernel(const BatchParams 
   in.pl = smem + IL.o_pl;
   in.ord = smem + IL.o_ord;
   in.lag = reinterpret_cast<const uint16_t*>(smem + IL.o_lag);
+  in.packed = reinterpret_cast<const uint32_t*>(smem + IL.o_pk32);
   in.npairs = B.npairs;
   Group<G> grp;
   const int gi = threadIdx.x / G;
@@ -835,7 +975,8 @@ __global__ void __launch_bounds__(128) decompose_batch_kernel(const BatchParams 
     }
     fm = grp.ror64(fm);
     grp.sync();
-    if (BOUND == kLB1) children_lb1<M, G>(grp, iv, in, mp, f);
+    if constexpr (BOUND == kLB1) children_lb1<M, G>(grp, iv, in, mp, f);
+    else if constexpr (G == 32) children_lb2_w<M>(iv, in, n, mp, f, fm);
     else children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
     grp.sync();
     const int dir = minmin<G>(grp, iv, f);

@@ -152,7 +152,8 @@ int64_t neh_host(int n, int m, const int32_t* p, int32_t* out) {
 // lexicographic; lag_j = sum_{k<i<l} p[j][i]; J1 = {a<b} ascending a+lag, then J2
 // descending b+lag, ties by ascending job.
 void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::vector<uint8_t>& pl,
-                std::vector<uint8_t>& ord, std::vector<uint16_t>& lag) {
+                std::vector<uint8_t>& ord, std::vector<uint16_t>& lag, std::vector<uint32_t>& packed,
+                bool& packable) {
   const int P = m * (m - 1) / 2;
   pk.resize(static_cast<size_t>(P));
   pl.resize(static_cast<size_t>(P));
@@ -183,6 +184,20 @@ void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::v
         return x < y;
       });
       for (int t = 0; t < n; ++t) ord[static_cast<size_t>(q) * n + t] = static_cast<uint8_t>(idx[static_cast<size_t>(t)]);
+    }
+  }
+  // transposed packed form [t][q] = job | a << 6 | b << 13 | lag << 20 (children_lb2_w)
+  packed.assign(static_cast<size_t>(P) * n, 0);
+  packable = n <= 64;
+  for (int qq = 0; qq < P; ++qq) {
+    for (int t = 0; t < n; ++t) {
+      const int j = ord[static_cast<size_t>(qq) * n + t];
+      const int a = p[static_cast<size_t>(j) * m + pk[static_cast<size_t>(qq)]];
+      const int b = p[static_cast<size_t>(j) * m + pl[static_cast<size_t>(qq)]];
+      const int lg = lag[static_cast<size_t>(qq) * n + j];
+      if (a > 127 || b > 127 || lg > 2047) packable = false;
+      packed[static_cast<size_t>(t) * P + qq] =
+          static_cast<uint32_t>(j) | static_cast<uint32_t>(a) << 6 | static_cast<uint32_t>(b) << 13 | static_cast<uint32_t>(lg) << 20;
     }
   }
 }
@@ -609,6 +624,7 @@ struct pbbgpu_pool {
   int *d_p32 = nullptr, *d_ptot = nullptr, *d_wrk = nullptr;
   uint8_t *d_pk = nullptr, *d_pl = nullptr, *d_ord = nullptr;
   uint16_t* d_lag = nullptr;
+  uint32_t* d_packed = nullptr;
   float* d_lgfact = nullptr;
   DevCounters* d_ctr = nullptr;
   DevCounters* h_ctr = nullptr;  // pinned
@@ -636,6 +652,7 @@ struct pbbgpu_pool {
     cudaFree(d_pl);
     cudaFree(d_ord);
     cudaFree(d_lag);
+    cudaFree(d_packed);
     cudaFree(d_lgfact);
     cudaFree(d_ctr);
     cudaFree(d_hist);
@@ -660,7 +677,7 @@ void xfer(pbbgpu_pool* P, void* dst, const void* src, size_t bytes, cudaMemcpyKi
 
 int pick_group(int n, int bound) {
   if (bound == kLB1) return n <= 24 ? 4 : 8;
-  return n <= 24 ? 8 : 16;
+  return 32;  // warp per explorer, lanes over machine pairs (children_lb2_w)
 }
 
 void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const pbbgpu_config_t* cfg) {
@@ -688,24 +705,32 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   ck(cudaEventCreate(&P->ev0), "event");
   ck(cudaEventCreate(&P->ev1), "event");
 
-  P->L = ivm_layout(n, m, bound);
-  P->mp = P->L.mp;
   std::vector<uint8_t> pk, pl, ord;
   std::vector<uint16_t> lag;
+  std::vector<uint32_t> packed;
+  bool packable = false;
   if (bound == kLB2) {
-    lb2_tables(n, m, p, pk, pl, ord, lag);
+    lb2_tables(n, m, p, pk, pl, ord, lag, packed, packable);
     P->npairs = m * (m - 1) / 2;
   }
-  P->IL = inst_layout(n, P->mp, P->npairs);
   P->G = P->cfg.group > 0 ? P->cfg.group : pick_group(n, bound);
   if (P->G != 4 && P->G != 8 && P->G != 16 && P->G != 32) throw std::invalid_argument("pbbgpu: group must be 4, 8, 16 or 32");
-  const int NG = 128 / P->G;
-  P->smem = static_cast<size_t>(P->IL.bytes) + static_cast<size_t>(NG) * P->L.sstride;
-  while (P->smem > 227 * 1024 && P->G < 32) {
+  if (bound == kLB2 && P->G == 32 && !packable) P->G = 16;  // packed (a, b, lag) do not fit 31 bits
+  auto size_for = [&](int G) {
+    const IvmLayout L = ivm_layout(n, m, bound, G);
+    const InstLayout IL = inst_layout(n, L.mp, P->npairs, bound == kLB2 && G == 32);
+    return std::make_pair(static_cast<size_t>(IL.bytes) + static_cast<size_t>(128 / G) * L.sstride, std::make_pair(L, IL));
+  };
+  auto sz = size_for(P->G);
+  while (sz.first > 227 * 1024 && P->G < 16) {
     P->G *= 2;
-    P->smem = static_cast<size_t>(P->IL.bytes) + static_cast<size_t>(128 / P->G) * P->L.sstride;
+    sz = size_for(P->G);
   }
-  if (P->smem > 227 * 1024) throw CapacityError("pbbgpu: explorer state exceeds shared memory");
+  if (sz.first > 227 * 1024) throw CapacityError("pbbgpu: explorer state exceeds shared memory");
+  P->smem = sz.first;
+  P->L = sz.second.first;
+  P->IL = sz.second.second;
+  P->mp = P->L.mp;
   P->efn = explore_fn(m, bound, P->G);
   P->bfn = batch_fn(m, bound, P->G);
   ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->efn), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
@@ -754,6 +779,8 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
     xfer(P, P->d_pl, pl.data(), pl.size(), cudaMemcpyHostToDevice, "copy");
     xfer(P, P->d_ord, ord.data(), ord.size(), cudaMemcpyHostToDevice, "copy");
     xfer(P, P->d_lag, lag.data(), lag.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, "copy");
+    ck(cudaMalloc(&P->d_packed, packed.size() * sizeof(uint32_t)), "malloc");
+    xfer(P, P->d_packed, packed.data(), packed.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, "copy");
   }
   DevCounters z{};
   z.best = INT_MAX;
@@ -811,6 +838,7 @@ ExploreParams explore_params(pbbgpu_pool* P) {
   E.pl = P->d_pl;
   E.order = P->d_ord;
   E.lag = P->d_lag;
+  E.packed = P->d_packed;
   E.ctr = P->d_ctr;
   E.hist = P->d_hist;
   E.dhist = P->d_dhist;
@@ -1302,6 +1330,7 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
     B.pl = P->d_pl;
     B.order = P->d_ord;
     B.lag = P->d_lag;
+    B.packed = P->d_packed;
     B.child_lb = dlb;
     B.lb_fwd = dlf;
     B.lb_bwd = dlbw;

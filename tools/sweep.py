@@ -1,0 +1,22 @@
+"""Config sweep (development tool): time-to-proof for a few pool configurations."""
+import json
+import sys
+import time
+
+sys.path.insert(0, ".")
+import paper_2012_09511_b200 as pbb
+
+name, ub, bound = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+inst = pbb.taillard_named(name)
+for spec in sys.argv[4:]:
+    kw = dict(kv.split("=") for kv in spec.split(",")) if spec != "default" else {}
+    cfg = pbb.PoolConfig(**{k: int(v) for k, v in kw.items()})
+    with pbb.GpuPool(inst, cfg, bound=bound) as pool:
+        from paper_2012_09511_b200.multi import solve_distributed
+        solve_distributed(pool, ub)  # warm
+        t0 = time.time()
+        r = solve_distributed(pool, ub)
+        dt = time.time() - t0
+        st = pool.stats()
+    print(json.dumps({"cfg": spec, "K": st.K, "G": st.group, "unique": r.unique, "s": round(dt, 4),
+                      "Mnodes_s": round(r.unique / dt / 1e6, 2), "rounds": r.rounds, "steals": r.local_steals}), flush=True)
