@@ -63,6 +63,7 @@ typedef struct {
   double time_limit_s;   /* pbbgpu_solve only; 0 = none */
   double min_steal_log2; /* log2 of the minimal stolen interval length; 0 = log2(8!) */
   int device;            /* CUDA device ordinal */
+  int block;             /* threads per CTA (128, 256, 512); 0 = auto */
 } pbbgpu_config_t;
 
 typedef struct {
@@ -86,6 +87,7 @@ typedef struct {
   uint64_t kernel_launches;     /* kernels launched by the pool so far (explore + steal + init) */
   uint64_t h2d_bytes;           /* host->device bytes copied by the pool so far */
   uint64_t d2h_bytes;           /* device->host bytes copied by the pool so far */
+  int block;                    /* threads per CTA of the explore kernel */
 } pbbgpu_stats_t;
 
 const char* pbbgpu_last_error(void);

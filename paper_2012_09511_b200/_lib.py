@@ -40,6 +40,7 @@ class Config(ctypes.Structure):
         ("time_limit_s", ctypes.c_double),
         ("min_steal_log2", ctypes.c_double),
         ("device", ctypes.c_int),
+        ("block", ctypes.c_int),
     ]
 
 
@@ -65,6 +66,7 @@ class Stats(ctypes.Structure):
         ("kernel_launches", ctypes.c_uint64),
         ("h2d_bytes", ctypes.c_uint64),
         ("d2h_bytes", ctypes.c_uint64),
+        ("block", ctypes.c_int),
     ]
 
     def as_dict(self) -> dict:

@@ -708,11 +708,11 @@ __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, con
 }
 
 template <int M, int G, int BOUND>
-__global__ void __launch_bounds__(128) explore_kernel(const ExploreParams P) {
+__global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = P.L;
   const int n = L.n, mp = L.mp;
-  constexpr int NG = 128 / G;
+  const int NG = blockDim.x / G;  // explorers per CTA
   constexpr bool PACKED = BOUND == kLB2 && G == 32;
   const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? P.npairs : 0, PACKED);
 
@@ -895,11 +895,11 @@ struct BatchParams {
 };
 
 template <int M, int G, int BOUND>
-__global__ void __launch_bounds__(128) decompose_batch_kernel(const BatchParams B) {
+__global__ void __launch_bounds__(512) decompose_batch_kernel(const BatchParams B) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = B.L;
   const int n = L.n, mp = L.mp;
-  constexpr int NG = 128 / G;
+  const int NG = blockDim.x / G;
   constexpr bool PACKED = BOUND == kLB2 && G == 32;
   const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? B.npairs : 0, PACKED);
   {

@@ -611,7 +611,7 @@ struct pbbgpu_pool {
   int n = 0, m = 0, mp = 0, bound = 0;
   pbbgpu_config_t cfg{};
   std::vector<int32_t> p;
-  int K = 0, G = 0, steps = 0, grid = 0;
+  int K = 0, G = 0, steps = 0, grid = 0, block = 128;
   size_t smem = 0;
   IvmLayout L{};
   InstLayout IL{};
@@ -676,7 +676,7 @@ void xfer(pbbgpu_pool* P, void* dst, const void* src, size_t bytes, cudaMemcpyKi
 }
 
 int pick_group(int n, int bound) {
-  if (bound == kLB1) return n <= 24 ? 4 : 8;
+  if (bound == kLB1) return 16;
   return 32;  // warp per explorer, lanes over machine pairs (children_lb2_w)
 }
 
@@ -716,17 +716,35 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   P->G = P->cfg.group > 0 ? P->cfg.group : pick_group(n, bound);
   if (P->G != 4 && P->G != 8 && P->G != 16 && P->G != 32) throw std::invalid_argument("pbbgpu: group must be 4, 8, 16 or 32");
   if (bound == kLB2 && P->G == 32 && !packable) P->G = 16;  // packed (a, b, lag) do not fit 31 bits
-  auto size_for = [&](int G) {
+  // CTA size: the instance tables are staged once per CTA, so larger CTAs amortize them;
+  // pick the block size that keeps the most explorers resident per SM.
+  auto size_for = [&](int G, int BS) {
     const IvmLayout L = ivm_layout(n, m, bound, G);
     const InstLayout IL = inst_layout(n, L.mp, P->npairs, bound == kLB2 && G == 32);
-    return std::make_pair(static_cast<size_t>(IL.bytes) + static_cast<size_t>(128 / G) * L.sstride, std::make_pair(L, IL));
+    return std::make_pair(static_cast<size_t>(IL.bytes) + static_cast<size_t>(BS / G) * L.sstride, std::make_pair(L, IL));
   };
-  auto sz = size_for(P->G);
-  while (sz.first > 227 * 1024 && P->G < 16) {
+  const size_t smem_cap = static_cast<size_t>(prop.sharedMemPerBlockOptin);
+  const size_t smem_sm = static_cast<size_t>(prop.sharedMemPerMultiprocessor);
+  int best_bs = 0;
+  long best_res = -1;
+  for (;;) {
+    for (int BS : {128, 256, 512}) {
+      const size_t need = size_for(P->G, BS).first;
+      if (need > smem_cap) continue;
+      const long ctas = std::min<long>({static_cast<long>(smem_sm / (need + 1024)), 2048L / BS, 32L});
+      const long res = ctas * (BS / P->G);
+      if (res > best_res) {
+        best_res = res;
+        best_bs = BS;
+      }
+    }
+    if (best_bs || P->G >= 32) break;
     P->G *= 2;
-    sz = size_for(P->G);
   }
-  if (sz.first > 227 * 1024) throw CapacityError("pbbgpu: explorer state exceeds shared memory");
+  if (!best_bs) throw CapacityError("pbbgpu: explorer state exceeds shared memory");
+  if (P->cfg.block > 0) best_bs = P->cfg.block;
+  P->block = best_bs;
+  const auto sz = size_for(P->G, P->block);
   P->smem = sz.first;
   P->L = sz.second.first;
   P->IL = sz.second.second;
@@ -736,16 +754,16 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->efn), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
   ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->bfn), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
   int per_sm = 0;
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(P->efn), 128, P->smem), "occupancy");
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(P->efn), P->block, P->smem), "occupancy");
   if (per_sm < 1) throw CapacityError("pbbgpu: explore kernel cannot be resident");
-  const int NGb = 128 / P->G;
+  const int NGb = P->block / P->G;
   if (P->cfg.explorers > 0) {
     P->K = P->cfg.explorers;
   } else {
     P->K = per_sm * prop.multiProcessorCount * NGb;
   }
   P->grid = (P->K + NGb - 1) / NGb;
-  P->steps = P->cfg.steps_per_round > 0 ? P->cfg.steps_per_round : (bound == kLB1 ? 4096 : 256);
+  P->steps = P->cfg.steps_per_round > 0 ? P->cfg.steps_per_round : (bound == kLB1 ? 4096 : 64);
 
   // device buffers
   const int mp = P->mp;
@@ -908,7 +926,7 @@ int run_round(pbbgpu_pool* P) {
   ExploreParams E = explore_params(P);
   if (P->cfg.pinned) E.pinned_ub = static_cast<int>(std::min<int64_t>(P->pinned_ub, INT_MAX));
   ck(cudaEventRecord(P->ev0, P->stream), "event");
-  P->efn<<<P->grid, 128, P->smem, P->stream>>>(E);
+  P->efn<<<P->grid, P->block, P->smem, P->stream>>>(E);
   ck(cudaGetLastError(), "explore_kernel launch");
   ck(cudaEventRecord(P->ev1, P->stream), "event");
   StealParams S{};
@@ -1269,6 +1287,7 @@ int pbbgpu_stats(pbbgpu_pool* P, pbbgpu_stats_t* out) {
     out->completed = P->last_active == 0;
     out->K = P->K;
     out->group = P->G;
+    out->block = P->block;
     out->steps_per_round = P->steps;
     out->kernel_launches = P->launches;
     out->h2d_bytes = P->h2d_bytes;
@@ -1336,9 +1355,9 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
     B.lb_bwd = dlbw;
     B.dir = ddir;
     B.pruned = dpr;
-    const int NG = 128 / P->G;
+    const int NG = P->block / P->G;
     const int grid = std::min((count + NG - 1) / NG, 148 * 8);
-    P->bfn<<<grid, 128, P->smem, P->stream>>>(B);
+    P->bfn<<<grid, P->block, P->smem, P->stream>>>(B);
     ck(cudaGetLastError(), "decompose_batch launch");
     ck(cudaStreamSynchronize(P->stream), "sync");
     std::vector<int> lb(cn), lf(cn), lbw(cn);

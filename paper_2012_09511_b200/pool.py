@@ -41,6 +41,7 @@ class PoolConfig:
     time_limit_s: float = 0.0
     min_steal_len: int = 0      # 0 = 8!
     device: int = 0
+    block: int = 0              # threads per CTA; 0 = auto
 
     def to_c(self) -> _lib.Config:
         c = _lib.Config()
@@ -52,6 +53,7 @@ class PoolConfig:
         c.time_limit_s = self.time_limit_s
         c.min_steal_log2 = float(np.log2(self.min_steal_len)) if self.min_steal_len > 1 else 0.0
         c.device = self.device
+        c.block = self.block
         return c
 
 
@@ -77,6 +79,7 @@ class PoolStats:
     kernel_launches: int = 0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    block: int = 0
 
 
 @dataclass
