@@ -64,6 +64,7 @@ typedef struct {
   double min_steal_log2; /* log2 of the minimal stolen interval length; 0 = log2(8!) */
   int device;            /* CUDA device ordinal */
   int block;             /* threads per CTA (128, 256, 512); 0 = auto */
+  double round_us;       /* device time per round; 0 = auto (2000 us, or steps_per_round if set) */
 } pbbgpu_config_t;
 
 typedef struct {

@@ -41,6 +41,7 @@ class Config(ctypes.Structure):
         ("min_steal_log2", ctypes.c_double),
         ("device", ctypes.c_int),
         ("block", ctypes.c_int),
+        ("round_us", ctypes.c_double),
     ]
 
 

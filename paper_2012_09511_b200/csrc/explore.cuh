@@ -599,7 +599,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
 }
 
 struct StepCounters {
-  unsigned int decomposed, leaves, dups, improvements, steps;
+  unsigned int decomposed, leaves, dups, improvements, steps, steals;
 };
 
 // Decompose the node at (level, sel) and branch (bound.cpp:98-139 + ivm.cpp:124-145).
@@ -707,6 +707,12 @@ __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, con
   grp.sync();
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int M, int G, int BOUND>
 __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -772,15 +778,21 @@ __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
 
   Group<G> grp;
   const int gi = threadIdx.x / G;
-  StepCounters sc = {0, 0, 0, 0, 0};
+  StepCounters sc = {0, 0, 0, 0, 0, 0};
   if (first + gi < P.K) {
     IvmView iv(ivbase + gi * L.sstride, L);
     int level = iv.hdr->level, state = iv.hdr->state, d1 = iv.hdr->d1, d2 = iv.hdr->d2;
     int rlev = iv.hdr->rlev, nrep = iv.hdr->nrep;
     const bool has_end = iv.hdr->has_end != 0;
     int best = *reinterpret_cast<volatile int*>(&P.ctr->best);
-    for (int step = 0; step < P.steps && state != kEmpty; ++step) {
+    int step = 0;
+    unsigned long long t_end = ~0ull;
+    if (P.budget_ns) t_end = globaltimer_ns() + P.budget_ns;
+    while (step < P.steps) {
+      if (P.budget_ns && (step & 3) == 0 && globaltimer_ns() >= t_end) break;
+      if (state == kEmpty) break;
       if ((step & 15) == 15) best = *reinterpret_cast<volatile int*>(&P.ctr->best);
+      ++step;
       const int prune = P.prune_mode == 0 ? best : (P.prune_mode == 1 ? P.pinned_ub : INT_MAX);
       const int improve = P.prune_mode == 1 ? 0 : best;
       ++sc.steps;
@@ -842,6 +854,7 @@ __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
       atomicAdd(&cnt[2], sc.dups);
       atomicAdd(&cnt[3], sc.improvements);
       atomicAdd(&cnt[4], sc.steps);
+      atomicAdd(&cnt[5], sc.steals);
     }
   }
   __syncthreads();
@@ -862,6 +875,10 @@ __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
       if (cnt[2]) atomicAdd(&P.ctr->dups, static_cast<unsigned long long>(cnt[2]));
       if (cnt[3]) atomicAdd(&P.ctr->improvements, static_cast<unsigned long long>(cnt[3]));
       if (cnt[4]) atomicAdd(&P.ctr->steps, static_cast<unsigned long long>(cnt[4]));
+      if (cnt[5]) {
+        atomicAdd(&P.ctr->steals, static_cast<unsigned long long>(cnt[5]));
+        atomicAdd(&P.ctr->inits, static_cast<unsigned long long>(cnt[5]));
+      }
     }
     for (int i = threadIdx.x; i <= n; i += blockDim.x) {
       if (shist[i]) atomicAdd(&P.hist[i], static_cast<unsigned long long>(shist[i]));

@@ -85,6 +85,7 @@ struct ExploreParams {
   unsigned long long* dhist;  // [n+1] replay duplicates by free-job count
   ImpRecord* imp;             // [kImpCap]
   int smem_inst_bytes;        // bytes of the per-CTA instance region
+  unsigned long long budget_ns;  // round length in device time (0 = steps only)
 };
 
 }  // namespace pbbgpu

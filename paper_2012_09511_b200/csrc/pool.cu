@@ -612,6 +612,7 @@ struct pbbgpu_pool {
   pbbgpu_config_t cfg{};
   std::vector<int32_t> p;
   int K = 0, G = 0, steps = 0, grid = 0, block = 128;
+  double round_us = 0;
   size_t smem = 0;
   IvmLayout L{};
   InstLayout IL{};
@@ -625,6 +626,7 @@ struct pbbgpu_pool {
   uint8_t *d_pk = nullptr, *d_pl = nullptr, *d_ord = nullptr;
   uint16_t* d_lag = nullptr;
   uint32_t* d_packed = nullptr;
+
   float* d_lgfact = nullptr;
   DevCounters* d_ctr = nullptr;
   DevCounters* h_ctr = nullptr;  // pinned
@@ -653,6 +655,7 @@ struct pbbgpu_pool {
     cudaFree(d_ord);
     cudaFree(d_lag);
     cudaFree(d_packed);
+
     cudaFree(d_lgfact);
     cudaFree(d_ctr);
     cudaFree(d_hist);
@@ -763,7 +766,8 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
     P->K = per_sm * prop.multiProcessorCount * NGb;
   }
   P->grid = (P->K + NGb - 1) / NGb;
-  P->steps = P->cfg.steps_per_round > 0 ? P->cfg.steps_per_round : (bound == kLB1 ? 4096 : 64);
+  P->steps = P->cfg.steps_per_round > 0 ? P->cfg.steps_per_round : (1 << 30);
+  P->round_us = P->cfg.round_us > 0 ? P->cfg.round_us : (P->cfg.steps_per_round > 0 ? 0.0 : 2000.0);
 
   // device buffers
   const int mp = P->mp;
@@ -785,6 +789,7 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   ck(cudaMalloc(&P->d_hist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
   ck(cudaMalloc(&P->d_dhist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
   ck(cudaMalloc(&P->d_imp, kImpCap * sizeof(ImpRecord)), "malloc");
+
   xfer(P, P->d_p32, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
   xfer(P, P->d_ptot, ptot.data(), ptot.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
   xfer(P, P->d_lgfact, lgf.data(), lgf.size() * sizeof(float), cudaMemcpyHostToDevice, "copy");
@@ -862,6 +867,7 @@ ExploreParams explore_params(pbbgpu_pool* P) {
   E.dhist = P->d_dhist;
   E.imp = P->d_imp;
   E.smem_inst_bytes = P->IL.bytes;
+  E.budget_ns = static_cast<unsigned long long>(P->round_us * 1000.0);
   return E;
 }
 
@@ -1233,15 +1239,32 @@ int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_n
       const unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
       const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
       if (h->state == kEmpty) continue;
-      if (c >= cap) throw CapacityError("snapshot buffer too small");
       const int8_t* V = reinterpret_cast<const int8_t*>(blk + P->L.o_v);
       const int8_t* E = reinterpret_cast<const int8_t*>(blk + P->L.o_end);
       const int8_t* T = reinterpret_cast<const int8_t*>(blk + P->L.o_tgt);
+      const int8_t* C = reinterpret_cast<const int8_t*>(blk + P->L.o_cells);
+      std::vector<int> pv(static_cast<size_t>(n));
+      for (int l = 0; l < n; ++l) pv[static_cast<size_t>(l)] = h->state == kInit ? T[l] : (l <= h->level ? V[l] : 0);
+      // an explorer parked on an evaluated leaf (consumed cell of the leaf row) has already
+      // covered `position`: the remaining work starts at position + 1
+      bool past_end = false;
+      if (h->state == kActive && h->level == n - 2 && C[tri_off(n - 2, n) + V[n - 2]] < 0) {
+        int l = n - 1;
+        for (; l >= 0; --l) {
+          if (++pv[static_cast<size_t>(l)] <= n - 1 - l) break;
+          pv[static_cast<size_t>(l)] = 0;
+        }
+        past_end = l < 0;
+      }
+      if (!past_end && h->has_end) {
+        int cmp = 0;
+        for (int l = 0; l < n && !cmp; ++l) cmp = pv[static_cast<size_t>(l)] < E[l] ? -1 : (pv[static_cast<size_t>(l)] > E[l] ? 1 : 0);
+        past_end = cmp >= 0;
+      }
+      if (past_end) continue;
+      if (c >= cap) throw CapacityError("snapshot buffer too small");
       for (int l = 0; l < n; ++l) {
-        int pv;
-        if (h->state == kInit) pv = T[l];  // not yet positioned: [target, end)
-        else pv = l <= h->level ? V[l] : 0;
-        pos[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(pv);
+        pos[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(pv[static_cast<size_t>(l)]);
         end[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(h->has_end ? E[l] : 0);
       }
       end_nf[c] = h->has_end ? 0 : 1;

@@ -42,6 +42,7 @@ class PoolConfig:
     min_steal_len: int = 0      # 0 = 8!
     device: int = 0
     block: int = 0              # threads per CTA; 0 = auto
+    round_us: float = 0.0       # device time per round; 0 = auto
 
     def to_c(self) -> _lib.Config:
         c = _lib.Config()
@@ -54,6 +55,7 @@ class PoolConfig:
         c.min_steal_log2 = float(np.log2(self.min_steal_len)) if self.min_steal_len > 1 else 0.0
         c.device = self.device
         c.block = self.block
+        c.round_us = self.round_us
         return c
 
 
