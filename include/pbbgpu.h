@@ -128,6 +128,9 @@ int pbbgpu_decompose_batch(pbbgpu_pool* pool, const int32_t* perms, const int32_
                            uint8_t* direction, uint8_t* pruned, int64_t* lb_fwd_or_null,
                            int64_t* lb_bwd_or_null);
 
+/* raw explorer blocks (debugging): K * gstride bytes; offsets = cells, V, dir, end, tgt, ft, R */
+int pbbgpu_debug_state(pbbgpu_pool* pool, uint8_t* out, int64_t cap, int* gstride, int* offsets);
+
 /* INT32 ALU microbenchmark (add + max streams, the bounding kernels' instruction mix):
  * measured integer-op throughput of the device, the roofline denominator of the bounding
  * kernels (MEASURED_PEAKS.json has no integer peak). */

@@ -37,7 +37,7 @@ __host__ __device__ inline int round_up(int x, int a) { return (x + a - 1) / a *
 
 // Per-CTA shared instance region (identical computation on host and device).
 struct InstLayout {
-  int o_p32, o_pk, o_pl, o_ord, o_lag, o_pk32, o_cnt, o_hist, o_dhist, bytes;
+  int o_p32, o_pk, o_pl, o_ord, o_lag, o_pk32, o_cnt, o_cta, o_hist, o_dhist, bytes;
 };
 
 // packed = warp-per-explorer LB2 (children_lb2_w): one uint32 per (position, pair),
@@ -59,6 +59,7 @@ __host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs, boo
   o += packed ? 0 : round_up(npairs * n, 16);
   s.o_cnt = o;
   o += 64;
+  s.o_cta = o;
   s.o_hist = o;
   o += round_up((n + 1) * 4, 16);
   s.o_dhist = o;
@@ -713,6 +714,85 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+// Effective start of an explorer's remaining work: the padded V, moved past the current
+// cell's subtree when that cell is pruned/consumed (an explorer parked on a pruned cell
+// after a replay, or on an evaluated leaf, has already covered the whole subtree; its
+// padded V lies *before* its actual progress). Returns false when nothing remains (>= n!).
+__device__ __forceinline__ bool effective_pos(const int8_t* V, int level, const int8_t* cells, int n, int* pos) {
+  for (int l = 0; l < n; ++l) pos[l] = l <= level ? V[l] : 0;
+  if (cells[tri_off(level, n) + V[level]] > 0) return true;
+  for (int l = level; l >= 0; --l) {  // + (n-1-level)!: increment digit `level` with carry
+    if (++pos[l] <= n - 1 - l) return true;
+    pos[l] = 0;
+  }
+  return false;
+}
+
+// log2 of end - pos: exact factoradic subtraction (borrows from the least significant digit;
+// end = n! when !has_end), then the leading non-zero digit (+ the next one) gives the
+// magnitude. -1 when nothing remains.
+__device__ __forceinline__ float remaining_log2_pos(const int* pos, const int8_t* E, bool has_end, int n,
+                                                    const float* lgfact) {
+  int lead = -1, d0 = 0, d1 = 0;
+  if (has_end) {
+    int borrow = 0;
+    int D1 = 0;
+    for (int l = n - 1; l >= 0; --l) {
+      int d = E[l] - pos[l] - borrow;
+      borrow = d < 0;
+      if (borrow) d += n - l;
+      if (d) {
+        lead = l;
+        d0 = d;
+        d1 = D1;
+      }
+      D1 = d;
+    }
+    if (borrow) return -1.f;
+  } else {  // n! - pos = ((n! - 1) - pos) + 1
+    int carry = 1, D1 = 0;
+    for (int l = n - 1; l >= 0; --l) {
+      int d = n - 1 - l - pos[l] + carry;
+      carry = d > n - 1 - l;
+      if (carry) d = 0;
+      if (d) {
+        lead = l;
+        d0 = d;
+        d1 = D1;
+      }
+      D1 = d;
+    }
+    if (carry) return lgfact[n];
+  }
+  if (lead < 0) return -1.f;
+  float d = static_cast<float>(d0);
+  if (lead + 1 < n) d += static_cast<float>(d1) / static_cast<float>(n - 1 - lead);
+  return lgfact[n - 1 - lead] + __log2f(d);
+}
+
+// mid = floor((pos + end) / 2) (src/factoradic.cpp:59-93); true when mid > pos.
+__device__ __forceinline__ bool midpoint_pos(const int* pos, const int8_t* E, bool has_end, int n, int* mid) {
+  int carry = 0;
+  if (has_end) {
+    for (int l = n - 1; l >= 0; --l) {
+      const int s = pos[l] + E[l] + carry, radix = n - l;
+      mid[l] = s % radix;
+      carry = s / radix;
+    }
+  } else {
+    for (int l = 0; l < n; ++l) mid[l] = pos[l];
+    carry = 1;
+  }
+  int rem = carry, cmp = 0;
+  for (int l = 0; l < n; ++l) {
+    const int cur = rem * (n - l) + mid[l];
+    mid[l] = cur / 2;
+    rem = cur % 2;
+    if (!cmp) cmp = mid[l] < pos[l] ? -1 : (mid[l] > pos[l] ? 1 : 0);
+  }
+  return cmp > 0;
+}
+
 template <int M, int G, int BOUND>
 __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -784,14 +864,14 @@ __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
     int level = iv.hdr->level, state = iv.hdr->state, d1 = iv.hdr->d1, d2 = iv.hdr->d2;
     int rlev = iv.hdr->rlev, nrep = iv.hdr->nrep;
     const bool has_end = iv.hdr->has_end != 0;
-    int best = *reinterpret_cast<volatile int*>(&P.ctr->best);
+    int best = grp.bcast(grp.g == 0 ? *reinterpret_cast<volatile int*>(&P.ctr->best) : 0, 0);
     int step = 0;
     unsigned long long t_end = ~0ull;
     if (P.budget_ns) t_end = globaltimer_ns() + P.budget_ns;
     while (step < P.steps) {
-      if (P.budget_ns && (step & 3) == 0 && globaltimer_ns() >= t_end) break;
+      if (P.budget_ns && (step & 3) == 0 && grp.bcast(grp.g == 0 ? (globaltimer_ns() >= t_end) : 0, 0)) break;
       if (state == kEmpty) break;
-      if ((step & 15) == 15) best = *reinterpret_cast<volatile int*>(&P.ctr->best);
+      if ((step & 15) == 15) best = grp.bcast(grp.g == 0 ? *reinterpret_cast<volatile int*>(&P.ctr->best) : 0, 0);
       ++step;
       const int prune = P.prune_mode == 0 ? best : (P.prune_mode == 1 ? P.pinned_ub : INT_MAX);
       const int improve = P.prune_mode == 1 ? 0 : best;

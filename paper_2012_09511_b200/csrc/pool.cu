@@ -273,29 +273,15 @@ struct StealParams {
 constexpr int kStealThreads = 1024;
 constexpr int kBins = 2048;
 
-__device__ float remaining_log2(const unsigned char* blk, const IvmLayout& L, const float* lgfact) {
+// log2 of the remaining leaves of an active explorer (effective position, see
+// effective_pos); -1 when it cannot be split. `pos` receives the effective position.
+__device__ float remaining_log2(const unsigned char* blk, const IvmLayout& L, const float* lgfact, int* pos) {
   const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
-  const int n = L.n;
-  const int8_t* V = reinterpret_cast<const int8_t*>(blk + L.o_v);
-  const int8_t* E = reinterpret_cast<const int8_t*>(blk + L.o_end);
   if (h->state != kActive || h->level < 0) return -1.f;
-  const int level = h->level;
-  if (!h->has_end) {  // n! - pos
-    const float d = static_cast<float>(n - V[0]) - (n > 1 && level >= 1 ? static_cast<float>(V[1]) / (n - 1) : 0.f);
-    return lgfact[n - 1] + log2f(fmaxf(d, 1e-3f));
-  }
-  for (int l = 0; l < n; ++l) {
-    const int pv = l <= level ? V[l] : 0;
-    if (pv == E[l]) continue;
-    if (pv > E[l]) return -1.f;
-    float d = static_cast<float>(E[l] - pv);
-    if (l + 1 < n) {
-      const int pv1 = l + 1 <= level ? V[l + 1] : 0;
-      d += static_cast<float>(E[l + 1] - pv1) / static_cast<float>(n - 1 - l);
-    }
-    return lgfact[n - 1 - l] + log2f(fmaxf(d, 1e-3f));
-  }
-  return -1.f;
+  if (!effective_pos(reinterpret_cast<const int8_t*>(blk + L.o_v), h->level,
+                     reinterpret_cast<const int8_t*>(blk + L.o_cells), L.n, pos))
+    return -1.f;
+  return remaining_log2_pos(pos, reinterpret_cast<const int8_t*>(blk + L.o_end), h->has_end != 0, L.n, lgfact);
 }
 
 // Steal phase (src/explorer.cpp:283-340, B200 form): triggered when fewer than 0.8 K
@@ -341,8 +327,9 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
     if (h->state == kEmpty) S.thief[r++] = i;
   }
   // victim buckets
+  int pos[kMaxN], mid[kMaxN];
   for (int i = lo; i < hi; ++i) {
-    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact);
+    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact, pos);
     if (lg >= S.min_log2 && lg >= 1.f) {
       const int b = min(kBins - 1, static_cast<int>(lg * 4.f));
       atomicAdd(&bins[b], 1);
@@ -362,7 +349,7 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
   const int nvict = s_tot[1];
   const int npairs = min(nvict, total_idle);
   for (int i = lo; i < hi; ++i) {
-    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact);
+    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact, pos);
     if (lg >= S.min_log2 && lg >= 1.f) {
       const int b = min(kBins - 1, static_cast<int>(lg * 4.f));
       const int rank = atomicAdd(&bins[b], 1);
@@ -378,32 +365,10 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
     IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
     const int8_t* V = reinterpret_cast<const int8_t*>(vb + S.L.o_v);
     int8_t* E = reinterpret_cast<int8_t*>(vb + S.L.o_end);
-    int pos[kMaxN], mid[kMaxN], sum[kMaxN], oend[kMaxN];
-    for (int l = 0; l < n; ++l) {
-      pos[l] = l <= vh->level ? V[l] : 0;
-      oend[l] = E[l];
-    }
-    // midpoint (src/factoradic.cpp:59-93)
-    int carry = 0;
-    if (vh->has_end) {
-      for (int l = n - 1; l >= 0; --l) {
-        const int s = pos[l] + oend[l] + carry, radix = n - l;
-        sum[l] = s % radix;
-        carry = s / radix;
-      }
-    } else {
-      for (int l = 0; l < n; ++l) sum[l] = pos[l];
-      carry = 1;
-    }
-    int rem = carry;
-    for (int l = 0; l < n; ++l) {
-      const int cur = rem * (n - l) + sum[l];
-      mid[l] = cur / 2;
-      rem = cur % 2;
-    }
-    int cmp = 0;
-    for (int l = 0; l < n && !cmp; ++l) cmp = mid[l] < pos[l] ? -1 : (mid[l] > pos[l] ? 1 : 0);
-    if (cmp <= 0) continue;  // end < pos + 2 (explorer.cpp:270)
+    int oend[kMaxN];
+    for (int l = 0; l < n; ++l) oend[l] = E[l];
+    if (!effective_pos(V, vh->level, reinterpret_cast<const int8_t*>(vb + S.L.o_cells), n, pos)) continue;
+    if (!midpoint_pos(pos, E, vh->has_end != 0, n, mid)) continue;  // end < pos + 2 (explorer.cpp:270)
     const bool had_end = vh->has_end != 0;
     seat_explorer(tb, S.L, S.ptot, mid, oend, had_end);
     for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(mid[l]);
@@ -434,8 +399,9 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
   for (int b = t; b < kBins; b += kStealThreads) bins[b] = 0;
   if (t < 2) s_tot[t] = 0;
   __syncthreads();
+  int pos[kMaxN], mid[kMaxN];
   for (int i = lo; i < hi; ++i) {
-    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact);
+    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact, pos);
     if (lg >= S.min_log2 && lg >= 1.f) atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
   }
   __syncthreads();
@@ -449,7 +415,7 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
   }
   __syncthreads();
   for (int i = lo; i < hi; ++i) {
-    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact);
+    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact, pos);
     if (lg >= S.min_log2 && lg >= 1.f) {
       const int rank = atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
       if (rank < want) S.victim[rank] = i;
@@ -463,28 +429,8 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
     IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
     const int8_t* V = reinterpret_cast<const int8_t*>(vb + S.L.o_v);
     int8_t* E = reinterpret_cast<int8_t*>(vb + S.L.o_end);
-    int pos[kMaxN], mid[kMaxN], sum[kMaxN];
-    for (int l = 0; l < n; ++l) pos[l] = l <= vh->level ? V[l] : 0;
-    int carry = 0;
-    if (vh->has_end) {
-      for (int l = n - 1; l >= 0; --l) {
-        const int s = pos[l] + E[l] + carry, radix = n - l;
-        sum[l] = s % radix;
-        carry = s / radix;
-      }
-    } else {
-      for (int l = 0; l < n; ++l) sum[l] = pos[l];
-      carry = 1;
-    }
-    int rem = carry;
-    for (int l = 0; l < n; ++l) {
-      const int cur = rem * (n - l) + sum[l];
-      mid[l] = cur / 2;
-      rem = cur % 2;
-    }
-    int cmp = 0;
-    for (int l = 0; l < n && !cmp; ++l) cmp = mid[l] < pos[l] ? -1 : (mid[l] > pos[l] ? 1 : 0);
-    if (cmp <= 0) continue;
+    if (!effective_pos(V, vh->level, reinterpret_cast<const int8_t*>(vb + S.L.o_cells), n, pos)) continue;
+    if (!midpoint_pos(pos, E, vh->has_end != 0, n, mid)) continue;
     const int slot = atomicAdd(&s_tot[0], 1);
     int* o = out_digits + static_cast<size_t>(slot) * 2 * n;
     for (int l = 0; l < n; ++l) {
@@ -868,6 +814,7 @@ ExploreParams explore_params(pbbgpu_pool* P) {
   E.imp = P->d_imp;
   E.smem_inst_bytes = P->IL.bytes;
   E.budget_ns = static_cast<unsigned long long>(P->round_us * 1000.0);
+
   return E;
 }
 
@@ -1245,11 +1192,12 @@ int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_n
       const int8_t* C = reinterpret_cast<const int8_t*>(blk + P->L.o_cells);
       std::vector<int> pv(static_cast<size_t>(n));
       for (int l = 0; l < n; ++l) pv[static_cast<size_t>(l)] = h->state == kInit ? T[l] : (l <= h->level ? V[l] : 0);
-      // an explorer parked on an evaluated leaf (consumed cell of the leaf row) has already
-      // covered `position`: the remaining work starts at position + 1
+      // an explorer parked on a pruned/consumed cell (evaluated leaf, replay into a pruned
+      // subtree) has covered that cell's whole subtree: the remaining work starts after it
+      // (effective_pos in explore.cuh)
       bool past_end = false;
-      if (h->state == kActive && h->level == n - 2 && C[tri_off(n - 2, n) + V[n - 2]] < 0) {
-        int l = n - 1;
+      if (h->state == kActive && h->level >= 0 && C[tri_off(h->level, n) + V[h->level]] <= 0) {
+        int l = h->level;
         for (; l >= 0; --l) {
           if (++pv[static_cast<size_t>(l)] <= n - 1 - l) break;
           pv[static_cast<size_t>(l)] = 0;
@@ -1271,6 +1219,22 @@ int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_n
       ++c;
     }
     *count = c;
+  });
+}
+
+int pbbgpu_debug_state(pbbgpu_pool* P, uint8_t* out, int64_t cap, int* gstride, int* offsets) {
+  return guarded([&] {
+    const size_t bytes = static_cast<size_t>(P->K) * P->L.gstride;
+    if (static_cast<int64_t>(bytes) > cap) throw std::invalid_argument("debug_state buffer too small");
+    xfer(P, out, P->d_state, bytes, cudaMemcpyDeviceToHost, "state copy");
+    *gstride = P->L.gstride;
+    offsets[0] = P->L.o_cells;
+    offsets[1] = P->L.o_v;
+    offsets[2] = P->L.o_dir;
+    offsets[3] = P->L.o_end;
+    offsets[4] = P->L.o_tgt;
+    offsets[5] = P->L.o_ft;
+    offsets[6] = P->L.o_r;
   });
 }
 

@@ -56,6 +56,7 @@ class PoolConfig:
         c.device = self.device
         c.block = self.block
         c.round_us = self.round_us
+
         return c
 
 
