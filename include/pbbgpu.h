@@ -65,6 +65,8 @@ typedef struct {
   int device;            /* CUDA device ordinal */
   int block;             /* threads per CTA (128, 256, 512); 0 = auto */
   double round_us;       /* device time per round; 0 = auto (2000 us, or steps_per_round if set) */
+  double steal_trigger;  /* steal phase when active < trigger*K; 0 = 1.0 (reference pool: 0.8) */
+  int rounds_per_sync;   /* (explore, steal) rounds per pbbgpu_run_round host sync; 0 = 2, max 8 */
 } pbbgpu_config_t;
 
 typedef struct {

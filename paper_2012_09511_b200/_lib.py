@@ -42,6 +42,8 @@ class Config(ctypes.Structure):
         ("device", ctypes.c_int),
         ("block", ctypes.c_int),
         ("round_us", ctypes.c_double),
+        ("steal_trigger", ctypes.c_double),
+        ("rounds_per_sync", ctypes.c_int),
     ]
 
 

@@ -922,6 +922,7 @@ __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
       ++sc.decomposed;
     }
     if (grp.g == 0) {
+      // remaining work of this explorer for the steal phase (read by steal_kernel)
       iv.hdr->level = static_cast<int16_t>(level);
       iv.hdr->state = static_cast<uint8_t>(state);
       iv.hdr->d1 = static_cast<uint8_t>(d1);

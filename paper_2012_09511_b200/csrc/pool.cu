@@ -268,38 +268,49 @@ struct StealParams {
   int* victim;  // [K]
   float min_log2;
   const float* lgfact;  // [n+1] log2(k!)
+  float trigger;        // steal when active < trigger * K (reference: 0.8, explorer.cpp:251)
+  const float* lens;    // [K] per-explorer log2 remaining (written by explore_kernel)
 };
 
 constexpr int kStealThreads = 1024;
 constexpr int kBins = 2048;
 
-// log2 of the remaining leaves of an active explorer (effective position, see
-// effective_pos); -1 when it cannot be split. `pos` receives the effective position.
-__device__ float remaining_log2(const unsigned char* blk, const IvmLayout& L, const float* lgfact, int* pos) {
+// Remaining work of every explorer after a round (grid-wide, one thread per explorer):
+// log2 of its remaining leaves from the effective position, -2 busy/unsplittable, -3 idle.
+__global__ void lens_kernel(IvmLayout L, const unsigned char* state, int K, const float* lgfact, float* lens) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  const unsigned char* blk = state + static_cast<size_t>(i) * L.gstride;
   const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
-  if (h->state != kActive || h->level < 0) return -1.f;
-  if (!effective_pos(reinterpret_cast<const int8_t*>(blk + L.o_v), h->level,
-                     reinterpret_cast<const int8_t*>(blk + L.o_cells), L.n, pos))
-    return -1.f;
-  return remaining_log2_pos(pos, reinterpret_cast<const int8_t*>(blk + L.o_end), h->has_end != 0, L.n, lgfact);
+  float lg = -3.f;
+  if (h->state == kInit) {
+    lg = -2.f;
+  } else if (h->state == kActive) {
+    int pos[kMaxN];
+    lg = -2.f;
+    if (effective_pos(reinterpret_cast<const int8_t*>(blk + L.o_v), h->level,
+                      reinterpret_cast<const int8_t*>(blk + L.o_cells), L.n, pos)) {
+      const float r = remaining_log2_pos(pos, reinterpret_cast<const int8_t*>(blk + L.o_end), h->has_end != 0, L.n, lgfact);
+      if (r >= 0.f) lg = r;
+    }
+  }
+  lens[i] = lg;
 }
 
-// Steal phase (src/explorer.cpp:283-340, B200 form): triggered when fewer than 0.8 K
-// explorers are active; idle explorers (thieves, in index order) are paired with active
-// explorers in decreasing order of remaining interval length (log2 buckets); the victim
-// keeps [pos, mid), the thief replays init_at(mid) with the victim's old end.
+// Steal phase (src/explorer.cpp:283-340, B200 form). The explore kernel leaves one float per
+// explorer in S.lens (log2 of its remaining leaves from the effective position, -2 busy /
+// not splittable, -3 idle), so this single CTA only scans that array: idle explorers
+// (thieves) are paired with the longest remaining intervals (log2 buckets, descending); the
+// victim keeps [pos, mid), the thief is seated for an init_at replay of [mid, end).
 __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
   __shared__ int s_idle[kStealThreads];
   __shared__ int bins[kBins];
   __shared__ int s_tot[4];
   const int t = threadIdx.x;
   const int K = S.K;
-  const int CH = (K + kStealThreads - 1) / kStealThreads;
-  const int lo = t * CH, hi = min(K, lo + CH);
   int idle = 0, active = 0;
-  for (int i = lo; i < hi; ++i) {
-    const IvmHdr* h = reinterpret_cast<const IvmHdr*>(S.state + static_cast<size_t>(i) * S.L.gstride);
-    if (h->state == kEmpty) ++idle;
+  for (int i = t; i < K; i += kStealThreads) {
+    if (S.lens[i] == -3.f) ++idle;
     else ++active;
   }
   s_idle[t] = idle;
@@ -307,8 +318,7 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
   if (t < 4) s_tot[t] = 0;
   __syncthreads();
   atomicAdd(&s_tot[0], active);
-  // inclusive scan of idle counts (Hillis-Steele)
-  for (int off = 1; off < kStealThreads; off <<= 1) {
+  for (int off = 1; off < kStealThreads; off <<= 1) {  // inclusive scan of idle counts
     const int v = t >= off ? s_idle[t - off] : 0;
     __syncthreads();
     s_idle[t] += v;
@@ -316,24 +326,15 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
   }
   const int total_idle = s_idle[kStealThreads - 1];
   const int total_active = s_tot[0];
-  if (total_active * 5 >= K * 4 || total_idle == 0 || total_active == 0) {
+  if (static_cast<float>(total_active) >= S.trigger * static_cast<float>(K) || total_idle == 0 || total_active == 0) {
     if (t == 0) S.ctr->active = total_active;
     return;
   }
-  // thieves in index order
   int r = s_idle[t] - idle;
-  for (int i = lo; i < hi; ++i) {
-    const IvmHdr* h = reinterpret_cast<const IvmHdr*>(S.state + static_cast<size_t>(i) * S.L.gstride);
-    if (h->state == kEmpty) S.thief[r++] = i;
-  }
-  // victim buckets
-  int pos[kMaxN], mid[kMaxN];
-  for (int i = lo; i < hi; ++i) {
-    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact, pos);
-    if (lg >= S.min_log2 && lg >= 1.f) {
-      const int b = min(kBins - 1, static_cast<int>(lg * 4.f));
-      atomicAdd(&bins[b], 1);
-    }
+  for (int i = t; i < K; i += kStealThreads) {
+    const float lg = S.lens[i];
+    if (lg == -3.f) S.thief[r++] = i;
+    else if (lg >= S.min_log2 && lg >= 1.f) atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
   }
   __syncthreads();
   if (t == 0) {  // descending exclusive offsets
@@ -346,26 +347,24 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
     s_tot[1] = acc;
   }
   __syncthreads();
-  const int nvict = s_tot[1];
-  const int npairs = min(nvict, total_idle);
-  for (int i = lo; i < hi; ++i) {
-    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact, pos);
+  const int npairs = min(s_tot[1], total_idle);
+  for (int i = t; i < K; i += kStealThreads) {
+    const float lg = S.lens[i];
     if (lg >= S.min_log2 && lg >= 1.f) {
-      const int b = min(kBins - 1, static_cast<int>(lg * 4.f));
-      const int rank = atomicAdd(&bins[b], 1);
+      const int rank = atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
       if (rank < npairs) S.victim[rank] = i;
     }
   }
   __syncthreads();
   int ok = 0;
   const int n = S.L.n;
+  int pos[kMaxN], mid[kMaxN], oend[kMaxN];
   for (int pidx = t; pidx < npairs; pidx += kStealThreads) {
     unsigned char* vb = S.state + static_cast<size_t>(S.victim[pidx]) * S.L.gstride;
     unsigned char* tb = S.state + static_cast<size_t>(S.thief[pidx]) * S.L.gstride;
     IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
     const int8_t* V = reinterpret_cast<const int8_t*>(vb + S.L.o_v);
     int8_t* E = reinterpret_cast<int8_t*>(vb + S.L.o_end);
-    int oend[kMaxN];
     for (int l = 0; l < n; ++l) oend[l] = E[l];
     if (!effective_pos(V, vh->level, reinterpret_cast<const int8_t*>(vb + S.L.o_cells), n, pos)) continue;
     if (!midpoint_pos(pos, E, vh->has_end != 0, n, mid)) continue;  // end < pos + 2 (explorer.cpp:270)
@@ -401,7 +400,7 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
   __syncthreads();
   int pos[kMaxN], mid[kMaxN];
   for (int i = lo; i < hi; ++i) {
-    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact, pos);
+    const float lg = S.lens[i];
     if (lg >= S.min_log2 && lg >= 1.f) atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
   }
   __syncthreads();
@@ -415,7 +414,7 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
   }
   __syncthreads();
   for (int i = lo; i < hi; ++i) {
-    const float lg = remaining_log2(S.state + static_cast<size_t>(i) * S.L.gstride, S.L, S.lgfact, pos);
+    const float lg = S.lens[i];
     if (lg >= S.min_log2 && lg >= 1.f) {
       const int rank = atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
       if (rank < want) S.victim[rank] = i;
@@ -567,6 +566,8 @@ struct pbbgpu_pool {
   BatchFn bfn = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evs[16] = {};
+  int rounds_per_sync = 2;
   unsigned char* d_state = nullptr;
   int *d_p32 = nullptr, *d_ptot = nullptr, *d_wrk = nullptr;
   uint8_t *d_pk = nullptr, *d_pl = nullptr, *d_ord = nullptr;
@@ -574,6 +575,7 @@ struct pbbgpu_pool {
   uint32_t* d_packed = nullptr;
 
   float* d_lgfact = nullptr;
+  float* d_lens = nullptr;
   DevCounters* d_ctr = nullptr;
   DevCounters* h_ctr = nullptr;  // pinned
   unsigned long long *d_hist = nullptr, *d_dhist = nullptr;
@@ -603,11 +605,14 @@ struct pbbgpu_pool {
     cudaFree(d_packed);
 
     cudaFree(d_lgfact);
+    cudaFree(d_lens);
     cudaFree(d_ctr);
     cudaFree(d_hist);
     cudaFree(d_dhist);
     cudaFree(d_imp);
     if (h_ctr) cudaFreeHost(h_ctr);
+    for (cudaEvent_t e : evs)
+      if (e) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -653,6 +658,8 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   ck(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking), "stream");
   ck(cudaEventCreate(&P->ev0), "event");
   ck(cudaEventCreate(&P->ev1), "event");
+  for (cudaEvent_t& e : P->evs) ck(cudaEventCreate(&e), "event");
+  P->rounds_per_sync = P->cfg.rounds_per_sync > 0 ? std::min(P->cfg.rounds_per_sync, 8) : 2;
 
   std::vector<uint8_t> pk, pl, ord;
   std::vector<uint16_t> lag;
@@ -730,6 +737,7 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   ck(cudaMalloc(&P->d_ptot, ptot.size() * sizeof(int)), "malloc");
   ck(cudaMalloc(&P->d_wrk, (static_cast<size_t>(P->K) * 2 + 1) * sizeof(int)), "malloc");
   ck(cudaMalloc(&P->d_lgfact, lgf.size() * sizeof(float)), "malloc");
+  ck(cudaMalloc(&P->d_lens, static_cast<size_t>(P->K) * sizeof(float)), "malloc");
   ck(cudaMalloc(&P->d_ctr, sizeof(DevCounters)), "malloc");
   ck(cudaMallocHost(&P->h_ctr, sizeof(DevCounters)), "malloc host");
   ck(cudaMalloc(&P->d_hist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
@@ -815,6 +823,7 @@ ExploreParams explore_params(pbbgpu_pool* P) {
   E.smem_inst_bytes = P->IL.bytes;
   E.budget_ns = static_cast<unsigned long long>(P->round_us * 1000.0);
 
+
   return E;
 }
 
@@ -878,10 +887,6 @@ int run_round(pbbgpu_pool* P) {
   }
   ExploreParams E = explore_params(P);
   if (P->cfg.pinned) E.pinned_ub = static_cast<int>(std::min<int64_t>(P->pinned_ub, INT_MAX));
-  ck(cudaEventRecord(P->ev0, P->stream), "event");
-  P->efn<<<P->grid, P->block, P->smem, P->stream>>>(E);
-  ck(cudaGetLastError(), "explore_kernel launch");
-  ck(cudaEventRecord(P->ev1, P->stream), "event");
   StealParams S{};
   S.L = P->L;
   S.state = P->d_state;
@@ -892,14 +897,29 @@ int run_round(pbbgpu_pool* P) {
   S.victim = P->d_wrk + P->K;
   S.min_log2 = static_cast<float>(P->cfg.min_steal_log2 > 0 ? P->cfg.min_steal_log2 : std::log2(40320.0));
   S.lgfact = P->d_lgfact;
-  steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
-  ck(cudaGetLastError(), "steal_kernel launch");
-  P->launches += 2;
+  S.trigger = static_cast<float>(P->cfg.steal_trigger > 0 ? P->cfg.steal_trigger : 1.0);
+  S.lens = P->d_lens;
+  // several (explore, steal) rounds back to back per host synchronization: the rounds are
+  // device-timed, and a round after exhaustion costs only the state copy of an empty launch
+  const int R = P->rounds_per_sync;
+  for (int r = 0; r < R; ++r) {
+    ck(cudaEventRecord(P->evs[2 * r], P->stream), "event");
+    P->efn<<<P->grid, P->block, P->smem, P->stream>>>(E);
+    ck(cudaGetLastError(), "explore_kernel launch");
+    ck(cudaEventRecord(P->evs[2 * r + 1], P->stream), "event");
+    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens);
+    ck(cudaGetLastError(), "lens_kernel launch");
+    steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
+    ck(cudaGetLastError(), "steal_kernel launch");
+    P->launches += 3;
+  }
   read_counters(P);
-  float ms = 0;
-  ck(cudaEventElapsedTime(&ms, P->ev0, P->ev1), "elapsed");
-  P->kernel_ms += ms;
-  ++P->rounds;
+  for (int r = 0; r < R; ++r) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, P->evs[2 * r], P->evs[2 * r + 1]), "elapsed");
+    P->kernel_ms += ms;
+  }
+  P->rounds += static_cast<uint64_t>(R);
   harvest(P);
   P->last_active = P->h_ctr->active;
   return P->h_ctr->active;
@@ -1139,6 +1159,10 @@ int pbbgpu_export(pbbgpu_pool* P, int max_count, uint16_t* a_out, uint16_t* b_ou
     S.victim = P->d_wrk + P->K;
     S.min_log2 = static_cast<float>(P->cfg.min_steal_log2 > 0 ? P->cfg.min_steal_log2 : std::log2(40320.0));
     S.lgfact = P->d_lgfact;
+    S.lens = P->d_lens;
+    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens);
+    ck(cudaGetLastError(), "lens_kernel");
+    P->launches += 1;
     export_kernel<<<1, kStealThreads, 0, P->stream>>>(S, want, d_dig, d_nf, d_cnt);
     ck(cudaGetLastError(), "export_kernel");
     P->launches += 1;

@@ -43,6 +43,8 @@ class PoolConfig:
     device: int = 0
     block: int = 0              # threads per CTA; 0 = auto
     round_us: float = 0.0       # device time per round; 0 = auto
+    steal_trigger: float = 0.0  # steal when active < trigger*K; 0 = 1.0 (reference: 0.8)
+    rounds_per_sync: int = 0    # device rounds per run_round() call; 0 = 2
 
     def to_c(self) -> _lib.Config:
         c = _lib.Config()
@@ -56,6 +58,8 @@ class PoolConfig:
         c.device = self.device
         c.block = self.block
         c.round_us = self.round_us
+        c.steal_trigger = self.steal_trigger
+        c.rounds_per_sync = self.rounds_per_sync
 
         return c
 

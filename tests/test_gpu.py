@@ -191,7 +191,7 @@ def test_pinned_mode_matches_oracle(name, ub):
 
 def test_pool_rounds_snapshot_and_offer_bound():
     inst = pbb.taillard_named("ta021")
-    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=512, batch_steps=256)) as pool:
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=512, batch_steps=256, rounds_per_sync=1)) as pool:
         pool.set_initial_bound(2297)
         pool.assign_fresh([(0, math.factorial(20))])
         assert pool.active_count() == 1

@@ -10,7 +10,7 @@ name, ub, bound = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 inst = pbb.taillard_named(name)
 for spec in sys.argv[4:]:
     kw = dict(kv.split("=") for kv in spec.split(",")) if spec != "default" else {}
-    cfg = pbb.PoolConfig(**{k: int(v) for k, v in kw.items()})
+    cfg = pbb.PoolConfig(**{k: (float(v) if '.' in v else int(v)) for k, v in kw.items()})
     with pbb.GpuPool(inst, cfg, bound=bound) as pool:
         from paper_2012_09511_b200.multi import solve_distributed
         solve_distributed(pool, ub)  # warm
