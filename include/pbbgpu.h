@@ -91,6 +91,7 @@ typedef struct {
   uint64_t h2d_bytes;           /* host->device bytes copied by the pool so far */
   uint64_t d2h_bytes;           /* device->host bytes copied by the pool so far */
   int block;                    /* threads per CTA of the explore kernel */
+  double batch_kernel_ms;       /* device time of decompose_batch kernels (CUDA events) */
 } pbbgpu_stats_t;
 
 const char* pbbgpu_last_error(void);
@@ -125,6 +126,8 @@ int pbbgpu_best(pbbgpu_pool* pool, int64_t* value, int32_t* perm_or_null, int* h
 int pbbgpu_offer_bound(pbbgpu_pool* pool, int64_t value);
 int pbbgpu_stats(pbbgpu_pool* pool, pbbgpu_stats_t* out);
 int pbbgpu_histogram(pbbgpu_pool* pool, uint64_t* hist_out, int len);
+/* n > 64 (up to 512, e.g. ta111): the pool is bounding-only (decompose_batch, one CTA per
+ * node); exploration entry points return PBBGPU_ERR_STATE. */
 int pbbgpu_decompose_batch(pbbgpu_pool* pool, const int32_t* perms, const int32_t* d1,
                            const int32_t* d2, int count, int64_t incumbent, int64_t* child_lb,
                            uint8_t* direction, uint8_t* pruned, int64_t* lb_fwd_or_null,

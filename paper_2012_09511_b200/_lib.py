@@ -70,6 +70,7 @@ class Stats(ctypes.Structure):
         ("h2d_bytes", ctypes.c_uint64),
         ("d2h_bytes", ctypes.c_uint64),
         ("block", ctypes.c_int),
+        ("batch_kernel_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -1,0 +1,237 @@
+// Batched decompose for large instances (64 < n <= 512, e.g. ta111 500x20): the
+// bounding-throughput path of BASELINE config 5. One 256-thread CTA per node.
+//
+//   node tables   front over sigma1 and tail over sigma2 as a warp wavefront (lane = machine,
+//                 step s processes job s - lane, left neighbour via __shfl_up_sync), remain
+//                 as per-warp partial sums (bound_tables, src/bound.cpp:20-46)
+//   LB1           threads over children, 4 integer ops per machine and direction
+//                 (children_bounds, src/bound.cpp:61-88)
+//   LB2           thread per machine pair (P = 190 for m = 20, one pass): forward pass over
+//                 the pair's Johnson order writes PM_j, the backward pass carries SM and
+//                 evaluates every child in O(1) (max-plus prefix/suffix form, explore.cuh);
+//                 per-child maxima over pairs by shared-memory atomicMax
+//   MinMin/prune  block reductions (src/bound.cpp:109-138)
+#pragma once
+
+#include "explore.cuh"
+
+namespace pbbgpu {
+
+constexpr int kBigMaxN = 512;
+constexpr int kBigThreads = 256;
+
+struct BigBatchParams {
+  int n, m, mp, npairs;
+  const int* perms;
+  const int* d1;
+  const int* d2;
+  int count;
+  int incumbent;
+  const int* p32;        // [n][mp]
+  const uint8_t* pk;
+  const uint8_t* pl;
+  const uint2* packed;   // [n][npairs]: x = job | a << 16, y = b | lag << 16
+  int* scratch;          // [gridDim.x][n][kBigThreads]: PM_j of the thread's pair
+  int* child_lb;         // [count*n]
+  int* lb_fwd;
+  int* lb_bwd;
+  uint8_t* dir;
+  uint8_t* pruned;
+};
+
+__host__ __device__ inline int big_smem_bytes(int n, int mp, int m) {
+  return n * mp * 4 + 2 * n * m * 2 + round_up(n, 16) + 2 * n * 4 + 3 * round_up(m, 4) * 4 + 64 * 4;
+}
+
+#ifdef __CUDACC__
+
+template <int M, int BOUND>
+__global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBatchParams B) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = B.n, mp = B.mp, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* sp = reinterpret_cast<int*>(smem);                         // [n][mp]
+  uint16_t* heads = reinterpret_cast<uint16_t*>(sp + n * mp);     // [job][M]
+  uint16_t* tails = heads + n * M;
+  uint8_t* isfree = reinterpret_cast<uint8_t*>(tails + n * M);   // [n]
+  int* accf = reinterpret_cast<int*>(isfree + round_up(n, 16));   // [job]
+  int* accb = accf + n;
+  int* fr = accb + n;  // [mp] each
+  int* tl = fr + round_up(M, 4);
+  int* rm = tl + round_up(M, 4);
+  int* red = rm + round_up(M, 4);  // 8 x 4 reduction scratch
+  for (int i = tid; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
+  __syncthreads();
+  for (int node = blockIdx.x; node < B.count; node += gridDim.x) {
+    const int* perm = B.perms + static_cast<size_t>(node) * n;
+    const int d1 = B.d1[node], d2 = B.d2[node], f = n - d1 - d2;
+    for (int j = tid; j < n; j += blockDim.x) {
+      isfree[j] = 0;
+      accf[j] = 0;
+      accb[j] = 0;
+    }
+    if (tid < M) rm[tid] = 0;
+    __syncthreads();
+    for (int c = tid; c < f; c += blockDim.x) isfree[perm[d1 + c]] = 1;
+    if (warp == 0) {  // front: wavefront over (job, machine)
+      int C = 0;
+      for (int s = 0; s < d1 + M - 1; ++s) {
+        const int left = __shfl_up_sync(0xffffffffu, C, 1);
+        const int i = s - lane;
+        if (lane < M && i >= 0 && i < d1) C = max(C, lane ? left : 0) + sp[perm[i] * mp + lane];
+      }
+      if (lane < M) fr[lane] = C;
+    } else if (warp == 1) {  // tail: same on the reversed schedule / machine order
+      int C = 0;
+      const int k = M - 1 - lane;
+      for (int s = 0; s < d2 + M - 1; ++s) {
+        const int left = __shfl_up_sync(0xffffffffu, C, 1);
+        const int i = s - lane;
+        if (lane < M && i >= 0 && i < d2) C = max(C, lane ? left : 0) + sp[perm[n - 1 - i] * mp + k];
+      }
+      if (lane < M) tl[k] = C;
+    }
+    {  // remain: per-warp partial sums over the free jobs, lane = machine
+      int acc = 0;
+      if (lane < M)
+        for (int c = warp; c < f; c += blockDim.x / 32) acc += sp[perm[d1 + c] * mp + lane];
+      __syncthreads();
+      if (lane < M) atomicAdd(&rm[lane], acc);
+    }
+    __syncthreads();
+    if (BOUND == kLB1) {
+      for (int c = tid; c < f; c += blockDim.x) {
+        const int j = perm[d1 + c];
+        const int* pr = sp + j * mp;
+        int prev = 0, best = 0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const int t = max(prev, fr[k]);
+          best = max(best, t + rm[k] + tl[k]);
+          prev = t + pr[k];
+        }
+        accf[j] = best;
+        prev = 0;
+        best = 0;
+#pragma unroll
+        for (int k = M - 1; k >= 0; --k) {
+          const int t = max(prev, tl[k]);
+          best = max(best, t + fr[k] + rm[k]);
+          prev = t + pr[k];
+        }
+        accb[j] = best;
+      }
+    } else {
+      for (int c = tid; c < f; c += blockDim.x) {  // child heads / tails, by job
+        const int j = perm[d1 + c];
+        const int* pr = sp + j * mp;
+        int prev = 0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          prev = max(prev, fr[k]) + pr[k];
+          heads[j * M + k] = static_cast<uint16_t>(prev);
+        }
+        prev = 0;
+#pragma unroll
+        for (int k = M - 1; k >= 0; --k) {
+          prev = max(prev, tl[k]) + pr[k];
+          tails[j * M + k] = static_cast<uint16_t>(prev);
+        }
+      }
+      __syncthreads();
+      int* PM = B.scratch + static_cast<size_t>(blockIdx.x) * n * kBigThreads + tid;
+      constexpr int NEG = -(1 << 29);
+      for (int q = tid; q < B.npairs; q += blockDim.x) {
+        const int k = B.pk[q], l = B.pl[q];
+        const int Atot = rm[k], Btot = rm[l];
+        const int qk = tl[k], ql = tl[l], rk = fr[k], rl = fr[l];
+        int A = 0, Bp = 0, pm = NEG;
+        for (int t = 0; t < n; ++t) {
+          const uint2 e = B.packed[static_cast<size_t>(t) * B.npairs + q];
+          const int j = e.x & 0xffff;
+          if (isfree[j]) {
+            A += e.x >> 16;
+            const int X = A + static_cast<int>(e.y >> 16) - Bp;
+            PM[j * kBigThreads] = pm;
+            pm = max(pm, X);
+            Bp += e.y & 0xffff;
+          }
+        }
+        int As = 0, Bs = Atot - Btot, sm = NEG;
+        for (int t = n - 1; t >= 0; --t) {
+          const uint2 e = B.packed[static_cast<size_t>(t) * B.npairs + q];
+          const int j = e.x & 0xffff;
+          if (isfree[j]) {
+            const int a = e.x >> 16, b = e.y & 0xffff;
+            Bs += b;
+            const int X = static_cast<int>(e.y >> 16) + Bs - As;
+            const int inner = max(PM[j * kBigThreads] - b, sm - a) + Btot;
+            const int hk = heads[j * M + k], hl = heads[j * M + l];
+            const int vF = max(hk + Atot - a + qk, max(hl + Btot - b, hk + inner) + ql);
+            const int vB = max(rk + Atot - a + tails[j * M + k], max(rl + Btot - b, rk + inner) + tails[j * M + l]);
+            atomicMax(&accf[j], vF);
+            atomicMax(&accb[j], vB);
+            sm = max(sm, X);
+            As += a;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // MinMin over children in decode order (src/bound.cpp:109-131)
+    int lo = INT_MAX;
+    for (int c = tid; c < f; c += blockDim.x) {
+      const int j = perm[d1 + c];
+      lo = min(lo, min(accf[j], accb[j]));
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    if (lane == 0) red[warp] = lo;
+    __syncthreads();
+    lo = INT_MAX;
+    for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) lo = min(lo, red[w]);
+    __syncthreads();
+    int cf = 0, cb = 0, sf = 0, sb = 0;
+    for (int c = tid; c < f; c += blockDim.x) {
+      const int j = perm[d1 + c];
+      cf += accf[j] == lo;
+      cb += accb[j] == lo;
+      sf += accf[j];
+      sb += accb[j];
+    }
+    cf = __reduce_add_sync(0xffffffffu, cf);
+    cb = __reduce_add_sync(0xffffffffu, cb);
+    sf = __reduce_add_sync(0xffffffffu, sf);
+    sb = __reduce_add_sync(0xffffffffu, sb);
+    if (lane == 0) {
+      red[8 + warp] = cf;
+      red[16 + warp] = cb;
+      red[24 + warp] = sf;
+      red[32 + warp] = sb;
+    }
+    __syncthreads();
+    cf = cb = sf = sb = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) {
+      cf += red[8 + w];
+      cb += red[16 + w];
+      sf += red[24 + w];
+      sb += red[32 + w];
+    }
+    int d = kFwd;
+    if (cf != cb) d = cf < cb ? kFwd : kBwd;
+    else if (sf != sb) d = sf > sb ? kFwd : kBwd;
+    for (int c = tid; c < f; c += blockDim.x) {
+      const int j = perm[d1 + c];
+      const int lb = d == kFwd ? accf[j] : accb[j];
+      const size_t o = static_cast<size_t>(node) * n + c;
+      B.child_lb[o] = lb;
+      B.lb_fwd[o] = accf[j];
+      B.lb_bwd[o] = accb[j];
+      B.pruned[o] = lb >= B.incumbent;
+    }
+    if (tid == 0) B.dir[node] = static_cast<uint8_t>(d);
+    __syncthreads();
+  }
+}
+
+#endif  // __CUDACC__
+
+}  // namespace pbbgpu

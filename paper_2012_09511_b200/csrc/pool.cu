@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/pbbgpu.h"
+#include "bound_big.cuh"
 #include "explore.cuh"
 
 using namespace pbbgpu;
@@ -153,11 +154,12 @@ int64_t neh_host(int n, int m, const int32_t* p, int32_t* out) {
 // descending b+lag, ties by ascending job.
 void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::vector<uint8_t>& pl,
                 std::vector<uint8_t>& ord, std::vector<uint16_t>& lag, std::vector<uint32_t>& packed,
-                bool& packable) {
+                bool& packable, std::vector<uint16_t>& ord16) {
   const int P = m * (m - 1) / 2;
   pk.resize(static_cast<size_t>(P));
   pl.resize(static_cast<size_t>(P));
   ord.resize(static_cast<size_t>(P) * n);
+  ord16.resize(static_cast<size_t>(P) * n);
   lag.resize(static_cast<size_t>(P) * n);
   int q = 0;
   std::vector<int> idx(static_cast<size_t>(n));
@@ -183,7 +185,10 @@ void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::v
         if (kx != ky) return first[static_cast<size_t>(x)] ? kx < ky : kx > ky;
         return x < y;
       });
-      for (int t = 0; t < n; ++t) ord[static_cast<size_t>(q) * n + t] = static_cast<uint8_t>(idx[static_cast<size_t>(t)]);
+      for (int t = 0; t < n; ++t) {
+        ord[static_cast<size_t>(q) * n + t] = static_cast<uint8_t>(idx[static_cast<size_t>(t)]);  // n <= 64 kernels
+        ord16[static_cast<size_t>(q) * n + t] = static_cast<uint16_t>(idx[static_cast<size_t>(t)]);
+      }
     }
   }
   // transposed packed form [t][q] = job | a << 6 | b << 13 | lag << 20 (children_lb2_w)
@@ -191,7 +196,7 @@ void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::v
   packable = n <= 64;
   for (int qq = 0; qq < P; ++qq) {
     for (int t = 0; t < n; ++t) {
-      const int j = ord[static_cast<size_t>(qq) * n + t];
+      const int j = ord16[static_cast<size_t>(qq) * n + t];
       const int a = p[static_cast<size_t>(j) * m + pk[static_cast<size_t>(qq)]];
       const int b = p[static_cast<size_t>(j) * m + pl[static_cast<size_t>(qq)]];
       const int lg = lag[static_cast<size_t>(qq) * n + j];
@@ -531,6 +536,24 @@ ExploreFn explore_fn(int m, int bound, int G) {
   return nullptr;
 }
 
+using BigFn = void (*)(BigBatchParams);
+BigFn big_fn(int m, int bound) {
+  if (bound == kLB1) {
+    switch (m) {
+      case 5: return decompose_big_kernel<5, kLB1>;
+      case 10: return decompose_big_kernel<10, kLB1>;
+      case 20: return decompose_big_kernel<20, kLB1>;
+    }
+  } else {
+    switch (m) {
+      case 5: return decompose_big_kernel<5, kLB2>;
+      case 10: return decompose_big_kernel<10, kLB2>;
+      case 20: return decompose_big_kernel<20, kLB2>;
+    }
+  }
+  return nullptr;
+}
+
 BatchFn batch_fn(int m, int bound, int G) {
   if (bound == kLB1) {
     switch (m) {
@@ -564,6 +587,12 @@ struct pbbgpu_pool {
   int npairs = 0;
   ExploreFn efn = nullptr;
   BatchFn bfn = nullptr;
+  bool batch_only = false;  // n > 64: bounding (decompose_batch) only
+  void (*big)(BigBatchParams) = nullptr;
+  uint2* d_packed64 = nullptr;
+  int* d_big_scratch = nullptr;
+  int big_grid = 0;
+  size_t big_smem = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t evs[16] = {};
@@ -588,6 +617,7 @@ struct pbbgpu_pool {
   std::vector<int32_t> best_sched;
   uint64_t rounds = 0;
   uint64_t launches = 0;
+  double batch_ms = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
   double kernel_ms = 0;
   int last_active = 0;
@@ -603,6 +633,8 @@ struct pbbgpu_pool {
     cudaFree(d_ord);
     cudaFree(d_lag);
     cudaFree(d_packed);
+    cudaFree(d_packed64);
+    cudaFree(d_big_scratch);
 
     cudaFree(d_lgfact);
     cudaFree(d_lens);
@@ -635,7 +667,7 @@ int pick_group(int n, int bound) {
 }
 
 void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const pbbgpu_config_t* cfg) {
-  if (n < 2 || n > kMaxN) throw std::invalid_argument("pbbgpu: n must be in [2, 64] for the shared-memory IVM store");
+  if (n < 2 || n > kBigMaxN) throw std::invalid_argument("pbbgpu: n must be in [2, 512]");
   if (m != 5 && m != 10 && m != 20) throw std::invalid_argument("pbbgpu: m must be 5, 10 or 20 (compiled machine counts)");
   if (bound != kLB1 && bound != kLB2) throw std::invalid_argument("pbbgpu: bound must be PBBGPU_LB1 or PBBGPU_LB2");
   int pmax = 0;
@@ -664,10 +696,51 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   std::vector<uint8_t> pk, pl, ord;
   std::vector<uint16_t> lag;
   std::vector<uint32_t> packed;
+  std::vector<uint16_t> ord16;
   bool packable = false;
   if (bound == kLB2) {
-    lb2_tables(n, m, p, pk, pl, ord, lag, packed, packable);
+    lb2_tables(n, m, p, pk, pl, ord, lag, packed, packable, ord16);
     P->npairs = m * (m - 1) / 2;
+  }
+  if (n > kMaxN) {  // batch-only pool: the large-n bounding kernel, no explorers
+    P->batch_only = true;
+    P->mp = round_up(m, 4);
+    P->big = big_fn(m, bound);
+    std::vector<int> p32(static_cast<size_t>(n) * P->mp, 0);
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < m; ++k) p32[static_cast<size_t>(j) * P->mp + k] = p[static_cast<size_t>(j) * m + k];
+    ck(cudaMalloc(&P->d_p32, p32.size() * sizeof(int)), "malloc");
+    xfer(P, P->d_p32, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
+    if (bound == kLB2) {
+      std::vector<uint2> pk64(static_cast<size_t>(n) * P->npairs);
+      for (int q = 0; q < P->npairs; ++q)
+        for (int t = 0; t < n; ++t) {
+          const int j = ord16[static_cast<size_t>(q) * n + t];
+          const int a = p[static_cast<size_t>(j) * m + pk[static_cast<size_t>(q)]];
+          const int bb = p[static_cast<size_t>(j) * m + pl[static_cast<size_t>(q)]];
+          const int lg = lag[static_cast<size_t>(q) * n + j];
+          if (a > 65535 || bb > 65535) throw std::invalid_argument("processing time exceeds 16 bits");
+          pk64[static_cast<size_t>(t) * P->npairs + q] =
+              make_uint2(static_cast<unsigned>(j) | static_cast<unsigned>(a) << 16, static_cast<unsigned>(bb) | static_cast<unsigned>(lg) << 16);
+        }
+      ck(cudaMalloc(&P->d_pk, pk.size()), "malloc");
+      ck(cudaMalloc(&P->d_pl, pl.size()), "malloc");
+      ck(cudaMalloc(&P->d_packed64, pk64.size() * sizeof(uint2)), "malloc");
+      xfer(P, P->d_pk, pk.data(), pk.size(), cudaMemcpyHostToDevice, "copy");
+      xfer(P, P->d_pl, pl.data(), pl.size(), cudaMemcpyHostToDevice, "copy");
+      xfer(P, P->d_packed64, pk64.data(), pk64.size() * sizeof(uint2), cudaMemcpyHostToDevice, "copy");
+    }
+    P->big_smem = static_cast<size_t>(big_smem_bytes(n, P->mp, m));
+    ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->big), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(P->big_smem)), "smem attr");
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(P->big), kBigThreads, P->big_smem), "occupancy");
+    if (per_sm < 1) throw CapacityError("pbbgpu: large-n bounding kernel cannot be resident");
+    P->big_grid = per_sm * prop.multiProcessorCount;
+    if (bound == kLB2)
+      ck(cudaMalloc(&P->d_big_scratch, static_cast<size_t>(P->big_grid) * n * kBigThreads * sizeof(int)), "malloc scratch");
+    P->K = 0;
+    return;
   }
   P->G = P->cfg.group > 0 ? P->cfg.group : pick_group(n, bound);
   if (P->G != 4 && P->G != 8 && P->G != 16 && P->G != 32) throw std::invalid_argument("pbbgpu: group must be 4, 8, 16 or 32");
@@ -828,6 +901,7 @@ ExploreParams explore_params(pbbgpu_pool* P) {
 }
 
 void assign_digits(pbbgpu_pool* P, const std::vector<int>& a, const std::vector<int>& b, const std::vector<uint8_t>& nf, const std::vector<int>& slots) {
+  if (P->batch_only) throw StateError("pbbgpu: n > 64 pools are bounding-only (decompose_batch); exploration needs n <= 64");
   const int cnt = static_cast<int>(slots.size());
   if (cnt == 0) return;
   int *da = nullptr, *db = nullptr, *ds = nullptr;
@@ -877,6 +951,7 @@ int count_active_host(pbbgpu_pool* P) {
 }
 
 int run_round(pbbgpu_pool* P) {
+  if (P->batch_only) throw StateError("pbbgpu: n > 64 pools are bounding-only (decompose_batch); exploration needs n <= 64");
   const int64_t offer = P->pending_offer.exchange(INT64_MAX);
   if (offer < P->best_value) {
     {
@@ -1281,6 +1356,14 @@ int pbbgpu_offer_bound(pbbgpu_pool* P, int64_t v) {
 
 int pbbgpu_stats(pbbgpu_pool* P, pbbgpu_stats_t* out) {
   return guarded([&] {
+    if (P->batch_only) {
+      std::memset(out, 0, sizeof(*out));
+      out->kernel_launches = P->launches;
+      out->batch_kernel_ms = P->batch_ms;
+      out->h2d_bytes = P->h2d_bytes;
+      out->d2h_bytes = P->d2h_bytes;
+      return;
+    }
     read_counters(P);
     const DevCounters& c = *P->h_ctr;
     std::memset(out, 0, sizeof(*out));
@@ -1301,6 +1384,7 @@ int pbbgpu_stats(pbbgpu_pool* P, pbbgpu_stats_t* out) {
     out->block = P->block;
     out->steps_per_round = P->steps;
     out->kernel_launches = P->launches;
+    out->batch_kernel_ms = P->batch_ms;
     out->h2d_bytes = P->h2d_bytes;
     out->d2h_bytes = P->d2h_bytes;
   });
@@ -1347,6 +1431,32 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
     xfer(P, dp, perms, cn * sizeof(int), cudaMemcpyHostToDevice, "copy");
     xfer(P, dd1, d1, count * sizeof(int), cudaMemcpyHostToDevice, "copy");
     xfer(P, dd2, d2, count * sizeof(int), cudaMemcpyHostToDevice, "copy");
+    if (P->batch_only) {
+      BigBatchParams G{};
+      G.n = n;
+      G.m = P->m;
+      G.mp = P->mp;
+      G.npairs = P->npairs;
+      G.perms = dp;
+      G.d1 = dd1;
+      G.d2 = dd2;
+      G.count = count;
+      G.incumbent = static_cast<int>(std::min<int64_t>(incumbent, INT_MAX));
+      G.p32 = P->d_p32;
+      G.pk = P->d_pk;
+      G.pl = P->d_pl;
+      G.packed = P->d_packed64;
+      G.scratch = P->d_big_scratch;
+      G.child_lb = dlb;
+      G.lb_fwd = dlf;
+      G.lb_bwd = dlbw;
+      G.dir = ddir;
+      G.pruned = dpr;
+      ck(cudaEventRecord(P->ev0, P->stream), "event");
+      P->big<<<std::min(count, P->big_grid), kBigThreads, P->big_smem, P->stream>>>(G);
+      ck(cudaGetLastError(), "decompose_big launch");
+      ck(cudaEventRecord(P->ev1, P->stream), "event");
+    }
     BatchParams B{};
     B.L = P->L;
     B.perms = dp;
@@ -1366,11 +1476,19 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
     B.lb_bwd = dlbw;
     B.dir = ddir;
     B.pruned = dpr;
-    const int NG = P->block / P->G;
-    const int grid = std::min((count + NG - 1) / NG, 148 * 8);
-    P->bfn<<<grid, P->block, P->smem, P->stream>>>(B);
-    ck(cudaGetLastError(), "decompose_batch launch");
+    if (!P->batch_only) {
+      const int NG = P->block / P->G;
+      const int grid = std::min((count + NG - 1) / NG, 148 * 8);
+      ck(cudaEventRecord(P->ev0, P->stream), "event");
+      P->bfn<<<grid, P->block, P->smem, P->stream>>>(B);
+      ck(cudaGetLastError(), "decompose_batch launch");
+      ck(cudaEventRecord(P->ev1, P->stream), "event");
+    }
+    P->launches += 1;
     ck(cudaStreamSynchronize(P->stream), "sync");
+    float bms = 0;
+    ck(cudaEventElapsedTime(&bms, P->ev0, P->ev1), "elapsed");
+    P->batch_ms += bms;
     std::vector<int> lb(cn), lf(cn), lbw(cn);
     std::vector<uint8_t> pr(cn);
     xfer(P, lb.data(), dlb, cn * sizeof(int), cudaMemcpyDeviceToHost, "copy");

@@ -87,6 +87,7 @@ class PoolStats:
     h2d_bytes: int = 0
     d2h_bytes: int = 0
     block: int = 0
+    batch_kernel_ms: float = 0.0
 
 
 @dataclass

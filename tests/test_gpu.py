@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import paper_2012_09511_b200 as pbb
+from paper_2012_09511_b200 import _lib
 from oracle import oracle as orc
 from tests import golden_io
 
@@ -224,3 +225,39 @@ def test_snapshot_resume_preserves_count():
     # they are discounted exactly like steal replays, so the totals add up
     assert done.unique + res.stats.unique >= ref["decomposed"]
     assert done.leaves + res.stats.leaves == ref["leaves"]
+
+
+# ---------------------------------------------------------------- large n (ta111, 500 x 20): bounding-only pools
+
+def _nodes_with_f(n, fs, seed):
+    rng = np.random.default_rng(seed)
+    perms, d1s, d2s = [], [], []
+    for f in fs:
+        perms.append(rng.permutation(n))
+        d1 = int(rng.integers(0, n - f + 1))
+        d1s.append(d1)
+        d2s.append(n - f - d1)
+    return np.array(perms), d1s, d2s
+
+
+@pytest.mark.parametrize("bound,fs", [("lb1", [1, 2, 7, 50, 137, 256, 499, 500, 333, 64, 65, 300] * 4),
+                                      ("lb2", [1, 2, 5, 17, 40, 64, 65, 90])])
+def test_large_n_decompose_matches_oracle(bound, fs):
+    inst = pbb.taillard_named("ta111")
+    perms, d1s, d2s = _nodes_with_f(inst.n, fs, 23)
+    prob = orc.Problem(inst.p, orc.LB1 if bound == "lb1" else orc.LB2)
+    inc = 26670
+    with pbb.GpuPool(inst, bound=bound) as pool:
+        assert pool.K() == 0
+        lb, dr, pr, lf, lbw = pool.decompose_batch(perms, d1s, d2s, inc)
+        with pytest.raises(_lib.PbbError):
+            pool.assign_split()
+    for i in range(len(fs)):
+        f = inst.n - d1s[i] - d2s[i]
+        fw, bw = prob.children_bounds(perms[i], d1s[i], d2s[i])
+        d, clb, cpr = prob.decompose(perms[i], d1s[i], d2s[i], inc)
+        assert [int(x) for x in lf[i, :f]] == fw
+        assert [int(x) for x in lbw[i, :f]] == bw
+        assert int(dr[i]) == d
+        assert [int(x) for x in lb[i, :f]] == clb
+        assert [int(x) for x in pr[i, :f]] == cpr
