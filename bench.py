@@ -163,6 +163,71 @@ def run_reference(args, wl, rank):
     return 0
 
 
+def run_extras(pbb, solve_distributed, dev, local, world, rank, peak, args):
+    """Secondary BASELINE.json configs, measured on the same GPUs (not the headline):
+    ta021 LB1 full proof; ta056 LB2 and ta041 LB1-pinned time-bounded rates; ta111 LB2/LB1
+    bounding sweep (rank 0 only). Device time via CUDA events, max over ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    def timed(fn):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = fn()
+        torch.cuda.synchronize()
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return r, ms
+
+    out = {}
+    inst = pbb.taillard_named("ta021")
+    with pbb.GpuPool(inst, pbb.PoolConfig(device=local), bound="lb1") as pool:
+        solve_distributed(pool, 2297, device=dev)
+        r, ms = timed(lambda: solve_distributed(pool, 2297, device=dev))
+    out["ta021_lb1_ub2297_full_proof"] = {
+        "ms": ms, "unique_nodes": r.unique, "leaves": r.leaves, "nodes_per_s": r.unique / (ms / 1e3),
+        "reference_1core_s": 534.8, "reference_note": "SURVEY.md Appendix C (reference K=1, this build container)"}
+    for key, name, bound, ub, pinned, secs in (("ta056_lb2_ub3679_timebounded", "ta056", "lb2", 3679, False, 5.0),
+                                               ("ta041_lb1_pinned3000_timebounded", "ta041", "lb1", 3000, True, 5.0)):
+        inst = pbb.taillard_named(name)
+        cfg = pbb.PoolConfig(device=local, pinned=pinned)
+        with pbb.GpuPool(inst, cfg, bound=bound) as pool:
+            r, ms = timed(lambda: solve_distributed(pool, ub, device=dev, time_limit_s=secs))
+        out[key] = {"ms": ms, "unique_nodes": r.unique, "leaves": r.leaves, "best": r.best_value,
+                    "nodes_per_s": r.unique / (ms / 1e3), "completed": r.completed}
+    if rank == 0:
+        inst = pbb.taillard_named("ta111")
+        n, m = inst.n, inst.m
+        rng = np.random.default_rng(1)
+        sweep = []
+        for bound in ("lb1", "lb2"):
+            with pbb.GpuPool(inst, pbb.PoolConfig(device=local), bound=bound) as pool:
+                for f in (50, 200, 499):
+                    cnt = 2048
+                    perms = np.array([rng.permutation(n) for _ in range(cnt)])
+                    d1 = rng.integers(0, n - f + 1, cnt)
+                    pool.decompose_batch(perms[:64], d1[:64], n - f - d1[:64], 26670)
+                    s0 = pool.stats().batch_kernel_ms
+                    pool.decompose_batch(perms, d1, n - f - d1, 26670)
+                    kms = pool.stats().batch_kernel_ms - s0
+                    W = (w_lb1 if bound == "lb1" else w_lb2)(f, n, m)
+                    rate = cnt / (kms / 1e3)
+                    sweep.append({"bound": bound.upper(), "f": f, "nodes_per_s": rate,
+                                  "alg_ops_per_s": rate * W, "alg_frac_of_int32_peak": rate * W / peak})
+        out["ta111_bounding_sweep"] = {"nodes_per_launch": 2048, "rows": sweep,
+                                       "note": "LB2 uses the O(P(n+f)) max-plus form: algorithmic W2 exceeds executed ops"}
+    return out
+
+
 def load_traffic():
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
@@ -184,6 +249,7 @@ def main():
     ap.add_argument("--ref-warmup-s", type=float, default=3.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
 
@@ -261,8 +327,8 @@ def main():
     peak = pbb.int32_peak(local)
     tr = load_traffic()
     traffic = tr.get(f"{args.workload}:explore_kernel_dram_bytes_per_launch")
-    roofline = {"bound": "int_alu", "achieved": ops / (kms / 1000.0) / 1e12, "peak": peak / 1e12, "unit": "Tops/s",
-                "frac": (ops / (kms / 1000.0)) / peak, "traffic": traffic,
+    roofline = {"bound": "int_alu", "achieved": ops / (kms / 1000.0) / 1e12, "peak": peak * world / 1e12,
+                "unit": "Tops/s", "frac": (ops / (kms / 1000.0)) / (peak * world), "traffic": traffic,
                 "kernel": "explore_kernel", "kernel_ms_per_step": kms,
                 "kernel_share_of_step": kms / statistics.mean(times),
                 "ops_per_step": ops, "ops_model": "SURVEY.md §8(d) W2(f)" if wl["bound"] == "lb2" else "SURVEY.md §8(d) W1(f)",
@@ -295,6 +361,10 @@ def main():
     if rank == 0 and not args.no_cpu and world == 1:
         cpu = cpu_sample(wl, args.cpu_sample_s, cpu_cores())
 
+    extra = None
+    if not args.no_extras:
+        extra = run_extras(pbb, solve_distributed, dev, local, world, rank, peak, args)
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "nodes/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": statistics.mean(times), "higher_is_better": True,
@@ -308,7 +378,7 @@ def main():
                            "l2": "256 MiB flush between steps, outside the per-step event brackets",
                            "desc": wl["desc"]},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clocks}
+                "clocks": clocks, "extra": extra}
         print(json.dumps(line), flush=True)
     pool.close()
     if world > 1:
