@@ -250,6 +250,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--round-us", type=float, default=0.0, help="device time per round (0 = library default)")
+    ap.add_argument("--rounds-per-sync", type=int, default=0, help="rounds per host sync / exchange (0 = default)")
+    ap.add_argument("--export-max", type=int, default=0, help="intervals one rank may donate per exchange")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
 
@@ -272,7 +275,7 @@ def main():
     inst = pbb.taillard_named(wl["instance"])
     n, m = inst.n, inst.m
     W = w_lb2 if wl["bound"] == "lb2" else w_lb1
-    cfg = pbb.PoolConfig(device=local)
+    cfg = pbb.PoolConfig(device=local, round_us=args.round_us, rounds_per_sync=args.rounds_per_sync)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -288,7 +291,7 @@ def main():
 
     def step(pool):
         before = pool.stats()
-        res = solve_distributed(pool, wl["ub"], device=dev)
+        res = solve_distributed(pool, wl["ub"], device=dev, export_max=args.export_max or None)
         after = pool.stats()
         return res, before, after
 

@@ -114,6 +114,9 @@ int pbbgpu_assign(pbbgpu_pool* pool, const uint16_t* a_digits, const uint16_t* b
 int pbbgpu_assign_split(pbbgpu_pool* pool, int pieces);
 /* pieces [first, first+count) of [0,n!) cut into `total` equal ranges (multi-GPU partition) */
 int pbbgpu_assign_split_range(pbbgpu_pool* pool, int first, int count, int total);
+/* pieces first, first+stride, ... (count of them) of [0,n!) cut into `total` ranges: the
+ * interleaved multi-GPU partition (rank r of W: first = r, stride = W) */
+int pbbgpu_assign_split_strided(pbbgpu_pool* pool, int first, int stride, int count, int total);
 /* hand the right halves [mid, end) of the `max_count` longest remaining intervals to another
  * pool (inter-GPU stealing); the explorers keep [pos, mid) */
 int pbbgpu_export(pbbgpu_pool* pool, int max_count, uint16_t* a_out, uint16_t* b_out,

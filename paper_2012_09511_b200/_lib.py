@@ -26,7 +26,7 @@ EXPORTS = (
     "pbbgpu_set_initial_bound", "pbbgpu_assign", "pbbgpu_assign_split", "pbbgpu_run_round",
     "pbbgpu_active_count", "pbbgpu_snapshot", "pbbgpu_best", "pbbgpu_offer_bound",
     "pbbgpu_stats", "pbbgpu_histogram", "pbbgpu_decompose_batch", "pbbgpu_solve", "pbbgpu_int32_peak",
-    "pbbgpu_assign_split_range", "pbbgpu_export", "pbbgpu_debug_state",
+    "pbbgpu_assign_split_range", "pbbgpu_export", "pbbgpu_debug_state", "pbbgpu_assign_split_strided",
 )
 
 
@@ -121,6 +121,7 @@ def load() -> ctypes.CDLL:
         "pbbgpu_decompose_batch": (ctypes.c_int, [P, i32p, i32p, i32p, ctypes.c_int, ctypes.c_int64,
                                                   i64p, u8p, u8p, i64p, i64p]),
         "pbbgpu_assign_split_range": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+        "pbbgpu_assign_split_strided": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
         "pbbgpu_export": (ctypes.c_int, [P, ctypes.c_int, u16p, u16p, u8p, ip]),
         "pbbgpu_debug_state": (ctypes.c_int, [P, u8p, ctypes.c_int64, ip, ip]),
         "pbbgpu_int32_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),

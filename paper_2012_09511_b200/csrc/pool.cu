@@ -1176,10 +1176,16 @@ int pbbgpu_assign(pbbgpu_pool* P, const uint16_t* a, const uint16_t* b, const ui
 }
 
 int pbbgpu_assign_split_range(pbbgpu_pool* P, int first, int count, int total) {
+  return pbbgpu_assign_split_strided(P, first, 1, count, total);
+}
+
+int pbbgpu_assign_split_strided(pbbgpu_pool* P, int first, int stride, int count, int total) {
   return guarded([&] {
     if (total <= 0) total = P->K;
     if (count < 0) count = total;
-    if (first < 0 || count > P->K || first + count > total) throw std::invalid_argument("bad split range");
+    if (stride < 1) throw std::invalid_argument("bad split stride");
+    if (first < 0 || count > P->K || (count > 0 && first + static_cast<int64_t>(count - 1) * stride >= total))
+      throw std::invalid_argument("bad split range");
     const int n = P->n;
     // floor(i * n! / total) in factoradic, digit by digit: d_l = floor(r (n-l) / C),
     // r <- r (n-l) mod C (exact rational expansion, no big integers needed)
@@ -1194,7 +1200,7 @@ int pbbgpu_assign_split_range(pbbgpu_pool* P, int first, int count, int total) {
     std::vector<int> a(static_cast<size_t>(count) * n), b(static_cast<size_t>(count) * n, 0), slots(static_cast<size_t>(count));
     std::vector<uint8_t> nf(static_cast<size_t>(count), 0);
     for (int c = 0; c < count; ++c) {
-      const int i = first + c;
+      const int i = first + c * stride;
       digits_of(i, &a[static_cast<size_t>(c) * n]);
       if (i + 1 < total) digits_of(i + 1, &b[static_cast<size_t>(c) * n]);
       else nf[static_cast<size_t>(c)] = 1;

@@ -1,7 +1,8 @@
 """Multi-GPU solve: one process per GPU, torch.distributed for the plumbing.
 
-  partition   [0, n!) cut into world*K equal ranges; rank r seats pieces [r*K, (r+1)*K)
-              (pbbgpu_assign_split_range) -- the intra-box analogue of the coordinator's
+  partition   [0, n!) cut into world*K equal ranges; rank r seats pieces r, r+W, r+2W, ...
+              (pbbgpu_assign_split_strided): interleaved so that every rank samples the
+              whole, highly irregular tree -- the intra-box analogue of the coordinator's
               initial work units (src/coordinator.cpp)
   per round   every rank runs one pool round (explore + intra-GPU steal kernels), then one
               all_gather of (active explorers, incumbent, exported intervals)
@@ -60,7 +61,12 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
     st0 = pool.stats()
     h0 = pool.histogram()
     pool.set_initial_bound(ub)
-    pool.assign_split_range(rank * K, K, world * K)
+    # interleaved partition: rank r seats pieces r, r + W, r + 2W, ... of [0,n!) cut into W*K
+    # ranges, so every rank samples the whole (highly irregular) tree from the start
+    if world > 1 and hasattr(pool, "assign_split_strided"):
+        pool.assign_split_strided(rank, world, K, world * K)
+    else:
+        pool.assign_split_range(rank * K, K, world * K)
     X = export_max if export_max else max(1, min(1024, K // 4))
     low = int(K * low_fraction)
     remote = 0

@@ -207,6 +207,9 @@ class GpuPool:
     def assign_split_range(self, first: int, count: int, total: int) -> None:
         _lib.check(self._lib.pbbgpu_assign_split_range(self._h, first, count, total))
 
+    def assign_split_strided(self, first: int, stride: int, count: int, total: int) -> None:
+        _lib.check(self._lib.pbbgpu_assign_split_strided(self._h, first, stride, count, total))
+
     def export_work(self, max_count: int):
         """Right halves of the longest remaining intervals, as digit arrays (a, b, b_is_nfact)."""
         n = self.inst.n
