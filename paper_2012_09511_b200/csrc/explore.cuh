@@ -37,7 +37,7 @@ __host__ __device__ inline int round_up(int x, int a) { return (x + a - 1) / a *
 
 // Per-CTA shared instance region (identical computation on host and device).
 struct InstLayout {
-  int o_p32, o_pk, o_pl, o_ord, o_lag, o_pk32, o_cnt, o_cta, o_hist, o_dhist, bytes;
+  int o_p32, o_pk, o_pl, o_ord, o_lag, o_pk32, o_inv, o_cnt, o_cta, o_hist, o_dhist, bytes;
 };
 
 // packed = warp-per-explorer LB2 (children_lb2_w): one uint32 per (position, pair),
@@ -51,6 +51,8 @@ __host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs, boo
   o += packed ? 0 : round_up(npairs * n * 2, 16);
   s.o_pk32 = o;
   o += packed ? round_up(npairs * n * 4, 16) : 0;
+  s.o_inv = o;  // [job][pair] position of the job in the pair's order (packed mode)
+  o += packed ? round_up(npairs * n, 16) : 0;
   s.o_pk = o;
   o += round_up(npairs, 16);
   s.o_pl = o;
@@ -226,6 +228,7 @@ struct InstView {
   const uint8_t* ord;
   const uint16_t* lag;
   const uint32_t* packed;  // [n][npairs]: job | a << 6 | b << 13 | lag << 20
+  const uint8_t* invord;   // [n][npairs]: position of job j in pair q's order
   int npairs;
 };
 
@@ -363,7 +366,7 @@ __device__ __forceinline__ void children_lb2(const Group<G>& grp, const IvmView&
 // Integer-exact, identical values to the per-child chains, O(P (n + f)) per node instead of
 // O(P f^2). Each lane owns a pair (32 pairs per round); per child the 32 pair bounds are
 // combined with one REDUX.MAX (__reduce_max_sync).
-template <int M>
+template <int M, bool SMALLN>
 __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView& in, int n, int mp, int f,
                                                unsigned long long fmask) {
   constexpr unsigned FULL = 0xffffffffu;
@@ -395,7 +398,36 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
     const bool live = q < P;
     const int k = live ? in.pk[q] : 0, l = live ? in.pl[q] : 0;
     const int Atot = iv.rm[k], Btot = iv.rm[l];
-    if (live) {
+    if constexpr (SMALLN) {
+     if (live) {
+      // the pair's free positions as a bitmask from the static inverse order (f lookups),
+      // then passes over exactly the f set bits: uniform trip count, no predicated slots
+      uint32_t Fq = 0;
+      for (int c = 0; c < f; ++c) Fq |= 1u << in.invord[iv.freej[c] * P + q];
+      int A = 0, Bp = 0, pm = NEG;
+      for (uint32_t w = Fq; w; w &= w - 1) {
+        const unsigned e = in.packed[(__ffs(w) - 1) * P + q];
+        const int j = e & 63;
+        A += (e >> 6) & 127;
+        const int X = A + static_cast<int>(e >> 20) - Bp;
+        PMl[j * 32] = static_cast<int16_t>(pm);
+        pm = max(pm, X);
+        Bp += (e >> 13) & 127;
+      }
+      int As = 0, Bs = Atot - Btot, sm = NEG;
+      for (uint32_t w = Fq; w;) {
+        const int t = 31 - __clz(w);
+        w ^= 1u << t;
+        const unsigned e = in.packed[t * P + q];
+        const int j = e & 63;
+        Bs += (e >> 13) & 127;
+        const int X = static_cast<int>(e >> 20) + Bs - As;
+        SMl[j * 32] = static_cast<int16_t>(sm);
+        sm = max(sm, X);
+        As += (e >> 6) & 127;
+      }
+     }
+    } else if (live) {
       int A = 0, Bp = 0, pm = NEG;
       for (int t = 0; t < n; ++t) {
         const unsigned e = in.packed[t * P + q];
@@ -604,7 +636,7 @@ struct StepCounters {
 };
 
 // Decompose the node at (level, sel) and branch (bound.cpp:98-139 + ivm.cpp:124-145).
-template <int M, int G, int BOUND>
+template <int M, int G, int BOUND, bool SMALLN>
 __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmView& iv,
                                                  const InstView& in, int n, int mp, int sel,
                                                  int prune, int& level, int& d1, int& d2,
@@ -621,7 +653,7 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
   if constexpr (BOUND == kLB1) {
     children_lb1<M, G>(grp, iv, in, mp, f);
   } else if constexpr (G == 32) {
-    children_lb2_w<M>(iv, in, n, mp, f, fm);
+    children_lb2_w<M, SMALLN>(iv, in, n, mp, f, fm);
   } else {
     children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
   }
@@ -793,7 +825,7 @@ __device__ __forceinline__ bool midpoint_pos(const int* pos, const int8_t* E, bo
   return cmp > 0;
 }
 
-template <int M, int G, int BOUND>
+template <int M, int G, int BOUND, bool SMALLN = false>
 __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = P.L;
@@ -808,7 +840,10 @@ __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = P.p32[i];
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
-      for (int i = threadIdx.x; i < P.npairs * n; i += blockDim.x) sk[i] = P.packed[i];
+      for (int i = threadIdx.x; i < P.npairs * n; i += blockDim.x) {
+        sk[i] = P.packed[i];
+        smem[IL.o_inv + i] = P.invord[i];
+      }
       for (int i = threadIdx.x; i < P.npairs; i += blockDim.x) {
         smem[IL.o_pk + i] = P.pk[i];
         smem[IL.o_pl + i] = P.pl[i];
@@ -852,6 +887,7 @@ __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
   in.ord = smem + IL.o_ord;
   in.lag = reinterpret_cast<const uint16_t*>(smem + IL.o_lag);
   in.packed = reinterpret_cast<const uint32_t*>(smem + IL.o_pk32);
+  in.invord = smem + IL.o_inv;
   in.npairs = P.npairs;
   unsigned* shist = reinterpret_cast<unsigned*>(smem + IL.o_hist);
   unsigned* sdhist = reinterpret_cast<unsigned*>(smem + IL.o_dhist);
@@ -903,7 +939,7 @@ __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
           state = kActive;
           continue;
         }
-        decompose_branch<M, G, BOUND>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist);
+        decompose_branch<M, G, BOUND, SMALLN>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist);
         ++sc.decomposed;
         ++nrep;
         rlev = level;
@@ -918,7 +954,7 @@ __global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
         leaf<M, G>(grp, iv, in, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc);
         continue;
       }
-      decompose_branch<M, G, BOUND>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist);
+      decompose_branch<M, G, BOUND, SMALLN>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist);
       ++sc.decomposed;
     }
     if (grp.g == 0) {
@@ -985,6 +1021,7 @@ struct BatchParams {
   const uint8_t* order;
   const uint16_t* lag;
   const uint32_t* packed;
+  const uint8_t* invord;
   int* child_lb;   // [count*n]
   int* lb_fwd;     // [count*n] both sets (before MinMin), for the parity tests
   int* lb_bwd;
@@ -992,7 +1029,7 @@ struct BatchParams {
   uint8_t* pruned; // [count*n]
 };
 
-template <int M, int G, int BOUND>
+template <int M, int G, int BOUND, bool SMALLN = false>
 __global__ void __launch_bounds__(512) decompose_batch_kernel(const BatchParams B) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = B.L;
@@ -1005,7 +1042,10 @@ __global__ void __launch_bounds__(512) decompose_batch_kernel(const BatchParams 
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
-      for (int i = threadIdx.x; i < B.npairs * n; i += blockDim.x) sk[i] = B.packed[i];
+      for (int i = threadIdx.x; i < B.npairs * n; i += blockDim.x) {
+        sk[i] = B.packed[i];
+        smem[IL.o_inv + i] = B.invord[i];
+      }
       for (int i = threadIdx.x; i < B.npairs; i += blockDim.x) {
         smem[IL.o_pk + i] = B.pk[i];
         smem[IL.o_pl + i] = B.pl[i];
@@ -1030,6 +1070,7 @@ __global__ void __launch_bounds__(512) decompose_batch_kernel(const BatchParams 
   in.ord = smem + IL.o_ord;
   in.lag = reinterpret_cast<const uint16_t*>(smem + IL.o_lag);
   in.packed = reinterpret_cast<const uint32_t*>(smem + IL.o_pk32);
+  in.invord = smem + IL.o_inv;
   in.npairs = B.npairs;
   Group<G> grp;
   const int gi = threadIdx.x / G;
@@ -1074,7 +1115,7 @@ __global__ void __launch_bounds__(512) decompose_batch_kernel(const BatchParams 
     fm = grp.ror64(fm);
     grp.sync();
     if constexpr (BOUND == kLB1) children_lb1<M, G>(grp, iv, in, mp, f);
-    else if constexpr (G == 32) children_lb2_w<M>(iv, in, n, mp, f, fm);
+    else if constexpr (G == 32) children_lb2_w<M, SMALLN>(iv, in, n, mp, f, fm);
     else children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
     grp.sync();
     const int dir = minmin<G>(grp, iv, f);

@@ -80,6 +80,7 @@ struct ExploreParams {
   const uint8_t* order;       // [npairs*n]
   const uint16_t* lag;        // [npairs*n] indexed by job
   const uint32_t* packed;     // [n*npairs] transposed packed order (warp-per-explorer LB2)
+  const uint8_t* invord;      // [n*npairs] position of job j in pair q's order
   DevCounters* ctr;
   unsigned long long* hist;   // [n+1] decomposed nodes by free-job count (raw)
   unsigned long long* dhist;  // [n+1] replay duplicates by free-job count

@@ -499,38 +499,39 @@ using ExploreFn = void (*)(ExploreParams);
 using BatchFn = void (*)(BatchParams);
 
 template <int M, int B>
-ExploreFn explore_for_group(int G) {
+ExploreFn explore_for_group(int G, bool small) {
   switch (G) {
     case 4: return explore_kernel<M, 4, B>;
     case 8: return explore_kernel<M, 8, B>;
     case 16: return explore_kernel<M, 16, B>;
-    case 32: return explore_kernel<M, 32, B>;
+    case 32: return (B == kLB2 && small) ? explore_kernel<M, 32, B, true> : explore_kernel<M, 32, B>;
   }
   return nullptr;
 }
 template <int M, int B>
-BatchFn batch_for_group(int G) {
+BatchFn batch_for_group(int G, bool small) {
   switch (G) {
     case 4: return decompose_batch_kernel<M, 4, B>;
     case 8: return decompose_batch_kernel<M, 8, B>;
     case 16: return decompose_batch_kernel<M, 16, B>;
-    case 32: return decompose_batch_kernel<M, 32, B>;
+    case 32: return (B == kLB2 && small) ? decompose_batch_kernel<M, 32, B, true> : decompose_batch_kernel<M, 32, B>;
   }
   return nullptr;
 }
 
-ExploreFn explore_fn(int m, int bound, int G) {
+// SMALLN (n <= 32): LB2 passes iterate the set bits of a 32-bit free-position mask
+ExploreFn explore_fn(int m, int bound, int G, bool small) {
   if (bound == kLB1) {
     switch (m) {
-      case 5: return explore_for_group<5, kLB1>(G);
-      case 10: return explore_for_group<10, kLB1>(G);
-      case 20: return explore_for_group<20, kLB1>(G);
+      case 5: return explore_for_group<5, kLB1>(G, false);
+      case 10: return explore_for_group<10, kLB1>(G, false);
+      case 20: return explore_for_group<20, kLB1>(G, false);
     }
   } else {
     switch (m) {
-      case 5: return explore_for_group<5, kLB2>(G);
-      case 10: return explore_for_group<10, kLB2>(G);
-      case 20: return explore_for_group<20, kLB2>(G);
+      case 5: return explore_for_group<5, kLB2>(G, small);
+      case 10: return explore_for_group<10, kLB2>(G, small);
+      case 20: return explore_for_group<20, kLB2>(G, small);
     }
   }
   return nullptr;
@@ -554,18 +555,18 @@ BigFn big_fn(int m, int bound) {
   return nullptr;
 }
 
-BatchFn batch_fn(int m, int bound, int G) {
+BatchFn batch_fn(int m, int bound, int G, bool small) {
   if (bound == kLB1) {
     switch (m) {
-      case 5: return batch_for_group<5, kLB1>(G);
-      case 10: return batch_for_group<10, kLB1>(G);
-      case 20: return batch_for_group<20, kLB1>(G);
+      case 5: return batch_for_group<5, kLB1>(G, false);
+      case 10: return batch_for_group<10, kLB1>(G, false);
+      case 20: return batch_for_group<20, kLB1>(G, false);
     }
   } else {
     switch (m) {
-      case 5: return batch_for_group<5, kLB2>(G);
-      case 10: return batch_for_group<10, kLB2>(G);
-      case 20: return batch_for_group<20, kLB2>(G);
+      case 5: return batch_for_group<5, kLB2>(G, small);
+      case 10: return batch_for_group<10, kLB2>(G, small);
+      case 20: return batch_for_group<20, kLB2>(G, small);
     }
   }
   return nullptr;
@@ -602,6 +603,7 @@ struct pbbgpu_pool {
   uint8_t *d_pk = nullptr, *d_pl = nullptr, *d_ord = nullptr;
   uint16_t* d_lag = nullptr;
   uint32_t* d_packed = nullptr;
+  uint8_t* d_invord = nullptr;
 
   float* d_lgfact = nullptr;
   float* d_lens = nullptr;
@@ -633,6 +635,7 @@ struct pbbgpu_pool {
     cudaFree(d_ord);
     cudaFree(d_lag);
     cudaFree(d_packed);
+    cudaFree(d_invord);
     cudaFree(d_packed64);
     cudaFree(d_big_scratch);
 
@@ -778,8 +781,8 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   P->L = sz.second.first;
   P->IL = sz.second.second;
   P->mp = P->L.mp;
-  P->efn = explore_fn(m, bound, P->G);
-  P->bfn = batch_fn(m, bound, P->G);
+  P->efn = explore_fn(m, bound, P->G, n <= 32);
+  P->bfn = batch_fn(m, bound, P->G, n <= 32);
   ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->efn), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
   ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->bfn), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
   int per_sm = 0;
@@ -831,6 +834,11 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
     xfer(P, P->d_lag, lag.data(), lag.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, "copy");
     ck(cudaMalloc(&P->d_packed, packed.size() * sizeof(uint32_t)), "malloc");
     xfer(P, P->d_packed, packed.data(), packed.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, "copy");
+    std::vector<uint8_t> inv(static_cast<size_t>(n) * P->npairs, 0);  // [job][pair] -> position
+    for (int q = 0; q < P->npairs; ++q)
+      for (int t = 0; t < n; ++t) inv[static_cast<size_t>(ord16[static_cast<size_t>(q) * n + t]) * P->npairs + q] = static_cast<uint8_t>(t);
+    ck(cudaMalloc(&P->d_invord, inv.size()), "malloc");
+    xfer(P, P->d_invord, inv.data(), inv.size(), cudaMemcpyHostToDevice, "copy");
   }
   DevCounters z{};
   z.best = INT_MAX;
@@ -889,6 +897,7 @@ ExploreParams explore_params(pbbgpu_pool* P) {
   E.order = P->d_ord;
   E.lag = P->d_lag;
   E.packed = P->d_packed;
+  E.invord = P->d_invord;
   E.ctr = P->d_ctr;
   E.hist = P->d_hist;
   E.dhist = P->d_dhist;
@@ -1477,6 +1486,7 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
     B.order = P->d_ord;
     B.lag = P->d_lag;
     B.packed = P->d_packed;
+    B.invord = P->d_invord;
     B.child_lb = dlb;
     B.lb_fwd = dlf;
     B.lb_bwd = dlbw;
