@@ -826,7 +826,7 @@ __device__ __forceinline__ bool midpoint_pos(const int* pos, const int8_t* E, bo
 }
 
 template <int M, int G, int BOUND, bool SMALLN = false>
-__global__ void __launch_bounds__(512) explore_kernel(const ExploreParams P) {
+__global__ void __launch_bounds__(1024) explore_kernel(const ExploreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = P.L;
   const int n = L.n, mp = L.mp;
@@ -1030,7 +1030,7 @@ struct BatchParams {
 };
 
 template <int M, int G, int BOUND, bool SMALLN = false>
-__global__ void __launch_bounds__(512) decompose_batch_kernel(const BatchParams B) {
+__global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams B) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = B.L;
   const int n = L.n, mp = L.mp;

@@ -760,7 +760,7 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   int best_bs = 0;
   long best_res = -1;
   for (;;) {
-    for (int BS : {128, 256, 512}) {
+    for (int BS : {128, 256, 512, 768, 1024}) {
       const size_t need = size_for(P->G, BS).first;
       if (need > smem_cap) continue;
       const long ctas = std::min<long>({static_cast<long>(smem_sm / (need + 1024)), 2048L / BS, 32L});
