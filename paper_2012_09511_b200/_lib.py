@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpbbgpu.so")
+LIB_PATH = os.environ.get("PBBGPU_LIB") or os.path.join(_HERE, "libpbbgpu.so")  # override: A/B dev runs
 
 PBBGPU_OK = 0
 PBBGPU_ERR_ARG = -1

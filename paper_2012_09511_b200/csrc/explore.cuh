@@ -428,30 +428,30 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
       }
      }
     } else if (live) {
+      // n <= 64: same set-bit iteration over a 64-bit free-position mask
+      unsigned long long Fq = 0;
+      for (int c = 0; c < f; ++c) Fq |= 1ull << in.invord[iv.freej[c] * P + q];
       int A = 0, Bp = 0, pm = NEG;
-      for (int t = 0; t < n; ++t) {
-        const unsigned e = in.packed[t * P + q];
+      for (unsigned long long w = Fq; w; w &= w - 1) {
+        const unsigned e = in.packed[(__ffsll(static_cast<long long>(w)) - 1) * P + q];
         const int j = e & 63;
-        if ((fmask >> j) & 1ull) {
-          A += (e >> 6) & 127;
-          const int X = A + static_cast<int>(e >> 20) - Bp;
-          PMl[j * 32] = static_cast<int16_t>(pm);
-          pm = max(pm, X);
-          Bp += (e >> 13) & 127;
-        }
+        A += (e >> 6) & 127;
+        const int X = A + static_cast<int>(e >> 20) - Bp;
+        PMl[j * 32] = static_cast<int16_t>(pm);
+        pm = max(pm, X);
+        Bp += (e >> 13) & 127;
       }
-      int As = 0, Bs = Atot - Btot, sm = NEG;  // Bs = B_{>=i} + (A - B)
-      for (int t = n - 1; t >= 0; --t) {
+      int As = 0, Bs = Atot - Btot, sm = NEG;
+      for (unsigned long long w = Fq; w;) {
+        const int t = 63 - __clzll(static_cast<long long>(w));
+        w ^= 1ull << t;
         const unsigned e = in.packed[t * P + q];
         const int j = e & 63;
-        if ((fmask >> j) & 1ull) {
-          Bs += (e >> 13) & 127;
-          // X'_i = A_{<=i} + lag_i - B_{<i} = (Atot - As) + lag_i + (B_{>=i} - Btot)
-          const int X = static_cast<int>(e >> 20) + Bs - As;
-          SMl[j * 32] = static_cast<int16_t>(sm);
-          sm = max(sm, X);
-          As += (e >> 6) & 127;
-        }
+        Bs += (e >> 13) & 127;
+        const int X = static_cast<int>(e >> 20) + Bs - As;
+        SMl[j * 32] = static_cast<int16_t>(sm);
+        sm = max(sm, X);
+        As += (e >> 6) & 127;
       }
     }
     const int qk = iv.tl[k], ql = iv.tl[l], rk = iv.fr[k], rl = iv.fr[l];
