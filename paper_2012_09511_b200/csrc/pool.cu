@@ -971,6 +971,10 @@ int run_round(pbbgpu_pool* P) {
   }
   ExploreParams E = explore_params(P);
   if (P->cfg.pinned) E.pinned_ub = static_cast<int>(std::min<int64_t>(P->pinned_ub, INT_MAX));
+  // adaptive round length: while many explorers are idle (ramp-up, tail) the steal phase is
+  // what matters, so rounds are 4x shorter; when (almost) all are busy, full-length rounds
+  if (E.budget_ns && P->rounds > 0 && P->last_active * 4 < P->K * 3)
+    E.budget_ns = std::max<unsigned long long>(E.budget_ns / 4, 250000ull);
   StealParams S{};
   S.L = P->L;
   S.state = P->d_state;
