@@ -39,6 +39,12 @@ WORKLOADS = {
                       desc="Taillard ta021 (20x20), LB2 Johnson bound, initial UB = optimum 2297, full proof per step"),
     "ta021-lb1": dict(instance="ta021", bound="lb1", ub=2297,
                       desc="Taillard ta021 (20x20), LB1 one-machine bound, initial UB = optimum 2297, full proof per step"),
+    "ta041-lb1-pinned": dict(instance="ta041", bound="lb1", ub=3000, pinned=True,
+                             desc="Taillard ta041 (50x10), LB1, pinned UB 3000 (prune >= 3000, never improve): "
+                                  "fixed tree of 520,458,272 nodes per step"),
+    "ta056-lb2": dict(instance="ta056", bound="lb2", ub=3679, time_limit=10.0,
+                      desc="Taillard ta056 (50x20), LB2, initial UB = best-known 3679, 10 s time-bounded "
+                           "exploration per step"),
 }
 
 # algorithmic 32-bit integer ops per decomposed node as a function of the
@@ -120,6 +126,15 @@ def cpu_cores():
 def cpu_sample(wl, seconds, cores):
     """Reference CPU arm on a bounded sample: nodes/s of the CPU implementation."""
     inst, bound, ub = wl["instance"], wl["bound"], wl["ub"]
+    if bound == "lb1" and wl.get("pinned"):
+        drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+        if os.path.exists(drv):
+            out = subprocess.run([drv, "pinned", inst, str(ub), str(cores), str(seconds), "3"],
+                                 capture_output=True, text=True, check=True).stdout
+            r = json.loads(out.strip().splitlines()[-1])
+            return {"value": r["nodes_per_s"], "unit": "nodes/s", "cores": cores, "kind": "reference",
+                    "sample": f"oracle/_ref/ref_driver pinned {inst} LB1 prune>={ub}, {cores} threads over "
+                              f"depth-3 prefix subtrees, {seconds:.0f} s ({r['unique']} unique nodes)"}
     if bound == "lb1":
         drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
         if os.path.exists(drv):
@@ -253,6 +268,7 @@ def main():
     ap.add_argument("--round-us", type=float, default=0.0, help="device time per round (0 = library default)")
     ap.add_argument("--rounds-per-sync", type=int, default=0, help="rounds per host sync / exchange (0 = default)")
     ap.add_argument("--export-max", type=int, default=0, help="intervals one rank may donate per exchange")
+    ap.add_argument("--max-split", type=int, default=0, help="thieves per victim per steal phase (0 = default)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
 
@@ -275,7 +291,10 @@ def main():
     inst = pbb.taillard_named(wl["instance"])
     n, m = inst.n, inst.m
     W = w_lb2 if wl["bound"] == "lb2" else w_lb1
-    cfg = pbb.PoolConfig(device=local, round_us=args.round_us, rounds_per_sync=args.rounds_per_sync)
+    world_ = world
+    cfg = pbb.PoolConfig(device=local, round_us=args.round_us, rounds_per_sync=args.rounds_per_sync,
+                         pinned=bool(wl.get("pinned", False)), max_split=args.max_split)
+    tlim = float(wl.get("time_limit", 0.0))
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -291,7 +310,7 @@ def main():
 
     def step(pool):
         before = pool.stats()
-        res = solve_distributed(pool, wl["ub"], device=dev, export_max=args.export_max or None)
+        res = solve_distributed(pool, wl["ub"], device=dev, export_max=args.export_max or None, time_limit_s=tlim)
         after = pool.stats()
         return res, before, after
 
@@ -319,9 +338,10 @@ def main():
             launches += after.kernel_launches - before.kernel_launches
     clocks = clk.summary()
     unique = results[-1].unique
-    assert all(r.unique == unique and r.completed for r in results), "fixed-tree steps must repeat exactly"
+    if not tlim:
+        assert all(r.unique == unique and r.completed for r in results), "fixed-tree steps must repeat exactly"
     total_ms = sum(times)
-    value = unique * len(times) / (total_ms / 1000.0)
+    value = sum(r.unique for r in results) / (total_ms / 1000.0)
 
     # roofline of the dominant kernel (explore_kernel): algorithmic int ops / its device time
     hist = results[-1].hist
@@ -340,23 +360,24 @@ def main():
     # e2e: the C-ABI call a user makes, HOST buffers in, results back to host, per step
     e2e = None
     if not args.no_e2e:
-        e_times, h2d, d2h = [], 0, 0
+        e_times, h2d, d2h, e_nodes = [], 0, 0, 0
         for i in range(1 + args.steps):
             flush.zero_()
             barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             p2 = pbb.GpuPool(pbb.Instance(n, m, inst.p.copy()), cfg, bound=wl["bound"])
-            r = solve_distributed(p2, wl["ub"], device=dev)
+            r = solve_distributed(p2, wl["ub"], device=dev, time_limit_s=tlim)
             st = p2.stats()
             p2.close()
             torch.cuda.synchronize()
             dt = maxred(time.perf_counter() - t0)
-            assert r.unique == unique
+            assert tlim or r.unique == unique
             if i > 0:  # first one warms the create path
                 e_times.append(dt)
+                e_nodes += r.unique
                 h2d, d2h = st.h2d_bytes, st.d2h_bytes
-        e2e = {"value": unique / statistics.mean(e_times), "unit": "nodes/s", "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": (e_nodes / sum(e_times)) if tlim else unique / statistics.mean(e_times), "unit": "nodes/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "s_per_step": statistics.mean(e_times),
                "path": "pbbgpu_create(host matrix) + pbbgpu_solve + stats/hist/best to host + pbbgpu_destroy"}
 
@@ -374,7 +395,8 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "int32",
                 "data": "synthetic (Taillard instance regenerated from its published seed; exact benchmark matrix)",
                 "config": {"workload": args.workload, "instance": wl["instance"], "bound": wl["bound"].upper(),
-                           "initial_ub": wl["ub"], "mode": "full proof (fixed tree) per step",
+                           "initial_ub": wl["ub"],
+                           "mode": (f"time-bounded ({tlim:g} s) per step" if tlim else "full proof (fixed tree) per step"),
                            "unique_nodes_per_step": unique, "leaves_per_step": results[-1].leaves,
                            "time_to_proof_ms": statistics.mean(times), "explorers_per_gpu": pool.K(),
                            "parallelism": f"dp{world}" if world > 1 else "single",

@@ -67,6 +67,7 @@ typedef struct {
   double round_us;       /* device time per round; 0 = auto (2000 us, or steps_per_round if set) */
   double steal_trigger;  /* steal phase when active < trigger*K; 0 = 1.0 (reference pool: 0.8) */
   int rounds_per_sync;   /* (explore, steal) rounds per pbbgpu_run_round host sync; 0 = 2, max 8 */
+  int max_split;         /* thieves one victim may feed per steal phase (multi-way split); 0 = 4 */
 } pbbgpu_config_t;
 
 typedef struct {

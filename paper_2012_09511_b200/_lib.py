@@ -44,6 +44,7 @@ class Config(ctypes.Structure):
         ("round_us", ctypes.c_double),
         ("steal_trigger", ctypes.c_double),
         ("rounds_per_sync", ctypes.c_int),
+        ("max_split", ctypes.c_int),
     ]
 
 

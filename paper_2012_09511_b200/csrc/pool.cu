@@ -275,6 +275,7 @@ struct StealParams {
   const float* lgfact;  // [n+1] log2(k!)
   float trigger;        // steal when active < trigger * K (reference: 0.8, explorer.cpp:251)
   const float* lens;    // [K] per-explorer log2 remaining (written by explore_kernel)
+  int max_split;        // thieves per victim in one steal phase (multi-way split), 1..63
 };
 
 constexpr int kStealThreads = 1024;
@@ -300,6 +301,96 @@ __global__ void lens_kernel(IvmLayout L, const unsigned char* state, int K, cons
     }
   }
   lens[i] = lg;
+}
+
+// ---- multi-way interval splitting (exact mixed-radix arithmetic, no big integers)
+// D = end - pos as digits plus a top unit of weight n! (end = n! when !has_end).
+__device__ bool diff_digits(const int* pos, const int8_t* E, bool has_end, int n, int* D, int& top) {
+  top = 0;
+  if (has_end) {
+    int borrow = 0;
+    for (int l = n - 1; l >= 0; --l) {
+      int d = E[l] - pos[l] - borrow;
+      borrow = d < 0;
+      if (borrow) d += n - l;
+      D[l] = d;
+    }
+    return !borrow;
+  }
+  int carry = 1;  // n! - pos = ((n! - 1) - pos) + 1
+  for (int l = n - 1; l >= 0; --l) {
+    int d = n - 1 - l - pos[l] + carry;
+    carry = d > n - 1 - l;
+    if (carry) d = 0;
+    D[l] = d;
+  }
+  top = carry;
+  return true;
+}
+
+// b = pos + floor(i * D / parts): long division from the most significant digit (the
+// remainder converts into units of the next, smaller weight), quotient digits normalized
+// from the least significant one, then a mixed-radix add.
+__device__ void split_point(const int* pos, const int* D, int top, int i, int parts, int n, int* b) {
+  int rem = i * top;
+  for (int l = 0; l < n; ++l) {
+    const int cur = rem * (n - l) + i * D[l];
+    b[l] = cur / parts;
+    rem = cur % parts;
+  }
+  for (int l = n - 1; l > 0; --l) {
+    if (b[l] > n - 1 - l) {
+      b[l - 1] += b[l] / (n - l);
+      b[l] %= n - l;
+    }
+  }
+  int carry = 0;
+  for (int l = n - 1; l >= 0; --l) {
+    const int s = pos[l] + b[l] + carry, radix = n - l;
+    b[l] = s % radix;
+    carry = s / radix;
+  }
+}
+
+// Cut the victim's remaining [pos, end) into r + 1 equal parts: the victim keeps the first,
+// thieves[0..r) are seated on the others (steal_right_half, generalised to r thieves).
+// Returns the number of thieves seated.
+__device__ int multi_split(unsigned char* vb, const IvmLayout& L, const int* ptot, unsigned char* const* tbs, int r,
+                           int* pos, int* D, int* b, int* prevb, int* oend) {
+  const int n = L.n;
+  IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
+  const int8_t* V = reinterpret_cast<const int8_t*>(vb + L.o_v);
+  int8_t* E = reinterpret_cast<int8_t*>(vb + L.o_end);
+  if (!effective_pos(V, vh->level, reinterpret_cast<const int8_t*>(vb + L.o_cells), n, pos)) return 0;
+  const bool had_end = vh->has_end != 0;
+  int top = 0;
+  if (!diff_digits(pos, E, had_end, n, D, top)) return 0;
+  // at least 2 leaves per part: shrink r while D < 2 (r + 1)
+  if (!top) {
+    long long small = 0;  // exact value when D is small (leading zeros)
+    bool big = false;
+    for (int l = 0; l < n && !big; ++l) {
+      small = small * (n - l) + D[l];
+      if (small > (1ll << 40)) big = true;
+    }
+    if (!big) {
+      if (small < 2) return 0;
+      r = static_cast<int>(min(static_cast<long long>(r), max(small / 2 - 1, 1ll)));
+    }
+  }
+  for (int l = 0; l < n; ++l) oend[l] = E[l];
+  const int parts = r + 1;
+  split_point(pos, D, top, 1, parts, n, prevb);  // end of the victim's part
+  for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(prevb[l]);
+  vh->has_end = 1;
+  for (int i = 1; i <= r; ++i) {
+    const bool last = i == r;
+    if (!last) split_point(pos, D, top, i + 1, parts, n, b);
+    seat_explorer(tbs[i - 1], L, ptot, prevb, last ? oend : b, last ? had_end : true);
+    if (!last)
+      for (int l = 0; l < n; ++l) prevb[l] = b[l];
+  }
+  return r;
 }
 
 // Steal phase (src/explorer.cpp:283-340, B200 form). The explore kernel leaves one float per
@@ -352,32 +443,24 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
     s_tot[1] = acc;
   }
   __syncthreads();
-  const int npairs = min(s_tot[1], total_idle);
+  // thieves per victim: one when victims suffice, otherwise r-way splits of the longest
+  const int nvict = s_tot[1];
+  const int rs = nvict >= total_idle ? 1 : min(S.max_split, total_idle / max(nvict, 1));
+  const int nv = min(nvict, total_idle / rs);
   for (int i = t; i < K; i += kStealThreads) {
     const float lg = S.lens[i];
     if (lg >= S.min_log2 && lg >= 1.f) {
       const int rank = atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
-      if (rank < npairs) S.victim[rank] = i;
+      if (rank < nv) S.victim[rank] = i;
     }
   }
   __syncthreads();
   int ok = 0;
-  const int n = S.L.n;
-  int pos[kMaxN], mid[kMaxN], oend[kMaxN];
-  for (int pidx = t; pidx < npairs; pidx += kStealThreads) {
-    unsigned char* vb = S.state + static_cast<size_t>(S.victim[pidx]) * S.L.gstride;
-    unsigned char* tb = S.state + static_cast<size_t>(S.thief[pidx]) * S.L.gstride;
-    IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
-    const int8_t* V = reinterpret_cast<const int8_t*>(vb + S.L.o_v);
-    int8_t* E = reinterpret_cast<int8_t*>(vb + S.L.o_end);
-    for (int l = 0; l < n; ++l) oend[l] = E[l];
-    if (!effective_pos(V, vh->level, reinterpret_cast<const int8_t*>(vb + S.L.o_cells), n, pos)) continue;
-    if (!midpoint_pos(pos, E, vh->has_end != 0, n, mid)) continue;  // end < pos + 2 (explorer.cpp:270)
-    const bool had_end = vh->has_end != 0;
-    seat_explorer(tb, S.L, S.ptot, mid, oend, had_end);
-    for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(mid[l]);
-    vh->has_end = 1;
-    ++ok;
+  int pos[kMaxN], D[kMaxN], b[kMaxN], pb[kMaxN], oend[kMaxN];
+  unsigned char* tbs[63];
+  for (int v = t; v < nv; v += kStealThreads) {
+    for (int i = 0; i < rs; ++i) tbs[i] = S.state + static_cast<size_t>(S.thief[v * rs + i]) * S.L.gstride;
+    ok += multi_split(S.state + static_cast<size_t>(S.victim[v]) * S.L.gstride, S.L, S.ptot, tbs, rs, pos, D, b, pb, oend);
   }
   atomicAdd(&s_tot[2], ok);
   __syncthreads();
@@ -398,13 +481,10 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
   __shared__ int bins[kBins];
   __shared__ int s_tot[2];
   const int t = threadIdx.x, K = S.K, n = S.L.n;
-  const int CH = (K + kStealThreads - 1) / kStealThreads;
-  const int lo = t * CH, hi = min(K, lo + CH);
   for (int b = t; b < kBins; b += kStealThreads) bins[b] = 0;
   if (t < 2) s_tot[t] = 0;
   __syncthreads();
-  int pos[kMaxN], mid[kMaxN];
-  for (int i = lo; i < hi; ++i) {
+  for (int i = t; i < K; i += kStealThreads) {
     const float lg = S.lens[i];
     if (lg >= S.min_log2 && lg >= 1.f) atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
   }
@@ -416,37 +496,67 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
       bins[b] = acc;
       acc += c;
     }
+    s_tot[1] = acc;
   }
   __syncthreads();
-  for (int i = lo; i < hi; ++i) {
+  // r parts exported per victim: one when victims suffice, more when only a few hold work
+  const int nvict = s_tot[1];
+  const int r = nvict >= want ? 1 : min(63, (want + max(nvict, 1) - 1) / max(nvict, 1));  // export: up to 63
+  const int nv = min(nvict, (want + r - 1) / r);
+  for (int i = t; i < K; i += kStealThreads) {
     const float lg = S.lens[i];
     if (lg >= S.min_log2 && lg >= 1.f) {
       const int rank = atomicAdd(&bins[min(kBins - 1, static_cast<int>(lg * 4.f))], 1);
-      if (rank < want) S.victim[rank] = i;
-      if (rank < want) atomicAdd(&s_tot[1], 1);
+      if (rank < nv) S.victim[rank] = i;
     }
   }
   __syncthreads();
-  const int npairs = s_tot[1];
-  for (int pidx = t; pidx < npairs; pidx += kStealThreads) {
-    unsigned char* vb = S.state + static_cast<size_t>(S.victim[pidx]) * S.L.gstride;
+  int pos[kMaxN], D[kMaxN], b[kMaxN], pb[kMaxN], oend[kMaxN];
+  for (int v = t; v < nv; v += kStealThreads) {
+    unsigned char* vb = S.state + static_cast<size_t>(S.victim[v]) * S.L.gstride;
     IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
     const int8_t* V = reinterpret_cast<const int8_t*>(vb + S.L.o_v);
     int8_t* E = reinterpret_cast<int8_t*>(vb + S.L.o_end);
     if (!effective_pos(V, vh->level, reinterpret_cast<const int8_t*>(vb + S.L.o_cells), n, pos)) continue;
-    if (!midpoint_pos(pos, E, vh->has_end != 0, n, mid)) continue;
-    const int slot = atomicAdd(&s_tot[0], 1);
-    int* o = out_digits + static_cast<size_t>(slot) * 2 * n;
-    for (int l = 0; l < n; ++l) {
-      o[l] = mid[l];
-      o[n + l] = vh->has_end ? E[l] : 0;
+    const bool had_end = vh->has_end != 0;
+    int top = 0;
+    if (!diff_digits(pos, E, had_end, n, D, top)) continue;
+    int rv = r;
+    if (!top) {
+      long long small = 0;
+      bool big = false;
+      for (int l = 0; l < n && !big; ++l) {
+        small = small * (n - l) + D[l];
+        if (small > (1ll << 40)) big = true;
+      }
+      if (!big) {
+        if (small < 2) continue;
+        rv = static_cast<int>(min(static_cast<long long>(rv), max(small / 2 - 1, 1ll)));
+      }
     }
-    out_nf[slot] = vh->has_end ? 0 : 1;
-    for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(mid[l]);
+    const int slot0 = atomicAdd(&s_tot[0], rv);
+    if (slot0 >= want) continue;
+    rv = min(rv, want - slot0);  // never more than the caller's buffer
+    for (int l = 0; l < n; ++l) oend[l] = E[l];
+    const int parts = rv + 1;
+    split_point(pos, D, top, 1, parts, n, pb);
+    for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(pb[l]);
     vh->has_end = 1;
+    for (int i = 1; i <= rv; ++i) {
+      const bool last = i == rv;
+      if (!last) split_point(pos, D, top, i + 1, parts, n, b);
+      int* o = out_digits + static_cast<size_t>(slot0 + i - 1) * 2 * n;
+      for (int l = 0; l < n; ++l) {
+        o[l] = pb[l];
+        o[n + l] = last ? (had_end ? oend[l] : 0) : b[l];
+      }
+      out_nf[slot0 + i - 1] = last ? (had_end ? 0 : 1) : 0;
+      if (!last)
+        for (int l = 0; l < n; ++l) pb[l] = b[l];
+    }
   }
   __syncthreads();
-  if (t == 0) *out_count = s_tot[0];
+  if (t == 0) *out_count = min(s_tot[0], want);
 }
 
 // Idle explorers in index order (slots for assign / import) and their count.
@@ -987,6 +1097,7 @@ int run_round(pbbgpu_pool* P) {
   S.lgfact = P->d_lgfact;
   S.trigger = static_cast<float>(P->cfg.steal_trigger > 0 ? P->cfg.steal_trigger : 1.0);
   S.lens = P->d_lens;
+  S.max_split = P->cfg.max_split > 0 ? std::min(P->cfg.max_split, 63) : 4;
   // several (explore, steal) rounds back to back per host synchronization: the rounds are
   // device-timed, and a round after exhaustion costs only the state copy of an empty launch
   const int R = P->rounds_per_sync;
@@ -1240,8 +1351,8 @@ int pbbgpu_export(pbbgpu_pool* P, int max_count, uint16_t* a_out, uint16_t* b_ou
     int* d_dig = nullptr;
     uint8_t* d_nf = nullptr;
     int* d_cnt = nullptr;
-    ck(cudaMalloc(&d_dig, static_cast<size_t>(want) * 2 * n * sizeof(int)), "malloc");
-    ck(cudaMalloc(&d_nf, static_cast<size_t>(want)), "malloc");
+    ck(cudaMalloc(&d_dig, static_cast<size_t>(want + 64) * 2 * n * sizeof(int)), "malloc");
+    ck(cudaMalloc(&d_nf, static_cast<size_t>(want + 64)), "malloc");
     ck(cudaMalloc(&d_cnt, sizeof(int)), "malloc");
     StealParams S{};
     S.L = P->L;

@@ -102,8 +102,11 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
         if int(g[:, 2].max()):
             completed = False
             break
-        receivers = [r for r in range(world) if actives[r] < low]
-        donors = [r for r in np.argsort(-actives, kind="stable") if actives[r] >= 2 * low and actives[r] > 0]
+        # receivers run low and hold less than half of the busiest rank; donors hold at least
+        # half of it (multi-way splits let even a handful of explorers feed a receiver)
+        amax = int(actives.max())
+        receivers = [r for r in range(world) if actives[r] < low and 2 * actives[r] < amax]
+        donors = [int(r) for r in np.argsort(-actives, kind="stable") if actives[r] > 0 and 2 * actives[r] >= amax]
         if not receivers or not donors:
             continue
         # phase 2: donors export, everybody gathers, receivers seat their share

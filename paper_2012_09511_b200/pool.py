@@ -45,6 +45,7 @@ class PoolConfig:
     round_us: float = 0.0       # device time per round; 0 = auto
     steal_trigger: float = 0.0  # steal when active < trigger*K; 0 = 1.0 (reference: 0.8)
     rounds_per_sync: int = 0    # device rounds per run_round() call; 0 = 2
+    max_split: int = 0          # thieves per victim per steal phase (multi-way split); 0 = 4
 
     def to_c(self) -> _lib.Config:
         c = _lib.Config()
@@ -60,6 +61,7 @@ class PoolConfig:
         c.round_us = self.round_us
         c.steal_trigger = self.steal_trigger
         c.rounds_per_sync = self.rounds_per_sync
+        c.max_split = self.max_split
 
         return c
 

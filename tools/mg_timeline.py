@@ -10,7 +10,8 @@ dist.init_process_group("nccl", device_id=dev)
 rank, world = dist.get_rank(), dist.get_world_size()
 name, ub, bound = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 low = float(sys.argv[4]) if len(sys.argv) > 4 else 0.25
-pool = pbb.GpuPool(pbb.taillard_named(name), pbb.PoolConfig(device=local), bound=bound)
+pinned = len(sys.argv) > 5 and sys.argv[5] == "pinned"
+pool = pbb.GpuPool(pbb.taillard_named(name), pbb.PoolConfig(device=local, pinned=pinned), bound=bound)
 multi.solve_distributed(pool, ub, device=dev, low_fraction=low)  # warm
 log = []
 orig = pool.run_round
