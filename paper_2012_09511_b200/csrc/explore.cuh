@@ -149,21 +149,10 @@ struct Group {
   }
   __device__ __forceinline__ void sync() const { __syncwarp(mask); }
   __device__ __forceinline__ int bcast(int v, int src) const { return __shfl_sync(mask, v, src, G); }
-  __device__ __forceinline__ int rmin(int v) const {
-#pragma unroll
-    for (int o = G / 2; o; o >>= 1) v = min(v, __shfl_xor_sync(mask, v, o, G));
-    return v;
-  }
-  __device__ __forceinline__ int rmax(int v) const {
-#pragma unroll
-    for (int o = G / 2; o; o >>= 1) v = max(v, __shfl_xor_sync(mask, v, o, G));
-    return v;
-  }
-  __device__ __forceinline__ int rsum(int v) const {
-#pragma unroll
-    for (int o = G / 2; o; o >>= 1) v += __shfl_xor_sync(mask, v, o, G);
-    return v;
-  }
+  // REDUX (sm_80+): one instruction per reduction over the group's lanes
+  __device__ __forceinline__ int rmin(int v) const { return __reduce_min_sync(mask, v); }
+  __device__ __forceinline__ int rmax(int v) const { return __reduce_max_sync(mask, v); }
+  __device__ __forceinline__ int rsum(int v) const { return __reduce_add_sync(mask, v); }
   __device__ __forceinline__ unsigned long long ror64(unsigned long long v) const {
 #pragma unroll
     for (int o = G / 2; o; o >>= 1) v |= __shfl_xor_sync(mask, v, o, G);
@@ -648,7 +637,9 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
   const int job = (x < 0 ? -x : x) - 1;
   const int dI = iv.dir[I];
   node_tables<M, G>(grp, iv, in, n, mp, job, dI, d1, d2);
-  const unsigned long long fm = grp.ror64(gather_free<G>(grp, iv, row, sel, f));
+  const unsigned long long fm0 = gather_free<G>(grp, iv, row, sel, f);
+  unsigned long long fm = 0;
+  if constexpr (BOUND == kLB2) fm = grp.ror64(fm0);  // LB1 does not use the free set mask
   grp.sync();
   if constexpr (BOUND == kLB1) {
     children_lb1<M, G>(grp, iv, in, mp, f);
