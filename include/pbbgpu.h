@@ -22,6 +22,9 @@
  *   pbbgpu_histogram                <- (new) decomposed nodes by free-job count (roofline)
  *   pbbgpu_decompose_batch          <- decompose(inst, sub, incumbent, ...) (bound.hpp:78-79)
  *   pbbgpu_solve                    <- pool_run(inst, ub, intervals, cfg) (explorer.hpp:145-146)
+ *   pbbgpu_insertion_ls             <- insertion_local_search           (heuristic.hpp:27, heuristic.cpp:105-155)
+ *   pbbgpu_offer_schedule           <- ExplorerPool::offer_schedule     (explorer.hpp:93)
+ *   pbbgpu_promote                  <- ExplorerPool::promote_solutions  (explorer.hpp:99, explorer.cpp:397-424)
  *   pbbgpu_int32_peak               <- (new) integer-ALU roofline denominator
  *   pbbgpu_taillard / pbbgpu_makespan / pbbgpu_neh
  *                                   <- generate_taillard / taillard_named / makespan / neh
@@ -139,6 +142,12 @@ int pbbgpu_decompose_batch(pbbgpu_pool* pool, const int32_t* perms, const int32_
 
 /* raw explorer blocks (debugging): K * gstride bytes; offsets = cells, V, dir, end, tgt, ft, R */
 int pbbgpu_debug_state(pbbgpu_pool* pool, uint8_t* out, int64_t cap, int* gstride, int* offsets);
+
+/* heuristic cooperation (the worker's heuristic agents) */
+int64_t pbbgpu_insertion_ls(int n, int m, const int32_t* p, const int32_t* seed_perm, uint64_t max_iter,
+                            double max_seconds, uint64_t rng_seed, int32_t* perm_out);
+int pbbgpu_offer_schedule(pbbgpu_pool* pool, const int32_t* perm, int64_t cmax, int* taken);
+int pbbgpu_promote(pbbgpu_pool* pool, int capacity, int32_t* perms_out, int64_t* cmax_out, int* count);
 
 /* INT32 ALU microbenchmark (add + max streams, the bounding kernels' instruction mix):
  * measured integer-op throughput of the device, the roofline denominator of the bounding

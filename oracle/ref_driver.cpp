@@ -16,6 +16,7 @@
 //   pinned <ta> <ub> <threads> <seconds> <prefix_depth>   prune>=ub, never improve
 //   neh    <ta>                                           NEH makespan + perm
 //   inst   <ta>                                           processing-time matrix
+//   ils    <ta> <iterations> <rng_seed>                   NEH + insertion_local_search
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -250,6 +251,20 @@ int cmd_neh(int argc, char** argv) {
   return 0;
 }
 
+// NEH then insertion_local_search (src/heuristic.cpp:105-155) with an iteration budget.
+int cmd_ils(int argc, char** argv) {
+  if (argc < 5) return 2;
+  Instance inst = taillard_named(argv[2]);
+  SearchBudget budget;
+  budget.max_iterations = std::strtoull(argv[3], nullptr, 10);
+  Schedule s = insertion_local_search(inst, neh(inst), budget, std::strtoull(argv[4], nullptr, 10));
+  std::printf("{\"mode\":\"ils\",\"instance\":\"%s\",\"iterations\":%s,\"rng_seed\":%s,\"cmax\":%lld,\"perm\":[",
+              argv[2], argv[3], argv[4], (long long)s.cmax);
+  for (std::size_t i = 0; i < s.perm.size(); ++i) std::printf("%s%d", i ? "," : "", s.perm[i]);
+  std::printf("]}\n");
+  return 0;
+}
+
 int cmd_inst(int argc, char** argv) {
   if (argc < 3) return 2;
   Instance inst = taillard_named(argv[2]);
@@ -277,6 +292,7 @@ int main(int argc, char** argv) {
     else if (mode == "pinned") rc = cmd_pinned(argc, argv);
     else if (mode == "neh") rc = cmd_neh(argc, argv);
     else if (mode == "inst") rc = cmd_inst(argc, argv);
+    else if (mode == "ils") rc = cmd_ils(argc, argv);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_driver: %s\n", e.what());
     return 1;

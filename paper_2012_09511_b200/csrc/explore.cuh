@@ -712,8 +712,10 @@ __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, con
       const int old = atomicMin(&ctr->best, mk);
       if (mk < old) {
         ++sc.improvements;
-        const int slot = atomicAdd(&ctr->imp_count, 1);
-        if (slot < kImpCap) {
+        // ring of records: the newest (best) improvements survive an overflow; the host
+        // re-evaluates every record's schedule and keeps the best valid one
+        const int slot = atomicAdd(&ctr->imp_count, 1) % kImpCap;
+        {
           ImpRecord* r = imp + slot;
           int a = 0, b = 0;
           for (int l = 0; l <= level; ++l) {

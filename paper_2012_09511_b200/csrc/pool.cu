@@ -17,6 +17,7 @@
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -147,6 +148,87 @@ int64_t neh_host(int n, int m, const int32_t* p, int32_t* out) {
   }
   for (int i = 0; i < n; ++i) out[i] = seq[static_cast<size_t>(i)];
   return last;
+}
+
+// Makespans of inserting `job` at every position 0..len of `seq` in O(len*m) total
+// (prefix heads e, suffix tails q; the scan of src/heuristic.cpp:24-69). Returns the values.
+void insertion_scan(int m, const int32_t* p, const std::vector<int>& seq, int job, std::vector<int64_t>& vals,
+                    std::vector<int64_t>& e, std::vector<int64_t>& q) {
+  const int len = static_cast<int>(seq.size());
+  e.assign(static_cast<size_t>(len + 1) * m, 0);
+  q.assign(static_cast<size_t>(len + 2) * m, 0);
+  for (int i = 1; i <= len; ++i) {
+    const int32_t* row = p + static_cast<size_t>(seq[static_cast<size_t>(i - 1)]) * m;
+    for (int k = 0; k < m; ++k) {
+      const int64_t up = k ? e[static_cast<size_t>(i) * m + k - 1] : 0;
+      e[static_cast<size_t>(i) * m + k] = std::max(up, e[static_cast<size_t>(i - 1) * m + k]) + row[k];
+    }
+  }
+  for (int i = len; i >= 1; --i) {
+    const int32_t* row = p + static_cast<size_t>(seq[static_cast<size_t>(i - 1)]) * m;
+    for (int k = m - 1; k >= 0; --k) {
+      const int64_t dn = k < m - 1 ? q[static_cast<size_t>(i) * m + k + 1] : 0;
+      q[static_cast<size_t>(i) * m + k] = std::max(dn, q[static_cast<size_t>(i + 1) * m + k]) + row[k];
+    }
+  }
+  const int32_t* jr = p + static_cast<size_t>(job) * m;
+  vals.assign(static_cast<size_t>(len + 1), 0);
+  std::vector<int64_t> f(static_cast<size_t>(m));
+  for (int pos = 0; pos <= len; ++pos) {
+    int64_t v = 0;
+    for (int k = 0; k < m; ++k) {
+      f[static_cast<size_t>(k)] = std::max(k ? f[static_cast<size_t>(k - 1)] : 0, e[static_cast<size_t>(pos) * m + k]) + jr[k];
+      v = std::max(v, f[static_cast<size_t>(k)] + q[static_cast<size_t>(pos + 1) * m + k]);
+    }
+    vals[static_cast<size_t>(pos)] = v;
+  }
+}
+
+// First-improvement remove-and-reinsert descent with seeded tie-breaking among equally good
+// positions (insertion_local_search, src/heuristic.cpp:105-155): positions scanned left to
+// right, until a local optimum or the budget (iterations / seconds) runs out.
+int64_t insertion_ls_host(int n, int m, const int32_t* p, const int32_t* seed, uint64_t max_iter, double max_s,
+                          uint64_t rng_seed, int32_t* out) {
+  if (max_iter == 0 && max_s <= 0) throw std::invalid_argument("search budget needs an iteration or time bound");
+  std::vector<int> cur(seed, seed + n);
+  int64_t cmax = makespan_host(n, m, p, seed);
+  std::mt19937_64 rng(rng_seed);
+  std::vector<int64_t> vals, e, q;
+  std::vector<int> reduced, ties;
+  const auto t0 = std::chrono::steady_clock::now();
+  uint64_t it = 0;
+  auto spent = [&] {
+    if (max_iter > 0 && it >= max_iter) return true;
+    if (max_s > 0) {
+      const std::chrono::duration<double> el = std::chrono::steady_clock::now() - t0;
+      if (el.count() >= max_s) return true;
+    }
+    return false;
+  };
+  bool improved = true;
+  while (improved && !spent()) {
+    improved = false;
+    for (int pos = 0; pos < n && !spent(); ++pos) {
+      const int job = cur[static_cast<size_t>(pos)];
+      reduced.assign(cur.begin(), cur.end());
+      reduced.erase(reduced.begin() + pos);
+      ++it;
+      insertion_scan(m, p, reduced, job, vals, e, q);
+      int64_t best = INT64_MAX;
+      for (int64_t v : vals) best = std::min(best, v);
+      if (best >= cmax) continue;
+      ties.clear();
+      for (int i = 0; i < n; ++i)
+        if (vals[static_cast<size_t>(i)] == best) ties.push_back(i);
+      const int choice = ties[std::uniform_int_distribution<std::size_t>(0, ties.size() - 1)(rng)];
+      reduced.insert(reduced.begin() + choice, job);
+      cur = reduced;
+      cmax = best;
+      improved = true;
+    }
+  }
+  for (int i = 0; i < n; ++i) out[i] = cur[static_cast<size_t>(i)];
+  return cmax;
 }
 
 // Johnson/Mitten order per machine pair for LB2: pairs (k<l)
@@ -972,17 +1054,24 @@ void set_device_best(pbbgpu_pool* P, int64_t v) {
 
 // Harvest leaf improvements recorded by the last round(s).
 void harvest(pbbgpu_pool* P) {
-  const int cnt = std::min(P->h_ctr->imp_count, kImpCap);
+  const int cnt = std::min(P->h_ctr->imp_count, kImpCap);  // ring: all slots valid once it wrapped
   if (cnt > 0) {
     std::vector<ImpRecord> recs(static_cast<size_t>(cnt));
     xfer(P, recs.data(), P->d_imp, recs.size() * sizeof(ImpRecord), cudaMemcpyDeviceToHost, "imp copy");
     std::scoped_lock lk(P->best_mu);
+    std::vector<int32_t> perm(static_cast<size_t>(P->n));
     for (const ImpRecord& r : recs) {
-      if (r.mk < P->best_sched_value) {
-        P->best_sched_value = r.mk;
-        P->best_sched.assign(r.perm, r.perm + P->n);
+      if (r.mk >= P->best_sched_value) continue;
+      for (int i = 0; i < P->n; ++i) perm[static_cast<size_t>(i)] = r.perm[i];
+      int64_t mk = -1;
+      try {
+        mk = makespan_host(P->n, P->m, P->p.data(), perm.data());
+      } catch (const std::exception&) {
+        continue;  // torn record (ring overwrite race): skip
       }
-      P->best_value = std::min<int64_t>(P->best_value, r.mk);
+      if (mk != r.mk) continue;
+      P->best_sched_value = r.mk;
+      P->best_sched = perm;
     }
     const int zero = 0;
     xfer(P, reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, imp_count), &zero, sizeof(int), cudaMemcpyHostToDevice, "imp reset");
@@ -1481,6 +1570,94 @@ int pbbgpu_offer_bound(pbbgpu_pool* P, int64_t v) {
     int64_t cur = P->pending_offer.load();
     while (v < cur && !P->pending_offer.compare_exchange_weak(cur, v)) {
     }
+  });
+}
+
+int64_t pbbgpu_insertion_ls(int n, int m, const int32_t* p, const int32_t* seed, uint64_t max_iter, double max_seconds,
+                            uint64_t rng_seed, int32_t* perm_out) {
+  try {
+    return insertion_ls_host(n, m, p, seed, max_iter, max_seconds, rng_seed, perm_out);
+  } catch (const std::exception& e) {
+    set_err(e);
+    return -1;
+  }
+}
+
+// offer_schedule (src/explorer.cpp:379-395): a schedule found elsewhere (heuristic agent);
+// taken when it beats the bound or the pool's best schedule; the bound reaches the device
+// at the next round (mailbox, like offer_bound).
+int pbbgpu_offer_schedule(pbbgpu_pool* P, const int32_t* perm, int64_t cmax, int* taken) {
+  return guarded([&] {
+    if (taken) *taken = 0;
+    if (!perm || cmax < 0) return;
+    if (makespan_host(P->n, P->m, P->p.data(), perm) != cmax) throw std::invalid_argument("offer_schedule: cmax does not match the schedule");
+    bool took = false;
+    {
+      std::scoped_lock lk(P->best_mu);
+      if (cmax < P->best_sched_value) {
+        P->best_sched.assign(perm, perm + P->n);
+        P->best_sched_value = cmax;
+        took = true;
+      }
+    }
+    int64_t cur = P->pending_offer.load();
+    while (cmax < cur && !P->pending_offer.compare_exchange_weak(cur, cmax)) {
+    }
+    if (cmax < P->best_value) took = true;
+    if (taken) *taken = took ? 1 : 0;
+  });
+}
+
+// promote_solutions (src/explorer.cpp:397-424): every active explorer's current node,
+// completed by ordering its free jobs as in the best schedule, evaluated, best first.
+int pbbgpu_promote(pbbgpu_pool* P, int capacity, int32_t* perms_out, int64_t* cmax_out, int* count) {
+  return guarded([&] {
+    *count = 0;
+    std::vector<int32_t> inc;
+    {
+      std::scoped_lock lk(P->best_mu);
+      inc = P->best_sched;
+    }
+    if (inc.empty() || capacity <= 0 || P->batch_only) return;
+    const int n = P->n;
+    std::vector<int> rank(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) rank[static_cast<size_t>(inc[static_cast<size_t>(i)])] = i;
+    std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
+    xfer(P, st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost, "state copy");
+    std::vector<std::pair<int64_t, std::vector<int32_t>>> cands;
+    std::vector<int32_t> perm(static_cast<size_t>(n));
+    for (int i = 0; i < P->K; ++i) {
+      const unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
+      const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
+      if (h->state != kActive || h->level < 0) continue;
+      const int8_t* C = reinterpret_cast<const int8_t*>(blk + P->L.o_cells);
+      const int8_t* V = reinterpret_cast<const int8_t*>(blk + P->L.o_v);
+      const uint8_t* dir = blk + P->L.o_dir;
+      const int level = h->level;
+      if (V[level] >= n - level) continue;
+      int d1 = 0, d2 = 0;  // decode (src/ivm.cpp:152-172)
+      for (int l = 0; l <= level; ++l) {
+        const int x = C[tri_off(l, n) + V[l]];
+        const int job = (x < 0 ? -x : x) - 1;
+        if (dir[l] == kFwd) perm[static_cast<size_t>(d1++)] = job;
+        else perm[static_cast<size_t>(n - 1 - d2++)] = job;
+      }
+      int pos = d1;
+      for (int c = 0; c < n - level; ++c) {
+        if (c == V[level]) continue;
+        const int x = C[tri_off(level, n) + c];
+        perm[static_cast<size_t>(pos++)] = (x < 0 ? -x : x) - 1;
+      }
+      std::sort(perm.begin() + d1, perm.end() - d2, [&](int a, int b) { return rank[static_cast<size_t>(a)] < rank[static_cast<size_t>(b)]; });
+      cands.emplace_back(makespan_host(n, P->m, P->p.data(), perm.data()), perm);
+    }
+    std::stable_sort(cands.begin(), cands.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    const int c = std::min(capacity, static_cast<int>(cands.size()));
+    for (int i = 0; i < c; ++i) {
+      cmax_out[i] = cands[static_cast<size_t>(i)].first;
+      std::copy(cands[static_cast<size_t>(i)].second.begin(), cands[static_cast<size_t>(i)].second.end(), perms_out + static_cast<size_t>(i) * n);
+    }
+    *count = c;
   });
 }
 

@@ -91,3 +91,17 @@ def neh(inst: Instance) -> Schedule:
     out = np.zeros(inst.n, dtype=np.int32)
     v = _lib.load().pbbgpu_neh(inst.n, inst.m, inst.ptr(), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
     return Schedule([int(x) for x in out], int(v))
+
+
+def insertion_local_search(inst: Instance, seed: Schedule, max_iterations: int = 0, max_seconds: float = 0.0,
+                           rng_seed: int = 0) -> Schedule:
+    """insertion_local_search (src/heuristic.cpp:105-155): first-improvement remove-and-reinsert
+    descent, ties among equally good positions broken by a seeded mt19937_64."""
+    sp = np.ascontiguousarray(np.asarray(seed.perm, dtype=np.int32))
+    out = np.zeros(inst.n, dtype=np.int32)
+    v = _lib.load().pbbgpu_insertion_ls(inst.n, inst.m, inst.ptr(), sp.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                        int(max_iterations), float(max_seconds), int(rng_seed),
+                                        out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)))
+    if v < 0:
+        _lib.check(_lib.PBBGPU_ERR_ARG)
+    return Schedule([int(x) for x in out], int(v))

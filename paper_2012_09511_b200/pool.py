@@ -278,6 +278,23 @@ class GpuPool:
     def offer_bound(self, value: int) -> None:
         _lib.check(self._lib.pbbgpu_offer_bound(self._h, int(value)))
 
+    def offer_schedule(self, sched: Schedule) -> bool:
+        """offer_schedule (explorer.cpp:379-395): True when it improved the bound or best schedule."""
+        arr = np.ascontiguousarray(np.asarray(sched.perm, dtype=np.int32))
+        taken = ctypes.c_int()
+        _lib.check(self._lib.pbbgpu_offer_schedule(self._h, arr.ctypes.data_as(_i32p), int(sched.cmax), ctypes.byref(taken)))
+        return bool(taken.value)
+
+    def promote_solutions(self, capacity: int) -> List[Schedule]:
+        """promote_solutions (explorer.cpp:397-424): current nodes completed in incumbent order."""
+        n = self.inst.n
+        perms = np.zeros((max(capacity, 1), n), dtype=np.int32)
+        cm = np.zeros(max(capacity, 1), dtype=np.int64)
+        cnt = ctypes.c_int()
+        _lib.check(self._lib.pbbgpu_promote(self._h, capacity, perms.ctypes.data_as(_i32p), cm.ctypes.data_as(_i64p),
+                                            ctypes.byref(cnt)))
+        return [Schedule([int(x) for x in perms[i]], int(cm[i])) for i in range(cnt.value)]
+
     def stats(self) -> PoolStats:
         s = _lib.Stats()
         _lib.check(self._lib.pbbgpu_stats(self._h, ctypes.byref(s)))

@@ -32,6 +32,8 @@ def main():
         counts[f"{name}@neh"] = json.loads(run("solve", name, "neh", 1, 1))
     for name in ("ta001", "ta011", "ta021", "ta031", "ta041", "ta056", "ta111"):
         counts[f"neh:{name}"] = json.loads(run("neh", name))
+    for name, iters, seed in (("ta001", 2000, 7), ("ta021", 2000, 11), ("ta041", 500, 3), ("ta056", 300, 5)):
+        counts[f"ils:{name}"] = json.loads(run("ils", name, iters, seed))
     with open(os.path.join(HERE, "ref_counts.json"), "w") as f:
         json.dump(counts, f, indent=1, sort_keys=True)
     # per-node decompose dumps (SURVEY.md §8(d) sampler): seed 42

@@ -261,3 +261,36 @@ def test_large_n_decompose_matches_oracle(bound, fs):
         assert int(dr[i]) == d
         assert [int(x) for x in lb[i, :f]] == clb
         assert [int(x) for x in pr[i, :f]] == cpr
+
+
+# ---------------------------------------------------------------- heuristic cooperation (§8(f) #1)
+
+def test_promote_and_offer_schedule():
+    inst = pbb.taillard_named("ta021")
+    start = pbb.neh(inst)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=512), bound="lb1") as pool:
+        pool.set_initial_bound(start.cmax, start.perm)
+        pool.assign_split()
+        pool.run_round()
+        proms = pool.promote_solutions(5)
+        assert 0 < len(proms) <= 5
+        assert [p.cmax for p in proms] == sorted(p.cmax for p in proms)
+        for p in proms:
+            assert sorted(p.perm) == list(range(20)) and pbb.makespan(inst, p.perm) == p.cmax
+        better = pbb.insertion_local_search(inst, start, max_iterations=500, rng_seed=1)
+        assert better.cmax < start.cmax
+        assert pool.offer_schedule(better)
+        pool.run_round()
+        assert pool.best_value() <= better.cmax
+        assert pool.best_schedule().cmax <= better.cmax
+        with pytest.raises(ValueError):
+            pool.offer_schedule(pbb.Schedule(better.perm, better.cmax - 1))  # cmax must match
+
+
+@pytest.mark.parametrize("name,opt,bound", [("ta041", 2991, "lb1"), ("ta011", 1582, "lb2"), ("ta031", 2724, "lb1")])
+def test_cooperative_solve_finds_optimum(name, opt, bound):
+    r = pbb.solve_cooperative(pbb.taillard_named(name), bound=bound, ls_iterations=500)
+    assert r.completed and r.best_value == opt
+    assert r.initial_ub >= opt
+    if r.best.perm:
+        assert pbb.makespan(pbb.taillard_named(name), r.best.perm) == r.best.cmax

@@ -124,3 +124,20 @@ def test_pool_without_gpu_fails_loudly():
     with pytest.raises(_lib.PbbError) as e:
         pbb.GpuPool(pbb.taillard_named("ta001"))
     assert e.value.code == _lib.PBBGPU_ERR_CUDA
+
+
+def test_insertion_local_search_matches_reference():
+    """Host insertion LS (seeded mt19937_64 tie-breaking) is bit-exact with the reference's."""
+    for key, ref in golden_io.ref_counts().items():
+        if not key.startswith("ils:"):
+            continue
+        inst = pbb.taillard_named(key[4:])
+        s = pbb.insertion_local_search(inst, pbb.neh(inst), max_iterations=ref["iterations"], rng_seed=ref["rng_seed"])
+        assert s.cmax == ref["cmax"] and s.perm == ref["perm"], key
+        assert pbb.makespan(inst, s.perm) == s.cmax
+
+
+def test_insertion_local_search_needs_a_budget():
+    inst = pbb.taillard_named("ta001")
+    with pytest.raises(ValueError):
+        pbb.insertion_local_search(inst, pbb.neh(inst))
