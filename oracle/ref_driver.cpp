@@ -17,6 +17,7 @@
 //   neh    <ta>                                           NEH makespan + perm
 //   inst   <ta>                                           processing-time matrix
 //   ils    <ta> <iterations> <rng_seed>                   NEH + insertion_local_search
+//   ckpt   <ta> <path>  /  ckptload <ta> <path>           checkpoint_save / checkpoint_load
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -29,6 +30,7 @@
 #include <vector>
 
 #include "pbb/bound.hpp"
+#include "pbb/coordinator.hpp"
 #include "pbb/explorer.hpp"
 #include "pbb/factoradic.hpp"
 #include "pbb/heuristic.hpp"
@@ -265,6 +267,42 @@ int cmd_ils(int argc, char** argv) {
   return 0;
 }
 
+// checkpoint_save / checkpoint_load (src/coordinator.cpp:22-102) on fixed sample data
+int cmd_ckpt(int argc, char** argv) {
+  if (argc < 4) return 2;
+  Instance inst = taillard_named(argv[2]);
+  CheckpointData d;
+  Schedule s = neh(inst);
+  d.best_value = s.cmax;
+  d.best_schedule = s.perm;
+  d.total_nodes = 123456789;
+  const BigCount nf = BigCount::factorial(inst.n);
+  WorkUnit u1;
+  u1.kmax = 4;
+  u1.intervals = {Interval(BigCount(0), BigCount(1000)), Interval(BigCount(5000), nf)};
+  WorkUnit u2;
+  u2.kmax = 2;
+  u2.intervals = {Interval(nf / 2, nf / 2 + BigCount(7))};
+  d.units = {u1, u2};
+  checkpoint_save(argv[3], inst, d);
+  return 0;
+}
+
+int cmd_ckptload(int argc, char** argv) {
+  if (argc < 4) return 2;
+  Instance inst = taillard_named(argv[2]);
+  CheckpointData d = checkpoint_load(argv[3], inst);
+  std::printf("{\"best\":%lld,\"nodes\":%llu,\"units\":[", (long long)d.best_value, (unsigned long long)d.total_nodes);
+  for (std::size_t u = 0; u < d.units.size(); ++u) {
+    std::printf("%s{\"kmax\":%u,\"intervals\":[", u ? "," : "", d.units[u].kmax);
+    for (std::size_t i = 0; i < d.units[u].intervals.size(); ++i)
+      std::printf("%s[\"%s\",\"%s\"]", i ? "," : "", d.units[u].intervals[i].a.str().c_str(), d.units[u].intervals[i].b.str().c_str());
+    std::printf("]}");
+  }
+  std::printf("]}\n");
+  return 0;
+}
+
 int cmd_inst(int argc, char** argv) {
   if (argc < 3) return 2;
   Instance inst = taillard_named(argv[2]);
@@ -293,6 +331,8 @@ int main(int argc, char** argv) {
     else if (mode == "neh") rc = cmd_neh(argc, argv);
     else if (mode == "inst") rc = cmd_inst(argc, argv);
     else if (mode == "ils") rc = cmd_ils(argc, argv);
+    else if (mode == "ckpt") rc = cmd_ckpt(argc, argv);
+    else if (mode == "ckptload") rc = cmd_ckptload(argc, argv);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_driver: %s\n", e.what());
     return 1;

@@ -294,3 +294,30 @@ def test_cooperative_solve_finds_optimum(name, opt, bound):
     assert r.initial_ub >= opt
     if r.best.perm:
         assert pbb.makespan(pbb.taillard_named(name), r.best.perm) == r.best.cmax
+
+
+# ---------------------------------------------------------------- checkpoint / restart (§8(f) #2)
+
+def test_checkpoint_restart_completes_the_proof(tmp_path):
+    """Stop a proof after a few rounds, checkpoint (reference format), resume in a new pool:
+    leaves add up exactly, the bound and schedule survive, and the reference can read it."""
+    from paper_2012_09511_b200 import checkpoint as ck
+
+    ref = golden_io.ref_counts()["ta011@1582"]
+    inst = pbb.taillard_named("ta011")
+    path = str(tmp_path / "ta011.ckpt")
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=256, batch_steps=64, rounds_per_sync=1)) as pool:
+        pool.set_initial_bound(1582)
+        pool.assign_split()
+        for _ in range(3):
+            pool.run_round()
+        first = pool.stats()
+        d = ck.save_pool(pool, path)
+    assert d.units[0].intervals
+    with ck.resume_pool(path, inst, pbb.PoolConfig(explorers=4096)) as pool2:
+        while pool2.run_round():
+            pass
+        rest = pool2.stats()
+        assert pool2.best_value() == 1582
+    assert first.leaves + rest.leaves == ref["leaves"]
+    assert first.unique + rest.unique >= ref["decomposed"]

@@ -1,5 +1,6 @@
 """CPU tests of the product's host side (libpbbgpu.so host C++ + the Python mirror).
 No GPU compute is called here."""
+import os
 import random
 
 import numpy as np
@@ -141,3 +142,29 @@ def test_insertion_local_search_needs_a_budget():
     inst = pbb.taillard_named("ta001")
     with pytest.raises(ValueError):
         pbb.insertion_local_search(inst, pbb.neh(inst))
+
+
+def test_checkpoint_format_matches_reference(tmp_path):
+    """Our writer reproduces the reference's checkpoint_save bytes; its file loads back."""
+    from math import factorial
+
+    from paper_2012_09511_b200 import checkpoint as ck
+
+    inst = pbb.taillard_named("ta021")
+    ref_path = os.path.join(golden_io.GOLDEN, "ref_checkpoint_ta021.ckpt")
+    d = ck.checkpoint_load(ref_path, inst)
+    s = pbb.neh(inst)
+    nf = factorial(20)
+    assert d.best_value == s.cmax and d.best_schedule == s.perm and d.total_nodes == 123456789
+    assert [(u.kmax, u.intervals) for u in d.units] == [(4, [(0, 1000), (5000, nf)]), (2, [(nf // 2, nf // 2 + 7)])]
+    out = tmp_path / "mine.ckpt"
+    ck.checkpoint_save(str(out), inst, d)
+    assert out.read_bytes() == open(ref_path, "rb").read()
+    with pytest.raises(ValueError):
+        ck.checkpoint_load(ref_path, pbb.taillard_named("ta022"))  # different instance
+
+
+def test_instance_fingerprint():
+    from paper_2012_09511_b200 import checkpoint as ck
+
+    assert f"{ck.instance_fingerprint(pbb.taillard_named('ta021')):016x}" == "23f4aba7591455ec"
