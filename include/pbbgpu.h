@@ -25,6 +25,7 @@
  *   pbbgpu_insertion_ls             <- insertion_local_search           (heuristic.hpp:27, heuristic.cpp:105-155)
  *   pbbgpu_offer_schedule           <- ExplorerPool::offer_schedule     (explorer.hpp:93)
  *   pbbgpu_promote                  <- ExplorerPool::promote_solutions  (explorer.hpp:99, explorer.cpp:397-424)
+ *   pbbgpu_explorer_lengths         <- timeline sampling                (explorer.cpp:71-85, 448-464)
  *   pbbgpu_int32_peak               <- (new) integer-ALU roofline denominator
  *   pbbgpu_taillard / pbbgpu_makespan / pbbgpu_neh
  *                                   <- generate_taillard / taillard_named / makespan / neh
@@ -148,6 +149,9 @@ int64_t pbbgpu_insertion_ls(int n, int m, const int32_t* p, const int32_t* seed_
                             double max_seconds, uint64_t rng_seed, int32_t* perm_out);
 int pbbgpu_offer_schedule(pbbgpu_pool* pool, const int32_t* perm, int64_t cmax, int* taken);
 int pbbgpu_promote(pbbgpu_pool* pool, int capacity, int32_t* perms_out, int64_t* cmax_out, int* count);
+
+/* activity timeline (explorer.cpp:448-464): per explorer log2 remaining leaves, -2 busy, -3 idle */
+int pbbgpu_explorer_lengths(pbbgpu_pool* pool, float* out, int cap);
 
 /* INT32 ALU microbenchmark (add + max streams, the bounding kernels' instruction mix):
  * measured integer-op throughput of the device, the roofline denominator of the bounding

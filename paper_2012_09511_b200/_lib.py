@@ -27,7 +27,7 @@ EXPORTS = (
     "pbbgpu_active_count", "pbbgpu_snapshot", "pbbgpu_best", "pbbgpu_offer_bound",
     "pbbgpu_stats", "pbbgpu_histogram", "pbbgpu_decompose_batch", "pbbgpu_solve", "pbbgpu_int32_peak",
     "pbbgpu_assign_split_range", "pbbgpu_export", "pbbgpu_debug_state", "pbbgpu_assign_split_strided",
-    "pbbgpu_insertion_ls", "pbbgpu_offer_schedule", "pbbgpu_promote",
+    "pbbgpu_insertion_ls", "pbbgpu_offer_schedule", "pbbgpu_promote", "pbbgpu_explorer_lengths",
 )
 
 
@@ -130,6 +130,7 @@ def load() -> ctypes.CDLL:
                                                  ctypes.c_double, ctypes.c_uint64, i32p]),
         "pbbgpu_offer_schedule": (ctypes.c_int, [P, i32p, ctypes.c_int64, ip]),
         "pbbgpu_promote": (ctypes.c_int, [P, ctypes.c_int, i32p, i64p, ip]),
+        "pbbgpu_explorer_lengths": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_float), ctypes.c_int]),
         "pbbgpu_int32_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]),
         "pbbgpu_solve": (ctypes.c_int, [P, ctypes.c_int64, u16p, u16p, u8p, ctypes.c_int, i64p, i32p,
                                         ip, ctypes.POINTER(Stats)]),

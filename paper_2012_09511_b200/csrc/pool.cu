@@ -1661,6 +1661,20 @@ int pbbgpu_promote(pbbgpu_pool* P, int capacity, int32_t* perms_out, int64_t* cm
   });
 }
 
+// Per-explorer activity after the last round (timeline rows, src/explorer.cpp:448-464):
+// log2 of the remaining leaves from the effective position; -2 = busy replaying (active, length
+// not tracked), -3 = idle.
+int pbbgpu_explorer_lengths(pbbgpu_pool* P, float* out, int cap) {
+  return guarded([&] {
+    if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
+    if (cap < P->K) throw std::invalid_argument("explorer_lengths buffer smaller than K");
+    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens);
+    ck(cudaGetLastError(), "lens_kernel");
+    P->launches += 1;
+    xfer(P, out, P->d_lens, static_cast<size_t>(P->K) * sizeof(float), cudaMemcpyDeviceToHost, "lens copy");
+  });
+}
+
 int pbbgpu_stats(pbbgpu_pool* P, pbbgpu_stats_t* out) {
   return guarded([&] {
     if (P->batch_only) {

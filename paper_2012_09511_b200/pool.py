@@ -302,6 +302,12 @@ class GpuPool:
         d["completed"] = bool(d["completed"])
         return PoolStats(**d)
 
+    def explorer_lengths(self) -> np.ndarray:
+        """log2 remaining leaves per explorer (-2 busy replaying, -3 idle)."""
+        out = np.zeros(self.K(), dtype=np.float32)
+        _lib.check(self._lib.pbbgpu_explorer_lengths(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), out.size))
+        return out
+
     def histogram(self) -> Dict[int, int]:
         n = self.inst.n
         h = np.zeros(n + 1, dtype=np.uint64)
@@ -361,3 +367,36 @@ def int32_peak(device: int = 0) -> float:
     v = ctypes.c_double()
     _lib.check(_lib.load().pbbgpu_int32_peak(device, ctypes.byref(v)))
     return v.value
+
+
+class Timeline:
+    """Activity timeline CSV (src/explorer.cpp:71-85, 448-471): one row per explorer per sample,
+    `timestamp_ms,explorer_id,active,interval_length_log2`, samples >= 50 ms apart, forced at
+    exhaustion. The GPU's per-explorer lengths come from pbbgpu_explorer_lengths."""
+
+    MIN_GAP_S = 0.05
+
+    def __init__(self, path: str):
+        import time
+        self._time = time
+        self.f = open(path, "w")
+        self.f.write("timestamp_ms,explorer_id,active,interval_length_log2\n")
+        self.t0 = time.monotonic()
+        self.last = -1e9
+
+    def sample(self, pool: "GpuPool", force: bool = False) -> bool:
+        now = self._time.monotonic()
+        if not force and now - self.last < self.MIN_GAP_S:
+            return False
+        self.last = now
+        ts = int((now - self.t0) * 1000)
+        lens = pool.explorer_lengths()
+        rows = []
+        for i, lg in enumerate(lens):
+            active = lg != -3.0
+            rows.append(f"{ts},{i},{1 if active else 0},{int(lg) if lg >= 0 else -1}")
+        self.f.write("\n".join(rows) + "\n")
+        return True
+
+    def close(self):
+        self.f.close()

@@ -321,3 +321,28 @@ def test_checkpoint_restart_completes_the_proof(tmp_path):
         assert pool2.best_value() == 1582
     assert first.leaves + rest.leaves == ref["leaves"]
     assert first.unique + rest.unique >= ref["decomposed"]
+
+
+def test_timeline_csv(tmp_path):
+    """Activity timeline rows in the reference format; forced sample at exhaustion."""
+    import csv
+
+    inst = pbb.taillard_named("ta011")
+    path = tmp_path / "tl.csv"
+    tl = pbb.Timeline(str(path))
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=300, rounds_per_sync=1)) as pool:
+        pool.set_initial_bound(1582)
+        pool.assign_split()
+        tl.sample(pool, force=True)
+        assert not tl.sample(pool)                 # < 50 ms after the previous sample
+        while pool.run_round():
+            tl.sample(pool, force=True)
+        tl.sample(pool, force=True)
+    tl.close()
+    rows = list(csv.reader(open(path)))
+    assert rows[0] == ["timestamp_ms", "explorer_id", "active", "interval_length_log2"]
+    body = rows[1:]
+    assert len(body) >= 2 * 300 and len(body) % 300 == 0
+    last = body[-300:]
+    assert all(r[2] == "0" and r[3] == "-1" for r in last)         # exhausted: all idle
+    assert any(r[2] == "1" and int(r[3]) > 0 for r in body[:-300])  # remaining work is tracked
