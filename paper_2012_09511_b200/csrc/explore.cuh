@@ -50,7 +50,7 @@ __host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs, boo
   s.o_lag = o;
   o += packed ? 0 : round_up(npairs * n * 2, 16);
   s.o_pk32 = o;
-  o += packed ? round_up(npairs * n * 4, 16) : 0;
+  o += packed ? round_up(round_up(npairs, 32) * n * 4, 16) : 0;
   s.o_inv = o;  // [job][pair] position of the job in the pair's order (packed mode)
   o += packed ? round_up(npairs * n, 16) : 0;
   s.o_pk = o;
@@ -380,6 +380,9 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
   __syncwarp();
   int accF0 = 0, accF1 = 0, accB0 = 0, accB1 = 0;
   const int P = in.npairs;
+  // packed rows are padded to a multiple of 32 pairs: lane q always reads bank q mod 32,
+  // whatever position t each lane is at (the set-bit passes diverge in t)
+  const int PS = round_up(P, 32);
   int16_t* PMl = iv.pm + lane;
   int16_t* SMl = iv.sm + lane;
   for (int q0 = 0; q0 < P; q0 += 32) {
@@ -395,7 +398,7 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
       for (int c = 0; c < f; ++c) Fq |= 1u << in.invord[iv.freej[c] * P + q];
       int A = 0, Bp = 0, pm = NEG;
       for (uint32_t w = Fq; w; w &= w - 1) {
-        const unsigned e = in.packed[(__ffs(w) - 1) * P + q];
+        const unsigned e = in.packed[(__ffs(w) - 1) * PS + q];
         const int j = e & 63;
         A += (e >> 6) & 127;
         const int X = A + static_cast<int>(e >> 20) - Bp;
@@ -407,7 +410,7 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
       for (uint32_t w = Fq; w;) {
         const int t = 31 - __clz(w);
         w ^= 1u << t;
-        const unsigned e = in.packed[t * P + q];
+        const unsigned e = in.packed[t * PS + q];
         const int j = e & 63;
         Bs += (e >> 13) & 127;
         const int X = static_cast<int>(e >> 20) + Bs - As;
@@ -422,7 +425,7 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
       for (int c = 0; c < f; ++c) Fq |= 1ull << in.invord[iv.freej[c] * P + q];
       int A = 0, Bp = 0, pm = NEG;
       for (unsigned long long w = Fq; w; w &= w - 1) {
-        const unsigned e = in.packed[(__ffsll(static_cast<long long>(w)) - 1) * P + q];
+        const unsigned e = in.packed[(__ffsll(static_cast<long long>(w)) - 1) * PS + q];
         const int j = e & 63;
         A += (e >> 6) & 127;
         const int X = A + static_cast<int>(e >> 20) - Bp;
@@ -434,7 +437,7 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
       for (unsigned long long w = Fq; w;) {
         const int t = 63 - __clzll(static_cast<long long>(w));
         w ^= 1ull << t;
-        const unsigned e = in.packed[t * P + q];
+        const unsigned e = in.packed[t * PS + q];
         const int j = e & 63;
         Bs += (e >> 13) & 127;
         const int X = static_cast<int>(e >> 20) + Bs - As;
@@ -833,10 +836,8 @@ __global__ void __launch_bounds__(1024) explore_kernel(const ExploreParams P) {
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = P.p32[i];
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
-      for (int i = threadIdx.x; i < P.npairs * n; i += blockDim.x) {
-        sk[i] = P.packed[i];
-        smem[IL.o_inv + i] = P.invord[i];
-      }
+      for (int i = threadIdx.x; i < round_up(P.npairs, 32) * n; i += blockDim.x) sk[i] = P.packed[i];
+      for (int i = threadIdx.x; i < P.npairs * n; i += blockDim.x) smem[IL.o_inv + i] = P.invord[i];
       for (int i = threadIdx.x; i < P.npairs; i += blockDim.x) {
         smem[IL.o_pk + i] = P.pk[i];
         smem[IL.o_pl + i] = P.pl[i];
@@ -1035,10 +1036,8 @@ __global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
-      for (int i = threadIdx.x; i < B.npairs * n; i += blockDim.x) {
-        sk[i] = B.packed[i];
-        smem[IL.o_inv + i] = B.invord[i];
-      }
+      for (int i = threadIdx.x; i < round_up(B.npairs, 32) * n; i += blockDim.x) sk[i] = B.packed[i];
+      for (int i = threadIdx.x; i < B.npairs * n; i += blockDim.x) smem[IL.o_inv + i] = B.invord[i];
       for (int i = threadIdx.x; i < B.npairs; i += blockDim.x) {
         smem[IL.o_pk + i] = B.pk[i];
         smem[IL.o_pl + i] = B.pl[i];

@@ -274,7 +274,8 @@ void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::v
     }
   }
   // transposed packed form [t][q] = job | a << 6 | b << 13 | lag << 20 (children_lb2_w)
-  packed.assign(static_cast<size_t>(P) * n, 0);
+  const int PS = round_up(P, 32);  // row stride padded to 32 pairs (bank-conflict-free passes)
+  packed.assign(static_cast<size_t>(PS) * n, 0);
   packable = n <= 64;
   for (int qq = 0; qq < P; ++qq) {
     for (int t = 0; t < n; ++t) {
@@ -283,7 +284,7 @@ void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::v
       const int b = p[static_cast<size_t>(j) * m + pl[static_cast<size_t>(qq)]];
       const int lg = lag[static_cast<size_t>(qq) * n + j];
       if (a > 127 || b > 127 || lg > 2047) packable = false;
-      packed[static_cast<size_t>(t) * P + qq] =
+      packed[static_cast<size_t>(t) * PS + qq] =
           static_cast<uint32_t>(j) | static_cast<uint32_t>(a) << 6 | static_cast<uint32_t>(b) << 13 | static_cast<uint32_t>(lg) << 20;
     }
   }
