@@ -97,6 +97,7 @@ typedef struct {
   uint64_t d2h_bytes;           /* device->host bytes copied by the pool so far */
   int block;                    /* threads per CTA of the explore kernel */
   double batch_kernel_ms;       /* device time of decompose_batch kernels (CUDA events) */
+  double steal_kernel_ms;       /* device time of the between-round lens + steal kernels (CUDA events) */
 } pbbgpu_stats_t;
 
 const char* pbbgpu_last_error(void);

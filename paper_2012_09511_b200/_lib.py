@@ -73,6 +73,7 @@ class Stats(ctypes.Structure):
         ("d2h_bytes", ctypes.c_uint64),
         ("block", ctypes.c_int),
         ("batch_kernel_ms", ctypes.c_double),
+        ("steal_kernel_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -37,7 +37,7 @@ __host__ __device__ inline int round_up(int x, int a) { return (x + a - 1) / a *
 
 // Per-CTA shared instance region (identical computation on host and device).
 struct InstLayout {
-  int o_p32, o_pk, o_pl, o_ord, o_lag, o_pk32, o_inv, o_cnt, o_cta, o_hist, o_dhist, bytes;
+  int o_p32, o_psf, o_psb, o_pk, o_pl, o_ord, o_lag, o_pk32, o_inv, o_cnt, o_cta, o_hist, o_dhist, bytes;
 };
 
 // packed = warp-per-explorer LB2 (children_lb2_w): one uint32 per (position, pair),
@@ -46,6 +46,10 @@ __host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs, boo
   InstLayout s;
   int o = 0;
   s.o_p32 = o;
+  o += n * mp * 4;
+  s.o_psf = o;  // [n][mp] prefix sums of p: exclusive | inclusive << 16
+  o += n * mp * 4;
+  s.o_psb = o;  // [n][mp] suffix sums of p: exclusive | inclusive << 16
   o += n * mp * 4;
   s.o_lag = o;
   o += packed ? 0 : round_up(npairs * n * 2, 16);
@@ -212,6 +216,8 @@ struct IvmView {
 
 struct InstView {
   const int* p32;  // [n][mp]
+  const uint32_t* psf;  // [n][mp] sum_{i<k} p | sum_{i<=k} p << 16
+  const uint32_t* psb;  // [n][mp] sum_{i>k} p | sum_{i>=k} p << 16
   const uint8_t* pk;
   const uint8_t* pl;
   const uint8_t* ord;
@@ -509,34 +515,76 @@ template <int M, int G>
 __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& iv,
                                             const InstView& in, int n, int mp, int job, int dI,
                                             int d1, int d2) {
+  // The extended table (front of sigma1.job, or tail of job.sigma2) is the max-plus
+  // recurrence e[k] = max(e[k-1], src[k]) + p[k] (e[M] = 0 backward). Unrolled with the
+  // prefix sums of p it is a prefix max: e[k] = Sin[k] + max_{i<=k} (src[i] - Sex[i])
+  // (suffix max backward), so each lane scans a chunk of C machines and the group joins the
+  // chunks with log2(G) shuffles instead of one lane walking all M machines.
+  constexpr int C = (M + G - 1) / G;
+  constexpr int NEG = -(1 << 30);
   const uint16_t* fsrc = iv.ft + (dI == kFwd ? d1 - 1 : d1) * M;
   const uint16_t* tsrc = iv.ft + (n - (dI == kBwd ? d2 - 1 : d2)) * M;
   const int* pr = in.p32 + job * mp;
-  for (int k = grp.g; k < M; k += G) {
-    iv.rm[k] = static_cast<int>(iv.R[k]) - pr[k];
-    if (dI != kFwd) iv.fr[k] = fsrc[k];
-    if (dI != kBwd) iv.tl[k] = tsrc[k];
-  }
-  if (grp.g == G - 1) {
-    int prev = 0;
-    if (dI == kFwd) {
+  const int k0 = grp.g * C;
+  int loc[C], inc[C];
+  int run = NEG;
+  if (dI == kFwd) {
+    const uint32_t* ps = in.psf + job * mp;
 #pragma unroll
-      for (int k = 0; k < M; ++k) {
-        prev = max(prev, static_cast<int>(fsrc[k])) + pr[k];
-        iv.fr[k] = prev;
+    for (int c = 0; c < C; ++c) {
+      const int k = k0 + c;
+      if (k < M) {
+        const uint32_t u = ps[k];
+        run = max(run, static_cast<int>(fsrc[k]) - static_cast<int>(u & 0xffffu));
+        inc[c] = static_cast<int>(u >> 16);
       }
-    } else {
-#pragma unroll
-      for (int k = M - 1; k >= 0; --k) {
-        prev = max(prev, static_cast<int>(tsrc[k])) + pr[k];
-        iv.tl[k] = prev;
-      }
+      loc[c] = run;
     }
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const int t = __shfl_up_sync(grp.mask, run, o, G);
+      if (grp.g >= o) run = max(run, t);
+    }
+    int ex = __shfl_up_sync(grp.mask, run, 1, G);
+    if (grp.g == 0) ex = NEG;
+#pragma unroll
+    for (int c = 0; c < C; ++c) loc[c] = max(loc[c], ex);
+  } else {
+    const uint32_t* ps = in.psb + job * mp;
+#pragma unroll
+    for (int c = C - 1; c >= 0; --c) {
+      const int k = k0 + c;
+      if (k < M) {
+        const uint32_t u = ps[k];
+        run = max(run, static_cast<int>(tsrc[k]) - static_cast<int>(u & 0xffffu));
+        inc[c] = static_cast<int>(u >> 16);
+      }
+      loc[c] = run;
+    }
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const int t = __shfl_down_sync(grp.mask, run, o, G);
+      if (grp.g + o < G) run = max(run, t);
+    }
+    int ex = __shfl_down_sync(grp.mask, run, 1, G);
+    if (grp.g == G - 1) ex = NEG;
+#pragma unroll
+    for (int c = 0; c < C; ++c) loc[c] = max(loc[c], ex);
   }
-  grp.sync();
-  for (int k = grp.g; k < M; k += G) {
-    iv.rt[k] = iv.rm[k] + iv.tl[k];
-    iv.frm[k] = iv.fr[k] + iv.rm[k];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int k = k0 + c;
+    if (k < M) {
+      const int e = inc[c] + loc[c];
+      const int rmk = static_cast<int>(iv.R[k]) - pr[k];
+      const int frk = dI == kFwd ? e : static_cast<int>(fsrc[k]);
+      const int tlk = dI == kFwd ? static_cast<int>(tsrc[k]) : e;
+      iv.rm[k] = rmk;
+      iv.fr[k] = frk;
+      iv.tl[k] = tlk;
+      iv.rt[k] = rmk + tlk;
+      iv.frm[k] = frk + rmk;
+    }
   }
 }
 
@@ -821,6 +869,29 @@ __device__ __forceinline__ bool midpoint_pos(const int* pos, const int8_t* E, bo
   return cmp > 0;
 }
 
+// Prefix / suffix sums of every job's row (node_tables' max-plus scans), built from the
+// global p32 table while the CTA stages the instance.
+__device__ __forceinline__ void stage_prefix_sums(unsigned char* smem, const InstLayout& IL, const int* p32, int n,
+                                                  int mp) {
+  uint32_t* pf = reinterpret_cast<uint32_t*>(smem + IL.o_psf);
+  uint32_t* pb = reinterpret_cast<uint32_t*>(smem + IL.o_psb);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const int* pr = p32 + j * mp;
+    uint32_t acc = 0;
+    for (int k = 0; k < mp; ++k) {
+      const uint32_t v = static_cast<uint32_t>(pr[k]);
+      pf[j * mp + k] = acc | ((acc + v) << 16);
+      acc += v;
+    }
+    acc = 0;
+    for (int k = mp - 1; k >= 0; --k) {
+      const uint32_t v = static_cast<uint32_t>(pr[k]);
+      pb[j * mp + k] = acc | ((acc + v) << 16);
+      acc += v;
+    }
+  }
+}
+
 template <int M, int G, int BOUND, bool SMALLN = false>
 __global__ void __launch_bounds__(1024) explore_kernel(const ExploreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -834,6 +905,7 @@ __global__ void __launch_bounds__(1024) explore_kernel(const ExploreParams P) {
   {
     int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = P.p32[i];
+    stage_prefix_sums(smem, IL, P.p32, n, mp);
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
       for (int i = threadIdx.x; i < round_up(P.npairs, 32) * n; i += blockDim.x) sk[i] = P.packed[i];
@@ -876,6 +948,8 @@ __global__ void __launch_bounds__(1024) explore_kernel(const ExploreParams P) {
 
   InstView in;
   in.p32 = reinterpret_cast<const int*>(smem + IL.o_p32);
+  in.psf = reinterpret_cast<const uint32_t*>(smem + IL.o_psf);
+  in.psb = reinterpret_cast<const uint32_t*>(smem + IL.o_psb);
   in.pk = smem + IL.o_pk;
   in.pl = smem + IL.o_pl;
   in.ord = smem + IL.o_ord;
@@ -1034,6 +1108,7 @@ __global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams
   {
     int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
+    stage_prefix_sums(smem, IL, B.p32, n, mp);
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
       for (int i = threadIdx.x; i < round_up(B.npairs, 32) * n; i += blockDim.x) sk[i] = B.packed[i];
@@ -1057,6 +1132,8 @@ __global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams
   __syncthreads();
   InstView in;
   in.p32 = reinterpret_cast<const int*>(smem + IL.o_p32);
+  in.psf = reinterpret_cast<const uint32_t*>(smem + IL.o_psf);
+  in.psb = reinterpret_cast<const uint32_t*>(smem + IL.o_psb);
   in.pk = smem + IL.o_pk;
   in.pl = smem + IL.o_pl;
   in.ord = smem + IL.o_ord;

@@ -359,6 +359,7 @@ struct StealParams {
   float trigger;        // steal when active < trigger * K (reference: 0.8, explorer.cpp:251)
   const float* lens;    // [K] per-explorer log2 remaining (written by explore_kernel)
   int max_split;        // thieves per victim in one steal phase (multi-way split), 1..63
+  int* plan;            // [2] victims paired this phase, thieves per victim (split kernels)
 };
 
 constexpr int kStealThreads = 1024;
@@ -435,22 +436,20 @@ __device__ void split_point(const int* pos, const int* D, int top, int i, int pa
   }
 }
 
-// Cut the victim's remaining [pos, end) into r + 1 equal parts: the victim keeps the first,
-// thieves[0..r) are seated on the others (steal_right_half, generalised to r thieves).
-// Returns the number of thieves seated.
-__device__ int multi_split(unsigned char* vb, const IvmLayout& L, const int* ptot, unsigned char* const* tbs, int r,
-                           int* pos, int* D, int* b, int* prevb, int* oend) {
+// Setup of an r-way split of a victim (shared by the grid-wide split kernels below, which
+// re-derive it independently per thread from the unchanged victim state): the effective
+// position, D = end - pos, and r shrunk so every part holds at least 2 leaves. 0 = no split.
+__device__ int split_setup(const unsigned char* vb, const IvmLayout& L, int r, int* pos, int* D, int& top) {
   const int n = L.n;
-  IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
-  const int8_t* V = reinterpret_cast<const int8_t*>(vb + L.o_v);
-  int8_t* E = reinterpret_cast<int8_t*>(vb + L.o_end);
-  if (!effective_pos(V, vh->level, reinterpret_cast<const int8_t*>(vb + L.o_cells), n, pos)) return 0;
-  const bool had_end = vh->has_end != 0;
-  int top = 0;
-  if (!diff_digits(pos, E, had_end, n, D, top)) return 0;
-  // at least 2 leaves per part: shrink r while D < 2 (r + 1)
+  const IvmHdr* vh = reinterpret_cast<const IvmHdr*>(vb);
+  if (vh->state != kActive) return 0;
+  const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
+  if (!effective_pos(reinterpret_cast<const int8_t*>(vb + L.o_v), vh->level,
+                     reinterpret_cast<const int8_t*>(vb + L.o_cells), n, pos))
+    return 0;
+  if (!diff_digits(pos, E, vh->has_end != 0, n, D, top)) return 0;
   if (!top) {
-    long long small = 0;  // exact value when D is small (leading zeros)
+    long long small = 0;
     bool big = false;
     for (int l = 0; l < n && !big; ++l) {
       small = small * (n - l) + D[l];
@@ -461,19 +460,61 @@ __device__ int multi_split(unsigned char* vb, const IvmLayout& L, const int* pto
       r = static_cast<int>(min(static_cast<long long>(r), max(small / 2 - 1, 1ll)));
     }
   }
-  for (int l = 0; l < n; ++l) oend[l] = E[l];
-  const int parts = r + 1;
-  split_point(pos, D, top, 1, parts, n, prevb);  // end of the victim's part
-  for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(prevb[l]);
-  vh->has_end = 1;
-  for (int i = 1; i <= r; ++i) {
-    const bool last = i == r;
-    if (!last) split_point(pos, D, top, i + 1, parts, n, b);
-    seat_explorer(tbs[i - 1], L, ptot, prevb, last ? oend : b, last ? had_end : true);
-    if (!last)
-      for (int l = 0; l < n; ++l) prevb[l] = b[l];
-  }
   return r;
+}
+
+// Thief seating of a steal phase, one thread per (victim, part): part i (1..r) of the victim's
+// [pos, end) cut into r + 1 equal parts goes to thief i - 1. Reads the victims only; their
+// ends are cut afterwards by split_victims_kernel (stream order).
+__global__ void split_thieves_kernel(IvmLayout L, unsigned char* state, const int* ptot, const int* thief,
+                                     const int* victim, const int* plan, DevCounters* ctr) {
+  const int nv = plan[0], rs = plan[1];
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  int ok = 0;
+  if (g < nv * rs) {
+    const int v = g / rs, i = g % rs + 1;
+    const unsigned char* vb = state + static_cast<size_t>(victim[v]) * L.gstride;
+    int pos[kMaxN], D[kMaxN], b0[kMaxN], b1[kMaxN];
+    int top = 0;
+    const int r = split_setup(vb, L, rs, pos, D, top);
+    if (i <= r) {
+      const int n = L.n;
+      const IvmHdr* vh = reinterpret_cast<const IvmHdr*>(vb);
+      const bool last = i == r;
+      split_point(pos, D, top, i, r + 1, n, b0);
+      if (last) {
+        const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
+        for (int l = 0; l < n; ++l) b1[l] = E[l];
+      } else {
+        split_point(pos, D, top, i + 1, r + 1, n, b1);
+      }
+      seat_explorer(state + static_cast<size_t>(thief[v * rs + i - 1]) * L.gstride, L, ptot, b0, b1,
+                    last ? vh->has_end != 0 : true);
+      ok = 1;
+    }
+  }
+  const unsigned cnt = __popc(__ballot_sync(0xffffffffu, ok));
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicAdd(&ctr->active, static_cast<int>(cnt));
+    atomicAdd(&ctr->steals, static_cast<unsigned long long>(cnt));
+    atomicAdd(&ctr->inits, static_cast<unsigned long long>(cnt));
+  }
+}
+
+// The victims keep the first part: end <- pos + D / (r + 1) (one thread per victim).
+__global__ void split_victims_kernel(IvmLayout L, unsigned char* state, const int* victim, const int* plan) {
+  const int nv = plan[0], rs = plan[1];
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  unsigned char* vb = state + static_cast<size_t>(victim[v]) * L.gstride;
+  int pos[kMaxN], D[kMaxN], b[kMaxN];
+  int top = 0;
+  const int r = split_setup(vb, L, rs, pos, D, top);
+  if (r < 1) return;
+  split_point(pos, D, top, 1, r + 1, L.n, b);
+  int8_t* E = reinterpret_cast<int8_t*>(vb + L.o_end);
+  for (int l = 0; l < L.n; ++l) E[l] = static_cast<int8_t>(b[l]);
+  reinterpret_cast<IvmHdr*>(vb)->has_end = 1;
 }
 
 // Steal phase (src/explorer.cpp:283-340, B200 form). The explore kernel leaves one float per
@@ -506,7 +547,10 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
   const int total_idle = s_idle[kStealThreads - 1];
   const int total_active = s_tot[0];
   if (static_cast<float>(total_active) >= S.trigger * static_cast<float>(K) || total_idle == 0 || total_active == 0) {
-    if (t == 0) S.ctr->active = total_active;
+    if (t == 0) {
+      S.ctr->active = total_active;
+      S.plan[0] = 0;
+    }
     return;
   }
   int r = s_idle[t] - idle;
@@ -538,19 +582,10 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
     }
   }
   __syncthreads();
-  int ok = 0;
-  int pos[kMaxN], D[kMaxN], b[kMaxN], pb[kMaxN], oend[kMaxN];
-  unsigned char* tbs[63];
-  for (int v = t; v < nv; v += kStealThreads) {
-    for (int i = 0; i < rs; ++i) tbs[i] = S.state + static_cast<size_t>(S.thief[v * rs + i]) * S.L.gstride;
-    ok += multi_split(S.state + static_cast<size_t>(S.victim[v]) * S.L.gstride, S.L, S.ptot, tbs, rs, pos, D, b, pb, oend);
-  }
-  atomicAdd(&s_tot[2], ok);
-  __syncthreads();
-  if (t == 0) {
-    S.ctr->active = total_active + s_tot[2];
-    S.ctr->steals += static_cast<unsigned long long>(s_tot[2]);
-    S.ctr->inits += static_cast<unsigned long long>(s_tot[2]);
+  if (t == 0) {  // the grid-wide split kernels that follow read the plan
+    S.plan[0] = nv;
+    S.plan[1] = rs;
+    S.ctr->active = total_active;
     S.ctr->steal_phases += 1ull;
   }
 }
@@ -789,7 +824,8 @@ struct pbbgpu_pool {
   size_t big_smem = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaEvent_t evs[16] = {};
+  cudaEvent_t evs[24] = {};  // per round: explore start, explore end, steal end
+  double steal_ms = 0;
   int rounds_per_sync = 2;
   unsigned char* d_state = nullptr;
   int *d_p32 = nullptr, *d_ptot = nullptr, *d_wrk = nullptr;
@@ -816,9 +852,15 @@ struct pbbgpu_pool {
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
   double kernel_ms = 0;
   int last_active = 0;
+  // grow-only device scratch for per-call staging (assign / export / decompose_batch): a
+  // cudaMalloc + cudaFree pair per call synchronizes the device and occasionally stalls for
+  // hundreds of milliseconds while the driver returns memory
+  void* scr[8] = {};
+  size_t scr_cap[8] = {};
 
   void release() {
     if (stream) cudaStreamSynchronize(stream);
+    for (void* q : scr) cudaFree(q);
     cudaFree(d_state);
     cudaFree(d_p32);
     cudaFree(d_ptot);
@@ -950,21 +992,35 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   };
   const size_t smem_cap = static_cast<size_t>(prop.sharedMemPerBlockOptin);
   const size_t smem_sm = static_cast<size_t>(prop.sharedMemPerMultiprocessor);
-  int best_bs = 0;
-  long best_res = -1;
-  for (;;) {
+  // (block size, explorers resident per SM) for group size G
+  auto choose = [&](int G) {
+    int bs = 0;
+    long res = -1;
     for (int BS : {128, 256, 512, 768, 1024}) {
-      const size_t need = size_for(P->G, BS).first;
+      const size_t need = size_for(G, BS).first;
       if (need > smem_cap) continue;
       const long ctas = std::min<long>({static_cast<long>(smem_sm / (need + 1024)), 2048L / BS, 32L});
-      const long res = ctas * (BS / P->G);
-      if (res > best_res) {
-        best_res = res;
-        best_bs = BS;
+      if (ctas * (BS / G) > res) {
+        res = ctas * (BS / G);
+        bs = BS;
       }
     }
+    return std::make_pair(bs, res);
+  };
+  int best_bs = 0;
+  for (;;) {
+    best_bs = choose(P->G).first;
     if (best_bs || P->G >= 32) break;
     P->G *= 2;
+  }
+  // LB1: 8 lanes per explorer (4 explorers per warp amortize the single-lane table
+  // extensions) when shared memory still seats >= 768 threads per SM; 16 otherwise
+  if (bound == kLB1 && P->cfg.group <= 0 && P->G == 16) {
+    const auto c8 = choose(8);
+    if (c8.first && c8.second * 8 >= 768) {
+      P->G = 8;
+      best_bs = c8.first;
+    }
   }
   if (!best_bs) throw CapacityError("pbbgpu: explorer state exceeds shared memory");
   if (P->cfg.block > 0) best_bs = P->cfg.block;
@@ -1004,7 +1060,7 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   ck(cudaMalloc(&P->d_state, static_cast<size_t>(P->K) * P->L.gstride), "malloc state");
   ck(cudaMalloc(&P->d_p32, p32.size() * sizeof(int)), "malloc");
   ck(cudaMalloc(&P->d_ptot, ptot.size() * sizeof(int)), "malloc");
-  ck(cudaMalloc(&P->d_wrk, (static_cast<size_t>(P->K) * 2 + 1) * sizeof(int)), "malloc");
+  ck(cudaMalloc(&P->d_wrk, (static_cast<size_t>(P->K) * 2 + 4) * sizeof(int)), "malloc");
   ck(cudaMalloc(&P->d_lgfact, lgf.size() * sizeof(float)), "malloc");
   ck(cudaMalloc(&P->d_lens, static_cast<size_t>(P->K) * sizeof(float)), "malloc");
   ck(cudaMalloc(&P->d_ctr, sizeof(DevCounters)), "malloc");
@@ -1109,16 +1165,31 @@ ExploreParams explore_params(pbbgpu_pool* P) {
   return E;
 }
 
+template <class T>
+T* scratch(pbbgpu_pool* P, int slot, size_t count) {
+  const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+  if (P->scr_cap[slot] < bytes) {
+    if (P->scr[slot]) {
+      ck(cudaStreamSynchronize(P->stream), "sync");
+      cudaFree(P->scr[slot]);
+      P->scr[slot] = nullptr;
+      P->scr_cap[slot] = 0;
+    }
+    const size_t cap = std::max(bytes, 2 * P->scr_cap[slot]);
+    ck(cudaMalloc(&P->scr[slot], cap), "malloc scratch");
+    P->scr_cap[slot] = cap;
+  }
+  return static_cast<T*>(P->scr[slot]);
+}
+
 void assign_digits(pbbgpu_pool* P, const std::vector<int>& a, const std::vector<int>& b, const std::vector<uint8_t>& nf, const std::vector<int>& slots) {
   if (P->batch_only) throw StateError("pbbgpu: n > 64 pools are bounding-only (decompose_batch); exploration needs n <= 64");
   const int cnt = static_cast<int>(slots.size());
   if (cnt == 0) return;
-  int *da = nullptr, *db = nullptr, *ds = nullptr;
-  uint8_t* dn = nullptr;
-  ck(cudaMalloc(&da, a.size() * sizeof(int)), "malloc");
-  ck(cudaMalloc(&db, b.size() * sizeof(int)), "malloc");
-  ck(cudaMalloc(&ds, slots.size() * sizeof(int)), "malloc");
-  ck(cudaMalloc(&dn, nf.size()), "malloc");
+  int* da = scratch<int>(P, 0, a.size());
+  int* db = scratch<int>(P, 1, b.size());
+  int* ds = scratch<int>(P, 2, slots.size());
+  uint8_t* dn = scratch<uint8_t>(P, 3, nf.size());
   xfer(P, da, a.data(), a.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
   xfer(P, db, b.data(), b.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
   xfer(P, ds, slots.data(), slots.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
@@ -1126,11 +1197,6 @@ void assign_digits(pbbgpu_pool* P, const std::vector<int>& a, const std::vector<
   init_kernel<<<(cnt + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, da, db, dn, ds, cnt);
   ck(cudaGetLastError(), "init_kernel");
   P->launches += 1;
-  ck(cudaStreamSynchronize(P->stream), "sync");
-  cudaFree(da);
-  cudaFree(db);
-  cudaFree(ds);
-  cudaFree(dn);
   read_counters(P);
   // inits counter
   unsigned long long inits = P->h_ctr->inits + static_cast<unsigned long long>(cnt);
@@ -1183,6 +1249,7 @@ int run_round(pbbgpu_pool* P) {
   S.ctr = P->d_ctr;
   S.thief = P->d_wrk;
   S.victim = P->d_wrk + P->K;
+  S.plan = P->d_wrk + 2 * P->K + 2;
   S.min_log2 = static_cast<float>(P->cfg.min_steal_log2 > 0 ? P->cfg.min_steal_log2 : std::log2(40320.0));
   S.lgfact = P->d_lgfact;
   S.trigger = static_cast<float>(P->cfg.steal_trigger > 0 ? P->cfg.steal_trigger : 1.0);
@@ -1192,21 +1259,29 @@ int run_round(pbbgpu_pool* P) {
   // device-timed, and a round after exhaustion costs only the state copy of an empty launch
   const int R = P->rounds_per_sync;
   for (int r = 0; r < R; ++r) {
-    ck(cudaEventRecord(P->evs[2 * r], P->stream), "event");
+    ck(cudaEventRecord(P->evs[3 * r], P->stream), "event");
     P->efn<<<P->grid, P->block, P->smem, P->stream>>>(E);
     ck(cudaGetLastError(), "explore_kernel launch");
-    ck(cudaEventRecord(P->evs[2 * r + 1], P->stream), "event");
+    ck(cudaEventRecord(P->evs[3 * r + 1], P->stream), "event");
     lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens);
     ck(cudaGetLastError(), "lens_kernel launch");
     steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
     ck(cudaGetLastError(), "steal_kernel launch");
-    P->launches += 3;
+    split_thieves_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, S.thief, S.victim,
+                                                                     S.plan, P->d_ctr);
+    ck(cudaGetLastError(), "split_thieves_kernel launch");
+    split_victims_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, S.victim, S.plan);
+    ck(cudaGetLastError(), "split_victims_kernel launch");
+    ck(cudaEventRecord(P->evs[3 * r + 2], P->stream), "event");
+    P->launches += 5;
   }
   read_counters(P);
   for (int r = 0; r < R; ++r) {
     float ms = 0;
-    ck(cudaEventElapsedTime(&ms, P->evs[2 * r], P->evs[2 * r + 1]), "elapsed");
+    ck(cudaEventElapsedTime(&ms, P->evs[3 * r], P->evs[3 * r + 1]), "elapsed");
     P->kernel_ms += ms;
+    ck(cudaEventElapsedTime(&ms, P->evs[3 * r + 1], P->evs[3 * r + 2]), "elapsed");
+    P->steal_ms += ms;
   }
   P->rounds += static_cast<uint64_t>(R);
   harvest(P);
@@ -1438,12 +1513,9 @@ int pbbgpu_export(pbbgpu_pool* P, int max_count, uint16_t* a_out, uint16_t* b_ou
     if (max_count <= 0) return;
     const int n = P->n;
     const int want = std::min(max_count, P->K);
-    int* d_dig = nullptr;
-    uint8_t* d_nf = nullptr;
-    int* d_cnt = nullptr;
-    ck(cudaMalloc(&d_dig, static_cast<size_t>(want + 64) * 2 * n * sizeof(int)), "malloc");
-    ck(cudaMalloc(&d_nf, static_cast<size_t>(want + 64)), "malloc");
-    ck(cudaMalloc(&d_cnt, sizeof(int)), "malloc");
+    int* d_dig = scratch<int>(P, 0, static_cast<size_t>(want + 64) * 2 * n);
+    uint8_t* d_nf = scratch<uint8_t>(P, 1, static_cast<size_t>(want + 64));
+    int* d_cnt = scratch<int>(P, 2, 1);
     StealParams S{};
     S.L = P->L;
     S.state = P->d_state;
@@ -1470,9 +1542,6 @@ int pbbgpu_export(pbbgpu_pool* P, int max_count, uint16_t* a_out, uint16_t* b_ou
       xfer(P, dig.data(), d_dig, dig.size() * sizeof(int), cudaMemcpyDeviceToHost, "copy");
       xfer(P, nf.data(), d_nf, nf.size(), cudaMemcpyDeviceToHost, "copy");
     }
-    cudaFree(d_dig);
-    cudaFree(d_nf);
-    cudaFree(d_cnt);
     for (int i = 0; i < cnt; ++i) {
       for (int l = 0; l < n; ++l) {
         a_out[static_cast<size_t>(i) * n + l] = static_cast<uint16_t>(dig[static_cast<size_t>(i) * 2 * n + l]);
@@ -1709,6 +1778,7 @@ int pbbgpu_stats(pbbgpu_pool* P, pbbgpu_stats_t* out) {
     out->batch_kernel_ms = P->batch_ms;
     out->h2d_bytes = P->h2d_bytes;
     out->d2h_bytes = P->d2h_bytes;
+    out->steal_kernel_ms = P->steal_ms;
   });
 }
 
@@ -1739,17 +1809,15 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
         seen[static_cast<size_t>(j)] = 1;
       }
     }
-    int *dp = nullptr, *dd1 = nullptr, *dd2 = nullptr, *dlb = nullptr, *dlf = nullptr, *dlbw = nullptr;
-    uint8_t *ddir = nullptr, *dpr = nullptr;
     const size_t cn = static_cast<size_t>(count) * n;
-    ck(cudaMalloc(&dp, cn * sizeof(int)), "malloc");
-    ck(cudaMalloc(&dd1, count * sizeof(int)), "malloc");
-    ck(cudaMalloc(&dd2, count * sizeof(int)), "malloc");
-    ck(cudaMalloc(&dlb, cn * sizeof(int)), "malloc");
-    ck(cudaMalloc(&dlf, cn * sizeof(int)), "malloc");
-    ck(cudaMalloc(&dlbw, cn * sizeof(int)), "malloc");
-    ck(cudaMalloc(&ddir, count), "malloc");
-    ck(cudaMalloc(&dpr, cn), "malloc");
+    int* dp = scratch<int>(P, 0, cn);
+    int* dd1 = scratch<int>(P, 1, count);
+    int* dd2 = scratch<int>(P, 2, count);
+    int* dlb = scratch<int>(P, 3, cn);
+    int* dlf = scratch<int>(P, 4, cn);
+    int* dlbw = scratch<int>(P, 5, cn);
+    uint8_t* ddir = scratch<uint8_t>(P, 6, count);
+    uint8_t* dpr = scratch<uint8_t>(P, 7, cn);
     xfer(P, dp, perms, cn * sizeof(int), cudaMemcpyHostToDevice, "copy");
     xfer(P, dd1, d1, count * sizeof(int), cudaMemcpyHostToDevice, "copy");
     xfer(P, dd2, d2, count * sizeof(int), cudaMemcpyHostToDevice, "copy");
@@ -1829,14 +1897,6 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
         if (lb_bwd) lb_bwd[s] = lbw[s];
       }
     }
-    cudaFree(dp);
-    cudaFree(dd1);
-    cudaFree(dd2);
-    cudaFree(dlb);
-    cudaFree(dlf);
-    cudaFree(dlbw);
-    cudaFree(ddir);
-    cudaFree(dpr);
   });
 }
 

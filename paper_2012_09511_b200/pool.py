@@ -90,6 +90,7 @@ class PoolStats:
     d2h_bytes: int = 0
     block: int = 0
     batch_kernel_ms: float = 0.0
+    steal_kernel_ms: float = 0.0
 
 
 @dataclass
