@@ -240,27 +240,44 @@ struct InstView {
 template <int M, int G>
 __device__ __forceinline__ void children_lb1(const Group<G>& grp, const IvmView& iv,
                                              const InstView& in, int mp, int f) {
+  // node tables and p rows are padded to mp (a multiple of 4) and 16-byte aligned: LDS.128
+  constexpr int Q = (M + 3) / 4;
+  const int4* fr4 = reinterpret_cast<const int4*>(iv.fr);
+  const int4* rt4 = reinterpret_cast<const int4*>(iv.rt);
+  const int4* tl4 = reinterpret_cast<const int4*>(iv.tl);
+  const int4* frm4 = reinterpret_cast<const int4*>(iv.frm);
   for (int c = grp.g; c < f; c += G) {
     const int j = iv.freej[c];
-    const int* pr = in.p32 + j * mp;
-    int p[M];
-#pragma unroll
-    for (int k = 0; k < M; ++k) p[k] = pr[k];
+    const int4* pr4 = reinterpret_cast<const int4*>(in.p32 + j * mp);
     int prev = 0, best = 0;
 #pragma unroll
-    for (int k = 0; k < M; ++k) {
-      const int t = max(prev, iv.fr[k]);
-      best = max(best, t + iv.rt[k]);
-      prev = t + p[k];
+    for (int q = 0; q < Q; ++q) {
+      const int4 a = fr4[q], r = rt4[q], w = pr4[q];
+      const int av[4] = {a.x, a.y, a.z, a.w}, rv[4] = {r.x, r.y, r.z, r.w}, pv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (4 * q + e < M) {
+          const int t = max(prev, av[e]);
+          best = max(best, t + rv[e]);
+          prev = t + pv[e];
+        }
+      }
     }
     iv.lbf[c] = best;
     prev = 0;
     best = 0;
 #pragma unroll
-    for (int k = M - 1; k >= 0; --k) {
-      const int t = max(prev, iv.tl[k]);
-      best = max(best, t + iv.frm[k]);
-      prev = t + p[k];
+    for (int q = Q - 1; q >= 0; --q) {
+      const int4 a = tl4[q], r = frm4[q], w = pr4[q];
+      const int av[4] = {a.x, a.y, a.z, a.w}, rv[4] = {r.x, r.y, r.z, r.w}, pv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 3; e >= 0; --e) {
+        if (4 * q + e < M) {
+          const int t = max(prev, av[e]);
+          best = max(best, t + rv[e]);
+          prev = t + pv[e];
+        }
+      }
     }
     iv.lbb[c] = best;
   }
@@ -490,22 +507,28 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
 // larger sum, then Forward.
 template <int G>
 __device__ __forceinline__ int minmin(const Group<G>& grp, const IvmView& iv, int f) {
-  int lo = INT_MAX;
-  for (int c = grp.g; c < f; c += G) lo = min(lo, min(iv.lbf[c], iv.lbb[c]));
-  lo = grp.rmin(lo);
-  int cnt = 0, sf = 0, sb = 0;
+  // one pass: per-lane minimum with its fwd/bwd occurrence counts and the running
+  // sum difference; lanes whose minimum is the group's contribute their count difference.
+  // One REDUX sums (cf - cb) << 24 + (sf - sb): |sf - sb| < 64 * 2^16 = 2^22 and
+  // |cf - cb| <= 64, so both fields survive in 32 bits.
+  int lo = INT_MAX, cf = 0, cb = 0, sd = 0;
   for (int c = grp.g; c < f; c += G) {
     const int a = iv.lbf[c], b = iv.lbb[c];
-    cnt += (a == lo) + ((b == lo) << 16);
-    sf += a;
-    sb += b;
+    const int mn = min(a, b);
+    if (mn < lo) {
+      lo = mn;
+      cf = 0;
+      cb = 0;
+    }
+    cf += a == lo;
+    cb += b == lo;
+    sd += a - b;
   }
-  cnt = grp.rsum(cnt);
-  sf = grp.rsum(sf);
-  sb = grp.rsum(sb);
-  const int cf = cnt & 0xffff, cb = cnt >> 16;
-  if (cf != cb) return cf < cb ? kFwd : kBwd;
-  if (sf != sb) return sf > sb ? kFwd : kBwd;
+  const int glo = grp.rmin(lo);
+  const int v = grp.rsum(((lo == glo ? cf - cb : 0) << 24) + sd);
+  const int cd = (v + (1 << 23)) >> 24;
+  if (cd) return cd < 0 ? kFwd : kBwd;  // fewer occurrences of lo wins
+  if (v) return v > 0 ? kFwd : kBwd;    // then the larger sum
   return kFwd;
 }
 
