@@ -916,7 +916,7 @@ __device__ __forceinline__ void stage_prefix_sums(unsigned char* smem, const Ins
 }
 
 template <int M, int G, int BOUND, bool SMALLN = false>
-__global__ void __launch_bounds__(1024) explore_kernel(const ExploreParams P) {
+__global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explore_kernel(const ExploreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = P.L;
   const int n = L.n, mp = L.mp;

@@ -996,10 +996,16 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   auto choose = [&](int G) {
     int bs = 0;
     long res = -1;
+    // register-limited threads per SM of this kernel variant (allocation: 256 per warp)
+    cudaFuncAttributes fa{};
+    ck(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(explore_fn(m, bound, G, n <= 32))), "func attrs");
+    const long warp_regs = static_cast<long>((fa.numRegs * 32 + 255) / 256 * 256);
+    const long max_threads = std::min<long>(2048L, prop.regsPerMultiprocessor / std::max(warp_regs, 1L) * 32);
     for (int BS : {128, 256, 512, 768, 1024}) {
+      if (BS > fa.maxThreadsPerBlock) continue;
       const size_t need = size_for(G, BS).first;
       if (need > smem_cap) continue;
-      const long ctas = std::min<long>({static_cast<long>(smem_sm / (need + 1024)), 2048L / BS, 32L});
+      const long ctas = std::min<long>({static_cast<long>(smem_sm / (need + 1024)), max_threads / BS, 32L});
       if (ctas * (BS / G) > res) {
         res = ctas * (BS / G);
         bs = BS;
