@@ -996,7 +996,10 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
     unsigned long long t_end = ~0ull;
     if (P.budget_ns) t_end = globaltimer_ns() + P.budget_ns;
     while (step < P.steps) {
-      if (P.budget_ns && (step & 3) == 0 && grp.bcast(grp.g == 0 ? (globaltimer_ns() >= t_end) : 0, 0)) break;
+      // budget check every 4th step; every step for LB2 warps (a step costs tens of us there,
+      // and the whole CTA waits for its slowest explorer at the round's end)
+      constexpr int kCheck = (BOUND == kLB2 && G == 32) ? 0 : 3;
+      if (P.budget_ns && (step & kCheck) == 0 && grp.bcast(grp.g == 0 ? (globaltimer_ns() >= t_end) : 0, 0)) break;
       if (state == kEmpty) break;
       if ((step & 15) == 15) best = grp.bcast(grp.g == 0 ? *reinterpret_cast<volatile int*>(&P.ctr->best) : 0, 0);
       ++step;

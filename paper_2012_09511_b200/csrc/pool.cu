@@ -991,23 +991,24 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
     return std::make_pair(static_cast<size_t>(IL.bytes) + static_cast<size_t>(BS / G) * L.sstride, std::make_pair(L, IL));
   };
   const size_t smem_cap = static_cast<size_t>(prop.sharedMemPerBlockOptin);
-  const size_t smem_sm = static_cast<size_t>(prop.sharedMemPerMultiprocessor);
   // (block size, explorers resident per SM) for group size G
   auto choose = [&](int G) {
+    // the occupancy calculator of this kernel variant (registers, smem, block limits) for
+    // every warp-multiple block size: the most explorers resident per SM wins
     int bs = 0;
     long res = -1;
-    // register-limited threads per SM of this kernel variant (allocation: 256 per warp)
+    const void* fn = reinterpret_cast<const void*>(explore_fn(m, bound, G, n <= 32));
     cudaFuncAttributes fa{};
-    ck(cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(explore_fn(m, bound, G, n <= 32))), "func attrs");
-    const long warp_regs = static_cast<long>((fa.numRegs * 32 + 255) / 256 * 256);
-    const long max_threads = std::min<long>(2048L, prop.regsPerMultiprocessor / std::max(warp_regs, 1L) * 32);
-    for (int BS : {128, 256, 512, 768, 1024}) {
-      if (BS > fa.maxThreadsPerBlock) continue;
+    ck(cudaFuncGetAttributes(&fa, fn), "func attrs");
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_cap)), "smem attr");
+    for (int BS = 64; BS <= 1024; BS += 32) {
+      if (BS > fa.maxThreadsPerBlock || BS % G) continue;
       const size_t need = size_for(G, BS).first;
       if (need > smem_cap) continue;
-      const long ctas = std::min<long>({static_cast<long>(smem_sm / (need + 1024)), max_threads / BS, 32L});
-      if (ctas * (BS / G) > res) {
-        res = ctas * (BS / G);
+      int ctas = 0;
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, fn, BS, need), "occupancy");
+      if (static_cast<long>(ctas) * (BS / G) > res) {
+        res = static_cast<long>(ctas) * (BS / G);
         bs = BS;
       }
     }
