@@ -113,6 +113,11 @@ int64_t pbbgpu_neh(int n, int m, const int32_t* p, int32_t* perm_out);
 int pbbgpu_create(int n, int m, const int32_t* p_jobmajor, int bound_kind,
                   const pbbgpu_config_t* cfg, pbbgpu_pool** out);
 void pbbgpu_destroy(pbbgpu_pool* pool);
+/* Reuse a pool for another instance of the same shape (n, m, bound): the instance tables are
+ * rebuilt and re-uploaded in place, counters / incumbent / explorers reset as after create
+ * (no device allocation; a serving loop keeps one pool per shape). Replaces constructing a
+ * new ExplorerPool per instance (include/pbb/explorer.hpp ExplorerPool(const Instance&, ...)). */
+int pbbgpu_load_instance(pbbgpu_pool* pool, const int32_t* p_jobmajor);
 int pbbgpu_K(const pbbgpu_pool* pool);
 int pbbgpu_set_initial_bound(pbbgpu_pool* pool, int64_t ub, const int32_t* sched, int len);
 int pbbgpu_assign(pbbgpu_pool* pool, const uint16_t* a_digits, const uint16_t* b_digits,

@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -804,6 +805,25 @@ BatchFn batch_fn(int m, int bound, int G, bool small) {
 
 // ------------------------------------------------------------------ pool
 
+// PBBGPU_TRACE=1: host-side timing of slow pool-management calls on stderr (diagnostics)
+static bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("PBBGPU_TRACE");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+struct TraceScope {
+  const char* what;
+  std::chrono::steady_clock::time_point t0;
+  explicit TraceScope(const char* w) : what(w), t0(std::chrono::steady_clock::now()) {}
+  ~TraceScope() {
+    if (!trace_on()) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms >= 5.0) std::fprintf(stderr, "[pbbgpu] %s: %.1f ms\n", what, ms);
+  }
+};
+
 struct pbbgpu_pool {
   int n = 0, m = 0, mp = 0, bound = 0;
   pbbgpu_config_t cfg{};
@@ -857,9 +877,16 @@ struct pbbgpu_pool {
   // hundreds of milliseconds while the driver returns memory
   void* scr[8] = {};
   size_t scr_cap[8] = {};
+  void* pin = nullptr;  // pinned host staging for table uploads (grow-only)
+  size_t pin_cap = 0;
 
   void release() {
-    if (stream) cudaStreamSynchronize(stream);
+    TraceScope ts("release");
+    {
+      TraceScope t1("release: stream sync");
+      if (stream) cudaStreamSynchronize(stream);
+    }
+    TraceScope t2("release: frees");
     for (void* q : scr) cudaFree(q);
     cudaFree(d_state);
     cudaFree(d_p32);
@@ -881,6 +908,7 @@ struct pbbgpu_pool {
     cudaFree(d_dhist);
     cudaFree(d_imp);
     if (h_ctr) cudaFreeHost(h_ctr);
+    if (pin) cudaFreeHost(pin);
     for (cudaEvent_t e : evs)
       if (e) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
@@ -904,16 +932,145 @@ int pick_group(int n, int bound) {
   return 32;  // warp per explorer, lanes over machine pairs (children_lb2_w)
 }
 
-void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const pbbgpu_config_t* cfg) {
-  if (n < 2 || n > kBigMaxN) throw std::invalid_argument("pbbgpu: n must be in [2, 512]");
-  if (m != 5 && m != 10 && m != 20) throw std::invalid_argument("pbbgpu: m must be 5, 10 or 20 (compiled machine counts)");
-  if (bound != kLB1 && bound != kLB2) throw std::invalid_argument("pbbgpu: bound must be PBBGPU_LB1 or PBBGPU_LB2");
+// Host-built instance tables (everything the kernels read about p), uploaded into the
+// pool's device buffers at create time and again by pbbgpu_load_instance.
+struct HostTables {
+  std::vector<int> p32, ptot;
+  std::vector<uint8_t> pk, pl, ord, inv;
+  std::vector<uint16_t> lag, ord16;
+  std::vector<uint32_t> packed;
+  std::vector<uint2> pk64;
+  bool packable = false;
+};
+
+void validate_times(int n, int m, const int32_t* p) {
   int pmax = 0;
   for (int i = 0; i < n * m; ++i) {
     if (p[i] < 0) throw std::invalid_argument("negative processing time");
     pmax = std::max(pmax, p[i]);
   }
   if (static_cast<int64_t>(n + m) * pmax >= 65536) throw std::invalid_argument("pbbgpu: (n+m)*max(p) must stay below 2^16");
+}
+
+HostTables build_tables(int n, int m, int bound, const int32_t* p, bool big) {
+  HostTables T;
+  const int mp = round_up(m, 4);
+  const int npairs = m * (m - 1) / 2;
+  T.p32.assign(static_cast<size_t>(n) * mp, 0);
+  T.ptot.assign(static_cast<size_t>(m), 0);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < m; ++k) {
+      T.p32[static_cast<size_t>(j) * mp + k] = p[static_cast<size_t>(j) * m + k];
+      T.ptot[static_cast<size_t>(k)] += p[static_cast<size_t>(j) * m + k];
+    }
+  if (bound != kLB2) return T;
+  lb2_tables(n, m, p, T.pk, T.pl, T.ord, T.lag, T.packed, T.packable, T.ord16);
+  if (big) {
+    T.pk64.resize(static_cast<size_t>(n) * npairs);
+    for (int q = 0; q < npairs; ++q)
+      for (int t = 0; t < n; ++t) {
+        const int j = T.ord16[static_cast<size_t>(q) * n + t];
+        const int a = p[static_cast<size_t>(j) * m + T.pk[static_cast<size_t>(q)]];
+        const int bb = p[static_cast<size_t>(j) * m + T.pl[static_cast<size_t>(q)]];
+        const int lg = T.lag[static_cast<size_t>(q) * n + j];
+        if (a > 65535 || bb > 65535) throw std::invalid_argument("processing time exceeds 16 bits");
+        T.pk64[static_cast<size_t>(t) * npairs + q] =
+            make_uint2(static_cast<unsigned>(j) | static_cast<unsigned>(a) << 16, static_cast<unsigned>(bb) | static_cast<unsigned>(lg) << 16);
+      }
+  } else {
+    T.inv.assign(static_cast<size_t>(n) * npairs, 0);  // [job][pair] -> position
+    for (int q = 0; q < npairs; ++q)
+      for (int t = 0; t < n; ++t) T.inv[static_cast<size_t>(T.ord16[static_cast<size_t>(q) * n + t]) * npairs + q] = static_cast<uint8_t>(t);
+  }
+  return T;
+}
+
+// Table uploads: allocate on first use, stage through the pool's pinned host buffer and
+// copy asynchronously; one stream sync at the end (counted host->device bytes).
+struct Uploader {
+  pbbgpu_pool* P;
+  size_t off = 0;
+  std::vector<std::pair<void*, std::pair<size_t, size_t>>> jobs;  // dst, (staging offset, bytes)
+  std::vector<const void*> srcs;
+  template <class D, class V>
+  void put(D*& dptr, const V& v) {
+    const size_t bytes = v.size() * sizeof(v[0]);
+    if (!bytes) return;
+    if (!dptr) ck(cudaMalloc(&dptr, bytes), "malloc");
+    jobs.push_back({dptr, {off, bytes}});
+    srcs.push_back(v.data());
+    off += (bytes + 15) / 16 * 16;
+  }
+  void run() {
+    if (P->pin_cap < off) {
+      if (P->pin) cudaFreeHost(P->pin);
+      P->pin = nullptr;
+      P->pin_cap = 0;
+      ck(cudaMallocHost(&P->pin, off), "malloc host");
+      P->pin_cap = off;
+    }
+    unsigned char* st = static_cast<unsigned char*>(P->pin);
+    for (size_t i = 0; i < jobs.size(); ++i) std::memcpy(st + jobs[i].second.first, srcs[i], jobs[i].second.second);
+    for (const auto& jb : jobs) {
+      ck(cudaMemcpyAsync(jb.first, st + jb.second.first, jb.second.second, cudaMemcpyHostToDevice, P->stream), "copy");
+      P->h2d_bytes += jb.second.second;
+    }
+    ck(cudaStreamSynchronize(P->stream), "sync");
+  }
+};
+
+template <class D, class V>
+void put(pbbgpu_pool* P, D*& dptr, const V& v) {
+  Uploader u{P};
+  u.put(dptr, v);
+  u.run();
+}
+
+void upload_tables(pbbgpu_pool* P, const HostTables& T) {
+  Uploader u{P};
+  u.put(P->d_p32, T.p32);
+  if (!P->batch_only) u.put(P->d_ptot, T.ptot);
+  if (P->bound == kLB2) {
+    u.put(P->d_pk, T.pk);
+    u.put(P->d_pl, T.pl);
+    if (P->batch_only) {
+      u.put(P->d_packed64, T.pk64);
+    } else {
+      u.put(P->d_ord, T.ord);
+      u.put(P->d_lag, T.lag);
+      u.put(P->d_packed, T.packed);
+      u.put(P->d_invord, T.inv);
+    }
+  }
+  u.run();
+}
+
+// counters, histograms, incumbent and explorer states back to a fresh pool's
+void reset_search(pbbgpu_pool* P) {
+  if (P->batch_only) return;  // bounding-only pools keep no search state
+  DevCounters z{};
+  z.best = INT_MAX;
+  xfer(P, P->d_ctr, &z, sizeof(z), cudaMemcpyHostToDevice, "copy");
+  ck(cudaMemsetAsync(P->d_hist, 0, (static_cast<size_t>(P->n) + 1) * sizeof(unsigned long long), P->stream), "memset");
+  ck(cudaMemsetAsync(P->d_dhist, 0, (static_cast<size_t>(P->n) + 1) * sizeof(unsigned long long), P->stream), "memset");
+  clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
+  ck(cudaGetLastError(), "clear_kernel");
+  P->launches += 1;
+  ck(cudaStreamSynchronize(P->stream), "sync");
+  std::scoped_lock lk(P->best_mu);
+  P->best_value = INT64_MAX;
+  P->best_sched_value = INT64_MAX;
+  P->pinned_ub = INT64_MAX;
+  P->best_sched.clear();
+  P->pending_offer.store(INT64_MAX);
+  P->last_active = 0;
+}
+
+void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const pbbgpu_config_t* cfg) {
+  if (n < 2 || n > kBigMaxN) throw std::invalid_argument("pbbgpu: n must be in [2, 512]");
+  if (m != 5 && m != 10 && m != 20) throw std::invalid_argument("pbbgpu: m must be 5, 10 or 20 (compiled machine counts)");
+  if (bound != kLB1 && bound != kLB2) throw std::invalid_argument("pbbgpu: bound must be PBBGPU_LB1 or PBBGPU_LB2");
+  validate_times(n, m, p);
   P->n = n;
   P->m = m;
   P->bound = bound;
@@ -921,53 +1078,27 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   if (cfg) P->cfg = *cfg;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw CudaError("pbbgpu: no CUDA device (the product path has no CPU fallback)");
-  ck(cudaSetDevice(P->cfg.device), "cudaSetDevice");
   cudaDeviceProp prop;
-  ck(cudaGetDeviceProperties(&prop, P->cfg.device), "cudaGetDeviceProperties");
-  if (prop.major < 10) throw CudaError("pbbgpu: kernels are built for sm_100a only");
-  ck(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking), "stream");
-  ck(cudaEventCreate(&P->ev0), "event");
-  ck(cudaEventCreate(&P->ev1), "event");
-  for (cudaEvent_t& e : P->evs) ck(cudaEventCreate(&e), "event");
+  {
+    TraceScope ts("create: device, stream, events");
+    ck(cudaSetDevice(P->cfg.device), "cudaSetDevice");
+    ck(cudaGetDeviceProperties(&prop, P->cfg.device), "cudaGetDeviceProperties");
+    if (prop.major < 10) throw CudaError("pbbgpu: kernels are built for sm_100a only");
+    ck(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreate(&P->ev0), "event");
+    ck(cudaEventCreate(&P->ev1), "event");
+    for (cudaEvent_t& e : P->evs) ck(cudaEventCreate(&e), "event");
+  }
   P->rounds_per_sync = P->cfg.rounds_per_sync > 0 ? std::min(P->cfg.rounds_per_sync, 8) : 2;
 
-  std::vector<uint8_t> pk, pl, ord;
-  std::vector<uint16_t> lag;
-  std::vector<uint32_t> packed;
-  std::vector<uint16_t> ord16;
-  bool packable = false;
-  if (bound == kLB2) {
-    lb2_tables(n, m, p, pk, pl, ord, lag, packed, packable, ord16);
-    P->npairs = m * (m - 1) / 2;
-  }
+  if (bound == kLB2) P->npairs = m * (m - 1) / 2;
+  const HostTables T = build_tables(n, m, bound, p, n > kMaxN);
+  const bool packable = T.packable;
   if (n > kMaxN) {  // batch-only pool: the large-n bounding kernel, no explorers
     P->batch_only = true;
     P->mp = round_up(m, 4);
     P->big = big_fn(m, bound);
-    std::vector<int> p32(static_cast<size_t>(n) * P->mp, 0);
-    for (int j = 0; j < n; ++j)
-      for (int k = 0; k < m; ++k) p32[static_cast<size_t>(j) * P->mp + k] = p[static_cast<size_t>(j) * m + k];
-    ck(cudaMalloc(&P->d_p32, p32.size() * sizeof(int)), "malloc");
-    xfer(P, P->d_p32, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
-    if (bound == kLB2) {
-      std::vector<uint2> pk64(static_cast<size_t>(n) * P->npairs);
-      for (int q = 0; q < P->npairs; ++q)
-        for (int t = 0; t < n; ++t) {
-          const int j = ord16[static_cast<size_t>(q) * n + t];
-          const int a = p[static_cast<size_t>(j) * m + pk[static_cast<size_t>(q)]];
-          const int bb = p[static_cast<size_t>(j) * m + pl[static_cast<size_t>(q)]];
-          const int lg = lag[static_cast<size_t>(q) * n + j];
-          if (a > 65535 || bb > 65535) throw std::invalid_argument("processing time exceeds 16 bits");
-          pk64[static_cast<size_t>(t) * P->npairs + q] =
-              make_uint2(static_cast<unsigned>(j) | static_cast<unsigned>(a) << 16, static_cast<unsigned>(bb) | static_cast<unsigned>(lg) << 16);
-        }
-      ck(cudaMalloc(&P->d_pk, pk.size()), "malloc");
-      ck(cudaMalloc(&P->d_pl, pl.size()), "malloc");
-      ck(cudaMalloc(&P->d_packed64, pk64.size() * sizeof(uint2)), "malloc");
-      xfer(P, P->d_pk, pk.data(), pk.size(), cudaMemcpyHostToDevice, "copy");
-      xfer(P, P->d_pl, pl.data(), pl.size(), cudaMemcpyHostToDevice, "copy");
-      xfer(P, P->d_packed64, pk64.data(), pk64.size() * sizeof(uint2), cudaMemcpyHostToDevice, "copy");
-    }
+    upload_tables(P, T);
     P->big_smem = static_cast<size_t>(big_smem_bytes(n, P->mp, m));
     ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->big), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(P->big_smem)), "smem attr");
@@ -1014,6 +1145,7 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
     }
     return std::make_pair(bs, res);
   };
+  TraceScope ts_choose("create: block choice");
   int best_bs = 0;
   for (;;) {
     best_bs = choose(P->G).first;
@@ -1055,55 +1187,19 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   P->round_us = P->cfg.round_us > 0 ? P->cfg.round_us : (P->cfg.steps_per_round > 0 ? 0.0 : 2000.0);
 
   // device buffers
-  const int mp = P->mp;
-  std::vector<int> p32(static_cast<size_t>(n) * mp, 0), ptot(static_cast<size_t>(m), 0);
-  for (int j = 0; j < n; ++j)
-    for (int k = 0; k < m; ++k) {
-      p32[static_cast<size_t>(j) * mp + k] = p[static_cast<size_t>(j) * m + k];
-      ptot[static_cast<size_t>(k)] += p[static_cast<size_t>(j) * m + k];
-    }
   std::vector<float> lgf(static_cast<size_t>(n) + 1, 0.f);
   for (int k = 2; k <= n; ++k) lgf[static_cast<size_t>(k)] = lgf[static_cast<size_t>(k - 1)] + std::log2(static_cast<float>(k));
   ck(cudaMalloc(&P->d_state, static_cast<size_t>(P->K) * P->L.gstride), "malloc state");
-  ck(cudaMalloc(&P->d_p32, p32.size() * sizeof(int)), "malloc");
-  ck(cudaMalloc(&P->d_ptot, ptot.size() * sizeof(int)), "malloc");
   ck(cudaMalloc(&P->d_wrk, (static_cast<size_t>(P->K) * 2 + 4) * sizeof(int)), "malloc");
-  ck(cudaMalloc(&P->d_lgfact, lgf.size() * sizeof(float)), "malloc");
   ck(cudaMalloc(&P->d_lens, static_cast<size_t>(P->K) * sizeof(float)), "malloc");
   ck(cudaMalloc(&P->d_ctr, sizeof(DevCounters)), "malloc");
   ck(cudaMallocHost(&P->h_ctr, sizeof(DevCounters)), "malloc host");
   ck(cudaMalloc(&P->d_hist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
   ck(cudaMalloc(&P->d_dhist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
   ck(cudaMalloc(&P->d_imp, kImpCap * sizeof(ImpRecord)), "malloc");
-
-  xfer(P, P->d_p32, p32.data(), p32.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
-  xfer(P, P->d_ptot, ptot.data(), ptot.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
-  xfer(P, P->d_lgfact, lgf.data(), lgf.size() * sizeof(float), cudaMemcpyHostToDevice, "copy");
-  if (bound == kLB2) {
-    ck(cudaMalloc(&P->d_pk, pk.size()), "malloc");
-    ck(cudaMalloc(&P->d_pl, pl.size()), "malloc");
-    ck(cudaMalloc(&P->d_ord, ord.size()), "malloc");
-    ck(cudaMalloc(&P->d_lag, lag.size() * sizeof(uint16_t)), "malloc");
-    xfer(P, P->d_pk, pk.data(), pk.size(), cudaMemcpyHostToDevice, "copy");
-    xfer(P, P->d_pl, pl.data(), pl.size(), cudaMemcpyHostToDevice, "copy");
-    xfer(P, P->d_ord, ord.data(), ord.size(), cudaMemcpyHostToDevice, "copy");
-    xfer(P, P->d_lag, lag.data(), lag.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, "copy");
-    ck(cudaMalloc(&P->d_packed, packed.size() * sizeof(uint32_t)), "malloc");
-    xfer(P, P->d_packed, packed.data(), packed.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, "copy");
-    std::vector<uint8_t> inv(static_cast<size_t>(n) * P->npairs, 0);  // [job][pair] -> position
-    for (int q = 0; q < P->npairs; ++q)
-      for (int t = 0; t < n; ++t) inv[static_cast<size_t>(ord16[static_cast<size_t>(q) * n + t]) * P->npairs + q] = static_cast<uint8_t>(t);
-    ck(cudaMalloc(&P->d_invord, inv.size()), "malloc");
-    xfer(P, P->d_invord, inv.data(), inv.size(), cudaMemcpyHostToDevice, "copy");
-  }
-  DevCounters z{};
-  z.best = INT_MAX;
-  xfer(P, P->d_ctr, &z, sizeof(z), cudaMemcpyHostToDevice, "copy");
-  ck(cudaMemset(P->d_hist, 0, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "memset");
-  ck(cudaMemset(P->d_dhist, 0, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "memset");
-  clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
-  ck(cudaGetLastError(), "clear_kernel");
-  ck(cudaStreamSynchronize(P->stream), "sync");
+  put(P, P->d_lgfact, lgf);
+  upload_tables(P, T);
+  reset_search(P);
 }
 
 void read_counters(pbbgpu_pool* P) {
@@ -1410,6 +1506,7 @@ int64_t pbbgpu_neh(int n, int m, const int32_t* p, int32_t* perm_out) {
 int pbbgpu_create(int n, int m, const int32_t* p, int bound_kind, const pbbgpu_config_t* cfg, pbbgpu_pool** out) {
   *out = nullptr;
   pbbgpu_pool* P = new pbbgpu_pool();
+  TraceScope ts("create");
   const int rc = guarded([&] { pool_init(P, n, m, p, bound_kind, cfg); });
   if (rc != PBBGPU_OK) {
     P->release();
@@ -1424,6 +1521,20 @@ void pbbgpu_destroy(pbbgpu_pool* P) {
   if (!P) return;
   P->release();
   delete P;
+}
+
+int pbbgpu_load_instance(pbbgpu_pool* P, const int32_t* p) {
+  return guarded([&] {
+    if (!P || !p) throw std::invalid_argument("pbbgpu_load_instance: null argument");
+    validate_times(P->n, P->m, p);
+    const HostTables T = build_tables(P->n, P->m, P->bound, p, P->batch_only);
+    if (P->bound == kLB2 && !P->batch_only && P->G == 32 && !T.packable)
+      throw CapacityError("pbbgpu_load_instance: this instance's LB2 tables do not pack into 31 bits; create a new pool");
+    ck(cudaStreamSynchronize(P->stream), "sync");
+    P->p.assign(p, p + static_cast<size_t>(P->n) * P->m);
+    upload_tables(P, T);
+    reset_search(P);
+  });
 }
 
 int pbbgpu_K(const pbbgpu_pool* P) { return P ? P->K : 0; }

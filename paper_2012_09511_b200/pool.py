@@ -175,6 +175,14 @@ class GpuPool:
             self._lib.pbbgpu_destroy(self._h)
             self._h = None
 
+    def load_instance(self, inst: Instance) -> None:
+        """Reuse this pool for another instance of the same shape (pbbgpu_load_instance): tables
+        re-uploaded in place, search state reset as after construction."""
+        if (inst.n, inst.m) != (self.inst.n, self.inst.m):
+            raise ValueError("load_instance needs an instance of the pool's shape (n, m)")
+        _lib.check(self._lib.pbbgpu_load_instance(self._h, inst.ptr()))
+        self.inst = inst
+
     def __del__(self):
         try:
             self.close()
@@ -343,24 +351,30 @@ def pool_run(inst: Instance, initial_ub: int, intervals: Sequence[Interval] = ()
     """pool_run (src/explorer.cpp:473-507) on one GPU: [0, n!) by default, cut evenly over K."""
     cfg = cfg or PoolConfig()
     with GpuPool(inst, cfg, bound) as pool:
-        lib = pool._lib
-        ivs = normalize(list(intervals))
-        a = b = inf = None
-        if ivs:
-            a, b, inf = _digits(ivs, inst.n)
-        best = ctypes.c_int64()
-        has = ctypes.c_int()
-        perm = np.zeros(inst.n, dtype=np.int32)
-        st = _lib.Stats()
-        _lib.check(lib.pbbgpu_solve(
-            pool._h, int(min(initial_ub, NO_INCUMBENT)),
-            a.ctypes.data_as(_u16p) if ivs else None, b.ctypes.data_as(_u16p) if ivs else None,
-            inf.ctypes.data_as(_u8p) if ivs else None, len(ivs), ctypes.byref(best),
-            perm.ctypes.data_as(_i32p), ctypes.byref(has), ctypes.byref(st)))
-        d = st.as_dict()
-        d["completed"] = bool(d["completed"])
-        sched = Schedule([int(x) for x in perm], int(best.value)) if has.value else Schedule([], -1)
-        return PoolResult(sched, int(best.value), PoolStats(**d), pool.histogram())
+        return solve_pool(pool, initial_ub, intervals)
+
+
+def solve_pool(pool: GpuPool, initial_ub: int, intervals: Sequence[Interval] = ()) -> PoolResult:
+    """One pbbgpu_solve on an existing pool (fresh, or re-loaded with GpuPool.load_instance)."""
+    inst = pool.inst
+    lib = pool._lib
+    ivs = normalize(list(intervals))
+    a = b = inf = None
+    if ivs:
+        a, b, inf = _digits(ivs, inst.n)
+    best = ctypes.c_int64()
+    has = ctypes.c_int()
+    perm = np.zeros(inst.n, dtype=np.int32)
+    st = _lib.Stats()
+    _lib.check(lib.pbbgpu_solve(
+        pool._h, int(min(initial_ub, NO_INCUMBENT)),
+        a.ctypes.data_as(_u16p) if ivs else None, b.ctypes.data_as(_u16p) if ivs else None,
+        inf.ctypes.data_as(_u8p) if ivs else None, len(ivs), ctypes.byref(best),
+        perm.ctypes.data_as(_i32p), ctypes.byref(has), ctypes.byref(st)))
+    d = st.as_dict()
+    d["completed"] = bool(d["completed"])
+    sched = Schedule([int(x) for x in perm], int(best.value)) if has.value else Schedule([], -1)
+    return PoolResult(sched, int(best.value), PoolStats(**d), pool.histogram())
 
 
 def int32_peak(device: int = 0) -> float:

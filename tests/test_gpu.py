@@ -346,3 +346,51 @@ def test_timeline_csv(tmp_path):
     last = body[-300:]
     assert all(r[2] == "0" and r[3] == "-1" for r in last)         # exhausted: all idle
     assert any(r[2] == "1" and int(r[3]) > 0 for r in body[:-300])  # remaining work is tracked
+
+
+# ---------------------------------------------------------------- pool reuse (serving loop)
+
+@pytest.mark.parametrize("bound", ["lb1", "lb2"])
+def test_load_instance_matches_fresh_pools(bound):
+    """One pool fed several same-shape instances gives exactly the fresh pools' results."""
+    ta001 = pbb.taillard_named("ta001")
+    others = [pbb.taillard_named(f"ta00{i}") for i in (2, 3)]
+    optimum = {"ta001": 1278, "ta002": 1359, "ta003": 1081}  # fixed trees: UB = optimum
+    with pbb.GpuPool(ta001, bound=bound) as pool:
+        for inst in others + [ta001]:
+            ub = optimum[inst.label]
+            pool.load_instance(inst)
+            got = pbb.solve_pool(pool, ub)
+            want = pbb.pool_run(inst, ub, bound=bound)
+            assert got.stats.completed and want.stats.completed
+            assert got.stats.unique == want.stats.unique
+            assert got.stats.leaves == want.stats.leaves
+            assert got.best_value == want.best_value
+            assert got.hist == want.hist
+            if got.best.perm:
+                assert pbb.makespan(inst, got.best.perm) == got.best_value
+    if bound == "lb1":
+        ref = golden_io.ref_counts()["ta001@1278"]
+        with pbb.GpuPool(others[0], bound=bound) as pool:
+            pool.load_instance(ta001)
+            res = pbb.solve_pool(pool, 1278)
+            assert res.stats.unique == ref["decomposed"]
+            assert _hist_str(res.hist) == ref["hist"]
+
+
+def test_load_instance_rejects_other_shapes():
+    with pbb.GpuPool(pbb.taillard_named("ta001"), bound="lb1") as pool:
+        with pytest.raises(ValueError):
+            pool.load_instance(pbb.taillard_named("ta011"))
+
+
+def test_load_instance_batch_only_pool():
+    a, b = pbb.taillard_named("ta111"), pbb.taillard_named("ta112")
+    perms, d1s, d2s = _nodes_with_f(a.n, [1, 50, 300, 499], 5)
+    with pbb.GpuPool(a, bound="lb2") as pool:
+        pool.load_instance(b)
+        got = pool.decompose_batch(perms, d1s, d2s, 1 << 30)
+    with pbb.GpuPool(b, bound="lb2") as fresh:
+        want = fresh.decompose_batch(perms, d1s, d2s, 1 << 30)
+    for x, y in zip(got, want):
+        assert np.array_equal(x, y)
