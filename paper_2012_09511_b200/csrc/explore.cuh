@@ -366,6 +366,18 @@ __device__ __forceinline__ void children_lb2(const Group<G>& grp, const IvmView&
   }
 }
 
+// 16x2 unsigned SIMD (sm_90+: VIADD.16x2 / VIADDMNMX.U16x2, one instruction each)
+__device__ __forceinline__ uint32_t add_u16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 // LB2, warp per explorer, lanes over machine pairs, exact max-plus prefix/suffix form.
 // For one pair (k,l) and the node's free jobs s_1..s_f in that pair's Johnson order the
 // chain of row a22 unrolls to
@@ -375,46 +387,60 @@ __device__ __forceinline__ void children_lb2(const Group<G>& grp, const IvmView&
 // SM_j = max_{i'>i} X_i' (one forward and one backward pass per pair):
 //   t0 = r_k + A - a_j,  t1 = max(r_l + B - b_j, r_k + max(PM_j - b_j, SM_j - a_j))
 //   lb_kl(child) = max(t0 + q_k, t1 + q_l)
-// Integer-exact, identical values to the per-child chains, O(P (n + f)) per node instead of
-// O(P f^2). Each lane owns a pair (32 pairs per round); per child the 32 pair bounds are
-// combined with one REDUX.MAX (__reduce_max_sync).
+// Integer-exact, identical values to the per-child chains, O(P (n + f)) per node.
+//
+// Evaluation form. The child's head on machine m is h_m = h'_m + p_jm with
+// h'_m = max(h_{m-1}, front_m) (tails alike: t_m = t'_m + p_jm), so the p_j terms cancel:
+//   fwd child (r = child heads, q = node tails):
+//     lb = max(h'_k + max(A + q_k, I' + q_l), h'_l + (B + q_l))
+//   bwd child (r = node fronts, q = child tails):
+//     lb = max(t'_l + max(r_l + B, r_k + I''), t'_k + (r_k + A))
+//   I' = max(PM_j + a_j - b_j, SM_j) + B,  I'' = I' + b_j - a_j
+// The backward pass stores S_j = max(A + q_k, I' + q_l) | max(r_l + B, r_k + I'') << 16 per
+// (job, lane); the child tables hold H'[c][m] = h'_m | t'_m << 16. Every term is a partial
+// sum of a bound below 2^16 (the (n+m) max p < 2^16 invariant), so one child costs two
+// byte permutes, one VIADD.16x2 and one VIADDMNMX.U16x2 for both directions. Each lane owns
+// a pair (32 pairs per round, the last round's spare lanes repeat pair P-1); per child the
+// 32 pair bounds are combined with REDUX.MAX.
 template <int M, bool SMALLN>
 __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView& in, int n, int mp, int f,
                                                unsigned long long fmask) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int NEG = -30000;
   const int lane = threadIdx.x & 31;
+  uint32_t* H = reinterpret_cast<uint32_t*>(iv.heads);  // [c][M] h' | t' << 16
   for (int c = lane; c < f; c += 32) {
     const int j = iv.freej[c];
     const int* pr = in.p32 + j * mp;
+    int hp[M];
     int prev = 0;
 #pragma unroll
     for (int k = 0; k < M; ++k) {
-      prev = max(prev, iv.fr[k]) + pr[k];
-      iv.heads[c * M + k] = static_cast<uint16_t>(prev);
+      hp[k] = max(prev, iv.fr[k]);
+      prev = hp[k] + pr[k];
     }
     prev = 0;
 #pragma unroll
     for (int k = M - 1; k >= 0; --k) {
-      prev = max(prev, iv.tl[k]) + pr[k];
-      iv.tails[c * M + k] = static_cast<uint16_t>(prev);
+      const int tp = max(prev, iv.tl[k]);
+      prev = tp + pr[k];
+      H[c * M + k] = static_cast<uint32_t>(hp[k]) | static_cast<uint32_t>(tp) << 16;
     }
   }
   __syncwarp();
-  int accF0 = 0, accF1 = 0, accB0 = 0, accB1 = 0;
+  uint32_t acc0 = 0, acc1 = 0;
   const int P = in.npairs;
   // packed rows are padded to a multiple of 32 pairs: lane q always reads bank q mod 32,
   // whatever position t each lane is at (the set-bit passes diverge in t)
   const int PS = round_up(P, 32);
-  int16_t* PMl = iv.pm + lane;
-  int16_t* SMl = iv.sm + lane;
+  int* Sl = reinterpret_cast<int*>(iv.pm) + lane;  // [j][32]: PM_j (forward pass), then S_j
   for (int q0 = 0; q0 < P; q0 += 32) {
-    const int q = q0 + lane;
-    const bool live = q < P;
-    const int k = live ? in.pk[q] : 0, l = live ? in.pl[q] : 0;
+    const int q = min(q0 + lane, P - 1);
+    const int k = in.pk[q], l = in.pl[q];
     const int Atot = iv.rm[k], Btot = iv.rm[l];
+    const int qk = iv.tl[k], ql = iv.tl[l], rk = iv.fr[k], rl = iv.fr[l];
+    const int cAq = Atot + qk, cRB = rl + Btot;
     if constexpr (SMALLN) {
-     if (live) {
       // the pair's free positions as a bitmask from the static inverse order (f lookups),
       // then passes over exactly the f set bits: uniform trip count, no predicated slots
       uint32_t Fq = 0;
@@ -425,7 +451,7 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
         const int j = e & 63;
         A += (e >> 6) & 127;
         const int X = A + static_cast<int>(e >> 20) - Bp;
-        PMl[j * 32] = static_cast<int16_t>(pm);
+        Sl[j * 32] = pm;
         pm = max(pm, X);
         Bp += (e >> 13) & 127;
       }
@@ -435,14 +461,16 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
         w ^= 1u << t;
         const unsigned e = in.packed[t * PS + q];
         const int j = e & 63;
-        Bs += (e >> 13) & 127;
+        const int a = (e >> 6) & 127, b = (e >> 13) & 127;
+        Bs += b;
         const int X = static_cast<int>(e >> 20) + Bs - As;
-        SMl[j * 32] = static_cast<int16_t>(sm);
+        const int I1 = max(Sl[j * 32] + a - b, sm) + Btot;
+        const int lo = max(cAq, I1 + ql), hi = max(cRB, rk + I1 + b - a);
+        Sl[j * 32] = static_cast<int>(static_cast<uint32_t>(lo) | static_cast<uint32_t>(hi) << 16);
         sm = max(sm, X);
-        As += (e >> 6) & 127;
+        As += a;
       }
-     }
-    } else if (live) {
+    } else {
       // n <= 64: same set-bit iteration over a 64-bit free-position mask
       unsigned long long Fq = 0;
       for (int c = 0; c < f; ++c) Fq |= 1ull << in.invord[iv.freej[c] * P + q];
@@ -452,7 +480,7 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
         const int j = e & 63;
         A += (e >> 6) & 127;
         const int X = A + static_cast<int>(e >> 20) - Bp;
-        PMl[j * 32] = static_cast<int16_t>(pm);
+        Sl[j * 32] = pm;
         pm = max(pm, X);
         Bp += (e >> 13) & 127;
       }
@@ -462,44 +490,39 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
         w ^= 1ull << t;
         const unsigned e = in.packed[t * PS + q];
         const int j = e & 63;
-        Bs += (e >> 13) & 127;
+        const int a = (e >> 6) & 127, b = (e >> 13) & 127;
+        Bs += b;
         const int X = static_cast<int>(e >> 20) + Bs - As;
-        SMl[j * 32] = static_cast<int16_t>(sm);
+        const int I1 = max(Sl[j * 32] + a - b, sm) + Btot;
+        const int lo = max(cAq, I1 + ql), hi = max(cRB, rk + I1 + b - a);
+        Sl[j * 32] = static_cast<int>(static_cast<uint32_t>(lo) | static_cast<uint32_t>(hi) << 16);
         sm = max(sm, X);
-        As += (e >> 6) & 127;
+        As += a;
       }
     }
-    const int qk = iv.tl[k], ql = iv.tl[l], rk = iv.fr[k], rl = iv.fr[l];
+    const uint32_t C = static_cast<uint32_t>(Btot + ql) | static_cast<uint32_t>(rk + Atot) << 16;
+    const uint32_t* Hk = H + k;
+    const uint32_t* Hl = H + l;
     for (int c = 0; c < f; ++c) {
       const int j = iv.freej[c];
-      int vF = 0, vB = 0;
-      if (live) {
-        const int a = in.p32[j * mp + k], b = in.p32[j * mp + l];
-        const int inner = max(PMl[j * 32] - b, SMl[j * 32] - a) + Btot;
-        const int hk = iv.heads[c * M + k], hl = iv.heads[c * M + l];
-        vF = max(hk + Atot - a + qk, max(hl + Btot - b, hk + inner) + ql);
-        vB = max(rk + Atot - a + iv.tails[c * M + k], max(rl + Btot - b, rk + inner) + iv.tails[c * M + l]);
-      }
-      vF = __reduce_max_sync(FULL, vF);
-      vB = __reduce_max_sync(FULL, vB);
+      const uint32_t hk = Hk[c * M], hl = Hl[c * M];
+      const uint32_t S = static_cast<uint32_t>(Sl[j * 32]);
+      const uint32_t V = max_u16x2(add_u16x2(__byte_perm(hk, hl, 0x7610), S), add_u16x2(__byte_perm(hl, hk, 0x7610), C));
+      const uint32_t vF = __reduce_max_sync(FULL, V & 0xffffu);
+      const uint32_t vB = __reduce_max_sync(FULL, V) & 0xffff0000u;
       if (lane == (c & 31)) {
-        if (c < 32) {
-          accF0 = max(accF0, vF);
-          accB0 = max(accB0, vB);
-        } else {
-          accF1 = max(accF1, vF);
-          accB1 = max(accB1, vB);
-        }
+        if (SMALLN || c < 32) acc0 = max_u16x2(acc0, vF | vB);
+        else acc1 = max_u16x2(acc1, vF | vB);
       }
     }
   }
   if (lane < f) {
-    iv.lbf[lane] = accF0;
-    iv.lbb[lane] = accB0;
+    iv.lbf[lane] = static_cast<int>(acc0 & 0xffffu);
+    iv.lbb[lane] = static_cast<int>(acc0 >> 16);
   }
-  if (lane + 32 < f) {
-    iv.lbf[lane + 32] = accF1;
-    iv.lbb[lane + 32] = accB1;
+  if (!SMALLN && lane + 32 < f) {
+    iv.lbf[lane + 32] = static_cast<int>(acc1 & 0xffffu);
+    iv.lbb[lane + 32] = static_cast<int>(acc1 >> 16);
   }
 }
 
