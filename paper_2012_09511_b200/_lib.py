@@ -46,6 +46,7 @@ class Config(ctypes.Structure):
         ("steal_trigger", ctypes.c_double),
         ("rounds_per_sync", ctypes.c_int),
         ("max_split", ctypes.c_int),
+        ("split_mode", ctypes.c_int),
     ]
 
 

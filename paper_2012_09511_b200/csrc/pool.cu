@@ -361,14 +361,64 @@ struct StealParams {
   const float* lens;    // [K] per-explorer log2 remaining (written by explore_kernel)
   int max_split;        // thieves per victim in one steal phase (multi-way split), 1..63
   int* plan;            // [2] victims paired this phase, thieves per victim (split kernels)
+  int split_mode;       // 0 live siblings, 1 factoradic midpoint
 };
 
 constexpr int kStealThreads = 1024;
 constexpr int kBins = 2048;
 
-// Remaining work of every explorer after a round (grid-wide, one thread per explorer):
-// log2 of its remaining leaves from the effective position, -2 busy/unsplittable, -3 idle.
-__global__ void lens_kernel(IvmLayout L, const unsigned char* state, int K, const float* lgfact, float* lens) {
+// ---- live-sibling splitting (split_mode 0)
+// An explorer's untouched work is the unexplored, unpruned cells right of its path: at level
+// l, cells c > V[l] of row l with a positive entry (negative = pruned by bound or consumed),
+// restricted to [pos, end): no level before the first digit where pos and end differ, and
+// only cells below end[d] at that level d. The shallowest level l* holding any dominates (a
+// cell there roots (n-1-l*)! leaves). Returns their count and positions (ascending).
+__device__ int live_siblings(const unsigned char* vb, const IvmLayout& L, int& lstar, int* cells) {
+  const int n = L.n;
+  const IvmHdr* h = reinterpret_cast<const IvmHdr*>(vb);
+  if (h->state != kActive) return 0;
+  const int8_t* V = reinterpret_cast<const int8_t*>(vb + L.o_v);
+  const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
+  const int8_t* C = reinterpret_cast<const int8_t*>(vb + L.o_cells);
+  const bool he = h->has_end != 0;
+  const int level = h->level;
+  int l = 0;
+  if (he) {
+    while (l <= level && V[l] == E[l]) ++l;
+    if (l <= level && V[l] > E[l]) return 0;
+  }
+  const int d = he ? l : -1;
+  for (; l <= level; ++l) {
+    const int8_t* row = C + tri_off(l, n);
+    const int lim = l == d ? E[l] : n - l;
+    int cnt = 0;
+    for (int c = V[l] + 1; c < lim; ++c)
+      if (row[c] > 0) cells[cnt++] = c;
+    if (cnt) {
+      lstar = l;
+      return cnt;
+    }
+  }
+  return 0;
+}
+
+// Items of a live split: item 0 is the explorer's own path (the current cell at l* with
+// everything below it), items 1..cnt the live siblings. g thieves cut the cnt + 1 items into
+// g + 1 contiguous groups; the victim keeps group 0. Start cell of group i (1..g):
+__device__ __forceinline__ int live_group_start(const int* cells, int cnt, int g, int i) {
+  return cells[i * (cnt + 1) / (g + 1) - 1];
+}
+
+// digits of (prefix V[0..l*-1], cell at l*, zeros)
+__device__ __forceinline__ void live_point(const int8_t* V, int lstar, int cell, int n, int* out) {
+  for (int l = 0; l < n; ++l) out[l] = l < lstar ? V[l] : (l == lstar ? cell : 0);
+}
+
+// Remaining work of every explorer after a round (grid-wide, one thread per explorer), as
+// log2 of leaves; -2 busy / unsplittable, -3 idle. mode 0: the live siblings of the
+// shallowest level holding any, (cnt + 1) (n-1-l*)!; mode 1: the exact factoradic length of
+// [effective position, end).
+__global__ void lens_kernel(IvmLayout L, const unsigned char* state, int K, const float* lgfact, float* lens, int mode) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= K) return;
   const unsigned char* blk = state + static_cast<size_t>(i) * L.gstride;
@@ -377,12 +427,19 @@ __global__ void lens_kernel(IvmLayout L, const unsigned char* state, int K, cons
   if (h->state == kInit) {
     lg = -2.f;
   } else if (h->state == kActive) {
-    int pos[kMaxN];
     lg = -2.f;
-    if (effective_pos(reinterpret_cast<const int8_t*>(blk + L.o_v), h->level,
-                      reinterpret_cast<const int8_t*>(blk + L.o_cells), L.n, pos)) {
-      const float r = remaining_log2_pos(pos, reinterpret_cast<const int8_t*>(blk + L.o_end), h->has_end != 0, L.n, lgfact);
-      if (r >= 0.f) lg = r;
+    if (mode == 0) {
+      int cells[kMaxN];
+      int lstar = 0;
+      const int cnt = live_siblings(blk, L, lstar, cells);
+      if (cnt > 0) lg = log2f(static_cast<float>(cnt + 1)) + lgfact[L.n - 1 - lstar];
+    } else {
+      int pos[kMaxN];
+      if (effective_pos(reinterpret_cast<const int8_t*>(blk + L.o_v), h->level,
+                        reinterpret_cast<const int8_t*>(blk + L.o_cells), L.n, pos)) {
+        const float r = remaining_log2_pos(pos, reinterpret_cast<const int8_t*>(blk + L.o_end), h->has_end != 0, L.n, lgfact);
+        if (r >= 0.f) lg = r;
+      }
     }
   }
   lens[i] = lg;
@@ -468,30 +525,52 @@ __device__ int split_setup(const unsigned char* vb, const IvmLayout& L, int r, i
 // [pos, end) cut into r + 1 equal parts goes to thief i - 1. Reads the victims only; their
 // ends are cut afterwards by split_victims_kernel (stream order).
 __global__ void split_thieves_kernel(IvmLayout L, unsigned char* state, const int* ptot, const int* thief,
-                                     const int* victim, const int* plan, DevCounters* ctr) {
+                                     const int* victim, const int* plan, DevCounters* ctr, int mode) {
   const int nv = plan[0], rs = plan[1];
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g0 = blockIdx.x * blockDim.x + threadIdx.x;
   int ok = 0;
-  if (g < nv * rs) {
-    const int v = g / rs, i = g % rs + 1;
+  if (g0 < nv * rs) {
+    const int v = g0 / rs, i = g0 % rs + 1;
     const unsigned char* vb = state + static_cast<size_t>(victim[v]) * L.gstride;
-    int pos[kMaxN], D[kMaxN], b0[kMaxN], b1[kMaxN];
-    int top = 0;
-    const int r = split_setup(vb, L, rs, pos, D, top);
-    if (i <= r) {
-      const int n = L.n;
-      const IvmHdr* vh = reinterpret_cast<const IvmHdr*>(vb);
-      const bool last = i == r;
-      split_point(pos, D, top, i, r + 1, n, b0);
-      if (last) {
-        const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
-        for (int l = 0; l < n; ++l) b1[l] = E[l];
-      } else {
-        split_point(pos, D, top, i + 1, r + 1, n, b1);
+    const IvmHdr* vh = reinterpret_cast<const IvmHdr*>(vb);
+    const int n = L.n;
+    int b0[kMaxN], b1[kMaxN];
+    if (mode == 0) {
+      int cells[kMaxN];
+      int lstar = 0;
+      const int cnt = live_siblings(vb, L, lstar, cells);
+      const int g = min(rs, cnt);
+      if (i <= g) {
+        const int8_t* V = reinterpret_cast<const int8_t*>(vb + L.o_v);
+        const bool last = i == g;
+        live_point(V, lstar, live_group_start(cells, cnt, g, i), n, b0);
+        if (last) {
+          const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
+          for (int l = 0; l < n; ++l) b1[l] = E[l];
+        } else {
+          live_point(V, lstar, live_group_start(cells, cnt, g, i + 1), n, b1);
+        }
+        seat_explorer(state + static_cast<size_t>(thief[v * rs + i - 1]) * L.gstride, L, ptot, b0, b1,
+                      last ? vh->has_end != 0 : true);
+        ok = 1;
       }
-      seat_explorer(state + static_cast<size_t>(thief[v * rs + i - 1]) * L.gstride, L, ptot, b0, b1,
-                    last ? vh->has_end != 0 : true);
-      ok = 1;
+    } else {
+      int pos[kMaxN], D[kMaxN];
+      int top = 0;
+      const int r = split_setup(vb, L, rs, pos, D, top);
+      if (i <= r) {
+        const bool last = i == r;
+        split_point(pos, D, top, i, r + 1, n, b0);
+        if (last) {
+          const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
+          for (int l = 0; l < n; ++l) b1[l] = E[l];
+        } else {
+          split_point(pos, D, top, i + 1, r + 1, n, b1);
+        }
+        seat_explorer(state + static_cast<size_t>(thief[v * rs + i - 1]) * L.gstride, L, ptot, b0, b1,
+                      last ? vh->has_end != 0 : true);
+        ok = 1;
+      }
     }
   }
   const unsigned cnt = __popc(__ballot_sync(0xffffffffu, ok));
@@ -503,17 +582,27 @@ __global__ void split_thieves_kernel(IvmLayout L, unsigned char* state, const in
 }
 
 // The victims keep the first part: end <- pos + D / (r + 1) (one thread per victim).
-__global__ void split_victims_kernel(IvmLayout L, unsigned char* state, const int* victim, const int* plan) {
+__global__ void split_victims_kernel(IvmLayout L, unsigned char* state, const int* victim, const int* plan, int mode) {
   const int nv = plan[0], rs = plan[1];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   unsigned char* vb = state + static_cast<size_t>(victim[v]) * L.gstride;
-  int pos[kMaxN], D[kMaxN], b[kMaxN];
-  int top = 0;
-  const int r = split_setup(vb, L, rs, pos, D, top);
-  if (r < 1) return;
-  split_point(pos, D, top, 1, r + 1, L.n, b);
   int8_t* E = reinterpret_cast<int8_t*>(vb + L.o_end);
+  int b[kMaxN];
+  if (mode == 0) {
+    int cells[kMaxN];
+    int lstar = 0;
+    const int cnt = live_siblings(vb, L, lstar, cells);
+    const int g = min(rs, cnt);
+    if (g < 1) return;
+    live_point(reinterpret_cast<const int8_t*>(vb + L.o_v), lstar, live_group_start(cells, cnt, g, 1), L.n, b);
+  } else {
+    int pos[kMaxN], D[kMaxN];
+    int top = 0;
+    const int r = split_setup(vb, L, rs, pos, D, top);
+    if (r < 1) return;
+    split_point(pos, D, top, 1, r + 1, L.n, b);
+  }
   for (int l = 0; l < L.n; ++l) E[l] = static_cast<int8_t>(b[l]);
   reinterpret_cast<IvmHdr*>(vb)->has_end = 1;
 }
@@ -636,8 +725,33 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
     IvmHdr* vh = reinterpret_cast<IvmHdr*>(vb);
     const int8_t* V = reinterpret_cast<const int8_t*>(vb + S.L.o_v);
     int8_t* E = reinterpret_cast<int8_t*>(vb + S.L.o_end);
-    if (!effective_pos(V, vh->level, reinterpret_cast<const int8_t*>(vb + S.L.o_cells), n, pos)) continue;
     const bool had_end = vh->has_end != 0;
+    if (S.split_mode == 0) {
+      int lstar = 0;
+      const int cnt = live_siblings(vb, S.L, lstar, D);  // D holds the live cells here
+      int rv = min(r, cnt);
+      if (rv < 1) continue;
+      const int slot0 = atomicAdd(&s_tot[0], rv);
+      if (slot0 >= want) continue;
+      rv = min(rv, want - slot0);  // never more than the caller's buffer
+      for (int l = 0; l < n; ++l) oend[l] = E[l];
+      for (int i = 1; i <= rv; ++i) {
+        const bool last = i == rv;
+        live_point(V, lstar, live_group_start(D, cnt, rv, i), n, pb);
+        if (!last) live_point(V, lstar, live_group_start(D, cnt, rv, i + 1), n, b);
+        int* o = out_digits + static_cast<size_t>(slot0 + i - 1) * 2 * n;
+        for (int l = 0; l < n; ++l) {
+          o[l] = pb[l];
+          o[n + l] = last ? (had_end ? oend[l] : 0) : b[l];
+        }
+        out_nf[slot0 + i - 1] = last ? (had_end ? 0 : 1) : 0;
+      }
+      live_point(V, lstar, live_group_start(D, cnt, rv, 1), n, pb);  // the victim keeps group 0
+      for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(pb[l]);
+      vh->has_end = 1;
+      continue;
+    }
+    if (!effective_pos(V, vh->level, reinterpret_cast<const int8_t*>(vb + S.L.o_cells), n, pos)) continue;
     int top = 0;
     if (!diff_digits(pos, E, had_end, n, D, top)) continue;
     int rv = r;
@@ -1358,6 +1472,7 @@ int run_round(pbbgpu_pool* P) {
   S.trigger = static_cast<float>(P->cfg.steal_trigger > 0 ? P->cfg.steal_trigger : 1.0);
   S.lens = P->d_lens;
   S.max_split = P->cfg.max_split > 0 ? std::min(P->cfg.max_split, 63) : 4;
+  S.split_mode = P->cfg.split_mode;
   // several (explore, steal) rounds back to back per host synchronization: the rounds are
   // device-timed, and a round after exhaustion costs only the state copy of an empty launch
   const int R = P->rounds_per_sync;
@@ -1366,14 +1481,14 @@ int run_round(pbbgpu_pool* P) {
     P->efn<<<P->grid, P->block, P->smem, P->stream>>>(E);
     ck(cudaGetLastError(), "explore_kernel launch");
     ck(cudaEventRecord(P->evs[3 * r + 1], P->stream), "event");
-    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens);
+    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, S.split_mode);
     ck(cudaGetLastError(), "lens_kernel launch");
     steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
     ck(cudaGetLastError(), "steal_kernel launch");
     split_thieves_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, S.thief, S.victim,
-                                                                     S.plan, P->d_ctr);
+                                                                     S.plan, P->d_ctr, S.split_mode);
     ck(cudaGetLastError(), "split_thieves_kernel launch");
-    split_victims_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, S.victim, S.plan);
+    split_victims_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, S.victim, S.plan, S.split_mode);
     ck(cudaGetLastError(), "split_victims_kernel launch");
     ck(cudaEventRecord(P->evs[3 * r + 2], P->stream), "event");
     P->launches += 5;
@@ -1645,7 +1760,8 @@ int pbbgpu_export(pbbgpu_pool* P, int max_count, uint16_t* a_out, uint16_t* b_ou
     S.min_log2 = static_cast<float>(P->cfg.min_steal_log2 > 0 ? P->cfg.min_steal_log2 : std::log2(40320.0));
     S.lgfact = P->d_lgfact;
     S.lens = P->d_lens;
-    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens);
+    S.split_mode = P->cfg.split_mode;
+    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, S.split_mode);
     ck(cudaGetLastError(), "lens_kernel");
     P->launches += 1;
     export_kernel<<<1, kStealThreads, 0, P->stream>>>(S, want, d_dig, d_nf, d_cnt);
@@ -1856,7 +1972,7 @@ int pbbgpu_explorer_lengths(pbbgpu_pool* P, float* out, int cap) {
   return guarded([&] {
     if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
     if (cap < P->K) throw std::invalid_argument("explorer_lengths buffer smaller than K");
-    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens);
+    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, 1);
     ck(cudaGetLastError(), "lens_kernel");
     P->launches += 1;
     xfer(P, out, P->d_lens, static_cast<size_t>(P->K) * sizeof(float), cudaMemcpyDeviceToHost, "lens copy");

@@ -109,14 +109,17 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
         donors = [int(r) for r in np.argsort(-actives, kind="stable") if actives[r] > 0 and 2 * actives[r] >= amax]
         if not receivers or not donors:
             continue
-        # phase 2: donors export, everybody gathers, receivers seat their share
+        # phase 2: donors export, everybody gathers, receivers seat their share. The phase-1
+        # counts are exact (no round runs in between): a donor exports at most its receivers'
+        # idle explorers, and each receiver takes a contiguous share no larger than its idle.
         pairs = {}
         for i, r in enumerate(receivers):
             pairs.setdefault(int(donors[i % len(donors)]), []).append(r)
         buf = np.zeros((X, width), dtype=np.int32)
         cnt = 0
         if rank in pairs:
-            a, b, nf = pool.export_work(X)
+            room = sum(K - int(actives[r]) for r in pairs[rank])
+            a, b, nf = pool.export_work(min(X, room))
             cnt = len(nf)
             buf[:cnt, :n] = a
             buf[:cnt, n:2 * n] = b
@@ -130,7 +133,17 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
             arr = allb[donor].cpu().numpy()
             c = int(arr[-1])
             rows = arr[:-1].reshape(X, width)[:c]
-            mine = rows[recvs.index(rank)::len(recvs)]
+            # shares in proportion to the receivers' idle explorers, in receiver order
+            idle = [K - int(actives[r]) for r in recvs]
+            tot = max(1, sum(idle))
+            shares = [c * i // tot for i in idle]
+            for i in range(c - sum(shares)):
+                shares[i % len(shares)] += 1
+            me = recvs.index(rank)
+            off = sum(shares[:me])
+            if shares[me] > idle[me]:
+                raise RuntimeError("inter-GPU exchange: share exceeds the receiver's idle explorers")
+            mine = rows[off:off + shares[me]]
             if len(mine):
                 pool.import_work(mine[:, :n].astype(np.uint16), mine[:, n:2 * n].astype(np.uint16),
                                  mine[:, 2 * n].astype(np.uint8))

@@ -46,6 +46,7 @@ class PoolConfig:
     steal_trigger: float = 0.0  # steal when active < trigger*K; 0 = 1.0 (reference: 0.8)
     rounds_per_sync: int = 0    # device rounds per run_round() call; 0 = 2
     max_split: int = 0          # thieves per victim per steal phase (multi-way split); 0 = 4
+    split_mode: int = 0         # 0 = live-sibling split, 1 = factoradic midpoint (reference)
 
     def to_c(self) -> _lib.Config:
         c = _lib.Config()
@@ -62,6 +63,7 @@ class PoolConfig:
         c.steal_trigger = self.steal_trigger
         c.rounds_per_sync = self.rounds_per_sync
         c.max_split = self.max_split
+        c.split_mode = self.split_mode
 
         return c
 

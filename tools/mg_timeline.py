@@ -11,8 +11,10 @@ rank, world = dist.get_rank(), dist.get_world_size()
 name, ub, bound = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 low = float(sys.argv[4]) if len(sys.argv) > 4 else 0.25
 pinned = len(sys.argv) > 5 and sys.argv[5] == "pinned"
+X = int(sys.argv[6]) if len(sys.argv) > 6 else None
+quiet = len(sys.argv) > 7
 pool = pbb.GpuPool(pbb.taillard_named(name), pbb.PoolConfig(device=local, pinned=pinned), bound=bound)
-multi.solve_distributed(pool, ub, device=dev, low_fraction=low)  # warm
+multi.solve_distributed(pool, ub, device=dev, low_fraction=low, export_max=X)  # warm
 log = []
 orig = pool.run_round
 t0 = [0.0]
@@ -22,12 +24,12 @@ def rr():
     return a
 pool.run_round = rr
 dist.barrier(); torch.cuda.synchronize(); t0[0] = time.time()
-r = multi.solve_distributed(pool, ub, device=dev, low_fraction=low)
+r = multi.solve_distributed(pool, ub, device=dev, low_fraction=low, export_max=X)
 torch.cuda.synchronize(); dt = time.time() - t0[0]
 allg = [None] * world
 dist.all_gather_object(allg, log)
 if rank == 0:
     print(json.dumps({"world": world, "low": low, "s": round(dt, 4), "unique": r.unique, "remote": r.remote_intervals, "rounds": r.rounds}))
-    for i in range(max(len(x) for x in allg)):
+    for i in (range(max(len(x) for x in allg)) if not quiet else []):
         print(i, " ".join(f"{x[i][0]:.3f}:{x[i][1]:5d}" if i < len(x) else "-" for x in allg))
 dist.destroy_process_group()
