@@ -39,9 +39,9 @@ WORKLOADS = {
                       desc="Taillard ta021 (20x20), LB2 Johnson bound, initial UB = optimum 2297, full proof per step"),
     "ta021-lb1": dict(instance="ta021", bound="lb1", ub=2297,
                       desc="Taillard ta021 (20x20), LB1 one-machine bound, initial UB = optimum 2297, full proof per step"),
-    "ta041-lb1-pinned": dict(instance="ta041", bound="lb1", ub=3000, pinned=True,
+    "ta041-lb1-pinned": dict(instance="ta041", bound="lb1", ub=3000, pinned=True, split_mode=1,
                              desc="Taillard ta041 (50x10), LB1, pinned UB 3000 (prune >= 3000, never improve): "
-                                  "fixed tree of 520,458,272 nodes per step"),
+                                  "fixed tree of 520,458,272 nodes per step; live-sibling work splitting"),
     "ta056-lb2": dict(instance="ta056", bound="lb2", ub=3679, time_limit=10.0,
                       desc="Taillard ta056 (50x20), LB2, initial UB = best-known 3679, 10 s time-bounded "
                            "exploration per step"),
@@ -214,7 +214,7 @@ def run_extras(pbb, solve_distributed, dev, local, world, rank, peak, args):
     for key, name, bound, ub, pinned, secs in (("ta056_lb2_ub3679_timebounded", "ta056", "lb2", 3679, False, 5.0),
                                                ("ta041_lb1_pinned3000_timebounded", "ta041", "lb1", 3000, True, 5.0)):
         inst = pbb.taillard_named(name)
-        cfg = pbb.PoolConfig(device=local, pinned=pinned)
+        cfg = pbb.PoolConfig(device=local, pinned=pinned, split_mode=1 if pinned else 0)
         with pbb.GpuPool(inst, cfg, bound=bound) as pool:
             r, ms = timed(lambda: solve_distributed(pool, ub, device=dev, time_limit_s=secs))
         out[key] = {"ms": ms, "unique_nodes": r.unique, "leaves": r.leaves, "best": r.best_value,
@@ -293,7 +293,8 @@ def main():
     W = w_lb2 if wl["bound"] == "lb2" else w_lb1
     world_ = world
     cfg = pbb.PoolConfig(device=local, round_us=args.round_us, rounds_per_sync=args.rounds_per_sync,
-                         pinned=bool(wl.get("pinned", False)), max_split=args.max_split)
+                         pinned=bool(wl.get("pinned", False)), max_split=args.max_split,
+                         split_mode=int(wl.get("split_mode", 0)))
     tlim = float(wl.get("time_limit", 0.0))
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
@@ -408,6 +409,7 @@ def main():
                            "mode": (f"time-bounded ({tlim:g} s) per step" if tlim else "full proof (fixed tree) per step"),
                            "unique_nodes_per_step": unique, "leaves_per_step": results[-1].leaves,
                            "time_to_proof_ms": statistics.mean(times), "explorers_per_gpu": pool.K(),
+                           "work_split": "live siblings" if int(wl.get("split_mode", 0)) == 1 else "factoradic (reference)",
                            "parallelism": f"dp{world}" if world > 1 else "single",
                            "l2": "256 MiB flush between steps, outside the per-step event brackets",
                            "desc": wl["desc"]},

@@ -72,9 +72,11 @@ typedef struct {
   double steal_trigger;  /* steal phase when active < trigger*K; 0 = 1.0 (reference pool: 0.8) */
   int rounds_per_sync;   /* (explore, steal) rounds per pbbgpu_run_round host sync; 0 = 2, max 8 */
   int max_split;         /* thieves one victim may feed per steal phase (multi-way split); 0 = 4 */
-  int split_mode;        /* 0 = live-sibling split (thieves take unexplored, unpruned subtrees of
-                            the shallowest level holding any), 1 = factoradic interval midpoint
-                            (the reference's steal_right_half, explorer.cpp:265-280) */
+  int split_mode;        /* 0 = factoradic interval split (the reference's steal_right_half,
+                            explorer.cpp:265-280, generalised to r-way); 1 = live-sibling split
+                            (thieves take unexplored, unpruned subtrees of the shallowest level
+                            holding any; best on irregular pinned trees); 2 = live-sibling where
+                            the victim has decomposed siblings left, factoradic otherwise */
 } pbbgpu_config_t;
 
 typedef struct {

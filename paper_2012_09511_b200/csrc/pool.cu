@@ -428,12 +428,14 @@ __global__ void lens_kernel(IvmLayout L, const unsigned char* state, int K, cons
     lg = -2.f;
   } else if (h->state == kActive) {
     lg = -2.f;
-    if (mode == 0) {
+    int cnt = 0;
+    if (mode != 1) {
       int cells[kMaxN];
       int lstar = 0;
-      const int cnt = live_siblings(blk, L, lstar, cells);
+      cnt = live_siblings(blk, L, lstar, cells);
       if (cnt > 0) lg = log2f(static_cast<float>(cnt + 1)) + lgfact[L.n - 1 - lstar];
-    } else {
+    }
+    if (mode == 1 || (mode == 0 && cnt == 0)) {
       int pos[kMaxN];
       if (effective_pos(reinterpret_cast<const int8_t*>(blk + L.o_v), h->level,
                         reinterpret_cast<const int8_t*>(blk + L.o_cells), L.n, pos)) {
@@ -535,10 +537,10 @@ __global__ void split_thieves_kernel(IvmLayout L, unsigned char* state, const in
     const IvmHdr* vh = reinterpret_cast<const IvmHdr*>(vb);
     const int n = L.n;
     int b0[kMaxN], b1[kMaxN];
-    if (mode == 0) {
-      int cells[kMaxN];
-      int lstar = 0;
-      const int cnt = live_siblings(vb, L, lstar, cells);
+    int cells[kMaxN];
+    int lstar = 0;
+    const int cnt = mode == 1 ? 0 : live_siblings(vb, L, lstar, cells);
+    if (cnt > 0 || mode == 2) {
       const int g = min(rs, cnt);
       if (i <= g) {
         const int8_t* V = reinterpret_cast<const int8_t*>(vb + L.o_v);
@@ -589,10 +591,10 @@ __global__ void split_victims_kernel(IvmLayout L, unsigned char* state, const in
   unsigned char* vb = state + static_cast<size_t>(victim[v]) * L.gstride;
   int8_t* E = reinterpret_cast<int8_t*>(vb + L.o_end);
   int b[kMaxN];
-  if (mode == 0) {
-    int cells[kMaxN];
-    int lstar = 0;
-    const int cnt = live_siblings(vb, L, lstar, cells);
+  int cells[kMaxN];
+  int lstar = 0;
+  const int cnt = mode == 1 ? 0 : live_siblings(vb, L, lstar, cells);
+  if (cnt > 0 || mode == 2) {
     const int g = min(rs, cnt);
     if (g < 1) return;
     live_point(reinterpret_cast<const int8_t*>(vb + L.o_v), lstar, live_group_start(cells, cnt, g, 1), L.n, b);
@@ -726,9 +728,9 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
     const int8_t* V = reinterpret_cast<const int8_t*>(vb + S.L.o_v);
     int8_t* E = reinterpret_cast<int8_t*>(vb + S.L.o_end);
     const bool had_end = vh->has_end != 0;
-    if (S.split_mode == 0) {
-      int lstar = 0;
-      const int cnt = live_siblings(vb, S.L, lstar, D);  // D holds the live cells here
+    int lstar = 0;
+    const int cnt = S.split_mode == 1 ? 0 : live_siblings(vb, S.L, lstar, D);  // D holds the live cells here
+    if (cnt > 0 || S.split_mode == 2) {
       int rv = min(r, cnt);
       if (rv < 1) continue;
       const int slot0 = atomicAdd(&s_tot[0], rv);
@@ -1316,6 +1318,16 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   reset_search(P);
 }
 
+// pbbgpu_config_t.split_mode (0 factoradic = reference, 1 live siblings, 2 live else
+// factoradic) -> the device kernels' mode (1 factoradic, 2 live only, 0 hybrid)
+int split_kind(int cfg_mode) {
+  switch (cfg_mode) {
+    case 1: return 2;
+    case 2: return 0;
+    default: return 1;
+  }
+}
+
 void read_counters(pbbgpu_pool* P) {
   xfer(P, P->h_ctr, P->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, "ctr copy");
 }
@@ -1472,7 +1484,7 @@ int run_round(pbbgpu_pool* P) {
   S.trigger = static_cast<float>(P->cfg.steal_trigger > 0 ? P->cfg.steal_trigger : 1.0);
   S.lens = P->d_lens;
   S.max_split = P->cfg.max_split > 0 ? std::min(P->cfg.max_split, 63) : 4;
-  S.split_mode = P->cfg.split_mode;
+  S.split_mode = split_kind(P->cfg.split_mode);
   // several (explore, steal) rounds back to back per host synchronization: the rounds are
   // device-timed, and a round after exhaustion costs only the state copy of an empty launch
   const int R = P->rounds_per_sync;
@@ -1760,7 +1772,7 @@ int pbbgpu_export(pbbgpu_pool* P, int max_count, uint16_t* a_out, uint16_t* b_ou
     S.min_log2 = static_cast<float>(P->cfg.min_steal_log2 > 0 ? P->cfg.min_steal_log2 : std::log2(40320.0));
     S.lgfact = P->d_lgfact;
     S.lens = P->d_lens;
-    S.split_mode = P->cfg.split_mode;
+    S.split_mode = split_kind(P->cfg.split_mode);
     lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, S.split_mode);
     ck(cudaGetLastError(), "lens_kernel");
     P->launches += 1;

@@ -46,7 +46,7 @@ _DELTA = ("unique", "decomposed", "leaves", "improvements", "local_steals")
 
 
 def solve_distributed(pool, ub: int, group=None, device=None, export_max: Optional[int] = None,
-                      low_fraction: float = 0.25, time_limit_s: float = 0.0) -> DistResult:
+                      low_fraction: float = 0.5, time_limit_s: float = 0.0) -> DistResult:
     """Run `pool` (a GpuPool, or any object with its surface) to exhaustion cooperatively with
     the other ranks of `group` (torch.distributed). world_size == 1 degenerates to pool_run."""
     import time
@@ -67,7 +67,7 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
         pool.assign_split_strided(rank, world, K, world * K)
     else:
         pool.assign_split_range(rank * K, K, world * K)
-    X = export_max if export_max else max(1, min(1024, K // 4))
+    X = export_max if export_max else max(1, K // 2)
     low = int(K * low_fraction)
     remote = 0
     rounds = 0

@@ -46,7 +46,7 @@ class PoolConfig:
     steal_trigger: float = 0.0  # steal when active < trigger*K; 0 = 1.0 (reference: 0.8)
     rounds_per_sync: int = 0    # device rounds per run_round() call; 0 = 2
     max_split: int = 0          # thieves per victim per steal phase (multi-way split); 0 = 4
-    split_mode: int = 0         # 0 = live-sibling split, 1 = factoradic midpoint (reference)
+    split_mode: int = 0         # 0 = factoradic (reference), 1 = live siblings, 2 = live else factoradic
 
     def to_c(self) -> _lib.Config:
         c = _lib.Config()

@@ -117,11 +117,13 @@ def test_fixed_tree_lb2_matches_oracle(key):
 
 
 @pytest.mark.timeout(180)
+@pytest.mark.parametrize("split_mode", [0, 1, 2])
 @pytest.mark.parametrize("steps,explorers,min_steal", [(64, 200, 2), (31, 333, 24), (200, 4096, 40320)])
-def test_unique_count_invariant_under_stealing(steps, explorers, min_steal):
-    """Tiny rounds + many thieves: the unique-count rule must hold under heavy stealing."""
+def test_unique_count_invariant_under_stealing(steps, explorers, min_steal, split_mode):
+    """Tiny rounds + many thieves: the unique-count rule must hold under heavy stealing, for
+    the factoradic, live-sibling and hybrid split policies."""
     ref = golden_io.ref_counts()["ta011@1582"]
-    cfg = pbb.PoolConfig(explorers=explorers, batch_steps=steps, min_steal_len=min_steal)
+    cfg = pbb.PoolConfig(explorers=explorers, batch_steps=steps, min_steal_len=min_steal, split_mode=split_mode)
     res = pbb.pool_run(pbb.taillard_named("ta011"), 1582, cfg=cfg)
     assert res.stats.unique == ref["decomposed"]
     assert res.stats.leaves == ref["leaves"]

@@ -13,7 +13,7 @@ from tests import golden_io
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, name, ub, bound, out):
+def _worker(rank, world, port, name, ub, bound, split_mode, out):
     import paper_2012_09511_b200 as pbb
     from paper_2012_09511_b200.multi import solve_distributed
 
@@ -21,7 +21,7 @@ def _worker(rank, world, port, name, ub, bound, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     dev = rank % torch.cuda.device_count()
-    pool = pbb.GpuPool(pbb.taillard_named(name), pbb.PoolConfig(device=dev, explorers=2048), bound=bound)
+    pool = pbb.GpuPool(pbb.taillard_named(name), pbb.PoolConfig(device=dev, explorers=2048, split_mode=split_mode), bound=bound)
     res = solve_distributed(pool, ub, device="cpu")
     out[rank] = (res.unique, res.leaves, res.best_value, res.remote_intervals, res.completed, res.hist)
     pool.close()
@@ -35,14 +35,16 @@ def _port():
 
 
 @pytest.mark.timeout(300)
-@pytest.mark.parametrize("name,ub,bound", [("ta011", 1582, "lb1"), ("ta041", 2991, "lb1"), ("ta011", 1582, "lb2")])
-def test_two_ranks_match_single_gpu_counts(name, ub, bound):
+@pytest.mark.parametrize("name,ub,bound,split_mode", [("ta011", 1582, "lb1", 0), ("ta041", 2991, "lb1", 0),
+                                                      ("ta011", 1582, "lb2", 0), ("ta041", 2991, "lb1", 1),
+                                                      ("ta011", 1582, "lb2", 2)])
+def test_two_ranks_match_single_gpu_counts(name, ub, bound, split_mode):
     gold = golden_io.ref_counts()[f"{name}@{ub}"] if bound == "lb1" else golden_io.lb2_counts()[f"{name}@{ub}"]
     want = gold["decomposed"] if bound == "lb1" else gold["unique"]
     ctx = mp.get_context("spawn")
     with ctx.Manager() as mgr:
         out = mgr.dict()
-        mp.start_processes(_worker, args=(2, _port(), name, ub, bound, out), nprocs=2, start_method="spawn", join=True)
+        mp.start_processes(_worker, args=(2, _port(), name, ub, bound, split_mode, out), nprocs=2, start_method="spawn", join=True)
         r0, r1 = out[0], out[1]
     assert r0[0] == r1[0] == want
     assert r0[1] == r1[1] == gold["leaves"]

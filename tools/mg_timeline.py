@@ -13,7 +13,7 @@ low = float(sys.argv[4]) if len(sys.argv) > 4 else 0.25
 pinned = len(sys.argv) > 5 and sys.argv[5] == "pinned"
 X = int(sys.argv[6]) if len(sys.argv) > 6 else None
 quiet = len(sys.argv) > 7
-pool = pbb.GpuPool(pbb.taillard_named(name), pbb.PoolConfig(device=local, pinned=pinned), bound=bound)
+pool = pbb.GpuPool(pbb.taillard_named(name), pbb.PoolConfig(device=local, pinned=pinned, split_mode=int(os.environ.get("SPLIT_MODE", "0"))), bound=bound)
 multi.solve_distributed(pool, ub, device=dev, low_fraction=low, export_max=X)  # warm
 log = []
 orig = pool.run_round
