@@ -39,9 +39,10 @@ WORKLOADS = {
                       desc="Taillard ta021 (20x20), LB2 Johnson bound, initial UB = optimum 2297, full proof per step"),
     "ta021-lb1": dict(instance="ta021", bound="lb1", ub=2297,
                       desc="Taillard ta021 (20x20), LB1 one-machine bound, initial UB = optimum 2297, full proof per step"),
-    "ta041-lb1-pinned": dict(instance="ta041", bound="lb1", ub=3000, pinned=True, split_mode=1,
+    "ta041-lb1-pinned": dict(instance="ta041", bound="lb1", ub=3000, pinned=True, split_mode=1, seed_div=16,
                              desc="Taillard ta041 (50x10), LB1, pinned UB 3000 (prune >= 3000, never improve): "
-                                  "fixed tree of 520,458,272 nodes per step; live-sibling work splitting"),
+                                  "fixed tree of 520,458,272 nodes per step; live-sibling work splitting, "
+                                  "breadth-first seeding"),
     "ta056-lb2": dict(instance="ta056", bound="lb2", ub=3679, time_limit=10.0,
                       desc="Taillard ta056 (50x20), LB2, initial UB = best-known 3679, 10 s time-bounded "
                            "exploration per step"),
@@ -311,7 +312,8 @@ def main():
 
     def step(pool):
         before = pool.stats()
-        res = solve_distributed(pool, wl["ub"], device=dev, export_max=args.export_max or None, time_limit_s=tlim)
+        res = solve_distributed(pool, wl["ub"], device=dev, export_max=args.export_max or None, time_limit_s=tlim,
+                                seed_div=int(wl.get("seed_div", 0)))
         after = pool.stats()
         return res, before, after
 
@@ -374,7 +376,7 @@ def main():
             s0 = p2.stats()
             t0 = time.perf_counter()
             p2.load_instance(host_inst)
-            r = solve_distributed(p2, wl["ub"], device=dev, time_limit_s=tlim)
+            r = solve_distributed(p2, wl["ub"], device=dev, time_limit_s=tlim, seed_div=int(wl.get("seed_div", 0)))
             st = p2.stats()
             bv = p2.best_value()
             torch.cuda.synchronize()
@@ -410,6 +412,8 @@ def main():
                            "unique_nodes_per_step": unique, "leaves_per_step": results[-1].leaves,
                            "time_to_proof_ms": statistics.mean(times), "explorers_per_gpu": pool.K(),
                            "work_split": "live siblings" if int(wl.get("split_mode", 0)) == 1 else "factoradic (reference)",
+                           "initial_partition": (f"breadth-first seeding into world*K/{wl['seed_div']} intervals"
+                                                 if wl.get("seed_div") else "world*K equal factoradic ranges, interleaved"),
                            "parallelism": f"dp{world}" if world > 1 else "single",
                            "l2": "256 MiB flush between steps, outside the per-step event brackets",
                            "desc": wl["desc"]},

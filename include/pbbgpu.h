@@ -133,6 +133,13 @@ int pbbgpu_assign_split_range(pbbgpu_pool* pool, int first, int count, int total
 /* pieces first, first+stride, ... (count of them) of [0,n!) cut into `total` ranges: the
  * interleaved multi-GPU partition (rank r of W: first = r, stride = W) */
 int pbbgpu_assign_split_strided(pbbgpu_pool* pool, int first, int stride, int count, int total);
+/* Breadth-first seeding: expand the top of the tree with the batch bounding kernel (prune at
+ * `bound`, the pool's pinned / disable_pruning flags respected) until the live frontier holds
+ * >= total nodes, cut [0,n!) at frontier nodes into <= total intervals (each starting at a
+ * live subtree) and seat intervals first, first+stride, ... (rank r of W: first = r,
+ * stride = W). total <= 0: stride*K. Replaces the equal-range split of pool_run's
+ * assign_fresh (explorer.cpp:473-507); counts are unchanged (any partition is exact). */
+int pbbgpu_seed(pbbgpu_pool* pool, int64_t bound, int first, int stride, int total);
 /* hand the right halves [mid, end) of the `max_count` longest remaining intervals to another
  * pool (inter-GPU stealing); the explorers keep [pos, mid) */
 int pbbgpu_export(pbbgpu_pool* pool, int max_count, uint16_t* a_out, uint16_t* b_out,

@@ -22,7 +22,7 @@ LB2 = 2
 # every symbol include/pbbgpu.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "pbbgpu_last_error", "pbbgpu_device_count", "pbbgpu_taillard", "pbbgpu_taillard_named",
-    "pbbgpu_makespan", "pbbgpu_neh", "pbbgpu_create", "pbbgpu_destroy", "pbbgpu_load_instance", "pbbgpu_K",
+    "pbbgpu_makespan", "pbbgpu_neh", "pbbgpu_create", "pbbgpu_destroy", "pbbgpu_load_instance", "pbbgpu_seed", "pbbgpu_K",
     "pbbgpu_set_initial_bound", "pbbgpu_assign", "pbbgpu_assign_split", "pbbgpu_run_round",
     "pbbgpu_active_count", "pbbgpu_snapshot", "pbbgpu_best", "pbbgpu_offer_bound",
     "pbbgpu_stats", "pbbgpu_histogram", "pbbgpu_decompose_batch", "pbbgpu_solve", "pbbgpu_int32_peak",
@@ -112,6 +112,7 @@ def load() -> ctypes.CDLL:
                                          ctypes.POINTER(Config), ctypes.POINTER(P)]),
         "pbbgpu_destroy": (None, [P]),
         "pbbgpu_load_instance": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_int32)]),
+        "pbbgpu_seed": (ctypes.c_int, [P, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
         "pbbgpu_K": (ctypes.c_int, [P]),
         "pbbgpu_set_initial_bound": (ctypes.c_int, [P, ctypes.c_int64, i32p, ctypes.c_int]),
         "pbbgpu_assign": (ctypes.c_int, [P, u16p, u16p, u8p, ctypes.c_int]),

@@ -1709,6 +1709,185 @@ int pbbgpu_assign(pbbgpu_pool* P, const uint16_t* a, const uint16_t* b, const ui
   });
 }
 
+// ---- breadth-first seeding (planning only)
+// The top of the tree is expanded level by level with the batch bounding kernel (the same
+// decompose as the explorers: rows in ascending job order, MinMin direction, prune at the
+// seeding bound) until the live frontier holds at least `target` nodes. [0, n!) is then cut
+// at frontier nodes into <= target intervals, each starting at a live subtree, instead of
+// n!/target-equal ranges that mostly start inside pruned subtrees and leave the explorers
+// to find the work by stealing (the ramp-up of a short proof). Only the cut points come
+// from the seeding: the explorers decompose everything in their intervals and the unique
+// count rule holds for any partition, so counts are unchanged.
+namespace {
+void batch_bound(pbbgpu_pool* P, const std::vector<int>& perms, const std::vector<int>& d1, const std::vector<int>& d2,
+                 int prune, std::vector<uint8_t>& pruned, std::vector<uint8_t>& dir) {
+  const int n = P->n, count = static_cast<int>(d1.size());
+  const size_t cn = static_cast<size_t>(count) * n;
+  int* dp = scratch<int>(P, 0, cn);
+  int* dd1 = scratch<int>(P, 1, count);
+  int* dd2 = scratch<int>(P, 2, count);
+  int* dlb = scratch<int>(P, 3, cn);
+  int* dlf = scratch<int>(P, 4, cn);
+  int* dlbw = scratch<int>(P, 5, cn);
+  uint8_t* ddir = scratch<uint8_t>(P, 6, count);
+  uint8_t* dpr = scratch<uint8_t>(P, 7, cn);
+  xfer(P, dp, perms.data(), cn * sizeof(int), cudaMemcpyHostToDevice, "copy");
+  xfer(P, dd1, d1.data(), count * sizeof(int), cudaMemcpyHostToDevice, "copy");
+  xfer(P, dd2, d2.data(), count * sizeof(int), cudaMemcpyHostToDevice, "copy");
+  BatchParams B{};
+  B.L = P->L;
+  B.perms = dp;
+  B.d1 = dd1;
+  B.d2 = dd2;
+  B.count = count;
+  B.incumbent = prune;
+  B.p32 = P->d_p32;
+  B.npairs = P->npairs;
+  B.pk = P->d_pk;
+  B.pl = P->d_pl;
+  B.order = P->d_ord;
+  B.lag = P->d_lag;
+  B.packed = P->d_packed;
+  B.invord = P->d_invord;
+  B.child_lb = dlb;
+  B.lb_fwd = dlf;
+  B.lb_bwd = dlbw;
+  B.dir = ddir;
+  B.pruned = dpr;
+  const int NG = P->block / P->G;
+  const int grid = std::min((count + NG - 1) / NG, 148 * 8);
+  P->bfn<<<grid, P->block, P->smem, P->stream>>>(B);
+  ck(cudaGetLastError(), "decompose_batch launch");
+  P->launches += 1;
+  pruned.resize(cn);
+  dir.resize(static_cast<size_t>(count));
+  xfer(P, pruned.data(), dpr, cn, cudaMemcpyDeviceToHost, "copy");
+  xfer(P, dir.data(), ddir, static_cast<size_t>(count), cudaMemcpyDeviceToHost, "copy");
+}
+
+// Sorted cut points (digit vectors, n each, the first cut > 0) of a <= target interval partition.
+std::vector<std::vector<int>> bfs_cuts(pbbgpu_pool* P, int prune, int target) {
+  TraceScope ts("seed: breadth-first cuts");
+  const int n = P->n;
+  target = std::max(target, 1);
+  // frontier nodes: digits (n each, zero padded) and perm = sigma1 ++ free ascending ++ sigma2
+  std::vector<int> dig(static_cast<size_t>(n) * n, 0), perm(static_cast<size_t>(n) * n), d1v(static_cast<size_t>(n), 1),
+      d2v(static_cast<size_t>(n), 0);
+  for (int j = 0; j < n; ++j) {  // the root's children: never bounded, all live, Forward
+    dig[static_cast<size_t>(j) * n] = j;
+    int* pp = &perm[static_cast<size_t>(j) * n];
+    int t = 0;
+    pp[t++] = j;
+    for (int x = 0; x < n; ++x)
+      if (x != j) pp[t++] = x;
+  }
+  auto cuts_of = [&](const std::vector<int>& dg, long long F) {
+    const long long G = std::min<long long>(F, target);
+    std::vector<std::vector<int>> cuts;
+    for (long long g = 1; g < G; ++g) {
+      const size_t idx = static_cast<size_t>(g * F / G);
+      cuts.emplace_back(dg.begin() + static_cast<long>(idx * n), dg.begin() + static_cast<long>((idx + 1) * n));
+    }
+    return cuts;
+  };
+  int depth = 1;
+  constexpr size_t kMaxChildren = size_t(1) << 22;
+  while (static_cast<int>(d1v.size()) < target && n - depth >= 3 &&
+         d1v.size() * static_cast<size_t>(n - depth) <= kMaxChildren) {
+    std::vector<uint8_t> pruned, dir;
+    batch_bound(P, perm, d1v, d2v, prune, pruned, dir);
+    const int cnt = static_cast<int>(d1v.size());
+    // live children per node (prefix offsets), then either the next frontier or, when it
+    // reaches the target, only the digits of the cut nodes
+    std::vector<long long> off(static_cast<size_t>(cnt) + 1, 0);
+    for (int i = 0; i < cnt; ++i) {
+      const int f = n - d1v[static_cast<size_t>(i)] - d2v[static_cast<size_t>(i)];
+      int live = 0;
+      for (int c = 0; c < f; ++c) live += !pruned[static_cast<size_t>(i) * n + c];
+      off[static_cast<size_t>(i) + 1] = off[static_cast<size_t>(i)] + live;
+    }
+    const long long F = off[static_cast<size_t>(cnt)];
+    if (F == 0) break;  // everything below this level is pruned: keep this frontier
+    auto child_digits = [&](long long k, int* out) {  // digits of live child number k
+      const int i = static_cast<int>(std::upper_bound(off.begin(), off.end(), k) - off.begin()) - 1;
+      long long r = k - off[static_cast<size_t>(i)];
+      int c = 0;
+      for (;; ++c)
+        if (!pruned[static_cast<size_t>(i) * n + c] && r-- == 0) break;
+      for (int l = 0; l < n; ++l) out[l] = l == depth ? c : dig[static_cast<size_t>(i) * n + l];
+    };
+    if (F >= target) {
+      const long long G = target;
+      std::vector<std::vector<int>> cuts;
+      for (long long g = 1; g < G; ++g) {
+        std::vector<int> v(static_cast<size_t>(n));
+        child_digits(g * F / G, v.data());
+        cuts.push_back(std::move(v));
+      }
+      return cuts;
+    }
+    std::vector<int> ndig(static_cast<size_t>(F) * n), nperm(static_cast<size_t>(F) * n), nd1(static_cast<size_t>(F)),
+        nd2(static_cast<size_t>(F));
+    long long k = 0;
+    for (int i = 0; i < cnt; ++i) {
+      const int a = d1v[static_cast<size_t>(i)], b = d2v[static_cast<size_t>(i)], f = n - a - b;
+      const int* pp = &perm[static_cast<size_t>(i) * n];
+      const bool fwd = dir[static_cast<size_t>(i)] == kFwd;
+      for (int c = 0; c < f; ++c) {
+        if (pruned[static_cast<size_t>(i) * n + c]) continue;
+        int* dg = &ndig[static_cast<size_t>(k) * n];
+        for (int l = 0; l < n; ++l) dg[l] = l == depth ? c : dig[static_cast<size_t>(i) * n + l];
+        int* np = &nperm[static_cast<size_t>(k) * n];
+        const int j = pp[a + c];
+        int t = 0;
+        for (int x = 0; x < a; ++x) np[t++] = pp[x];
+        if (fwd) np[t++] = j;
+        for (int x = 0; x < f; ++x)
+          if (x != c) np[t++] = pp[a + x];
+        if (!fwd) np[t++] = j;
+        for (int x = n - b; x < n; ++x) np[t++] = pp[x];
+        nd1[static_cast<size_t>(k)] = a + fwd;
+        nd2[static_cast<size_t>(k)] = b + !fwd;
+        ++k;
+      }
+    }
+    dig.swap(ndig);
+    perm.swap(nperm);
+    d1v.swap(nd1);
+    d2v.swap(nd2);
+    ++depth;
+  }
+  return cuts_of(dig, static_cast<long long>(d1v.size()));
+}
+}  // namespace
+
+int pbbgpu_seed(pbbgpu_pool* P, int64_t bound, int first, int stride, int total) {
+  return guarded([&] {
+    if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
+    if (stride < 1 || first < 0 || first >= stride) throw std::invalid_argument("bad seed rank/stride");
+    if (total <= 0) total = stride * P->K;
+    const int n = P->n;
+    int prune = static_cast<int>(std::min<int64_t>(std::max<int64_t>(bound, 1), INT_MAX));
+    if (P->cfg.disable_pruning) prune = INT_MAX;
+    const std::vector<std::vector<int>> cuts = bfs_cuts(P, prune, total);
+    const int I = static_cast<int>(cuts.size()) + 1;  // intervals [0, c1), [c1, c2), ..., [c_last, n!)
+    std::vector<int> a, b, slots;
+    std::vector<uint8_t> nf;
+    for (int i = first; i < I; i += stride) {
+      if (static_cast<int>(slots.size()) >= P->K) throw CapacityError("pbbgpu_seed: more intervals than explorers");
+      for (int l = 0; l < n; ++l) a.push_back(i == 0 ? 0 : cuts[static_cast<size_t>(i - 1)][static_cast<size_t>(l)]);
+      const bool last = i == I - 1;
+      for (int l = 0; l < n; ++l) b.push_back(last ? 0 : cuts[static_cast<size_t>(i)][static_cast<size_t>(l)]);
+      nf.push_back(last ? 1 : 0);
+      slots.push_back(static_cast<int>(slots.size()));
+    }
+    clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
+    ck(cudaGetLastError(), "clear_kernel");
+    P->launches += 1;
+    assign_digits(P, a, b, nf, slots);
+  });
+}
+
 int pbbgpu_assign_split_range(pbbgpu_pool* P, int first, int count, int total) {
   return pbbgpu_assign_split_strided(P, first, 1, count, total);
 }

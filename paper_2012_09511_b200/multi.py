@@ -46,9 +46,13 @@ _DELTA = ("unique", "decomposed", "leaves", "improvements", "local_steals")
 
 
 def solve_distributed(pool, ub: int, group=None, device=None, export_max: Optional[int] = None,
-                      low_fraction: float = 0.5, time_limit_s: float = 0.0) -> DistResult:
+                      low_fraction: float = 0.5, time_limit_s: float = 0.0, seed_div: int = 0) -> DistResult:
     """Run `pool` (a GpuPool, or any object with its surface) to exhaustion cooperatively with
-    the other ranks of `group` (torch.distributed). world_size == 1 degenerates to pool_run."""
+    the other ranks of `group` (torch.distributed). world_size == 1 degenerates to pool_run.
+
+    The initial partition is [0, n!) cut into world*K equal ranges, interleaved over the ranks
+    (seed_div = 0), or breadth-first seeding (pbbgpu_seed) into world*K/seed_div intervals
+    that each start at a live subtree (better on irregular trees such as pinned ta041)."""
     import time
 
     import torch
@@ -63,7 +67,9 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
     pool.set_initial_bound(ub)
     # interleaved partition: rank r seats pieces r, r + W, r + 2W, ... of [0,n!) cut into W*K
     # ranges, so every rank samples the whole (highly irregular) tree from the start
-    if world > 1 and hasattr(pool, "assign_split_strided"):
+    if seed_div > 0 and hasattr(pool, "seed"):  # breadth-first seeding, interleaved over the ranks
+        pool.seed(ub, rank, world, max(world, world * K // seed_div))
+    elif world > 1 and hasattr(pool, "assign_split_strided"):
         pool.assign_split_strided(rank, world, K, world * K)
     else:
         pool.assign_split_range(rank * K, K, world * K)

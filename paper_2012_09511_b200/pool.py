@@ -223,6 +223,11 @@ class GpuPool:
     def assign_split_strided(self, first: int, stride: int, count: int, total: int) -> None:
         _lib.check(self._lib.pbbgpu_assign_split_strided(self._h, first, stride, count, total))
 
+    def seed(self, bound: int, first: int = 0, stride: int = 1, total: int = 0) -> None:
+        """Breadth-first seeding (pbbgpu_seed): [0, n!) cut at live frontier nodes, intervals
+        first, first + stride, ... seated."""
+        _lib.check(self._lib.pbbgpu_seed(self._h, int(min(bound, NO_INCUMBENT)), first, stride, total))
+
     def export_work(self, max_count: int):
         """Right halves of the longest remaining intervals, as digit arrays (a, b, b_is_nfact)."""
         n = self.inst.n

@@ -396,3 +396,18 @@ def test_load_instance_batch_only_pool():
         want = fresh.decompose_batch(perms, d1s, d2s, 1 << 30)
     for x, y in zip(got, want):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("key", ["ta011@1582", "ta041@2991"])
+@pytest.mark.parametrize("div", [1, 16])
+def test_breadth_first_seeding_keeps_counts(key, div):
+    """pbbgpu_seed cuts [0, n!) at live frontier nodes: any partition keeps the exact count."""
+    from paper_2012_09511_b200.multi import solve_distributed
+    ref = golden_io.ref_counts()[key]
+    name, ub = key.split("@")
+    with pbb.GpuPool(pbb.taillard_named(name), bound="lb1") as pool:
+        r = solve_distributed(pool, int(ub), seed_div=div)
+    assert r.completed
+    assert r.unique == ref["decomposed"]
+    assert r.leaves == ref["leaves"]
+    assert _hist_str(r.hist) == ref["hist"]
