@@ -293,7 +293,7 @@ def main():
     n, m = inst.n, inst.m
     W = w_lb2 if wl["bound"] == "lb2" else w_lb1
     world_ = world
-    cfg = pbb.PoolConfig(device=local, round_us=args.round_us, rounds_per_sync=args.rounds_per_sync,
+    cfg = pbb.PoolConfig(device=local, round_us=args.round_us, rounds_per_sync=args.rounds_per_sync or (3 if world > 1 else 0),
                          pinned=bool(wl.get("pinned", False)), max_split=args.max_split,
                          split_mode=int(wl.get("split_mode", 0)))
     tlim = float(wl.get("time_limit", 0.0))

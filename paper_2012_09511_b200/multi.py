@@ -81,6 +81,13 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
     completed = True
     t0 = time.time()
     width = 2 * n + 1
+    # phase-1 buffers, allocated once: pinned host row -> device -> all_gather -> pinned host
+    dev = torch.device(device) if device is not None else torch.device("cpu")
+    pin = dev.type == "cuda"
+    info_h = torch.zeros(3, dtype=torch.int64, pin_memory=pin)
+    info_d = info_h.to(dev)
+    gath_d = torch.zeros(world * 3, dtype=torch.int64, device=dev)
+    gath_h = torch.zeros(world * 3, dtype=torch.int64, pin_memory=pin)
     while True:
         active = pool.run_round()
         rounds += 1
@@ -95,10 +102,13 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
         best = pool.best_value()
         stop = int(bool(time_limit_s) and time.time() - t0 >= time_limit_s)
         # phase 1: who is idle, who is busy, incumbent, time limit
-        info = torch.tensor([active, min(best, (1 << 62)), stop], dtype=torch.int64, device=device)
-        gathered = [torch.zeros_like(info) for _ in range(world)]
-        dist.all_gather(gathered, info, group=group)
-        g = torch.stack(gathered).cpu().numpy()
+        info_h[0], info_h[1], info_h[2] = active, min(best, (1 << 62)), stop
+        info_d.copy_(info_h, non_blocking=pin)
+        dist.all_gather_into_tensor(gath_d, info_d, group=group)
+        gath_h.copy_(gath_d, non_blocking=pin)
+        if pin:
+            torch.cuda.current_stream(dev).synchronize()
+        g = gath_h.numpy().reshape(world, 3)
         actives, bests = g[:, 0], g[:, 1]
         gbest = int(bests.min())
         if gbest < best:
