@@ -222,7 +222,7 @@ struct InstView {
   const uint8_t* pl;
   const uint8_t* ord;
   const uint16_t* lag;
-  const uint32_t* packed;  // [n][npairs]: job | a << 6 | b << 13 | lag << 20
+  const uint32_t* packed;  // [n][npairs]: a | job << 7 | b << 13 | lag << 20
   const uint8_t* invord;   // [n][npairs]: position of job j in pair q's order
   int npairs;
 };
@@ -372,6 +372,11 @@ __device__ __forceinline__ uint32_t add_u16x2(uint32_t a, uint32_t b) {
   asm("add.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
   return d;
 }
+__device__ __forceinline__ int bfind_u32(uint32_t x) {  // index of the highest set bit (FLO)
+  int r;
+  asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
 __device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
   uint32_t d;
   asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
@@ -440,33 +445,41 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
     const int Atot = iv.rm[k], Btot = iv.rm[l];
     const int qk = iv.tl[k], ql = iv.tl[l], rk = iv.fr[k], rl = iv.fr[l];
     const int cAq = Atot + qk, cRB = rl + Btot;
+    // packed entries e = a | job << 7 | b << 13 | lag << 20 in rows of PS words; e & 0x1f80 is
+    // the byte offset of row `job` of the per-lane [job][32] int32 table
+    const unsigned char* pq = reinterpret_cast<const unsigned char*>(in.packed + q);
+    const int strideB = PS * 4;
+    unsigned char* Sb = reinterpret_cast<unsigned char*>(Sl);
     if constexpr (SMALLN) {
-      // the pair's free positions as a bitmask from the static inverse order (f lookups),
-      // then passes over exactly the f set bits: uniform trip count, no predicated slots
-      uint32_t Fq = 0;
-      for (int c = 0; c < f; ++c) Fq |= 1u << in.invord[iv.freej[c] * P + q];
+      // the pair's free positions as a bitmask (bit t = position t in the pair's order) from
+      // the static inverse order (f lookups); both passes walk exactly the f set bits with
+      // bfind: the backward pass on the mask, the forward pass on its bit reversal
+      uint32_t Fr = 0;
+      for (int c = 0; c < f; ++c) Fr |= 1u << in.invord[iv.freej[c] * P + q];
+      const unsigned char* pq31 = pq + 31 * strideB;
       int A = 0, Bp = 0, pm = NEG;
-      for (uint32_t w = Fq; w; w &= w - 1) {
-        const unsigned e = in.packed[(__ffs(w) - 1) * PS + q];
-        const int j = e & 63;
-        A += (e >> 6) & 127;
+      for (uint32_t w = __brev(Fr); w;) {  // ascending positions t = 31 - u
+        const int u = bfind_u32(w);
+        w ^= 1u << u;
+        const unsigned e = *reinterpret_cast<const unsigned*>(pq31 - u * strideB);
+        A += e & 127;
         const int X = A + static_cast<int>(e >> 20) - Bp;
-        Sl[j * 32] = pm;
+        *reinterpret_cast<int*>(Sb + (e & 0x1f80u)) = pm;
         pm = max(pm, X);
         Bp += (e >> 13) & 127;
       }
       int As = 0, Bs = Atot - Btot, sm = NEG;
-      for (uint32_t w = Fq; w;) {
-        const int t = 31 - __clz(w);
+      for (uint32_t w = Fr; w;) {  // descending positions
+        const int t = bfind_u32(w);
         w ^= 1u << t;
-        const unsigned e = in.packed[t * PS + q];
-        const int j = e & 63;
-        const int a = (e >> 6) & 127, b = (e >> 13) & 127;
+        const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
+        int* slot = reinterpret_cast<int*>(Sb + (e & 0x1f80u));
+        const int a = e & 127, b = (e >> 13) & 127;
         Bs += b;
         const int X = static_cast<int>(e >> 20) + Bs - As;
-        const int I1 = max(Sl[j * 32] + a - b, sm) + Btot;
+        const int I1 = max(*slot + a - b, sm) + Btot;
         const int lo = max(cAq, I1 + ql), hi = max(cRB, rk + I1 + b - a);
-        Sl[j * 32] = static_cast<int>(static_cast<uint32_t>(lo) | static_cast<uint32_t>(hi) << 16);
+        *slot = static_cast<int>(static_cast<uint32_t>(lo) | static_cast<uint32_t>(hi) << 16);
         sm = max(sm, X);
         As += a;
       }
@@ -476,11 +489,11 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
       for (int c = 0; c < f; ++c) Fq |= 1ull << in.invord[iv.freej[c] * P + q];
       int A = 0, Bp = 0, pm = NEG;
       for (unsigned long long w = Fq; w; w &= w - 1) {
-        const unsigned e = in.packed[(__ffsll(static_cast<long long>(w)) - 1) * PS + q];
-        const int j = e & 63;
-        A += (e >> 6) & 127;
+        const int t = __ffsll(static_cast<long long>(w)) - 1;
+        const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
+        A += e & 127;
         const int X = A + static_cast<int>(e >> 20) - Bp;
-        Sl[j * 32] = pm;
+        *reinterpret_cast<int*>(Sb + (e & 0x1f80u)) = pm;
         pm = max(pm, X);
         Bp += (e >> 13) & 127;
       }
@@ -488,14 +501,14 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
       for (unsigned long long w = Fq; w;) {
         const int t = 63 - __clzll(static_cast<long long>(w));
         w ^= 1ull << t;
-        const unsigned e = in.packed[t * PS + q];
-        const int j = e & 63;
-        const int a = (e >> 6) & 127, b = (e >> 13) & 127;
+        const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
+        int* slot = reinterpret_cast<int*>(Sb + (e & 0x1f80u));
+        const int a = e & 127, b = (e >> 13) & 127;
         Bs += b;
         const int X = static_cast<int>(e >> 20) + Bs - As;
-        const int I1 = max(Sl[j * 32] + a - b, sm) + Btot;
+        const int I1 = max(*slot + a - b, sm) + Btot;
         const int lo = max(cAq, I1 + ql), hi = max(cRB, rk + I1 + b - a);
-        Sl[j * 32] = static_cast<int>(static_cast<uint32_t>(lo) | static_cast<uint32_t>(hi) << 16);
+        *slot = static_cast<int>(static_cast<uint32_t>(lo) | static_cast<uint32_t>(hi) << 16);
         sm = max(sm, X);
         As += a;
       }

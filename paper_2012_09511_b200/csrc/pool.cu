@@ -274,7 +274,8 @@ void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::v
       }
     }
   }
-  // transposed packed form [t][q] = job | a << 6 | b << 13 | lag << 20 (children_lb2_w)
+  // transposed packed form [t][q] = a | job << 7 | b << 13 | lag << 20 (children_lb2_w; the
+  // job field is pre-shifted to the byte offset of its row in the per-lane [job][32] int32 table)
   const int PS = round_up(P, 32);  // row stride padded to 32 pairs (bank-conflict-free passes)
   packed.assign(static_cast<size_t>(PS) * n, 0);
   packable = n <= 64;
@@ -286,7 +287,7 @@ void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::v
       const int lg = lag[static_cast<size_t>(qq) * n + j];
       if (a > 127 || b > 127 || lg > 2047) packable = false;
       packed[static_cast<size_t>(t) * PS + qq] =
-          static_cast<uint32_t>(j) | static_cast<uint32_t>(a) << 6 | static_cast<uint32_t>(b) << 13 | static_cast<uint32_t>(lg) << 20;
+          static_cast<uint32_t>(a) | static_cast<uint32_t>(j) << 7 | static_cast<uint32_t>(b) << 13 | static_cast<uint32_t>(lg) << 20;
     }
   }
 }
