@@ -1792,7 +1792,8 @@ std::vector<std::vector<int>> bfs_cuts(pbbgpu_pool* P, int prune, int target) {
     return cuts;
   };
   int depth = 1;
-  constexpr size_t kMaxChildren = size_t(1) << 22;
+  // host memory of the next frontier (digits + perm, 8 bytes per job) capped at 64 MB
+  const size_t kMaxChildren = (size_t(64) << 20) / (static_cast<size_t>(n) * 8);
   while (static_cast<int>(d1v.size()) < target && n - depth >= 3 &&
          d1v.size() * static_cast<size_t>(n - depth) <= kMaxChildren) {
     std::vector<uint8_t> pruned, dir;
