@@ -68,9 +68,9 @@ typedef struct {
   double min_steal_log2; /* log2 of the minimal stolen interval length; 0 = log2(8!) */
   int device;            /* CUDA device ordinal */
   int block;             /* threads per CTA (128, 256, 512); 0 = auto */
-  double round_us;       /* device time per round; 0 = auto (2000 us, or steps_per_round if set) */
+  double round_us;       /* device time per round; 0 = auto (2000 us, 2500 us for warp explorers, or steps_per_round if set) */
   double steal_trigger;  /* steal phase when active < trigger*K; 0 = 1.0 (reference pool: 0.8) */
-  int rounds_per_sync;   /* (explore, steal) rounds per pbbgpu_run_round host sync; 0 = 2, max 8 */
+  int rounds_per_sync;   /* (explore, steal) rounds per pbbgpu_run_round host sync; 0 = 3, max 8 */
   int max_split;         /* thieves one victim may feed per steal phase (multi-way split); 0 = 4 */
   int split_mode;        /* 0 = factoradic interval split (the reference's steal_right_half,
                             explorer.cpp:265-280, generalised to r-way); 1 = live-sibling split

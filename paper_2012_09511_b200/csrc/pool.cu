@@ -1206,7 +1206,7 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
     ck(cudaEventCreate(&P->ev1), "event");
     for (cudaEvent_t& e : P->evs) ck(cudaEventCreate(&e), "event");
   }
-  P->rounds_per_sync = P->cfg.rounds_per_sync > 0 ? std::min(P->cfg.rounds_per_sync, 8) : 2;
+  P->rounds_per_sync = P->cfg.rounds_per_sync > 0 ? std::min(P->cfg.rounds_per_sync, 8) : 3;
 
   if (bound == kLB2) P->npairs = m * (m - 1) / 2;
   const HostTables T = build_tables(n, m, bound, p, n > kMaxN);
@@ -1301,7 +1301,8 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   }
   P->grid = (P->K + NGb - 1) / NGb;
   P->steps = P->cfg.steps_per_round > 0 ? P->cfg.steps_per_round : (1 << 30);
-  P->round_us = P->cfg.round_us > 0 ? P->cfg.round_us : (P->cfg.steps_per_round > 0 ? 0.0 : 2000.0);
+  // warp explorers (LB2) take tens of us per step: longer rounds amortize the round-end wait
+  P->round_us = P->cfg.round_us > 0 ? P->cfg.round_us : (P->cfg.steps_per_round > 0 ? 0.0 : (P->G == 32 ? 2500.0 : 2000.0));
 
   // device buffers
   std::vector<float> lgf(static_cast<size_t>(n) + 1, 0.f);

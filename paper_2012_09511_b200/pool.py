@@ -44,7 +44,7 @@ class PoolConfig:
     block: int = 0              # threads per CTA; 0 = auto
     round_us: float = 0.0       # device time per round; 0 = auto
     steal_trigger: float = 0.0  # steal when active < trigger*K; 0 = 1.0 (reference: 0.8)
-    rounds_per_sync: int = 0    # device rounds per run_round() call; 0 = 2
+    rounds_per_sync: int = 0    # device rounds per run_round() call; 0 = 3
     max_split: int = 0          # thieves per victim per steal phase (multi-way split); 0 = 4
     split_mode: int = 0         # 0 = factoradic (reference), 1 = live siblings, 2 = live else factoradic
 
