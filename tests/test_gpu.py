@@ -188,6 +188,11 @@ def test_pinned_mode_matches_oracle(name, ub):
     assert res.stats.unique == ref["unique"]
     assert res.stats.leaves == ref["leaves"]
     assert res.stats.improvements == 0
+    # the bench's pinned configuration: live-sibling splitting + breadth-first seeding
+    from paper_2012_09511_b200.multi import solve_distributed
+    with pbb.GpuPool(inst, pbb.PoolConfig(pinned=True, split_mode=1), bound="lb1") as pool:
+        r = solve_distributed(pool, ub, seed_div=16)
+    assert r.completed and r.unique == ref["unique"] and r.leaves == ref["leaves"] and r.improvements == 0
 
 
 # ---------------------------------------------------------------- pool surface
