@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpbbgpu.so")
 SOURCES = [os.path.join(CSRC, "pool.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("explore.cuh", "pbb_layout.h")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("explore.cuh", "bound_big.cuh", "pbb_layout.h")] + [
     os.path.join(ROOT, "include", "pbbgpu.h")]
 
 NVCC_FLAGS = [

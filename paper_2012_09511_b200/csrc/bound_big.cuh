@@ -234,4 +234,174 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
 
 #endif  // __CUDACC__
 
+// LB1 for large n: one WARP per node, kBig1Warps nodes in flight per CTA, the instance
+// table staged once per CTA.
+//   tables     front over sigma1 / tail over sigma2 as lane-per-machine wavefronts
+//              (bound_tables, src/bound.cpp:20-46); for M <= 16 the front runs in lanes 0-15
+//              and the tail in lanes 16-31 of the same loop. The same loads accumulate the
+//              fixed jobs' machine sums, so remain = ptot - sum(sigma1) - sum(sigma2) costs no
+//              pass over the free jobs.
+//   children   lane per child (children_bounds, src/bound.cpp:61-88), rows as LDS.128,
+//              results stored coalesced; MinMin (src/bound.cpp:109-131) from per-lane
+//              (min, count-at-min, sum) triples reduced with REDUX, so one pass suffices;
+//              the second pass writes child_lb / pruned from the chosen direction.
+constexpr int kBig1Warps = 16;
+
+__host__ __device__ inline int big1_smem_bytes(int n, int mp, int m) {
+  return n * mp * 4 + kBig1Warps * (round_up(n, 8) * 2 + 4 * round_up(m, 4) * 4);
+}
+
+#ifdef __CUDACC__
+
+template <int M>
+__global__ void __launch_bounds__(kBig1Warps * 32, M > 16 ? 1 : 2) decompose_big_lb1_kernel(const BigBatchParams B, const int* ptot) {
+  constexpr int MP = (M + 3) / 4 * 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = B.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* sp = reinterpret_cast<int*>(smem);  // [n][MP]
+  uint16_t* spm = reinterpret_cast<uint16_t*>(sp + n * MP) + warp * round_up(n, 8);  // this warp's perm
+  int* wt = reinterpret_cast<int*>(reinterpret_cast<uint16_t*>(sp + n * MP) + kBig1Warps * round_up(n, 8)) +
+            warp * 4 * MP;
+  int* fr = wt;            // front
+  int* tl = wt + MP;       // tail
+  int* rt = wt + 2 * MP;   // remain + tail
+  int* frm = wt + 3 * MP;  // front + remain
+  for (int i = tid; i < n * MP; i += blockDim.x) sp[i] = B.p32[i];
+  __syncthreads();
+  constexpr bool kDual = M <= 16;
+  const int half = lane >> 4, hk = lane & 15;
+  for (int node = blockIdx.x * kBig1Warps + warp; node < B.count; node += gridDim.x * kBig1Warps) {
+    const int* perm = B.perms + static_cast<size_t>(node) * n;
+    const int d1 = B.d1[node], d2 = B.d2[node], f = n - d1 - d2;
+    for (int i = lane; i < n; i += 32) spm[i] = static_cast<uint16_t>(perm[i]);
+    __syncwarp();
+    int sum = 0;  // fixed jobs' processing times on this lane's machine
+    if (kDual) {
+      // lanes 0..15: front, machine hk over sigma1; lanes 16..31: tail, machine M-1-hk over sigma2
+      const int len = half ? d2 : d1;
+      const int k = half ? M - 1 - hk : hk;
+      const int steps = max(d1, d2) + M - 1;
+      int C = 0;
+      for (int s = 0; s < steps; ++s) {
+        int left = __shfl_up_sync(0xffffffffu, C, 1);
+        if (hk == 0) left = 0;
+        const int i = s - hk;
+        if (hk < M && i >= 0 && i < len) {
+          const int pv = sp[spm[half ? n - 1 - i : i] * MP + k];
+          C = max(C, left) + pv;
+          sum += pv;
+        }
+      }
+      if (hk < M) (half ? tl : fr)[k] = C;
+      // machine k's fixed sum = front lane k + tail lane 16 + (M-1-k)
+      const int tsum = __shfl_sync(0xffffffffu, sum, half ? lane : 16 + ((M - 1 - hk) & 15));
+      if (!half && hk < M) frm[hk] = ptot[hk] - sum - tsum;  // remain, folded below
+    } else {
+      int C = 0;
+      for (int s = 0; s < d1 + M - 1; ++s) {
+        int left = __shfl_up_sync(0xffffffffu, C, 1);
+        if (lane == 0) left = 0;
+        const int i = s - lane;
+        if (lane < M && i >= 0 && i < d1) {
+          const int pv = sp[spm[i] * MP + lane];
+          C = max(C, left) + pv;
+          sum += pv;
+        }
+      }
+      if (lane < M) fr[lane] = C;
+      C = 0;
+      const int k = M - 1 - lane;
+      int tsum = 0;
+      for (int s = 0; s < d2 + M - 1; ++s) {
+        int left = __shfl_up_sync(0xffffffffu, C, 1);
+        if (lane == 0) left = 0;
+        const int i = s - lane;
+        if (lane < M && i >= 0 && i < d2) {
+          const int pv = sp[spm[n - 1 - i] * MP + k];
+          C = max(C, left) + pv;
+          tsum += pv;
+        }
+      }
+      if (lane < M) tl[k] = C;
+      __syncwarp();
+      const int ts = __shfl_sync(0xffffffffu, tsum, (M - 1 - lane) & 31);
+      if (lane < M) frm[lane] = ptot[lane] - sum - ts;  // remain, fixed below
+    }
+    __syncwarp();
+    if (lane < M) {
+      const int r = frm[lane];
+      rt[lane] = r + tl[lane];
+      frm[lane] = fr[lane] + r;
+    }
+    __syncwarp();
+    // children: lane per child; per-lane MinMin triples
+    int lo = INT_MAX, cf = 0, cb = 0, sf = 0, sb = 0;
+    const size_t ob = static_cast<size_t>(node) * n;
+    for (int c = lane; c < f; c += 32) {
+      const int4* pr4 = reinterpret_cast<const int4*>(sp + spm[d1 + c] * MP);
+      const int4* fr4 = reinterpret_cast<const int4*>(fr);
+      const int4* rt4 = reinterpret_cast<const int4*>(rt);
+      const int4* tl4 = reinterpret_cast<const int4*>(tl);
+      const int4* fm4 = reinterpret_cast<const int4*>(frm);
+      int prev = 0, vf = 0;
+#pragma unroll
+      for (int k4 = 0; k4 < MP / 4; ++k4) {
+        const int4 a = fr4[k4], r = rt4[k4], w = pr4[k4];
+        const int av[4] = {a.x, a.y, a.z, a.w}, rv[4] = {r.x, r.y, r.z, r.w}, pv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (k4 * 4 + u < M) {
+            const int t = max(prev, av[u]);
+            vf = max(vf, t + rv[u]);
+            prev = t + pv[u];
+          }
+        }
+      }
+      prev = 0;
+      int vb = 0;
+#pragma unroll
+      for (int k4 = MP / 4 - 1; k4 >= 0; --k4) {
+        const int4 a = tl4[k4], r = fm4[k4], w = pr4[k4];
+        const int av[4] = {a.x, a.y, a.z, a.w}, rv[4] = {r.x, r.y, r.z, r.w}, pv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int u = 3; u >= 0; --u) {
+          if (k4 * 4 + u < M) {
+            const int t = max(prev, av[u]);
+            vb = max(vb, t + rv[u]);
+            prev = t + pv[u];
+          }
+        }
+      }
+      B.lb_fwd[ob + c] = vf;
+      B.lb_bwd[ob + c] = vb;
+      const int v = min(vf, vb);
+      if (v < lo) {
+        lo = v;
+        cf = cb = 0;
+      }
+      cf += vf == lo;
+      cb += vb == lo;
+      sf += vf;
+      sb += vb;
+    }
+    const int glo = __reduce_min_sync(0xffffffffu, lo);
+    cf = __reduce_add_sync(0xffffffffu, lo == glo ? cf : 0);
+    cb = __reduce_add_sync(0xffffffffu, lo == glo ? cb : 0);
+    sf = __reduce_add_sync(0xffffffffu, sf);
+    sb = __reduce_add_sync(0xffffffffu, sb);
+    int d = kFwd;
+    if (cf != cb) d = cf < cb ? kFwd : kBwd;
+    else if (sf != sb) d = sf > sb ? kFwd : kBwd;
+    for (int c = lane; c < f; c += 32) {
+      const int lb = d == kFwd ? B.lb_fwd[ob + c] : B.lb_bwd[ob + c];
+      B.child_lb[ob + c] = lb;
+      B.pruned[ob + c] = lb >= B.incumbent;
+    }
+    if (lane == 0) B.dir[node] = static_cast<uint8_t>(d);
+    __syncwarp();
+  }
+}
+
+#endif  // __CUDACC__
+
 }  // namespace pbbgpu

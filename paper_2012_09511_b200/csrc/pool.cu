@@ -884,6 +884,16 @@ ExploreFn explore_fn(int m, int bound, int G, bool small) {
 }
 
 using BigFn = void (*)(BigBatchParams);
+using Big1Fn = void (*)(BigBatchParams, const int*);
+Big1Fn big1_fn(int m) {
+  switch (m) {
+    case 5: return decompose_big_lb1_kernel<5>;
+    case 10: return decompose_big_lb1_kernel<10>;
+    case 20: return decompose_big_lb1_kernel<20>;
+  }
+  return nullptr;
+}
+
 BigFn big_fn(int m, int bound) {
   if (bound == kLB1) {
     switch (m) {
@@ -955,6 +965,7 @@ struct pbbgpu_pool {
   BatchFn bfn = nullptr;
   bool batch_only = false;  // n > 64: bounding (decompose_batch) only
   void (*big)(BigBatchParams) = nullptr;
+  void (*big1)(BigBatchParams, const int*) = nullptr;  // LB1: warp per node
   uint2* d_packed64 = nullptr;
   int* d_big_scratch = nullptr;
   int big_grid = 0;
@@ -1146,7 +1157,7 @@ void put(pbbgpu_pool* P, D*& dptr, const V& v) {
 void upload_tables(pbbgpu_pool* P, const HostTables& T) {
   Uploader u{P};
   u.put(P->d_p32, T.p32);
-  if (!P->batch_only) u.put(P->d_ptot, T.ptot);
+  u.put(P->d_ptot, T.ptot);
   if (P->bound == kLB2) {
     u.put(P->d_pk, T.pk);
     u.put(P->d_pl, T.pl);
@@ -1216,11 +1227,19 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
     P->mp = round_up(m, 4);
     P->big = big_fn(m, bound);
     upload_tables(P, T);
-    P->big_smem = static_cast<size_t>(big_smem_bytes(n, P->mp, m));
-    ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->big), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(P->big_smem)), "smem attr");
+    const void* kfn = reinterpret_cast<const void*>(P->big);
+    int threads = kBigThreads;
+    if (bound == kLB1) {  // warp per node
+      P->big1 = big1_fn(m);
+      kfn = reinterpret_cast<const void*>(P->big1);
+      threads = kBig1Warps * 32;
+      P->big_smem = static_cast<size_t>(big1_smem_bytes(n, P->mp, m));
+    } else {
+      P->big_smem = static_cast<size_t>(big_smem_bytes(n, P->mp, m));
+    }
+    ck(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->big_smem)), "smem attr");
     int per_sm = 0;
-    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(P->big), kBigThreads, P->big_smem), "occupancy");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, P->big_smem), "occupancy");
     if (per_sm < 1) throw CapacityError("pbbgpu: large-n bounding kernel cannot be resident");
     P->big_grid = per_sm * prop.multiProcessorCount;
     if (bound == kLB2)
@@ -2271,7 +2290,10 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
       G.dir = ddir;
       G.pruned = dpr;
       ck(cudaEventRecord(P->ev0, P->stream), "event");
-      P->big<<<std::min(count, P->big_grid), kBigThreads, P->big_smem, P->stream>>>(G);
+      if (P->big1)
+        P->big1<<<std::min((count + kBig1Warps - 1) / kBig1Warps, P->big_grid), kBig1Warps * 32, P->big_smem, P->stream>>>(G, P->d_ptot);
+      else
+        P->big<<<std::min(count, P->big_grid), kBigThreads, P->big_smem, P->stream>>>(G);
       ck(cudaGetLastError(), "decompose_big launch");
       ck(cudaEventRecord(P->ev1, P->stream), "event");
     }

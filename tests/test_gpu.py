@@ -270,6 +270,35 @@ def test_large_n_decompose_matches_oracle(bound, fs):
         assert [int(x) for x in pr[i, :f]] == cpr
 
 
+@pytest.mark.parametrize("name", ["ta111", "ta091", "ta081", "ta061"])
+def test_large_n_lb1_warp_per_node_batch(name):
+    """The warp-per-node LB1 kernel over a batch that fills many CTAs (ragged f from 1 to n,
+    every warp slot of the last CTA partially used), m = 20 (two wavefront passes) and
+    m = 5 / 10 (front and tail in the two half-warps), against the oracle node by node."""
+    inst = pbb.taillard_named(name)
+    n = inst.n
+    rng = np.random.default_rng(7)
+    cnt = 16 * 148 + 13
+    fs = rng.integers(1, n + 1, cnt)
+    fs[:4] = [1, n, 2, n - 1]
+    perms = rng.random((cnt, n)).argsort(axis=1).astype(np.int32)
+    d1s = np.array([int(rng.integers(0, n - f + 1)) for f in fs])
+    d2s = n - fs - d1s
+    prob = orc.Problem(inst.p, orc.LB1)
+    inc = int(rng.integers(1000, 30000))
+    with pbb.GpuPool(inst, bound="lb1") as pool:
+        lb, dr, pr, lf, lbw = pool.decompose_batch(perms, d1s, d2s, inc)
+    for i in list(range(64)) + list(rng.integers(0, cnt, 400)) + [cnt - 1]:
+        f = int(fs[i])
+        fw, bw = prob.children_bounds(perms[i], int(d1s[i]), int(d2s[i]))
+        d, clb, cpr = prob.decompose(perms[i], int(d1s[i]), int(d2s[i]), inc)
+        assert [int(x) for x in lf[i, :f]] == fw, i
+        assert [int(x) for x in lbw[i, :f]] == bw, i
+        assert int(dr[i]) == d, i
+        assert [int(x) for x in lb[i, :f]] == clb, i
+        assert [int(x) for x in pr[i, :f]] == cpr, i
+
+
 # ---------------------------------------------------------------- heuristic cooperation (§8(f) #1)
 
 def test_promote_and_offer_schedule():

@@ -17,8 +17,8 @@ peak = pbb.int32_peak()
 for bound in ("lb1", "lb2"):
     with pbb.GpuPool(inst, bound=bound) as pool:
         for f in (10, 50, 100, 200, 300, 400, 499):
-            cnt = 4096 if bound == "lb1" else (2048 if f <= 100 else 1024)
-            perms = np.array([rng.permutation(n) for _ in range(cnt)])
+            cnt = 32768 if bound == "lb1" else (2048 if f <= 100 else 1024)
+            perms = rng.random((cnt, n)).argsort(axis=1).astype(np.int32)
             d1 = rng.integers(0, n - f + 1, cnt)
             d2 = n - f - d1
             pool.decompose_batch(perms[:64], d1[:64], d2[:64], 26670)
