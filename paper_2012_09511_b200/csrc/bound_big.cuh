@@ -19,6 +19,7 @@ namespace pbbgpu {
 
 constexpr int kBigMaxN = 512;
 constexpr int kBigThreads = 256;
+constexpr int kPf = 16;  // LB2 pair passes: order entries prefetched per thread
 
 struct BigBatchParams {
   int n, m, mp, npairs;
@@ -40,10 +41,39 @@ struct BigBatchParams {
 };
 
 __host__ __device__ inline int big_smem_bytes(int n, int mp, int m) {
-  return n * mp * 4 + 2 * n * m * 2 + round_up(n, 16) + 2 * n * 4 + 3 * round_up(m, 4) * 4 + 64 * 4;
+  return n * mp * 4 + 2 * n * m * 2 + round_up(n, 16) + 2 * n * 4 + 3 * round_up(m, 4) * 4 + 64 * 4 + round_up(n, 8) * 2;
 }
 
 #ifdef __CUDACC__
+
+// One lane of a max-plus wavefront over `len` jobs of the warp's staged perm (forward from
+// position 0, or backward from n-1 when rev): at step s the lane at wave position wp handles
+// job s - wp on machine k. The loads are independent of the chain, so they run two steps
+// ahead (indices clamped into range; out-of-range steps leave C unchanged and add 0).
+// MP = 0: row stride passed at run time.
+template <int MP>
+__device__ __forceinline__ void big_wave(const int* sp, const uint16_t* spm, int n, int len, bool rev, int k,
+                                         int wp, bool act, int steps, int& C, int& sum, int mp = MP) {
+  const int hi = max(len - 1, 0);
+  auto at = [&](int s) {
+    const int i = min(max(s - wp, 0), hi);
+    return static_cast<int>(spm[rev ? n - 1 - i : i]);
+  };
+  int jn = at(1);
+  int pn = sp[at(0) * mp + k];
+  for (int s = 0; s < steps; ++s) {
+    const int pv = pn;
+    pn = sp[jn * mp + k];
+    jn = at(s + 2);
+    int left = __shfl_up_sync(0xffffffffu, C, 1);
+    if (wp == 0) left = 0;
+    const int i = s - wp;
+    if (act && i >= 0 && i < len) {
+      C = max(C, left) + pv;
+      sum += pv;
+    }
+  }
+}
 
 template <int M, int BOUND>
 __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBatchParams B) {
@@ -59,6 +89,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
   int* tl = fr + round_up(M, 4);
   int* rm = tl + round_up(M, 4);
   int* red = rm + round_up(M, 4);  // 8 x 4 reduction scratch
+  uint16_t* spm = reinterpret_cast<uint16_t*>(red + 64);  // the node's perm
   for (int i = tid; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
   __syncthreads();
   for (int node = blockIdx.x; node < B.count; node += gridDim.x) {
@@ -72,23 +103,14 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
     if (tid < M) rm[tid] = 0;
     __syncthreads();
     for (int c = tid; c < f; c += blockDim.x) isfree[perm[d1 + c]] = 1;
-    if (warp == 0) {  // front: wavefront over (job, machine)
-      int C = 0;
-      for (int s = 0; s < d1 + M - 1; ++s) {
-        const int left = __shfl_up_sync(0xffffffffu, C, 1);
-        const int i = s - lane;
-        if (lane < M && i >= 0 && i < d1) C = max(C, lane ? left : 0) + sp[perm[i] * mp + lane];
-      }
-      if (lane < M) fr[lane] = C;
-    } else if (warp == 1) {  // tail: same on the reversed schedule / machine order
-      int C = 0;
-      const int k = M - 1 - lane;
-      for (int s = 0; s < d2 + M - 1; ++s) {
-        const int left = __shfl_up_sync(0xffffffffu, C, 1);
-        const int i = s - lane;
-        if (lane < M && i >= 0 && i < d2) C = max(C, lane ? left : 0) + sp[perm[n - 1 - i] * mp + k];
-      }
-      if (lane < M) tl[k] = C;
+    for (int i = tid; i < n; i += blockDim.x) spm[i] = static_cast<uint16_t>(perm[i]);
+    __syncthreads();
+    if (warp < 2) {  // front (warp 0) / tail (warp 1): wavefronts over (job, machine)
+      int C = 0, unused = 0;
+      const int k = warp ? M - 1 - lane : lane;
+      if (warp == 0) big_wave<0>(sp, spm, n, d1, false, lane < M ? k : 0, lane, lane < M, d1 + M - 1, C, unused, mp);
+      else big_wave<0>(sp, spm, n, d2, true, lane < M ? k : 0, lane, lane < M, d2 + M - 1, C, unused, mp);
+      if (lane < M) (warp ? tl : fr)[k] = C;
     }
     {  // remain: per-warp partial sums over the free jobs, lane = machine
       int acc = 0;
@@ -145,26 +167,45 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
         const int Atot = rm[k], Btot = rm[l];
         const int qk = tl[k], ql = tl[l], rk = fr[k], rl = fr[l];
         int A = 0, Bp = 0, pm = NEG;
-        for (int t = 0; t < n; ++t) {
-          const uint2 e = B.packed[static_cast<size_t>(t) * B.npairs + q];
-          const int j = e.x & 0xffff;
-          if (isfree[j]) {
-            A += e.x >> 16;
-            const int X = A + static_cast<int>(e.y >> 16) - Bp;
-            PM[j * kBigThreads] = pm;
-            pm = max(pm, X);
-            Bp += e.y & 0xffff;
+        // the pair's Johnson order streams from L2: kPf entries in flight per thread
+        const uint2* col = B.packed + q;
+        for (int t0 = 0; t0 < n; t0 += kPf) {
+          uint2 ev[kPf];
+#pragma unroll
+          for (int u = 0; u < kPf; ++u) ev[u] = t0 + u < n ? col[static_cast<size_t>(t0 + u) * B.npairs] : make_uint2(0, 0);
+#pragma unroll
+          for (int u = 0; u < kPf; ++u) {
+            const uint2 e = ev[u];
+            const int j = e.x & 0xffff;
+            if (t0 + u < n && isfree[j]) {
+              A += e.x >> 16;
+              const int X = A + static_cast<int>(e.y >> 16) - Bp;
+              PM[j * kBigThreads] = pm;
+              pm = max(pm, X);
+              Bp += e.y & 0xffff;
+            }
           }
         }
         int As = 0, Bs = Atot - Btot, sm = NEG;
-        for (int t = n - 1; t >= 0; --t) {
-          const uint2 e = B.packed[static_cast<size_t>(t) * B.npairs + q];
+        for (int t0 = n - 1; t0 >= 0; t0 -= kPf) {
+          uint2 ev[kPf];
+#pragma unroll
+          for (int u = 0; u < kPf; ++u) ev[u] = t0 - u >= 0 ? col[static_cast<size_t>(t0 - u) * B.npairs] : make_uint2(0, 0);
+          int pmv[kPf];  // the forward pass's PM_j of this batch's free jobs, all loads in flight
+#pragma unroll
+          for (int u = 0; u < kPf; ++u) {
+            const int j = ev[u].x & 0xffff;
+            pmv[u] = t0 - u >= 0 && isfree[j] ? PM[j * kBigThreads] : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < kPf; ++u) {
+          const uint2 e = ev[u];
           const int j = e.x & 0xffff;
-          if (isfree[j]) {
+          if (t0 - u >= 0 && isfree[j]) {
             const int a = e.x >> 16, b = e.y & 0xffff;
             Bs += b;
             const int X = static_cast<int>(e.y >> 16) + Bs - As;
-            const int inner = max(PM[j * kBigThreads] - b, sm - a) + Btot;
+            const int inner = max(pmv[u] - b, sm - a) + Btot;
             const int hk = heads[j * M + k], hl = heads[j * M + l];
             const int vF = max(hk + Atot - a + qk, max(hl + Btot - b, hk + inner) + ql);
             const int vB = max(rk + Atot - a + tails[j * M + k], max(rl + Btot - b, rk + inner) + tails[j * M + l]);
@@ -172,6 +213,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
             atomicMax(&accb[j], vB);
             sm = max(sm, X);
             As += a;
+          }
           }
         }
       }
@@ -282,46 +324,19 @@ __global__ void __launch_bounds__(kBig1Warps * 32, M > 16 ? 1 : 2) decompose_big
       const int k = half ? M - 1 - hk : hk;
       const int steps = max(d1, d2) + M - 1;
       int C = 0;
-      for (int s = 0; s < steps; ++s) {
-        int left = __shfl_up_sync(0xffffffffu, C, 1);
-        if (hk == 0) left = 0;
-        const int i = s - hk;
-        if (hk < M && i >= 0 && i < len) {
-          const int pv = sp[spm[half ? n - 1 - i : i] * MP + k];
-          C = max(C, left) + pv;
-          sum += pv;
-        }
-      }
+      big_wave<MP>(sp, spm, n, len, half, k, hk, hk < M, steps, C, sum);
       if (hk < M) (half ? tl : fr)[k] = C;
       // machine k's fixed sum = front lane k + tail lane 16 + (M-1-k)
       const int tsum = __shfl_sync(0xffffffffu, sum, half ? lane : 16 + ((M - 1 - hk) & 15));
       if (!half && hk < M) frm[hk] = ptot[hk] - sum - tsum;  // remain, folded below
     } else {
       int C = 0;
-      for (int s = 0; s < d1 + M - 1; ++s) {
-        int left = __shfl_up_sync(0xffffffffu, C, 1);
-        if (lane == 0) left = 0;
-        const int i = s - lane;
-        if (lane < M && i >= 0 && i < d1) {
-          const int pv = sp[spm[i] * MP + lane];
-          C = max(C, left) + pv;
-          sum += pv;
-        }
-      }
+      big_wave<MP>(sp, spm, n, d1, false, lane < M ? lane : 0, lane, lane < M, d1 + M - 1, C, sum);
       if (lane < M) fr[lane] = C;
       C = 0;
       const int k = M - 1 - lane;
       int tsum = 0;
-      for (int s = 0; s < d2 + M - 1; ++s) {
-        int left = __shfl_up_sync(0xffffffffu, C, 1);
-        if (lane == 0) left = 0;
-        const int i = s - lane;
-        if (lane < M && i >= 0 && i < d2) {
-          const int pv = sp[spm[n - 1 - i] * MP + k];
-          C = max(C, left) + pv;
-          tsum += pv;
-        }
-      }
+      big_wave<MP>(sp, spm, n, d2, true, lane < M ? k : 0, lane, lane < M, d2 + M - 1, C, tsum);
       if (lane < M) tl[k] = C;
       __syncwarp();
       const int ts = __shfl_sync(0xffffffffu, tsum, (M - 1 - lane) & 31);

@@ -14,9 +14,9 @@ inst = pbb.taillard_named(name)
 n, m = inst.n, inst.m
 rng = np.random.default_rng(1)
 peak = pbb.int32_peak()
-for bound in ("lb1", "lb2"):
+for bound in (sys.argv[2].split(",") if len(sys.argv) > 2 else ("lb1", "lb2")):
     with pbb.GpuPool(inst, bound=bound) as pool:
-        for f in (10, 50, 100, 200, 300, 400, 499):
+        for f in ((10, 50, 100, 200, 300, 400, 499) if n >= 500 else (10, 50, n - 1)):
             cnt = 32768 if bound == "lb1" else (2048 if f <= 100 else 1024)
             perms = rng.random((cnt, n)).argsort(axis=1).astype(np.int32)
             d1 = rng.integers(0, n - f + 1, cnt)
