@@ -295,65 +295,19 @@ __host__ __device__ inline int big1_smem_bytes(int n, int mp, int m) {
 
 #ifdef __CUDACC__
 
-template <int M>
-__global__ void __launch_bounds__(kBig1Warps * 32, M > 16 ? 1 : 2) decompose_big_lb1_kernel(const BigBatchParams B, const int* ptot) {
-  constexpr int MP = (M + 3) / 4 * 4;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int n = B.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int* sp = reinterpret_cast<int*>(smem);  // [n][MP]
-  uint16_t* spm = reinterpret_cast<uint16_t*>(sp + n * MP) + warp * round_up(n, 8);  // this warp's perm
-  int* wt = reinterpret_cast<int*>(reinterpret_cast<uint16_t*>(sp + n * MP) + kBig1Warps * round_up(n, 8)) +
-            warp * 4 * MP;
-  int* fr = wt;            // front
-  int* tl = wt + MP;       // tail
-  int* rt = wt + 2 * MP;   // remain + tail
-  int* frm = wt + 3 * MP;  // front + remain
-  for (int i = tid; i < n * MP; i += blockDim.x) sp[i] = B.p32[i];
-  __syncthreads();
-  constexpr bool kDual = M <= 16;
-  const int half = lane >> 4, hk = lane & 15;
-  for (int node = blockIdx.x * kBig1Warps + warp; node < B.count; node += gridDim.x * kBig1Warps) {
-    const int* perm = B.perms + static_cast<size_t>(node) * n;
-    const int d1 = B.d1[node], d2 = B.d2[node], f = n - d1 - d2;
-    for (int i = lane; i < n; i += 32) spm[i] = static_cast<uint16_t>(perm[i]);
-    __syncwarp();
-    int sum = 0;  // fixed jobs' processing times on this lane's machine
-    if (kDual) {
-      // lanes 0..15: front, machine hk over sigma1; lanes 16..31: tail, machine M-1-hk over sigma2
-      const int len = half ? d2 : d1;
-      const int k = half ? M - 1 - hk : hk;
-      const int steps = max(d1, d2) + M - 1;
-      int C = 0;
-      big_wave<MP>(sp, spm, n, len, half, k, hk, hk < M, steps, C, sum);
-      if (hk < M) (half ? tl : fr)[k] = C;
-      // machine k's fixed sum = front lane k + tail lane 16 + (M-1-k)
-      const int tsum = __shfl_sync(0xffffffffu, sum, half ? lane : 16 + ((M - 1 - hk) & 15));
-      if (!half && hk < M) frm[hk] = ptot[hk] - sum - tsum;  // remain, folded below
-    } else {
-      int C = 0;
-      big_wave<MP>(sp, spm, n, d1, false, lane < M ? lane : 0, lane, lane < M, d1 + M - 1, C, sum);
-      if (lane < M) fr[lane] = C;
-      C = 0;
-      const int k = M - 1 - lane;
-      int tsum = 0;
-      big_wave<MP>(sp, spm, n, d2, true, lane < M ? k : 0, lane, lane < M, d2 + M - 1, C, tsum);
-      if (lane < M) tl[k] = C;
-      __syncwarp();
-      const int ts = __shfl_sync(0xffffffffu, tsum, (M - 1 - lane) & 31);
-      if (lane < M) frm[lane] = ptot[lane] - sum - ts;  // remain, fixed below
-    }
-    __syncwarp();
-    if (lane < M) {
-      const int r = frm[lane];
-      rt[lane] = r + tl[lane];
-      frm[lane] = fr[lane] + r;
-    }
-    __syncwarp();
+// Children of one node, lane per child (children_bounds, src/bound.cpp:61-88), and MinMin
+// (src/bound.cpp:109-131) from per-lane (min, count-at-min, sum) triples; fr/tl/rt/frm are the
+// node's warp-uniform tables in shared memory, jobs[d1 + c] its free jobs in decode order.
+template <int M, int MP, typename JobT>
+__device__ __forceinline__ void big1_children(const BigBatchParams& B, const int* sp, const JobT* jobs, int d1, int f,
+                                              int node, const int* fr, const int* tl, const int* rt, const int* frm,
+                                              int lane) {
+    const int n = B.n;
     // children: lane per child; per-lane MinMin triples
     int lo = INT_MAX, cf = 0, cb = 0, sf = 0, sb = 0;
     const size_t ob = static_cast<size_t>(node) * n;
     for (int c = lane; c < f; c += 32) {
-      const int4* pr4 = reinterpret_cast<const int4*>(sp + spm[d1 + c] * MP);
+      const int4* pr4 = reinterpret_cast<const int4*>(sp + jobs[d1 + c] * MP);
       const int4* fr4 = reinterpret_cast<const int4*>(fr);
       const int4* rt4 = reinterpret_cast<const int4*>(rt);
       const int4* tl4 = reinterpret_cast<const int4*>(tl);
@@ -413,6 +367,161 @@ __global__ void __launch_bounds__(kBig1Warps * 32, M > 16 ? 1 : 2) decompose_big
       B.pruned[ob + c] = lb >= B.incumbent;
     }
     if (lane == 0) B.dir[node] = static_cast<uint8_t>(d);
+}
+
+template <int M>
+__global__ void __launch_bounds__(kBig1Warps * 32, M > 16 ? 1 : 2) decompose_big_lb1_kernel(const BigBatchParams B, const int* ptot) {
+  constexpr int MP = (M + 3) / 4 * 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = B.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* sp = reinterpret_cast<int*>(smem);  // [n][MP]
+  uint16_t* spm = reinterpret_cast<uint16_t*>(sp + n * MP) + warp * round_up(n, 8);  // this warp's perm
+  int* wt = reinterpret_cast<int*>(reinterpret_cast<uint16_t*>(sp + n * MP) + kBig1Warps * round_up(n, 8)) +
+            warp * 4 * MP;
+  int* fr = wt;            // front
+  int* tl = wt + MP;       // tail
+  int* rt = wt + 2 * MP;   // remain + tail
+  int* frm = wt + 3 * MP;  // front + remain
+  for (int i = tid; i < n * MP; i += blockDim.x) sp[i] = B.p32[i];
+  __syncthreads();
+  constexpr bool kDual = M <= 16;
+  const int half = lane >> 4, hk = lane & 15;
+  for (int node = blockIdx.x * kBig1Warps + warp; node < B.count; node += gridDim.x * kBig1Warps) {
+    const int* perm = B.perms + static_cast<size_t>(node) * n;
+    const int d1 = B.d1[node], d2 = B.d2[node], f = n - d1 - d2;
+    for (int i = lane; i < n; i += 32) spm[i] = static_cast<uint16_t>(perm[i]);
+    __syncwarp();
+    int sum = 0;  // fixed jobs' processing times on this lane's machine
+    if (kDual) {
+      // lanes 0..15: front, machine hk over sigma1; lanes 16..31: tail, machine M-1-hk over sigma2
+      const int len = half ? d2 : d1;
+      const int k = half ? M - 1 - hk : hk;
+      const int steps = max(d1, d2) + M - 1;
+      int C = 0;
+      big_wave<MP>(sp, spm, n, len, half, k, hk, hk < M, steps, C, sum);
+      if (hk < M) (half ? tl : fr)[k] = C;
+      // machine k's fixed sum = front lane k + tail lane 16 + (M-1-k)
+      const int tsum = __shfl_sync(0xffffffffu, sum, half ? lane : 16 + ((M - 1 - hk) & 15));
+      if (!half && hk < M) frm[hk] = ptot[hk] - sum - tsum;  // remain, folded below
+    } else {
+      int C = 0;
+      big_wave<MP>(sp, spm, n, d1, false, lane < M ? lane : 0, lane, lane < M, d1 + M - 1, C, sum);
+      if (lane < M) fr[lane] = C;
+      C = 0;
+      const int k = M - 1 - lane;
+      int tsum = 0;
+      big_wave<MP>(sp, spm, n, d2, true, lane < M ? k : 0, lane, lane < M, d2 + M - 1, C, tsum);
+      if (lane < M) tl[k] = C;
+      __syncwarp();
+      const int ts = __shfl_sync(0xffffffffu, tsum, (M - 1 - lane) & 31);
+      if (lane < M) frm[lane] = ptot[lane] - sum - ts;  // remain, fixed below
+    }
+    __syncwarp();
+    if (lane < M) {
+      const int r = frm[lane];
+      rt[lane] = r + tl[lane];
+      frm[lane] = fr[lane] + r;
+    }
+    __syncwarp();
+    big1_children<M, MP>(B, sp, spm, d1, f, node, fr, tl, rt, frm, lane);
+    __syncwarp();
+  }
+}
+
+
+// LB1 for large n, node tables lane-per-node: a warp takes 32 nodes at a time; each lane runs
+// its node's front over sigma1 and then its tail over reversed sigma2 as one sequence of
+// d1 + d2 fixed jobs (bound_tables, src/bound.cpp:20-46) -- the tail reads machine-reversed
+// rows, so both halves are the same register recurrence C[k] = max(C[k], C[k-1]) + p[k]
+// (20 VIADDMNMX-class ops per job and lane, rows as LDS.128, no shuffles). The 32 nodes'
+// tables go through shared memory to the lane-per-child children pass (big1_children).
+constexpr int kBig1gWarps = 8;
+
+__host__ __device__ inline int big1g_smem_bytes(int n, int mp) {
+  return 2 * n * mp * 4 + kBig1gWarps * 32 * 4 * mp * 4;
+}
+
+template <int M>
+__global__ void __launch_bounds__(kBig1gWarps * 32, 1) decompose_big_lb1g_kernel(const BigBatchParams B, const int* ptot) {
+  constexpr int MP = (M + 3) / 4 * 4;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = B.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* sp = reinterpret_cast<int*>(smem);  // [n][MP] rows
+  int* sr = sp + n * MP;                   // [n][MP] machine-reversed rows
+  int* stage = sr + n * MP + warp * 32 * 4 * MP;  // [32 nodes][fr | tl | rt | frm][MP]
+  for (int i = tid; i < n * MP; i += blockDim.x) {
+    const int j = i / MP, k = i - j * MP;
+    sp[i] = B.p32[i];
+    sr[i] = k < M ? B.p32[j * MP + M - 1 - k] : 0;
+  }
+  __syncthreads();
+  const int groups = (B.count + 31) / 32;
+  for (int g = blockIdx.x * kBig1gWarps + warp; g < groups; g += gridDim.x * kBig1gWarps) {
+    const int node = g * 32 + lane;
+    const bool live = node < B.count;
+    const int d1 = live ? B.d1[node] : 0, d2 = live ? B.d2[node] : 0;
+    const int len = d1 + d2;
+    const int steps = __reduce_max_sync(0xffffffffu, len);
+    const int* perm = B.perms + static_cast<size_t>(live ? node : 0) * n;
+    int C[M], S[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) C[k] = S[k] = 0;
+    int* st = stage + lane * 4 * MP;
+    auto flip = [&]() {  // end of sigma1: save the front, restart for the tail, reverse the sums
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        st[k] = C[k];
+        C[k] = 0;
+      }
+#pragma unroll
+      for (int k = 0; k < M / 2; ++k) {
+        const int t = S[k];
+        S[k] = S[M - 1 - k];
+        S[M - 1 - k] = t;
+      }
+    };
+    for (int t = 0; t < steps; ++t) {
+      if (t == d1 && t < len) flip();
+      if (t < len) {
+        const bool tail = t >= d1;
+        const int j = perm[tail ? n - 1 - (t - d1) : t];
+        const int4* r4 = reinterpret_cast<const int4*>((tail ? sr : sp) + j * MP);
+        int prev = 0;
+#pragma unroll
+        for (int k4 = 0; k4 < MP / 4; ++k4) {
+          const int4 w = r4[k4];
+          const int pv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (k4 * 4 + u < M) {
+              prev = max(C[k4 * 4 + u], prev) + pv[u];
+              C[k4 * 4 + u] = prev;
+              S[k4 * 4 + u] += pv[u];
+            }
+          }
+        }
+      }
+    }
+    if (len == d1) flip();  // no tail jobs (also covers len == 0)
+    // C = tail in reversed machine order, S = fixed sums in reversed order
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      const int tlk = C[M - 1 - k];
+      const int rem = ptot[k] - S[M - 1 - k];
+      const int frk = st[k];
+      st[MP + k] = tlk;
+      st[2 * MP + k] = rem + tlk;
+      st[3 * MP + k] = frk + rem;
+    }
+    __syncwarp();
+    const int last = min(32, B.count - g * 32);
+    for (int q = 0; q < last; ++q) {
+      const int nd = g * 32 + q;
+      const int* sq = stage + q * 4 * MP;
+      const int qd1 = __shfl_sync(0xffffffffu, d1, q), qd2 = __shfl_sync(0xffffffffu, d2, q);
+      big1_children<M, MP>(B, sp, B.perms + static_cast<size_t>(nd) * n, qd1, n - qd1 - qd2, nd, sq, sq + MP,
+                           sq + 2 * MP, sq + 3 * MP, lane);
+    }
     __syncwarp();
   }
 }

@@ -894,6 +894,15 @@ Big1Fn big1_fn(int m) {
   return nullptr;
 }
 
+Big1Fn big1g_fn(int m) {
+  switch (m) {
+    case 5: return decompose_big_lb1g_kernel<5>;
+    case 10: return decompose_big_lb1g_kernel<10>;
+    case 20: return decompose_big_lb1g_kernel<20>;
+  }
+  return nullptr;
+}
+
 BigFn big_fn(int m, int bound) {
   if (bound == kLB1) {
     switch (m) {
@@ -965,7 +974,10 @@ struct pbbgpu_pool {
   BatchFn bfn = nullptr;
   bool batch_only = false;  // n > 64: bounding (decompose_batch) only
   void (*big)(BigBatchParams) = nullptr;
-  void (*big1)(BigBatchParams, const int*) = nullptr;  // LB1: warp per node
+  void (*big1)(BigBatchParams, const int*) = nullptr;   // LB1: warp per node (children-heavy batches)
+  void (*big1g)(BigBatchParams, const int*) = nullptr;  // LB1: lane-per-node tables (table-heavy batches)
+  int big1g_grid = 0;
+  size_t big1g_smem = 0;
   uint2* d_packed64 = nullptr;
   int* d_big_scratch = nullptr;
   int big_grid = 0;
@@ -1234,6 +1246,14 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
       kfn = reinterpret_cast<const void*>(P->big1);
       threads = kBig1Warps * 32;
       P->big_smem = static_cast<size_t>(big1_smem_bytes(n, P->mp, m));
+      P->big1g = big1g_fn(m);
+      P->big1g_smem = static_cast<size_t>(big1g_smem_bytes(n, P->mp));
+      const void* gfn = reinterpret_cast<const void*>(P->big1g);
+      ck(cudaFuncSetAttribute(gfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->big1g_smem)), "smem attr");
+      int per_sm_g = 0;
+      ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_g, gfn, kBig1gWarps * 32, P->big1g_smem), "occupancy");
+      if (per_sm_g < 1) throw CapacityError("pbbgpu: large-n bounding kernel cannot be resident");
+      P->big1g_grid = per_sm_g * prop.multiProcessorCount;
     } else {
       P->big_smem = static_cast<size_t>(big_smem_bytes(n, P->mp, m));
     }
@@ -2290,8 +2310,16 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
       G.dir = ddir;
       G.pruned = dpr;
       ck(cudaEventRecord(P->ev0, P->stream), "event");
-      if (P->big1)
-        P->big1<<<std::min((count + kBig1Warps - 1) / kBig1Warps, P->big_grid), kBig1Warps * 32, P->big_smem, P->stream>>>(G, P->d_ptot);
+      // LB1: the node tables cost ~(d1 + d2) steps, the children ~f; lane-per-node tables win
+      // when the fixed part dominates (measured crossover on ta111 near f = n/2)
+      long long fsum = 0;
+      for (int i = 0; i < count; ++i) fsum += n - d1[i] - d2[i];
+      if (P->big1 && fsum * 2 < static_cast<long long>(count) * n)
+        P->big1g<<<std::min((count + 32 * kBig1gWarps - 1) / (32 * kBig1gWarps), P->big1g_grid), kBig1gWarps * 32,
+                    P->big1g_smem, P->stream>>>(G, P->d_ptot);
+      else if (P->big1)
+        P->big1<<<std::min((count + kBig1Warps - 1) / kBig1Warps, P->big_grid), kBig1Warps * 32, P->big_smem, P->stream>>>(
+            G, P->d_ptot);
       else
         P->big<<<std::min(count, P->big_grid), kBigThreads, P->big_smem, P->stream>>>(G);
       ck(cudaGetLastError(), "decompose_big launch");

@@ -271,18 +271,22 @@ def test_large_n_decompose_matches_oracle(bound, fs):
 
 
 @pytest.mark.parametrize("name", ["ta111", "ta091", "ta081", "ta061"])
-def test_large_n_lb1_warp_per_node_batch(name):
-    """The warp-per-node LB1 kernel over a batch that fills many CTAs (ragged f from 1 to n,
-    every warp slot of the last CTA partially used), m = 20 (two wavefront passes) and
-    m = 5 / 10 (front and tail in the two half-warps), against the oracle node by node."""
+@pytest.mark.parametrize("fdist", ["deep", "shallow"])
+def test_large_n_lb1_batch_kernels(name, fdist):
+    """Both large-n LB1 kernels over batches that fill many CTAs (ragged f, partial last
+    group): "deep" batches (mean f < n/2) run the lane-per-node table kernel, "shallow" ones
+    the warp-per-node kernel; m = 20 (two wavefront passes) and m = 5 / 10 (front and tail in
+    the two half-warps); d2 = 0 and d1 = 0 nodes included. Node by node against the oracle."""
     inst = pbb.taillard_named(name)
     n = inst.n
     rng = np.random.default_rng(7)
     cnt = 16 * 148 + 13
-    fs = rng.integers(1, n + 1, cnt)
+    fs = rng.integers(1, n // 3, cnt) if fdist == "deep" else rng.integers(2 * n // 3, n + 1, cnt)
     fs[:4] = [1, n, 2, n - 1]
     perms = rng.random((cnt, n)).argsort(axis=1).astype(np.int32)
     d1s = np.array([int(rng.integers(0, n - f + 1)) for f in fs])
+    d1s[4:40:3] = 0
+    d1s[5:40:3] = n - fs[5:40:3]  # d2 = 0
     d2s = n - fs - d1s
     prob = orc.Problem(inst.p, orc.LB1)
     inc = int(rng.integers(1000, 30000))
