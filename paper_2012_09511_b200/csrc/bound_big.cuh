@@ -1,16 +1,19 @@
 // Batched decompose for large instances (64 < n <= 512, e.g. ta111 500x20): the
-// bounding-throughput path of BASELINE config 5. One 256-thread CTA per node.
+// bounding-throughput path of BASELINE config 5.
 //
-//   node tables   front over sigma1 and tail over sigma2 as a warp wavefront (lane = machine,
-//                 step s processes job s - lane, left neighbour via __shfl_up_sync), remain
-//                 as per-warp partial sums (bound_tables, src/bound.cpp:20-46)
-//   LB1           threads over children, 4 integer ops per machine and direction
-//                 (children_bounds, src/bound.cpp:61-88)
-//   LB2           thread per machine pair (P = 190 for m = 20, one pass): forward pass over
-//                 the pair's Johnson order writes PM_j, the backward pass carries SM and
-//                 evaluates every child in O(1) (max-plus prefix/suffix form, explore.cuh);
-//                 per-child maxima over pairs by shared-memory atomicMax
-//   MinMin/prune  block reductions (src/bound.cpp:109-138)
+//   LB1  two kernels, chosen per batch by the host (mean f vs n/2):
+//        decompose_big_lb1g_kernel  lane-per-node node tables (one register recurrence over
+//                                   sigma1 then reversed sigma2), lane-per-child children
+//        decompose_big_lb1_kernel   warp per node: lane-per-machine wavefront tables,
+//                                   lane-per-child children
+//        (bound_tables / children_bounds / decompose, src/bound.cpp:20-139)
+//   LB2  decompose_big_kernel, one 256-thread CTA per node: wavefront node tables, child
+//        heads/tails, then a thread per machine pair (P = 190 for m = 20) walks only the
+//        free positions of its Johnson order (per-pair bitmask built from the inverse-order
+//        table, f set bits): the forward pass stores PM_j, the backward pass carries SM and
+//        evaluates every child in O(1) (max-plus prefix/suffix form, explore.cuh); the
+//        order entries stream from L2 16 per thread in flight; per-child maxima over pairs
+//        by shared-memory atomicMax; block MinMin (src/bound.cpp:109-138)
 #pragma once
 
 #include "explore.cuh"
@@ -32,6 +35,7 @@ struct BigBatchParams {
   const uint8_t* pk;
   const uint8_t* pl;
   const uint2* packed;   // [n][npairs]: x = job | a << 16, y = b | lag << 16
+  const uint16_t* inv16; // [n][npairs]: position of job j in pair q's Johnson order
   int* scratch;          // [gridDim.x][n][kBigThreads]: PM_j of the thread's pair
   int* child_lb;         // [count*n]
   int* lb_fwd;
@@ -41,7 +45,8 @@ struct BigBatchParams {
 };
 
 __host__ __device__ inline int big_smem_bytes(int n, int mp, int m) {
-  return n * mp * 4 + 2 * n * m * 2 + round_up(n, 16) + 2 * n * 4 + 3 * round_up(m, 4) * 4 + 64 * 4 + round_up(n, 8) * 2;
+  return n * mp * 4 + 2 * n * m * 2 + round_up(n, 16) + 2 * n * 4 + 3 * round_up(m, 4) * 4 + 64 * 4 + round_up(n, 8) * 2 +
+         m * (m - 1) / 2 * ((n + 31) / 32) * 4;
 }
 
 #ifdef __CUDACC__
@@ -90,6 +95,8 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
   int* rm = tl + round_up(M, 4);
   int* red = rm + round_up(M, 4);  // 8 x 4 reduction scratch
   uint16_t* spm = reinterpret_cast<uint16_t*>(red + 64);  // the node's perm
+  const int MW = (n + 31) >> 5;
+  uint32_t* fmask = reinterpret_cast<uint32_t*>(spm + round_up(n, 8));  // LB2: [pair][MW] free positions
   for (int i = tid; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
   __syncthreads();
   for (int node = blockIdx.x; node < B.count; node += gridDim.x) {
@@ -101,10 +108,18 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
       accb[j] = 0;
     }
     if (tid < M) rm[tid] = 0;
+    if (BOUND == kLB2)
+      for (int i = tid; i < B.npairs * MW; i += blockDim.x) fmask[i] = 0;
     __syncthreads();
     for (int c = tid; c < f; c += blockDim.x) isfree[perm[d1 + c]] = 1;
     for (int i = tid; i < n; i += blockDim.x) spm[i] = static_cast<uint16_t>(perm[i]);
     __syncthreads();
+    if (BOUND == kLB2)  // per pair, the free jobs' positions in its Johnson order as a bitmask
+      for (int idx = tid; idx < f * B.npairs; idx += blockDim.x) {
+        const int c = idx / B.npairs, q = idx - c * B.npairs;
+        const int pos = B.inv16[static_cast<size_t>(spm[d1 + c]) * B.npairs + q];
+        atomicOr(&fmask[q * MW + (pos >> 5)], 1u << (pos & 31));
+      }
     if (warp < 2) {  // front (warp 0) / tail (warp 1): wavefronts over (job, machine)
       int C = 0, unused = 0;
       const int k = warp ? M - 1 - lane : lane;
@@ -167,17 +182,30 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
         const int Atot = rm[k], Btot = rm[l];
         const int qk = tl[k], ql = tl[l], rk = fr[k], rl = fr[l];
         int A = 0, Bp = 0, pm = NEG;
-        // the pair's Johnson order streams from L2: kPf entries in flight per thread
         const uint2* col = B.packed + q;
-        for (int t0 = 0; t0 < n; t0 += kPf) {
+        {
+        // the pair's Johnson order streams from L2, only at the free positions (set bits of
+        // the pair's mask, f of them): kPf entries in flight per thread
+        const uint32_t* mk = fmask + q * MW;
+        int w = 0;
+        uint32_t bits = mk[0];
+        for (int left = f; left > 0; left -= kPf) {
+          const int cnt = min(left, kPf);
           uint2 ev[kPf];
 #pragma unroll
-          for (int u = 0; u < kPf; ++u) ev[u] = t0 + u < n ? col[static_cast<size_t>(t0 + u) * B.npairs] : make_uint2(0, 0);
+          for (int u = 0; u < kPf; ++u) {
+            if (u < cnt) {
+              while (bits == 0) bits = mk[++w];
+              const int t = w * 32 + __ffs(bits) - 1;
+              bits &= bits - 1;
+              ev[u] = col[static_cast<size_t>(t) * B.npairs];
+            }
+          }
 #pragma unroll
           for (int u = 0; u < kPf; ++u) {
-            const uint2 e = ev[u];
-            const int j = e.x & 0xffff;
-            if (t0 + u < n && isfree[j]) {
+            if (u < cnt) {
+              const uint2 e = ev[u];
+              const int j = e.x & 0xffff;
               A += e.x >> 16;
               const int X = A + static_cast<int>(e.y >> 16) - Bp;
               PM[j * kBigThreads] = pm;
@@ -187,34 +215,42 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
           }
         }
         int As = 0, Bs = Atot - Btot, sm = NEG;
-        for (int t0 = n - 1; t0 >= 0; t0 -= kPf) {
+        w = MW - 1;
+        bits = mk[w];
+        for (int left = f; left > 0; left -= kPf) {
+          const int cnt = min(left, kPf);
           uint2 ev[kPf];
 #pragma unroll
-          for (int u = 0; u < kPf; ++u) ev[u] = t0 - u >= 0 ? col[static_cast<size_t>(t0 - u) * B.npairs] : make_uint2(0, 0);
-          int pmv[kPf];  // the forward pass's PM_j of this batch's free jobs, all loads in flight
+          for (int u = 0; u < kPf; ++u) {
+            if (u < cnt) {
+              while (bits == 0) bits = mk[--w];
+              const int b = 31 - __clz(bits);
+              bits &= ~(1u << b);
+              ev[u] = col[static_cast<size_t>(w * 32 + b) * B.npairs];
+            }
+          }
+          int pmv[kPf];  // the forward pass's PM_j of this batch, all loads in flight
+#pragma unroll
+          for (int u = 0; u < kPf; ++u) pmv[u] = u < cnt ? PM[(ev[u].x & 0xffff) * kBigThreads] : 0;
 #pragma unroll
           for (int u = 0; u < kPf; ++u) {
-            const int j = ev[u].x & 0xffff;
-            pmv[u] = t0 - u >= 0 && isfree[j] ? PM[j * kBigThreads] : 0;
+            if (u < cnt) {
+              const uint2 e = ev[u];
+              const int j = e.x & 0xffff;
+              const int a = e.x >> 16, b = e.y & 0xffff;
+              Bs += b;
+              const int X = static_cast<int>(e.y >> 16) + Bs - As;
+              const int inner = max(pmv[u] - b, sm - a) + Btot;
+              const int hk = heads[j * M + k], hl = heads[j * M + l];
+              const int vF = max(hk + Atot - a + qk, max(hl + Btot - b, hk + inner) + ql);
+              const int vB = max(rk + Atot - a + tails[j * M + k], max(rl + Btot - b, rk + inner) + tails[j * M + l]);
+              atomicMax(&accf[j], vF);
+              atomicMax(&accb[j], vB);
+              sm = max(sm, X);
+              As += a;
+            }
           }
-#pragma unroll
-          for (int u = 0; u < kPf; ++u) {
-          const uint2 e = ev[u];
-          const int j = e.x & 0xffff;
-          if (t0 - u >= 0 && isfree[j]) {
-            const int a = e.x >> 16, b = e.y & 0xffff;
-            Bs += b;
-            const int X = static_cast<int>(e.y >> 16) + Bs - As;
-            const int inner = max(pmv[u] - b, sm - a) + Btot;
-            const int hk = heads[j * M + k], hl = heads[j * M + l];
-            const int vF = max(hk + Atot - a + qk, max(hl + Btot - b, hk + inner) + ql);
-            const int vB = max(rk + Atot - a + tails[j * M + k], max(rl + Btot - b, rk + inner) + tails[j * M + l]);
-            atomicMax(&accf[j], vF);
-            atomicMax(&accb[j], vB);
-            sm = max(sm, X);
-            As += a;
-          }
-          }
+        }
         }
       }
     }
@@ -480,11 +516,18 @@ __global__ void __launch_bounds__(kBig1gWarps * 32, 1) decompose_big_lb1g_kernel
         S[M - 1 - k] = t;
       }
     };
+    // the lane's job sequence (sigma1, then sigma2 from the end) is read 4 steps ahead
+    auto job_at = [&](int t) { return t < len ? perm[t < d1 ? t : n - 1 - (t - d1)] : 0; };
+    int q0 = job_at(0), q1 = job_at(1), q2 = job_at(2), q3 = job_at(3);
     for (int t = 0; t < steps; ++t) {
+      const int j = q0;
+      q0 = q1;
+      q1 = q2;
+      q2 = q3;
+      q3 = job_at(t + 4);
       if (t == d1 && t < len) flip();
       if (t < len) {
         const bool tail = t >= d1;
-        const int j = perm[tail ? n - 1 - (t - d1) : t];
         const int4* r4 = reinterpret_cast<const int4*>((tail ? sr : sp) + j * MP);
         int prev = 0;
 #pragma unroll

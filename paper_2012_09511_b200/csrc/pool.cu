@@ -979,6 +979,7 @@ struct pbbgpu_pool {
   int big1g_grid = 0;
   size_t big1g_smem = 0;
   uint2* d_packed64 = nullptr;
+  uint16_t* d_inv16 = nullptr;
   int* d_big_scratch = nullptr;
   int big_grid = 0;
   size_t big_smem = 0;
@@ -1039,6 +1040,7 @@ struct pbbgpu_pool {
     cudaFree(d_packed);
     cudaFree(d_invord);
     cudaFree(d_packed64);
+    cudaFree(d_inv16);
     cudaFree(d_big_scratch);
 
     cudaFree(d_lgfact);
@@ -1077,7 +1079,7 @@ int pick_group(int n, int bound) {
 struct HostTables {
   std::vector<int> p32, ptot;
   std::vector<uint8_t> pk, pl, ord, inv;
-  std::vector<uint16_t> lag, ord16;
+  std::vector<uint16_t> lag, ord16, inv16;
   std::vector<uint32_t> packed;
   std::vector<uint2> pk64;
   bool packable = false;
@@ -1117,6 +1119,10 @@ HostTables build_tables(int n, int m, int bound, const int32_t* p, bool big) {
         T.pk64[static_cast<size_t>(t) * npairs + q] =
             make_uint2(static_cast<unsigned>(j) | static_cast<unsigned>(a) << 16, static_cast<unsigned>(bb) | static_cast<unsigned>(lg) << 16);
       }
+    T.inv16.assign(static_cast<size_t>(n) * npairs, 0);  // [job][pair] -> position
+    for (int q = 0; q < npairs; ++q)
+      for (int t = 0; t < n; ++t)
+        T.inv16[static_cast<size_t>(T.ord16[static_cast<size_t>(q) * n + t]) * npairs + q] = static_cast<uint16_t>(t);
   } else {
     T.inv.assign(static_cast<size_t>(n) * npairs, 0);  // [job][pair] -> position
     for (int q = 0; q < npairs; ++q)
@@ -1175,6 +1181,7 @@ void upload_tables(pbbgpu_pool* P, const HostTables& T) {
     u.put(P->d_pl, T.pl);
     if (P->batch_only) {
       u.put(P->d_packed64, T.pk64);
+      u.put(P->d_inv16, T.inv16);
     } else {
       u.put(P->d_ord, T.ord);
       u.put(P->d_lag, T.lag);
@@ -2303,6 +2310,7 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
       G.pk = P->d_pk;
       G.pl = P->d_pl;
       G.packed = P->d_packed64;
+      G.inv16 = P->d_inv16;
       G.scratch = P->d_big_scratch;
       G.child_lb = dlb;
       G.lb_fwd = dlf;
