@@ -276,6 +276,8 @@ def main():
     ap.add_argument("--rounds-per-sync", type=int, default=0, help="rounds per host sync / exchange (0 = default)")
     ap.add_argument("--export-max", type=int, default=0, help="intervals one rank may donate per exchange")
     ap.add_argument("--max-split", type=int, default=0, help="thieves per victim per steal phase (0 = default)")
+    ap.add_argument("--seed-div", type=int, default=-1,
+                    help="breadth-first seeding into world*K/seed_div intervals (0 = equal ranges; -1 = workload default)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
 
@@ -316,10 +318,12 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    seed_div = args.seed_div if args.seed_div >= 0 else int(wl.get("seed_div", 0))
+
     def step(pool):
         before = pool.stats()
         res = solve_distributed(pool, wl["ub"], device=dev, export_max=args.export_max or None, time_limit_s=tlim,
-                                seed_div=int(wl.get("seed_div", 0)))
+                                seed_div=seed_div)
         after = pool.stats()
         return res, before, after
 
@@ -382,7 +386,7 @@ def main():
             s0 = p2.stats()
             t0 = time.perf_counter()
             p2.load_instance(host_inst)
-            r = solve_distributed(p2, wl["ub"], device=dev, time_limit_s=tlim, seed_div=int(wl.get("seed_div", 0)))
+            r = solve_distributed(p2, wl["ub"], device=dev, time_limit_s=tlim, seed_div=seed_div)
             st = p2.stats()
             bv = p2.best_value()
             torch.cuda.synchronize()
@@ -418,8 +422,8 @@ def main():
                            "unique_nodes_per_step": unique, "leaves_per_step": results[-1].leaves,
                            "time_to_proof_ms": statistics.mean(times), "explorers_per_gpu": pool.K(),
                            "work_split": "live siblings" if int(wl.get("split_mode", 0)) == 1 else "factoradic (reference)",
-                           "initial_partition": (f"breadth-first seeding into world*K/{wl['seed_div']} intervals"
-                                                 if wl.get("seed_div") else "world*K equal factoradic ranges, interleaved"),
+                           "initial_partition": (f"breadth-first seeding into world*K/{seed_div} intervals"
+                                                 if seed_div else "world*K equal factoradic ranges, interleaved"),
                            "parallelism": f"dp{world}" if world > 1 else "single",
                            "l2": "256 MiB flush between steps, outside the per-step event brackets",
                            "desc": wl["desc"]},
