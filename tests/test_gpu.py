@@ -303,6 +303,29 @@ def test_large_n_lb1_batch_kernels(name, fdist):
         assert [int(x) for x in pr[i, :f]] == cpr, i
 
 
+@pytest.mark.parametrize("name", ["ta111", "ta081"])
+def test_large_n_lb2_shallow_batch(name):
+    """LB2 on shallow nodes (f up to n: every position of each pair's Johnson order is free,
+    the free-position bitmask walk crosses all 16 mask words), against the oracle."""
+    inst = pbb.taillard_named(name)
+    n = inst.n
+    fs = [n, n - 1, 2 * n // 3, 3 * n // 4, n - 7, 1, 3, n // 2 + 1] * 2
+    perms, d1s, d2s = _nodes_with_f(n, fs, 29)
+    prob = orc.Problem(inst.p, orc.LB2)
+    inc = 26670 if name == "ta111" else 6000
+    with pbb.GpuPool(inst, bound="lb2") as pool:
+        lb, dr, pr, lf, lbw = pool.decompose_batch(perms, d1s, d2s, inc)
+    for i in range(len(fs)):
+        f = n - d1s[i] - d2s[i]
+        fw, bw = prob.children_bounds(perms[i], d1s[i], d2s[i])
+        d, clb, cpr = prob.decompose(perms[i], d1s[i], d2s[i], inc)
+        assert [int(x) for x in lf[i, :f]] == fw, i
+        assert [int(x) for x in lbw[i, :f]] == bw, i
+        assert int(dr[i]) == d, i
+        assert [int(x) for x in lb[i, :f]] == clb, i
+        assert [int(x) for x in pr[i, :f]] == cpr, i
+
+
 # ---------------------------------------------------------------- heuristic cooperation (§8(f) #1)
 
 def test_promote_and_offer_schedule():
