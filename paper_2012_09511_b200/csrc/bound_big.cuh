@@ -516,15 +516,17 @@ __global__ void __launch_bounds__(kBig1gWarps * 32, 1) decompose_big_lb1g_kernel
         S[M - 1 - k] = t;
       }
     };
-    // the lane's job sequence (sigma1, then sigma2 from the end) is read 4 steps ahead
+    // the lane's job sequence (sigma1, then sigma2 from the end) is read kJq steps ahead
+    constexpr int kJq = 8;
     auto job_at = [&](int t) { return t < len ? perm[t < d1 ? t : n - 1 - (t - d1)] : 0; };
-    int q0 = job_at(0), q1 = job_at(1), q2 = job_at(2), q3 = job_at(3);
+    int jq[kJq];
+#pragma unroll
+    for (int u = 0; u < kJq; ++u) jq[u] = job_at(u);
     for (int t = 0; t < steps; ++t) {
-      const int j = q0;
-      q0 = q1;
-      q1 = q2;
-      q2 = q3;
-      q3 = job_at(t + 4);
+      const int j = jq[0];
+#pragma unroll
+      for (int u = 0; u + 1 < kJq; ++u) jq[u] = jq[u + 1];
+      jq[kJq - 1] = job_at(t + kJq);
       if (t == d1 && t < len) flip();
       if (t < len) {
         const bool tail = t >= d1;
