@@ -114,12 +114,17 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
     for (int c = tid; c < f; c += blockDim.x) isfree[perm[d1 + c]] = 1;
     for (int i = tid; i < n; i += blockDim.x) spm[i] = static_cast<uint16_t>(perm[i]);
     __syncthreads();
-    if (BOUND == kLB2)  // per pair, the free jobs' positions in its Johnson order as a bitmask
-      for (int idx = tid; idx < f * B.npairs; idx += blockDim.x) {
-        const int c = idx / B.npairs, q = idx - c * B.npairs;
-        const int pos = B.inv16[static_cast<size_t>(spm[d1 + c]) * B.npairs + q];
-        atomicOr(&fmask[q * MW + (pos >> 5)], 1u << (pos & 31));
+    if (BOUND == kLB2) {  // per pair, the free jobs' positions in its Johnson order as a bitmask
+      const int P = B.npairs, cs = blockDim.x / P;  // thread -> (pair, first child), cs children apart
+      if (tid < cs * P) {
+        const int q = tid % P;
+#pragma unroll 4
+        for (int c = tid / P; c < f; c += cs) {
+          const int pos = B.inv16[static_cast<size_t>(spm[d1 + c]) * P + q];
+          atomicOr(&fmask[q * MW + (pos >> 5)], 1u << (pos & 31));
+        }
       }
+    }
     if (warp < 2) {  // front (warp 0) / tail (warp 1): wavefronts over (job, machine)
       int C = 0, unused = 0;
       const int k = warp ? M - 1 - lane : lane;
