@@ -497,7 +497,9 @@ __global__ void __launch_bounds__(kBig1gWarps * 32, 1) decompose_big_lb1g_kernel
   }
   __syncthreads();
   const int groups = (B.count + 31) / 32;
-  for (int g = blockIdx.x * kBig1gWarps + warp; g < groups; g += gridDim.x * kBig1gWarps) {
+  // groups interleaved over the CTAs (warp-major), so a batch smaller than one full wave
+  // still spreads over every SM
+  for (int g = warp * gridDim.x + blockIdx.x; g < groups; g += gridDim.x * kBig1gWarps) {
     const int node = g * 32 + lane;
     const bool live = node < B.count;
     const int d1 = live ? B.d1[node] : 0, d2 = live ? B.d2[node] : 0;

@@ -2323,7 +2323,7 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
       long long fsum = 0;
       for (int i = 0; i < count; ++i) fsum += n - d1[i] - d2[i];
       if (P->big1 && fsum * 2 < static_cast<long long>(count) * n)
-        P->big1g<<<std::min((count + 32 * kBig1gWarps - 1) / (32 * kBig1gWarps), P->big1g_grid), kBig1gWarps * 32,
+        P->big1g<<<std::min((count + 31) / 32, P->big1g_grid), kBig1gWarps * 32,
                     P->big1g_smem, P->stream>>>(G, P->d_ptot);
       else if (P->big1)
         P->big1<<<std::min((count + kBig1Warps - 1) / kBig1Warps, P->big_grid), kBig1Warps * 32, P->big_smem, P->stream>>>(
