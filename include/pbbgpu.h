@@ -17,6 +17,7 @@
  *   pbbgpu_active_count             <- ExplorerPool::active_count       (explorer.hpp:87)
  *   pbbgpu_snapshot                 <- ExplorerPool::snapshot_intervals (explorer.hpp:88)
  *   pbbgpu_best                     <- best_value / best_schedule       (explorer.hpp:90-91)
+ *   pbbgpu_best_schedule            <- best_schedule with its own makespan (explorer.cpp:352-377)
  *   pbbgpu_offer_bound              <- ExplorerPool::offer_bound        (explorer.hpp:92)
  *   pbbgpu_stats                    <- ExplorerPool::stats              (explorer.hpp:101)
  *   pbbgpu_histogram                <- (new) decomposed nodes by free-job count (roofline)
@@ -148,7 +149,17 @@ int pbbgpu_run_round(pbbgpu_pool* pool, int* active_out);
 int pbbgpu_active_count(pbbgpu_pool* pool, int* active_out);
 int pbbgpu_snapshot(pbbgpu_pool* pool, uint16_t* pos_digits, uint16_t* end_digits,
                     uint8_t* end_is_nfact, int cap, int* count);
+/* snapshot + exact restart accounting: *resume_recount = nodes this pool already counted that
+ * a pool resumed on the snapshot intervals counts again (path nodes of the explorers between
+ * lnz(pos) and their level; partial replays). A checkpoint stores unique - resume_recount, so
+ * checkpointed + resumed counts add up to one run's count exactly (fixed tree). */
+int pbbgpu_snapshot_ex(pbbgpu_pool* pool, uint16_t* pos_digits, uint16_t* end_digits,
+                       uint8_t* end_is_nfact, int cap, int* count, uint64_t* resume_recount);
 int pbbgpu_best(pbbgpu_pool* pool, int64_t* value, int32_t* perm_or_null, int* has_perm);
+/* the pool's best schedule and ITS makespan (best_sched_value_, src/explorer.cpp:352-377);
+ * *cmax = INT64_MAX and *has_perm = 0 when the pool holds no schedule. May exceed the
+ * pool's bound (an offered bound has no schedule behind it). */
+int pbbgpu_best_schedule(pbbgpu_pool* pool, int64_t* cmax, int32_t* perm_or_null, int* has_perm);
 int pbbgpu_offer_bound(pbbgpu_pool* pool, int64_t value);
 int pbbgpu_stats(pbbgpu_pool* pool, pbbgpu_stats_t* out);
 int pbbgpu_histogram(pbbgpu_pool* pool, uint64_t* hist_out, int len);

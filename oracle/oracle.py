@@ -56,6 +56,7 @@ def load():
         _lib.or_children_bounds.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(ctypes.c_int), ctypes.c_int,
                                             ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
                                             ctypes.POINTER(ctypes.c_int64)]
+        _lib.or_children_bounds_lb2_exact.argtypes = _lib.or_children_bounds.argtypes
         _lib.or_lb1_node.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.c_int]
         _lib.or_lb1_node.restype = ctypes.c_int64
         _lib.or_taillard_named.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
@@ -158,6 +159,19 @@ class Problem:
                                      fw.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                      bw.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))):
             raise ValueError("children_bounds: no free jobs")
+        return [int(x) for x in fw], [int(x) for x in bw]
+
+    def children_bounds_lb2_exact(self, perm, d1, d2) -> Tuple[List[int], List[int]]:
+        """LB2 child bounds from the definition: per machine pair the optimum over ALL orders of
+        the free jobs of the two-machine time-lag relaxation (subset DP; f <= 16)."""
+        f = self.n - d1 - d2
+        pr = np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+        fw = np.zeros(f, dtype=np.int64)
+        bw = np.zeros(f, dtype=np.int64)
+        if load().or_children_bounds_lb2_exact(ctypes.byref(self._pr), _ip(pr), d1, d2,
+                                               fw.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                               bw.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))):
+            raise ValueError("children_bounds_lb2_exact: needs 1 <= f <= 16 and m >= 2")
         return [int(x) for x in fw], [int(x) for x in bw]
 
     def lb1(self, perm, d1, d2) -> int:

@@ -316,6 +316,78 @@ int or_children_bounds(const or_problem* pr, const int* perm, int d1, int d2, in
   return 0;
 }
 
+/* LB2 pinned to its definition instead of to the restated order: for every machine pair
+ * (k, l) the value is the OPTIMUM over all orders of the child's free jobs of the two-machine
+ * time-lag relaxation (Lageweg et al. 1978; Mitten/Johnson):
+ *     t0 = r_k + sum a,   t1 = chain  t1 <- max(t1, t0 + lag_j) + b_j  over the order,
+ *     lb_kl = max(t0 + q_k, t1 + q_l)
+ * t0 does not depend on the order and every chain step is nondecreasing in its input t1, so
+ * the minimal final t1 over all orders is the subset DP
+ *     D[S] = min_{j in S} max(D[S - j], r_k + a(S) + lag_j) + b_j,   D[{}] = r_l
+ * (principle of optimality), exact for any tie structure. No Johnson order is used: this is
+ * the independent check that the restated order (row a22) attains the relaxation's optimum.
+ * Cost O(2^(f-1) (f-1)) per child and pair; f <= 16. */
+int or_children_bounds_lb2_exact(const or_problem* pr, const int* perm, int d1, int d2, int64_t* lb_fwd,
+                                 int64_t* lb_bwd) {
+  const int n = pr->n, m = pr->m;
+  const int f = n - d1 - d2;
+  if (f < 1 || f > 16 || m < 2 || m > 64 || n > 512) return -1;
+  int64_t front[64], tail[64], remain[64];
+  or_tables(pr, perm, d1, d2, front, tail, remain);
+  const int fm = f - 1;  /* jobs left in a child */
+  int64_t* D = (int64_t*)malloc(sizeof(int64_t) << fm);
+  int64_t* SA = (int64_t*)malloc(sizeof(int64_t) << fm);
+  int jobs[16];
+  for (int c = 0; c < 2 * f; ++c) {
+    const int fwd = c < f, cc = fwd ? c : c - f;
+    const int jc = perm[d1 + cc];
+    const int32_t* rowc = pr->p + (size_t)jc * m;
+    int64_t r[64], q[64];
+    int64_t prev = 0;
+    for (int k = 0; k < m; ++k) {  /* forward child: extended head, node tail */
+      if (fwd) prev = max64(prev, front[k]) + rowc[k];
+      r[k] = fwd ? prev : front[k];
+    }
+    prev = 0;
+    for (int k = m - 1; k >= 0; --k) {  /* backward child: node head, extended tail */
+      if (!fwd) prev = max64(prev, tail[k]) + rowc[k];
+      q[k] = fwd ? tail[k] : prev;
+    }
+    int t = 0;
+    for (int x = 0; x < f; ++x)
+      if (x != cc) jobs[t++] = perm[d1 + x];
+    int64_t best = 0;
+    for (int k = 0; k < m; ++k) {
+      for (int l = k + 1; l < m; ++l) {
+        SA[0] = 0;
+        D[0] = r[l];
+        for (uint32_t S = 1; S < (1u << fm); ++S) {
+          const int low = __builtin_ctz(S);
+          SA[S] = SA[S & (S - 1)] + pr->p[(size_t)jobs[low] * m + k];
+          int64_t v = INT64_MAX;
+          for (uint32_t w = S; w; w &= w - 1) {
+            const int i = __builtin_ctz(w);
+            const int32_t* row = pr->p + (size_t)jobs[i] * m;
+            int64_t lag = 0;
+            for (int z = k + 1; z < l; ++z) lag += row[z];
+            const int64_t e = max64(D[S & ~(1u << i)], r[k] + SA[S] + lag) + row[l];
+            if (e < v) v = e;
+          }
+          D[S] = v;
+        }
+        const uint32_t all = (1u << fm) - 1u;
+        const int64_t lb = max64(r[k] + SA[all] + q[k], D[all] + q[l]);
+        if (lb > best) best = lb;
+      }
+    }
+    if (fwd) lb_fwd[cc] = best;
+    else lb_bwd[cc] = best;
+  }
+  free(D);
+  free(SA);
+  return 0;
+}
+
 /* decompose (src/bound.cpp:98-139): MinMin over the union minimum, ties to the larger
  * LB sum, then Forward; pruned = child_lb >= incumbent. */
 int or_decompose(const or_problem* pr, const int* perm, int d1, int d2, int64_t incumbent,

@@ -14,8 +14,11 @@
  *   neh                                   src/heuristic.cpp:24-103
  * LB2 (Johnson two-machine bound with lags over all machine pairs) has no reference
  * implementation; it follows SURVEY.md §8 row a22 (Lageweg et al. 1978 as cited at
- * PAPER.md:286-288). LB2 parity is pinned only by this restatement ("parity unpinned"
- * for LB2 — see DESIGN.md); LB1 parity is pinned by oracle/_ref (the compiled reference).
+ * PAPER.md:286-288). The reference cannot pin it, so LB2 is pinned to its DEFINITION:
+ * or_children_bounds_lb2_exact computes every pair's two-machine relaxation optimum over all
+ * job orders (subset DP, no Johnson order), and the tests require the restated order's
+ * chains (and the GPU) to equal it; LB1 parity is pinned by oracle/_ref (the compiled
+ * reference).
  */
 #ifndef PFSP_ORACLE_H
 #define PFSP_ORACLE_H
@@ -70,6 +73,10 @@ int or_decompose(const or_problem* pr, const int* perm, int d1, int d2, int64_t 
 int or_children_bounds(const or_problem* pr, const int* perm, int d1, int d2, int64_t* lb_fwd,
                        int64_t* lb_bwd);
 int64_t or_lb1_node(const or_problem* pr, const int* perm, int d1, int d2);
+/* LB2 from its definition: per pair the exact optimum over all orders of the two-machine
+ * time-lag relaxation (subset DP, no Johnson order); f <= 16. Pins the restated order. */
+int or_children_bounds_lb2_exact(const or_problem* pr, const int* perm, int d1, int d2, int64_t* lb_fwd,
+                                 int64_t* lb_bwd);
 
 /* factoradic helpers (digits MSD first, radix n-l) */
 int or_fact_compare(int n, const int* a, const int* b);

@@ -28,6 +28,7 @@ EXPORTS = (
     "pbbgpu_stats", "pbbgpu_histogram", "pbbgpu_decompose_batch", "pbbgpu_solve", "pbbgpu_int32_peak",
     "pbbgpu_assign_split_range", "pbbgpu_export", "pbbgpu_debug_state", "pbbgpu_assign_split_strided",
     "pbbgpu_insertion_ls", "pbbgpu_offer_schedule", "pbbgpu_promote", "pbbgpu_explorer_lengths",
+    "pbbgpu_best_schedule", "pbbgpu_snapshot_ex",
 )
 
 
@@ -121,6 +122,8 @@ def load() -> ctypes.CDLL:
         "pbbgpu_active_count": (ctypes.c_int, [P, ip]),
         "pbbgpu_snapshot": (ctypes.c_int, [P, u16p, u16p, u8p, ctypes.c_int, ip]),
         "pbbgpu_best": (ctypes.c_int, [P, i64p, i32p, ip]),
+        "pbbgpu_best_schedule": (ctypes.c_int, [P, i64p, i32p, ip]),
+        "pbbgpu_snapshot_ex": (ctypes.c_int, [P, u16p, u16p, u8p, ctypes.c_int, ip, u64p]),
         "pbbgpu_offer_bound": (ctypes.c_int, [P, ctypes.c_int64]),
         "pbbgpu_stats": (ctypes.c_int, [P, ctypes.POINTER(Stats)]),
         "pbbgpu_histogram": (ctypes.c_int, [P, u64p, ctypes.c_int]),

@@ -119,21 +119,33 @@ def checkpoint_load(path: str, inst: Instance) -> CheckpointData:
     return d
 
 
-def save_pool(pool: GpuPool, path: str, total_nodes: Optional[int] = None) -> CheckpointData:
-    """Snapshot a pool between rounds (snapshot_intervals, explorer.cpp:342-350) into a file."""
+def save_pool(pool: GpuPool, path: str, total_nodes: Optional[int] = None, base_nodes: int = 0) -> CheckpointData:
+    """Snapshot a pool between rounds (snapshot_intervals, explorer.cpp:342-350) into a file.
+
+    `nodes` = base_nodes (what earlier runs of this proof had already counted, e.g. the
+    `total_nodes` a resumed pool carries) + this pool's unique count - the resume recount
+    (nodes the resumed pool will decompose again), so node totals stay exact across any
+    number of checkpoint/restart cycles. The schedule is written only when its own makespan
+    is the recorded bound (an offered bound has no schedule behind it)."""
     st = pool.stats()
     best = pool.best_schedule()
-    d = CheckpointData([WorkUnitData(pool.K(), pool.snapshot_intervals())], pool.best_value(),
-                       best.perm if best.perm and best.cmax == pool.best_value() else [],
-                       st.unique if total_nodes is None else total_nodes)
+    ivs, recount = pool.snapshot()
+    bv = pool.best_value()
+    base = getattr(pool, "resumed_nodes", 0) + base_nodes
+    d = CheckpointData([WorkUnitData(pool.K(), ivs)], bv,
+                       best.perm if best.perm and best.cmax == bv else [],
+                       base + st.unique - recount if total_nodes is None else total_nodes)
     checkpoint_save(path, pool.inst, d)
     return d
 
 
 def resume_pool(path: str, inst: Instance, cfg: Optional[PoolConfig] = None, bound="lb1") -> GpuPool:
-    """A fresh pool seated on a checkpoint's remaining intervals (Coordinator::restore analogue)."""
+    """A fresh pool seated on a checkpoint's remaining intervals (Coordinator::restore analogue,
+    src/coordinator.cpp:129-140). The checkpoint's node total is kept on the pool
+    (`resumed_nodes`) and added by the next save_pool, like the coordinator's running total."""
     d = checkpoint_load(path, inst)
     pool = GpuPool(inst, cfg, bound)
+    pool.resumed_nodes = d.total_nodes
     pool.set_initial_bound(d.best_value, d.best_schedule)
     ivs = normalize([iv for u in d.units for iv in u.intervals])
     if ivs:

@@ -1728,6 +1728,9 @@ int pbbgpu_set_initial_bound(pbbgpu_pool* P, int64_t ub, const int32_t* sched, i
         P->best_sched_value = INT64_MAX;
       }
       P->pinned_ub = ub;
+      // a stale offer (e.g. a MIN exchanged at the end of the previous solve) must not lower
+      // the new bound below a value that has no schedule behind it
+      P->pending_offer.store(INT64_MAX);
     }
     set_device_best(P, ub);
   });
@@ -2039,8 +2042,23 @@ int pbbgpu_active_count(pbbgpu_pool* P, int* active_out) {
 }
 
 int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_nf, int cap, int* count) {
+  uint64_t recount = 0;
+  return pbbgpu_snapshot_ex(P, pos, end, end_nf, cap, count, &recount);
+}
+
+// Exact restart accounting. A resumed interval [pos, end) is re-seated by an init_at replay
+// whose duplicates are discounted as min(L, lnz(pos)) (the steal rule). The path nodes at
+// levels lnz(pos) .. level-1 of an explorer that is about to select pos's node were already
+// decomposed (and counted) by this pool, and the replay counts them again; an explorer still
+// replaying (kInit) has counted nrep replay decompositions that its re-seat redoes from
+// scratch. Their sum is returned so that snapshot_count - resume_recount + the resumed
+// pool's unique count equals a single run's count (fixed tree: same incumbent on both sides).
+int pbbgpu_snapshot_ex(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_nf, int cap, int* count,
+                       uint64_t* resume_recount) {
   return guarded([&] {
+    if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
     const int n = P->n;
+    uint64_t recount = 0;
     std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
     xfer(P, st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost, "state copy");
     int c = 0;
@@ -2058,7 +2076,9 @@ int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_n
       // subtree) has covered that cell's whole subtree: the remaining work starts after it
       // (effective_pos in explore.cuh)
       bool past_end = false;
+      bool parked = false;
       if (h->state == kActive && h->level >= 0 && C[tri_off(h->level, n) + V[h->level]] <= 0) {
+        parked = true;
         int l = h->level;
         for (; l >= 0; --l) {
           if (++pv[static_cast<size_t>(l)] <= n - 1 - l) break;
@@ -2073,6 +2093,14 @@ int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_n
       }
       if (past_end) continue;
       if (c >= cap) throw CapacityError("snapshot buffer too small");
+      if (h->state == kInit) {
+        recount += h->nrep;
+      } else if (!parked) {
+        int lnz = 0;
+        for (int l = 0; l < n; ++l)
+          if (pv[static_cast<size_t>(l)] != 0) lnz = l;
+        recount += static_cast<uint64_t>(std::max(0, h->level - lnz));
+      }
       for (int l = 0; l < n; ++l) {
         pos[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(pv[static_cast<size_t>(l)]);
         end[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(h->has_end ? E[l] : 0);
@@ -2081,6 +2109,7 @@ int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_n
       ++c;
     }
     *count = c;
+    if (resume_recount) *resume_recount = recount;
   });
 }
 
@@ -2104,6 +2133,15 @@ int pbbgpu_best(pbbgpu_pool* P, int64_t* value, int32_t* perm, int* has_perm) {
   return guarded([&] {
     std::scoped_lock lk(P->best_mu);
     *value = P->best_value;
+    if (has_perm) *has_perm = P->best_sched.empty() ? 0 : 1;
+    if (perm && !P->best_sched.empty()) std::copy(P->best_sched.begin(), P->best_sched.end(), perm);
+  });
+}
+
+int pbbgpu_best_schedule(pbbgpu_pool* P, int64_t* cmax, int32_t* perm, int* has_perm) {
+  return guarded([&] {
+    std::scoped_lock lk(P->best_mu);
+    *cmax = P->best_sched.empty() ? INT64_MAX : P->best_sched_value;
     if (has_perm) *has_perm = P->best_sched.empty() ? 0 : 1;
     if (perm && !P->best_sched.empty()) std::copy(P->best_sched.begin(), P->best_sched.end(), perm);
   });
@@ -2147,7 +2185,10 @@ int pbbgpu_offer_schedule(pbbgpu_pool* P, const int32_t* perm, int64_t cmax, int
     int64_t cur = P->pending_offer.load();
     while (cmax < cur && !P->pending_offer.compare_exchange_weak(cur, cmax)) {
     }
-    if (cmax < P->best_value) took = true;
+    {
+      std::scoped_lock lk(P->best_mu);  // run_round updates best_value under the same lock
+      if (cmax < P->best_value) took = true;
+    }
     if (taken) *taken = took ? 1 : 0;
   });
 }

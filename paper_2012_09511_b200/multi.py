@@ -179,13 +179,17 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
         for f, v in hist.items():
             hv[f] = v
         dist.all_reduce(hv, group=group)
-        bv = torch.tensor([pool.best_value(), rank], dtype=torch.int64, device=device)
+        # the schedule owner: the rank holding the best schedule by ITS makespan (every rank's
+        # bound equals the global MIN after the exchanges, so bound values cannot tell)
+        sv = bsched.cmax if bsched.perm else (1 << 62)
+        bv = torch.tensor([pool.best_value(), sv, rank], dtype=torch.int64, device=device)
         allbv = [torch.zeros_like(bv) for _ in range(world)]
         dist.all_gather(allbv, bv, group=group)
         bvals = torch.stack(allbv).cpu().numpy()
-        owner = int(bvals[np.argmin(bvals[:, 0]), 1])
+        owner = int(bvals[np.argmin(bvals[:, 1]), 2])
         pv = torch.tensor(bsched.perm if bsched.perm else [-1] * n, dtype=torch.int64, device=device)
-        dist.broadcast(pv, src=owner, group=group)
+        src = dist.get_global_rank(group, owner) if group is not None else owner
+        dist.broadcast(pv, src=src, group=group)
         perm = [int(x) for x in pv.cpu().numpy()]
         v = vec.cpu().numpy()
         return DistResult(int(bvals[:, 0].min()), perm if perm[0] >= 0 else [], int(v[0]), int(v[1]), int(v[2]),

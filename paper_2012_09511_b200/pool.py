@@ -171,6 +171,7 @@ class GpuPool:
         c = self.cfg.to_c()
         _lib.check(self._lib.pbbgpu_create(inst.n, inst.m, inst.ptr(), self.bound, ctypes.byref(c), ctypes.byref(h)))
         self._h = h
+        self.resumed_nodes = 0  # node total carried over from a checkpoint (checkpoint.resume_pool)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -261,13 +262,21 @@ class GpuPool:
         return act.value
 
     def snapshot_intervals(self) -> List[Interval]:
+        """snapshot_intervals (explorer.cpp:342-350): the remaining work [position, end)."""
+        return self.snapshot()[0]
+
+    def snapshot(self) -> Tuple[List[Interval], int]:
+        """Remaining intervals plus the resume recount (pbbgpu_snapshot_ex): nodes this pool has
+        counted that a pool resumed on these intervals will count again. A checkpoint records
+        unique - recount, so checkpointed + resumed counts equal one run's count exactly."""
         K, n = self.K(), self.inst.n
         pos = np.zeros((K, n), dtype=np.uint16)
         end = np.zeros((K, n), dtype=np.uint16)
         inf = np.zeros(K, dtype=np.uint8)
         cnt = ctypes.c_int()
-        _lib.check(self._lib.pbbgpu_snapshot(self._h, pos.ctypes.data_as(_u16p), end.ctypes.data_as(_u16p),
-                                             inf.ctypes.data_as(_u8p), K, ctypes.byref(cnt)))
+        rec = ctypes.c_uint64()
+        _lib.check(self._lib.pbbgpu_snapshot_ex(self._h, pos.ctypes.data_as(_u16p), end.ctypes.data_as(_u16p),
+                                                inf.ctypes.data_as(_u8p), K, ctypes.byref(cnt), ctypes.byref(rec)))
         nf = factorial(n)
         out = []
         for i in range(cnt.value):
@@ -275,7 +284,7 @@ class GpuPool:
             b = nf if inf[i] else to_decimal([int(x) for x in end[i]])
             if a < b:
                 out.append((a, b))
-        return normalize(out)
+        return normalize(out), int(rec.value)
 
     def best_value(self) -> int:
         v = ctypes.c_int64()
@@ -283,10 +292,13 @@ class GpuPool:
         return v.value
 
     def best_schedule(self) -> Schedule:
+        """best_schedule (explorer.cpp:356-362): the best schedule seen and ITS makespan
+        (cmax = -1 and an empty perm when the pool holds none)."""
         v = ctypes.c_int64()
         has = ctypes.c_int()
         perm = np.zeros(self.inst.n, dtype=np.int32)
-        _lib.check(self._lib.pbbgpu_best(self._h, ctypes.byref(v), perm.ctypes.data_as(_i32p), ctypes.byref(has)))
+        _lib.check(self._lib.pbbgpu_best_schedule(self._h, ctypes.byref(v), perm.ctypes.data_as(_i32p),
+                                                  ctypes.byref(has)))
         if not has.value:
             return Schedule([], -1)
         return Schedule([int(x) for x in perm], int(v.value))

@@ -215,22 +215,25 @@ def test_pool_rounds_snapshot_and_offer_bound():
         assert st.rounds == 4 and st.decomposed > 0
 
 
-def test_snapshot_resume_preserves_count():
+@pytest.mark.parametrize("name,ub,rounds", [("ta011", 1582, 3), ("ta011", 1582, 7), ("ta021", 2297, 5)])
+def test_snapshot_resume_preserves_count(name, ub, rounds):
     """Snapshot the remaining work after a few rounds, restart it in a fresh pool:
-    nodes before + nodes after == full count (apply_work_update-style handover)."""
-    ref = golden_io.ref_counts()["ta011@1582"]
-    inst = pbb.taillard_named("ta011")
-    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=256, batch_steps=64)) as pool:
-        pool.set_initial_bound(1582)
+    nodes before - resume recount + nodes after == the reference's count, exactly."""
+    # ta021@2297: the reference's 534.8-s K=1 proof (SURVEY.md §8(c), Appendix C)
+    ref = golden_io.ref_counts().get(f"{name}@{ub}", {"decomposed": 462443491, "leaves": 1440})
+    inst = pbb.taillard_named(name)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=256, batch_steps=64, rounds_per_sync=1)) as pool:
+        pool.set_initial_bound(ub)
         pool.assign_split(256)
-        for _ in range(3):
+        for _ in range(rounds):
             pool.run_round()
-        snap = pool.snapshot_intervals()
+        snap, recount = pool.snapshot()
         done = pool.stats()
-    res = pbb.pool_run(inst, 1582, intervals=snap, cfg=pbb.PoolConfig(explorers=max(256, len(snap))))
-    # nodes on the path to each resumed position are re-decomposed by the new pool's replay;
-    # they are discounted exactly like steal replays, so the totals add up
-    assert done.unique + res.stats.unique >= ref["decomposed"]
+    assert snap and recount >= 0
+    res = pbb.pool_run(inst, ub, intervals=snap, cfg=pbb.PoolConfig(explorers=max(512, len(snap))))
+    # path nodes between lnz(pos) and each explorer's level are decomposed again by the resumed
+    # pool's replays (partial replays: redone from scratch); the recount removes exactly those
+    assert done.unique - recount + res.stats.unique == ref["decomposed"]
     assert done.leaves + res.stats.leaves == ref["leaves"]
 
 
@@ -362,8 +365,9 @@ def test_cooperative_solve_finds_optimum(name, opt, bound):
 # ---------------------------------------------------------------- checkpoint / restart (§8(f) #2)
 
 def test_checkpoint_restart_completes_the_proof(tmp_path):
-    """Stop a proof after a few rounds, checkpoint (reference format), resume in a new pool:
-    leaves add up exactly, the bound and schedule survive, and the reference can read it."""
+    """Stop a proof after a few rounds, checkpoint (reference format), resume in a new pool,
+    checkpoint again, resume again, finish: node and leaf totals equal the reference's
+    single-run counts exactly, the bound and schedule survive."""
     from paper_2012_09511_b200 import checkpoint as ck
 
     ref = golden_io.ref_counts()["ta011@1582"]
@@ -376,14 +380,20 @@ def test_checkpoint_restart_completes_the_proof(tmp_path):
             pool.run_round()
         first = pool.stats()
         d = ck.save_pool(pool, path)
-    assert d.units[0].intervals
-    with ck.resume_pool(path, inst, pbb.PoolConfig(explorers=4096)) as pool2:
-        while pool2.run_round():
+    assert d.units[0].intervals and d.total_nodes <= first.unique
+    with ck.resume_pool(path, inst, pbb.PoolConfig(explorers=4096, batch_steps=64, rounds_per_sync=1)) as pool2:
+        assert pool2.resumed_nodes == d.total_nodes
+        for _ in range(2):
+            pool2.run_round()
+        second = pool2.stats()
+        d2 = ck.save_pool(pool2, path)   # carries the first checkpoint's total
+    with ck.resume_pool(path, inst, pbb.PoolConfig(explorers=4096)) as pool3:
+        while pool3.run_round():
             pass
-        rest = pool2.stats()
-        assert pool2.best_value() == 1582
-    assert first.leaves + rest.leaves == ref["leaves"]
-    assert first.unique + rest.unique >= ref["decomposed"]
+        rest = pool3.stats()
+        assert pool3.best_value() == 1582
+    assert first.leaves + second.leaves + rest.leaves == ref["leaves"]
+    assert d2.total_nodes + rest.unique == ref["decomposed"]
 
 
 def test_timeline_csv(tmp_path):
@@ -472,3 +482,56 @@ def test_breadth_first_seeding_keeps_counts(key, div):
     assert r.unique == ref["decomposed"]
     assert r.leaves == ref["leaves"]
     assert _hist_str(r.hist) == ref["hist"]
+
+
+# ---------------------------------------------------------------- LB2 pinned to its definition
+
+def _nodes_small_f(n, count, fmax, seed):
+    rng = np.random.default_rng(seed)
+    perms, d1s, d2s = [], [], []
+    for _ in range(count):
+        perms.append(rng.permutation(n))
+        f = int(rng.integers(1, min(fmax, n) + 1))
+        d1 = int(rng.integers(0, n - f + 1))
+        d1s.append(d1)
+        d2s.append(n - f - d1)
+    return np.array(perms), d1s, d2s
+
+
+@pytest.mark.parametrize("name,fmax,count", [("ta001", 12, 300), ("ta021", 10, 100), ("ta056", 10, 60),
+                                             ("ta041", 11, 120), ("ta111", 8, 12)])
+def test_gpu_lb2_equals_relaxation_optimum(name, fmax, count):
+    """Every GPU LB2 child bound (small-n warp kernel, and the large-n kernel for ta111) equals
+    the maximum over machine pairs of the two-machine time-lag relaxation's optimum over ALL job
+    orders (oracle subset DP, no Johnson order involved)."""
+    inst = pbb.taillard_named(name)
+    perms, d1s, d2s = _nodes_small_f(inst.n, count, fmax, 31)
+    prob = orc.Problem(inst.p, orc.LB2)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=256), bound="lb2") as pool:
+        _, _, _, lf, lbw = pool.decompose_batch(perms, d1s, d2s, 10 ** 6)
+    for i in range(count):
+        f = inst.n - d1s[i] - d2s[i]
+        fw, bw = prob.children_bounds_lb2_exact(perms[i], d1s[i], d2s[i])
+        assert [int(x) for x in lf[i, :f]] == fw
+        assert [int(x) for x in lbw[i, :f]] == bw
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("m", [5, 10, 20])
+def test_gpu_lb2_optimal_under_ties(seed, m):
+    """Tie-heavy instances (times in {1, 2, 3}, one constant column): a = b jobs, equal keys."""
+    rng = np.random.default_rng(4000 + 10 * m + seed)
+    n = 12
+    p = rng.integers(1, 4, size=(n, m)).astype(np.int32)
+    if seed % 2 == 0:
+        p[:, int(rng.integers(0, m))] = 2
+    inst = pbb.Instance(n, m, p)
+    perms, d1s, d2s = _nodes_small_f(n, 60, 9, seed)
+    prob = orc.Problem(p, orc.LB2)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=128), bound="lb2") as pool:
+        _, _, _, lf, lbw = pool.decompose_batch(perms, d1s, d2s, 10 ** 6)
+    for i in range(len(d1s)):
+        f = n - d1s[i] - d2s[i]
+        fw, bw = prob.children_bounds_lb2_exact(perms[i], d1s[i], d2s[i])
+        assert [int(x) for x in lf[i, :f]] == fw
+        assert [int(x) for x in lbw[i, :f]] == bw

@@ -43,8 +43,9 @@ class _Stats:
 class FakePool:
     """K explorers over integer intervals; a round processes `speed` units per explorer."""
 
-    def __init__(self, K, total, speed, rank, skew):
+    def __init__(self, K, total, speed, rank, skew, best_rank=0):
         self.inst = _Inst()
+        self.found = 1000 + 10 * abs(rank - best_rank)  # the best_rank finds the best incumbent
         self.K_, self.total, self.speed, self.rank, self.skew = K, total, speed, rank, skew
         self.iv = [None] * K
         self.done = 0
@@ -77,7 +78,7 @@ class FakePool:
                 self.done += step
                 self.iv[k] = [a + step, b] if a + step < b else None
         if self.best is not None and self.done > 0:
-            self.best = min(self.best, 1000 + 10 * self.rank)  # rank 0 finds the better incumbent
+            self.best = min(self.best, self.found)
         return sum(1 for x in self.iv if x)
 
     def best_value(self):
@@ -117,14 +118,15 @@ class FakePool:
     def best_schedule(self):
         class S:
             perm = [3, 2, 1, 0] if self.rank == 0 else [0, 1, 2, 3]
+            cmax = self.found
         return S()
 
 
-def _worker(rank, world, port, total, out):
+def _worker(rank, world, port, total, out, best_rank=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    pool = FakePool(K=64, total=total, speed=1000, rank=rank, skew=True)
+    pool = FakePool(K=64, total=total, speed=1000, rank=rank, skew=True, best_rank=best_rank)
     res = solve_distributed(pool, ub=5000, device="cpu")
     out[rank] = (res.unique, res.best_value, res.remote_intervals, res.best_perm, res.completed, pool.done)
     dist.destroy_process_group()
@@ -154,3 +156,17 @@ def test_two_rank_exchange_processes_everything_once():
     assert r0[1] == r1[1] == 1000                # global incumbent
     assert r0[3] == r1[3] == [3, 2, 1, 0]        # schedule of the owner of the best value
     assert r0[4] and r1[4]
+
+
+@pytest.mark.timeout(120)
+def test_best_schedule_comes_from_the_rank_that_found_it():
+    """Rank 1 finds the optimum: after the MIN exchange every rank's bound is equal, so the
+    schedule owner must be picked by the schedules' own makespans (not by bound values)."""
+    total = 64 * 2 * 20000
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_worker, args=(2, _free_port(), total, out, 1), nprocs=2, start_method="spawn", join=True)
+        r0, r1 = out[0], out[1]
+    assert r0[1] == r1[1] == 1000
+    assert r0[3] == r1[3] == [0, 1, 2, 3]        # rank 1's schedule
