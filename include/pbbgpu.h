@@ -14,6 +14,12 @@
  *   pbbgpu_export                   <- split_unit right halves for another worker
  *                                      (src/workunit.cpp:59-74, src/coordinator.cpp:170-187)
  *   pbbgpu_run_round                <- ExplorerPool::run_round          (explorer.hpp:85)
+ *   pbbgpu_apply_work_update        <- ExplorerPool::apply_work_update  (explorer.hpp:78-81)
+ *   pbbgpu_improved_since_mark      <- ExplorerPool::improved_since_mark (explorer.hpp:94)
+ *   pbbgpu_steals_since_mark / pbbgpu_reset_steal_mark
+ *                                   <- steals_since_mark / reset_steal_mark (explorer.hpp:95-96)
+ *   pbbgpu_take_census              <- ExplorerPool::take_census        (explorer.hpp:102)
+ *   pbbgpu_flush_timeline           <- ExplorerPool::flush_timeline     (explorer.hpp:103)
  *   pbbgpu_active_count             <- ExplorerPool::active_count       (explorer.hpp:87)
  *   pbbgpu_snapshot                 <- ExplorerPool::snapshot_intervals (explorer.hpp:88)
  *   pbbgpu_best                     <- best_value / best_schedule       (explorer.hpp:90-91)
@@ -78,6 +84,16 @@ typedef struct {
                             (thieves take unexplored, unpruned subtrees of the shallowest level
                             holding any; best on irregular pinned trees); 2 = live-sibling where
                             the victim has decomposed siblings left, factoradic otherwise */
+  int steal_policy;      /* 0 = B200 policy (every idle explorer is a thief each round, longest
+                            remaining intervals split r ways); 1 = the reference's steal_phase
+                            exactly (explorer.cpp:251-340: trigger active*5 < 4K, eligible
+                            len > avg and > min_steal_len, 4-ary hypercube matching when K = 4^c,
+                            else largest eligible; midpoint of the raw position; rounds of
+                            steps_per_round steps (default 1024 = batch_steps) whose replays are
+                            free): raw PoolStats then equal the reference's on fixed trees. n <= 30 */
+  int record_census;     /* PoolConfig.record_census (explorer.hpp:39): leaf positions, n <= 20 */
+  int census_cap;        /* census capacity (leaf positions held between take_census calls); 0 = 2^20 */
+  const char* timeline_path; /* PoolConfig.timeline_path (explorer.hpp:40): activity CSV, NULL = none */
 } pbbgpu_config_t;
 
 typedef struct {
@@ -146,6 +162,26 @@ int pbbgpu_seed(pbbgpu_pool* pool, int64_t bound, int first, int stride, int tot
 int pbbgpu_export(pbbgpu_pool* pool, int max_count, uint16_t* a_out, uint16_t* b_out,
                   uint8_t* b_is_nfact_out, int* count);
 int pbbgpu_run_round(pbbgpu_pool* pool, int* active_out);
+/* apply_work_update (explorer.hpp:78-81, src/explorer.cpp:162-199): the new interval set
+ * (normalized here) intersected with every explorer's remaining [position, end): an explorer
+ * whose intersection is one interval starting at its position keeps its search state (its
+ * end shrinks to the interval's end); any other explorer goes idle; the update minus what was
+ * kept is seated on idle explorers. More intervals than K: PBBGPU_ERR_ARG; more fragments
+ * than idle explorers: PBBGPU_ERR_CAPACITY (std::runtime_error in the reference). */
+int pbbgpu_apply_work_update(pbbgpu_pool* pool, const uint16_t* a_digits, const uint16_t* b_digits,
+                             const uint8_t* b_is_nfact, int count);
+/* improved_since_mark (explorer.hpp:94, explorer.cpp:379-386): 1 when the best schedule improved
+ * on the mark (the mark moves to it), else 0. */
+int pbbgpu_improved_since_mark(pbbgpu_pool* pool, int* improved);
+/* steals_since_mark / reset_steal_mark (explorer.hpp:95-96) */
+int pbbgpu_steals_since_mark(pbbgpu_pool* pool, uint64_t* steals);
+int pbbgpu_reset_steal_mark(pbbgpu_pool* pool);
+/* take_census (explorer.hpp:102, explorer.cpp:438-445): leaf positions (decimal, position_u64)
+ * recorded since the last call (record_census), then cleared. PBBGPU_ERR_CAPACITY when more
+ * than census_cap leaves were recorded (or more than cap requested). */
+int pbbgpu_take_census(pbbgpu_pool* pool, uint64_t* out, int64_t cap, int64_t* count);
+/* flush_timeline (explorer.hpp:103, explorer.cpp:466-471): forced timeline sample + flush */
+int pbbgpu_flush_timeline(pbbgpu_pool* pool);
 int pbbgpu_active_count(pbbgpu_pool* pool, int* active_out);
 int pbbgpu_snapshot(pbbgpu_pool* pool, uint16_t* pos_digits, uint16_t* end_digits,
                     uint8_t* end_is_nfact, int cap, int* count);

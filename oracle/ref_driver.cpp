@@ -18,6 +18,10 @@
 //   inst   <ta>                                           processing-time matrix
 //   ils    <ta> <iterations> <rng_seed>                   NEH + insertion_local_search
 //   ckpt   <ta> <path>  /  ckptload <ta> <path>           checkpoint_save / checkpoint_load
+//   stats  <ta|gen:n:m:seed> <ub> <K> <threads> <batch_steps> <disable_pruning> <census>
+//                                                         pool_run with every PoolStats field
+//                                                         (+ the sorted census when asked)
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -303,6 +307,42 @@ int cmd_ckptload(int argc, char** argv) {
   return 0;
 }
 
+Instance named_or_generated(const char* s) {
+  if (std::strncmp(s, "gen:", 4) == 0) {
+    int n = 0, m = 0;
+    long seed = 0;
+    if (std::sscanf(s + 4, "%d:%d:%ld", &n, &m, &seed) != 3) throw std::invalid_argument("gen:n:m:seed");
+    return generate_taillard(n, m, static_cast<std::int32_t>(seed));
+  }
+  return taillard_named(s);
+}
+
+int cmd_stats(int argc, char** argv) {
+  if (argc < 9) return 2;
+  Instance inst = named_or_generated(argv[2]);
+  const std::int64_t ub = parse_ub(inst, argv[3]);
+  PoolConfig cfg;
+  cfg.explorers = std::atoi(argv[4]);
+  cfg.threads = std::atoi(argv[5]);
+  cfg.batch_steps = std::atoi(argv[6]);
+  cfg.disable_pruning = std::atoi(argv[7]) != 0;
+  cfg.record_census = std::atoi(argv[8]) != 0;
+  PoolResult r = pool_run(inst, ub, {}, cfg);
+  std::sort(r.census.begin(), r.census.end());
+  std::printf(
+      "{\"mode\":\"stats\",\"instance\":\"%s\",\"initial_ub\":%lld,\"best_value\":%lld,\"explorers\":%d,"
+      "\"threads\":%d,\"batch_steps\":%d,\"disable_pruning\":%d,\"decomposed\":%llu,\"leaves\":%llu,"
+      "\"improvements\":%llu,\"local_steals\":%llu,\"steal_phases\":%llu,\"intervals_initialized\":%llu,"
+      "\"completed\":%s,\"census_size\":%zu,\"census_distinct\":%zu}\n",
+      argv[2], (long long)ub, (long long)r.best_value, cfg.explorers, cfg.threads, cfg.batch_steps,
+      cfg.disable_pruning ? 1 : 0, (unsigned long long)r.stats.decomposed, (unsigned long long)r.stats.leaves,
+      (unsigned long long)r.stats.improvements, (unsigned long long)r.stats.local_steals,
+      (unsigned long long)r.stats.steal_phases, (unsigned long long)r.stats.intervals_initialized,
+      r.stats.completed ? "true" : "false", r.census.size(),
+      static_cast<size_t>(std::unique(r.census.begin(), r.census.end()) - r.census.begin()));
+  return 0;
+}
+
 int cmd_inst(int argc, char** argv) {
   if (argc < 3) return 2;
   Instance inst = taillard_named(argv[2]);
@@ -333,6 +373,7 @@ int main(int argc, char** argv) {
     else if (mode == "ils") rc = cmd_ils(argc, argv);
     else if (mode == "ckpt") rc = cmd_ckpt(argc, argv);
     else if (mode == "ckptload") rc = cmd_ckptload(argc, argv);
+    else if (mode == "stats") rc = cmd_stats(argc, argv);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_driver: %s\n", e.what());
     return 1;

@@ -28,7 +28,8 @@ EXPORTS = (
     "pbbgpu_stats", "pbbgpu_histogram", "pbbgpu_decompose_batch", "pbbgpu_solve", "pbbgpu_int32_peak",
     "pbbgpu_assign_split_range", "pbbgpu_export", "pbbgpu_debug_state", "pbbgpu_assign_split_strided",
     "pbbgpu_insertion_ls", "pbbgpu_offer_schedule", "pbbgpu_promote", "pbbgpu_explorer_lengths",
-    "pbbgpu_best_schedule", "pbbgpu_snapshot_ex",
+    "pbbgpu_best_schedule", "pbbgpu_snapshot_ex", "pbbgpu_apply_work_update", "pbbgpu_improved_since_mark",
+    "pbbgpu_steals_since_mark", "pbbgpu_reset_steal_mark", "pbbgpu_take_census", "pbbgpu_flush_timeline",
 )
 
 
@@ -48,6 +49,10 @@ class Config(ctypes.Structure):
         ("rounds_per_sync", ctypes.c_int),
         ("max_split", ctypes.c_int),
         ("split_mode", ctypes.c_int),
+        ("steal_policy", ctypes.c_int),
+        ("record_census", ctypes.c_int),
+        ("census_cap", ctypes.c_int),
+        ("timeline_path", ctypes.c_char_p),
     ]
 
 
@@ -124,6 +129,12 @@ def load() -> ctypes.CDLL:
         "pbbgpu_best": (ctypes.c_int, [P, i64p, i32p, ip]),
         "pbbgpu_best_schedule": (ctypes.c_int, [P, i64p, i32p, ip]),
         "pbbgpu_snapshot_ex": (ctypes.c_int, [P, u16p, u16p, u8p, ctypes.c_int, ip, u64p]),
+        "pbbgpu_apply_work_update": (ctypes.c_int, [P, u16p, u16p, u8p, ctypes.c_int]),
+        "pbbgpu_improved_since_mark": (ctypes.c_int, [P, ip]),
+        "pbbgpu_steals_since_mark": (ctypes.c_int, [P, u64p]),
+        "pbbgpu_reset_steal_mark": (ctypes.c_int, [P]),
+        "pbbgpu_take_census": (ctypes.c_int, [P, u64p, ctypes.c_int64, i64p]),
+        "pbbgpu_flush_timeline": (ctypes.c_int, [P]),
         "pbbgpu_offer_bound": (ctypes.c_int, [P, ctypes.c_int64]),
         "pbbgpu_stats": (ctypes.c_int, [P, ctypes.POINTER(Stats)]),
         "pbbgpu_histogram": (ctypes.c_int, [P, u64p, ctypes.c_int]),

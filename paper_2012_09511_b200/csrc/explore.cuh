@@ -788,7 +788,8 @@ template <int M, int G>
 __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, const InstView& in,
                                      int n, int mp, int sel, int level, int d1, int d2,
                                      int improve, DevCounters* ctr, ImpRecord* imp,
-                                     StepCounters& sc) {
+                                     StepCounters& sc, unsigned long long* census = nullptr,
+                                     int census_cap = 0) {
   int8_t* row = iv.cells + tri_off(level, n);
   const int x = row[sel];
   const int job = (x < 0 ? -x : x) - 1;
@@ -818,6 +819,12 @@ __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, con
     }
     row[sel] = static_cast<int8_t>(x < 0 ? x : -x);  // prune_current
     ++sc.leaves;
+    if (census) {  // census->push_back(ivm.position_u64()) (src/explorer.cpp:47)
+      unsigned long long pos = 0;
+      for (int l = 0; l < n; ++l) pos = pos * static_cast<unsigned long long>(n - l) + (l <= level ? iv.V[l] : 0);
+      const unsigned slot = atomicAdd(&ctr->census_count, 1u);
+      if (static_cast<int>(slot) < census_cap) census[slot] = pos;
+    }
     if (mk < improve) {
       const int old = atomicMin(&ctr->best, mk);
       if (mk < old) {
@@ -1027,6 +1034,7 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
     int level = iv.hdr->level, state = iv.hdr->state, d1 = iv.hdr->d1, d2 = iv.hdr->d2;
     int rlev = iv.hdr->rlev, nrep = iv.hdr->nrep;
     const bool has_end = iv.hdr->has_end != 0;
+    if (grp.g == 0 && state != kEmpty) atomicAdd(reinterpret_cast<unsigned*>(smem + IL.o_cnt) + 6, 1u);
     int best = grp.bcast(grp.g == 0 ? *reinterpret_cast<volatile int*>(&P.ctr->best) : 0, 0);
     int step = 0;
     unsigned long long t_end = ~0ull;
@@ -1043,7 +1051,9 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
       const int improve = P.prune_mode == 1 ? 0 : best;
       ++sc.steps;
       if (state == kInit) {
-        // one replay level of init_at (src/ivm.cpp:70-86)
+        // one replay level of init_at (src/ivm.cpp:70-86); under the reference steal policy the
+        // replay is part of the steal phase (synchronous there), not of the round's batch steps
+        step -= P.free_replay;
         const int l = rlev;
         const int digit = iv.tgt[l];
         int8_t* row = iv.cells + tri_off(l, n);
@@ -1081,7 +1091,7 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
         break;
       }
       if (n - 1 - level <= 1) {
-        leaf<M, G>(grp, iv, in, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc);
+        leaf<M, G>(grp, iv, in, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc, P.census, P.census_cap);
         continue;
       }
       decompose_branch<M, G, BOUND, SMALLN>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist);
@@ -1126,6 +1136,7 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
         atomicAdd(&P.ctr->steals, static_cast<unsigned long long>(cnt[5]));
         atomicAdd(&P.ctr->inits, static_cast<unsigned long long>(cnt[5]));
       }
+      if (cnt[6]) atomicAdd(&P.ctr->round_live, static_cast<int>(cnt[6]));
     }
     for (int i = threadIdx.x; i <= n; i += blockDim.x) {
       if (shist[i]) atomicAdd(&P.hist[i], static_cast<unsigned long long>(shist[i]));

@@ -56,6 +56,8 @@ struct DevCounters {
   int active;                      // explorers not Empty after the last steal phase
   int imp_count;                   // improvement records written this round
   int best;                        // device incumbent (makespan units)
+  int round_live;                  // explorers not Empty when the last explore launch started
+  unsigned int census_count;       // leaf positions recorded (record_census)
   int pad;
 };
 
@@ -87,6 +89,9 @@ struct ExploreParams {
   ImpRecord* imp;             // [kImpCap]
   int smem_inst_bytes;        // bytes of the per-CTA instance region
   unsigned long long budget_ns;  // round length in device time (0 = steps only)
+  int free_replay;            // init_at replay levels do not consume steps (reference policy)
+  int census_cap;             // record_census: capacity of `census` (0 = off)
+  unsigned long long* census; // leaf positions as decimals (position_u64, explorer.cpp:47)
 };
 
 }  // namespace pbbgpu

@@ -610,6 +610,8 @@ __global__ void split_victims_kernel(IvmLayout L, unsigned char* state, const in
   reinterpret_cast<IvmHdr*>(vb)->has_end = 1;
 }
 
+#include "steal_ref.cuh"
+
 // Steal phase (src/explorer.cpp:283-340, B200 form). The explore kernel leaves one float per
 // explorer in S.lens (log2 of its remaining leaves from the effective position, -2 busy /
 // not splittable, -3 idle), so this single CTA only scans that array: idle explorers
@@ -1020,6 +1022,22 @@ struct pbbgpu_pool {
   size_t scr_cap[8] = {};
   void* pin = nullptr;  // pinned host staging for table uploads (grow-only)
   size_t pin_cap = 0;
+  // the reference steal policy (steal_policy = 1): exact lengths, flags, pairs
+  u128* d_ref_len = nullptr;
+  uint8_t* d_ref_flags = nullptr;
+  int* d_ref_pairs = nullptr;
+  u128 ref_min_steal = 0;
+  // record_census
+  unsigned long long* d_census = nullptr;
+  int census_cap = 0;
+  // activity timeline (explorer.cpp:71-85, 448-471)
+  FILE* timeline = nullptr;
+  std::chrono::steady_clock::time_point t_start{}, t_last_sample{};
+  bool sampled = false;
+  // marks (explorer.hpp:94-96)
+  int64_t improvement_mark = INT64_MAX;
+  uint64_t steal_mark = 0;
+  uint64_t host_improvements = 0;  // offer_schedule improvements of the bound (explorer.cpp:379-386)
 
   void release() {
     TraceScope ts("release");
@@ -1049,6 +1067,11 @@ struct pbbgpu_pool {
     cudaFree(d_hist);
     cudaFree(d_dhist);
     cudaFree(d_imp);
+    cudaFree(d_ref_len);
+    cudaFree(d_ref_flags);
+    cudaFree(d_ref_pairs);
+    cudaFree(d_census);
+    if (timeline) std::fclose(timeline);
     if (h_ctr) cudaFreeHost(h_ctr);
     if (pin) cudaFreeHost(pin);
     for (cudaEvent_t e : evs)
@@ -1211,6 +1234,9 @@ void reset_search(pbbgpu_pool* P) {
   P->best_sched.clear();
   P->pending_offer.store(INT64_MAX);
   P->last_active = 0;
+  P->improvement_mark = INT64_MAX;
+  P->steal_mark = 0;
+  P->host_improvements = 0;
 }
 
 void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const pbbgpu_config_t* cfg) {
@@ -1218,6 +1244,9 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   if (m != 5 && m != 10 && m != 20) throw std::invalid_argument("pbbgpu: m must be 5, 10 or 20 (compiled machine counts)");
   if (bound != kLB1 && bound != kLB2) throw std::invalid_argument("pbbgpu: bound must be PBBGPU_LB1 or PBBGPU_LB2");
   validate_times(n, m, p);
+  if (cfg && cfg->record_census && n > 20) throw std::invalid_argument("record_census needs n <= 20 (position_u64)");
+  if (cfg && cfg->steal_policy == 1 && n > 30) throw std::invalid_argument("the reference steal policy needs n <= 30");
+  if (cfg && (cfg->steal_policy < 0 || cfg->steal_policy > 1)) throw std::invalid_argument("steal_policy must be 0 or 1");
   P->n = n;
   P->m = m;
   P->bound = bound;
@@ -1346,6 +1375,7 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
     P->K = per_sm * prop.multiProcessorCount * NGb;
   }
   P->grid = (P->K + NGb - 1) / NGb;
+  if (P->cfg.steal_policy == 1 && P->cfg.steps_per_round <= 0) P->cfg.steps_per_round = 1024;  // batch_steps
   P->steps = P->cfg.steps_per_round > 0 ? P->cfg.steps_per_round : (1 << 30);
   // warp explorers (LB2) take tens of us per step: longer rounds amortize the round-end wait
   P->round_us = P->cfg.round_us > 0 ? P->cfg.round_us : (P->cfg.steps_per_round > 0 ? 0.0 : (P->G == 32 ? 2500.0 : 2000.0));
@@ -1361,6 +1391,29 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   ck(cudaMalloc(&P->d_hist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
   ck(cudaMalloc(&P->d_dhist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
   ck(cudaMalloc(&P->d_imp, kImpCap * sizeof(ImpRecord)), "malloc");
+  if (P->cfg.steal_policy == 1) {
+    ck(cudaMalloc(&P->d_ref_len, static_cast<size_t>(P->K) * sizeof(u128)), "malloc");
+    ck(cudaMalloc(&P->d_ref_flags, static_cast<size_t>(P->K)), "malloc");
+    ck(cudaMalloc(&P->d_ref_pairs, static_cast<size_t>(P->K) * 3 * sizeof(int)), "malloc");
+    // min_steal_len = min(8!, ceil(n!/4K)) (explorer.cpp:96-103), or the configured length
+    u128 nf = 1;
+    for (int i = 2; i <= n; ++i) nf *= static_cast<u128>(i);
+    const u128 div = static_cast<u128>(4) * static_cast<u128>(P->K);
+    const u128 quarter = (nf + div - 1) / div;
+    P->ref_min_steal = quarter < static_cast<u128>(40320) ? quarter : static_cast<u128>(40320);
+    if (P->cfg.min_steal_log2 > 0) P->ref_min_steal = static_cast<u128>(std::llround(std::exp2(P->cfg.min_steal_log2)));
+  }
+  if (P->cfg.record_census) {
+    P->census_cap = P->cfg.census_cap > 0 ? P->cfg.census_cap : (1 << 20);
+    ck(cudaMalloc(&P->d_census, static_cast<size_t>(P->census_cap) * sizeof(unsigned long long)), "malloc census");
+  }
+  if (P->cfg.timeline_path && *P->cfg.timeline_path) {
+    P->timeline = std::fopen(P->cfg.timeline_path, "w");
+    if (!P->timeline) throw std::runtime_error(std::string("cannot open timeline file: ") + P->cfg.timeline_path);
+    std::fputs("timestamp_ms,explorer_id,active,interval_length_log2\n", P->timeline);
+  }
+  P->cfg.timeline_path = nullptr;  // the caller's string is not kept
+  P->t_start = std::chrono::steady_clock::now();
   put(P, P->d_lgfact, lgf);
   upload_tables(P, T);
   reset_search(P);
@@ -1437,7 +1490,9 @@ ExploreParams explore_params(pbbgpu_pool* P) {
   E.imp = P->d_imp;
   E.smem_inst_bytes = P->IL.bytes;
   E.budget_ns = static_cast<unsigned long long>(P->round_us * 1000.0);
-
+  E.free_replay = P->cfg.steal_policy == 1 ? 1 : 0;
+  E.census = P->d_census;
+  E.census_cap = P->census_cap;
 
   return E;
 }
@@ -1502,6 +1557,103 @@ int count_active_host(pbbgpu_pool* P) {
   return P->K - cnt;
 }
 
+// ---- host views of explorer blocks (snapshot, timeline, work updates)
+std::vector<unsigned char> download_state(pbbgpu_pool* P) {
+  std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
+  xfer(P, st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost, "state copy");
+  return st;
+}
+
+// Remaining work of an explorer block: [pos, end), pos the effective position (a parked
+// explorer's consumed cell excluded, as pbbgpu_snapshot reports it; kInit: the replay target).
+// False when nothing remains.
+// raw = the reference's position() (zero-padded V, ivm.cpp:180-184) instead of the effective one.
+bool block_span(const pbbgpu_pool* P, const unsigned char* blk, std::vector<int>& pos, std::vector<int>& end,
+                bool& end_nf, bool raw = false) {
+  const int n = P->n;
+  const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
+  if (h->state == kEmpty) return false;
+  const int8_t* V = reinterpret_cast<const int8_t*>(blk + P->L.o_v);
+  const int8_t* E = reinterpret_cast<const int8_t*>(blk + P->L.o_end);
+  const int8_t* T = reinterpret_cast<const int8_t*>(blk + P->L.o_tgt);
+  const int8_t* C = reinterpret_cast<const int8_t*>(blk + P->L.o_cells);
+  pos.assign(static_cast<size_t>(n), 0);
+  end.assign(static_cast<size_t>(n), 0);
+  for (int l = 0; l < n; ++l) pos[static_cast<size_t>(l)] = h->state == kInit ? T[l] : (l <= h->level ? V[l] : 0);
+  if (!raw && h->state == kActive && h->level >= 0 && C[tri_off(h->level, n) + V[h->level]] <= 0) {
+    int l = h->level;
+    for (; l >= 0; --l) {
+      if (++pos[static_cast<size_t>(l)] <= n - 1 - l) break;
+      pos[static_cast<size_t>(l)] = 0;
+    }
+    if (l < 0) return false;
+  }
+  end_nf = !h->has_end;
+  for (int l = 0; l < n; ++l) end[static_cast<size_t>(l)] = h->has_end ? E[l] : 0;
+  if (!end_nf) {
+    int cmp = 0;
+    for (int l = 0; l < n && !cmp; ++l) cmp = pos[static_cast<size_t>(l)] < end[static_cast<size_t>(l)] ? -1 : (pos[static_cast<size_t>(l)] > end[static_cast<size_t>(l)] ? 1 : 0);
+    if (cmp >= 0) return false;
+  }
+  return true;
+}
+
+// floor(log2(end - pos)) exactly (multi-word): to_decimal by Horner in base 2^32 limbs.
+long exact_log2_len(const std::vector<int>& pos, const std::vector<int>& end, bool end_nf, int n) {
+  auto big = [n](const std::vector<int>* d, bool nfact) {
+    std::vector<uint32_t> v(1, 0);
+    auto mul_add = [&v](uint32_t mul, uint32_t add) {
+      uint64_t carry = add;
+      for (uint32_t& w : v) {
+        const uint64_t x = static_cast<uint64_t>(w) * mul + carry;
+        w = static_cast<uint32_t>(x);
+        carry = x >> 32;
+      }
+      if (carry) v.push_back(static_cast<uint32_t>(carry));
+    };
+    if (nfact) {
+      v[0] = 1;
+      for (int i = 2; i <= n; ++i) mul_add(static_cast<uint32_t>(i), 0);
+    } else {
+      for (int l = 0; l < n; ++l) mul_add(static_cast<uint32_t>(n - l), static_cast<uint32_t>((*d)[static_cast<size_t>(l)]));
+    }
+    return v;
+  };
+  std::vector<uint32_t> e = big(&end, end_nf), p = big(&pos, false);
+  p.resize(std::max(p.size(), e.size()), 0);
+  e.resize(p.size(), 0);
+  int64_t borrow = 0;
+  for (size_t i = 0; i < e.size(); ++i) {
+    int64_t x = static_cast<int64_t>(e[i]) - p[i] - borrow;
+    borrow = x < 0;
+    if (borrow) x += int64_t(1) << 32;
+    e[i] = static_cast<uint32_t>(x);
+  }
+  if (borrow) return -1;
+  for (size_t i = e.size(); i-- > 0;)
+    if (e[i]) return static_cast<long>(32 * i + 31 - __builtin_clz(e[i]));
+  return -1;
+}
+
+// sample_timeline (src/explorer.cpp:448-464): one row per explorer, >= 50 ms apart unless forced.
+void sample_timeline(pbbgpu_pool* P, bool force) {
+  const auto now = std::chrono::steady_clock::now();
+  if (!force && P->sampled && now - P->t_last_sample < std::chrono::milliseconds(50)) return;
+  P->sampled = true;
+  P->t_last_sample = now;
+  const long long ts = std::chrono::duration_cast<std::chrono::milliseconds>(now - P->t_start).count();
+  const std::vector<unsigned char> st = download_state(P);
+  std::vector<int> pos, end;
+  for (int i = 0; i < P->K; ++i) {
+    const unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
+    const bool active = reinterpret_cast<const IvmHdr*>(blk)->state != kEmpty;
+    bool nf = false;
+    long lg = -1;
+    if (active && block_span(P, blk, pos, end, nf, true)) lg = exact_log2_len(pos, end, nf, P->n);
+    std::fprintf(P->timeline, "%lld,%d,%d,%ld\n", ts, i, active ? 1 : 0, lg);
+  }
+}
+
 int run_round(pbbgpu_pool* P) {
   if (P->batch_only) throw StateError("pbbgpu: n > 64 pools are bounding-only (decompose_batch); exploration needs n <= 64");
   const int64_t offer = P->pending_offer.exchange(INT64_MAX);
@@ -1536,11 +1688,31 @@ int run_round(pbbgpu_pool* P) {
   // several (explore, steal) rounds back to back per host synchronization: the rounds are
   // device-timed, and a round after exhaustion costs only the state copy of an empty launch
   const int R = P->rounds_per_sync;
+  StealRefParams SR{};
+  if (P->cfg.steal_policy == 1) {
+    SR.L = P->L;
+    SR.state = P->d_state;
+    SR.K = P->K;
+    SR.ptot = P->d_ptot;
+    SR.ctr = P->d_ctr;
+    SR.len = P->d_ref_len;
+    SR.flags = P->d_ref_flags;
+    SR.pairs = P->d_ref_pairs;
+    SR.order = P->d_ref_pairs + 2 * P->K;
+    SR.min_steal = P->ref_min_steal;
+  }
   for (int r = 0; r < R; ++r) {
     ck(cudaEventRecord(P->evs[3 * r], P->stream), "event");
     P->efn<<<P->grid, P->block, P->smem, P->stream>>>(E);
     ck(cudaGetLastError(), "explore_kernel launch");
     ck(cudaEventRecord(P->evs[3 * r + 1], P->stream), "event");
+    if (P->cfg.steal_policy == 1) {  // the reference's steal_phase (explorer.cpp:251-340)
+      steal_ref_kernel<<<1, kRefThreads, 0, P->stream>>>(SR);
+      ck(cudaGetLastError(), "steal_ref_kernel launch");
+      ck(cudaEventRecord(P->evs[3 * r + 2], P->stream), "event");
+      P->launches += 2;
+      continue;
+    }
     lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, S.split_mode);
     ck(cudaGetLastError(), "lens_kernel launch");
     steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
@@ -1564,6 +1736,7 @@ int run_round(pbbgpu_pool* P) {
   P->rounds += static_cast<uint64_t>(R);
   harvest(P);
   P->last_active = P->h_ctr->active;
+  if (P->timeline) sample_timeline(P, P->h_ctr->active == 0);
   return P->h_ctr->active;
 }
 
@@ -1728,6 +1901,7 @@ int pbbgpu_set_initial_bound(pbbgpu_pool* P, int64_t ub, const int32_t* sched, i
         P->best_sched_value = INT64_MAX;
       }
       P->pinned_ub = ub;
+      P->improvement_mark = ub;  // explorer.cpp:112-120
       // a stale offer (e.g. a MIN exchanged at the end of the previous solve) must not lower
       // the new bound below a value that has no schedule behind it
       P->pending_offer.store(INT64_MAX);
@@ -2187,7 +2361,10 @@ int pbbgpu_offer_schedule(pbbgpu_pool* P, const int32_t* perm, int64_t cmax, int
     }
     {
       std::scoped_lock lk(P->best_mu);  // run_round updates best_value under the same lock
-      if (cmax < P->best_value) took = true;
+      if (cmax < P->best_value) {
+        took = true;
+        ++P->host_improvements;  // explorer.cpp:383-386
+      }
     }
     if (taken) *taken = took ? 1 : 0;
   });
@@ -2277,7 +2454,7 @@ int pbbgpu_stats(pbbgpu_pool* P, pbbgpu_stats_t* out) {
     out->replay_dups = c.dups;
     out->unique = c.decomposed - c.dups;
     out->leaves = c.leaves;
-    out->improvements = c.improvements;
+    out->improvements = c.improvements + P->host_improvements;
     out->local_steals = c.steals;
     out->steal_phases = c.steal_phases;
     out->intervals_initialized = c.inits;
@@ -2424,6 +2601,244 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
         if (lb_bwd) lb_bwd[s] = lbw[s];
       }
     }
+  });
+}
+
+// ---- apply_work_update (src/explorer.cpp:162-199) on factoradic digit intervals: BigCount
+// comparisons are lexicographic digit comparisons; an end of n! is a flag (greater than any
+// digit vector). normalize / intersect_units / subtract_units follow src/workunit.cpp:8-51 and
+// src/explorer.cpp:143-160.
+namespace {
+struct DInterval {
+  std::vector<int> a, b;
+  bool b_nf;
+};
+int dcmp(const std::vector<int>& x, const std::vector<int>& y) {
+  for (size_t l = 0; l < x.size(); ++l)
+    if (x[l] != y[l]) return x[l] < y[l] ? -1 : 1;
+  return 0;
+}
+// point comparison with the n! flag
+int pcmp(const std::vector<int>& x, bool xnf, const std::vector<int>& y, bool ynf) {
+  if (xnf || ynf) return xnf == ynf ? 0 : (xnf ? 1 : -1);
+  return dcmp(x, y);
+}
+bool dempty(const DInterval& iv) { return pcmp(iv.a, false, iv.b, iv.b_nf) >= 0; }
+
+std::vector<DInterval> dnormalize(std::vector<DInterval> ivs) {
+  ivs.erase(std::remove_if(ivs.begin(), ivs.end(), dempty), ivs.end());
+  std::sort(ivs.begin(), ivs.end(), [](const DInterval& x, const DInterval& y) {
+    const int c = dcmp(x.a, y.a);
+    if (c) return c < 0;
+    return pcmp(x.b, x.b_nf, y.b, y.b_nf) < 0;
+  });
+  std::vector<DInterval> out;
+  for (DInterval& iv : ivs) {
+    if (!out.empty() && pcmp(iv.a, false, out.back().b, out.back().b_nf) < 0) {
+      if (pcmp(iv.b, iv.b_nf, out.back().b, out.back().b_nf) > 0) {
+        out.back().b = iv.b;
+        out.back().b_nf = iv.b_nf;
+      }
+    } else {
+      out.push_back(std::move(iv));
+    }
+  }
+  return out;
+}
+
+std::vector<DInterval> dintersect(const std::vector<DInterval>& A, const std::vector<DInterval>& B) {
+  std::vector<DInterval> out;
+  size_t i = 0, j = 0;
+  while (i < A.size() && j < B.size()) {
+    const std::vector<int>& lo = dcmp(A[i].a, B[j].a) > 0 ? A[i].a : B[j].a;
+    const bool a_hi = pcmp(A[i].b, A[i].b_nf, B[j].b, B[j].b_nf) < 0;
+    const DInterval& h = a_hi ? A[i] : B[j];
+    if (pcmp(lo, false, h.b, h.b_nf) < 0) out.push_back({lo, h.b, h.b_nf});
+    if (pcmp(A[i].b, A[i].b_nf, B[j].b, B[j].b_nf) <= 0) ++i;
+    else ++j;
+  }
+  return out;
+}
+
+std::vector<DInterval> dsubtract(const std::vector<DInterval>& A, const std::vector<DInterval>& B) {
+  std::vector<DInterval> out;
+  for (const DInterval& iv : A) {
+    std::vector<int> cur = iv.a;
+    bool cur_nf = false;
+    for (const DInterval& c : B) {
+      if (pcmp(c.b, c.b_nf, cur, cur_nf) <= 0) continue;
+      if (pcmp(c.a, false, iv.b, iv.b_nf) >= 0) break;
+      if (pcmp(c.a, false, cur, cur_nf) > 0) out.push_back({cur, c.a, false});
+      cur = c.b;
+      cur_nf = c.b_nf;
+      if (pcmp(cur, cur_nf, iv.b, iv.b_nf) >= 0) break;
+    }
+    if (pcmp(cur, cur_nf, iv.b, iv.b_nf) < 0) out.push_back({cur, iv.b, iv.b_nf});
+  }
+  return out;
+}
+}  // namespace
+
+int pbbgpu_apply_work_update(pbbgpu_pool* P, const uint16_t* a, const uint16_t* b, const uint8_t* nf, int count) {
+  return guarded([&] {
+    if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
+    if (count < 0) throw std::invalid_argument("negative interval count");
+    if (count > P->K) throw std::invalid_argument("work update holds more intervals than explorers");
+    const int n = P->n;
+    std::vector<DInterval> incoming;
+    for (int i = 0; i < count; ++i) {
+      check_digits(n, a + static_cast<size_t>(i) * n);
+      const bool inf = nf && nf[i];
+      if (!inf) check_digits(n, b + static_cast<size_t>(i) * n);
+      DInterval iv{std::vector<int>(a + static_cast<size_t>(i) * n, a + static_cast<size_t>(i + 1) * n),
+                   std::vector<int>(static_cast<size_t>(n), 0), inf};
+      if (!inf) iv.b.assign(b + static_cast<size_t>(i) * n, b + static_cast<size_t>(i + 1) * n);
+      if (pcmp(iv.a, false, iv.b, iv.b_nf) > 0) throw std::invalid_argument("interval with a > b");
+      incoming.push_back(std::move(iv));
+    }
+    incoming = dnormalize(std::move(incoming));
+    std::vector<unsigned char> st = download_state(P);
+    std::vector<DInterval> kept;
+    std::vector<int> idle;
+    std::vector<unsigned long long> extra(static_cast<size_t>(n) + 1, 0);  // replay dups by f
+    unsigned long long extra_dups = 0;
+    // explorers re-seated from scratch: their start and the levels [lo, hi) whose path nodes
+    // they have already counted (pbbgpu_snapshot_ex's recount), plus the dups a partial replay
+    // would have been discounted had it finished (levels [0, min(nrep, lz)))
+    struct Reset {
+      std::vector<int> start;
+      int lo, hi, lzcut;
+    };
+    std::vector<Reset> resets;
+    std::vector<int> pos, end;
+    for (int i = 0; i < P->K; ++i) {
+      unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
+      IvmHdr* h = reinterpret_cast<IvmHdr*>(blk);
+      if (h->state == kEmpty) {
+        idle.push_back(i);
+        continue;
+      }
+      bool end_nf = false;
+      std::vector<DInterval> mine;
+      const bool has_span = block_span(P, blk, pos, end, end_nf);
+      if (has_span) mine = dintersect(incoming, {{pos, end, end_nf}});
+      if (mine.size() == 1 && dcmp(mine[0].a, pos) == 0) {
+        if (pcmp(mine[0].b, mine[0].b_nf, end, end_nf) < 0) {  // shrink_end (ivm.cpp:186-189)
+          int8_t* E = reinterpret_cast<int8_t*>(blk + P->L.o_end);
+          for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(mine[0].b[static_cast<size_t>(l)]);
+          h->has_end = 1;
+        }
+        kept.push_back(std::move(mine[0]));
+      } else {
+        if (has_span) {
+          const int8_t* V = reinterpret_cast<const int8_t*>(blk + P->L.o_v);
+          const int8_t* C = reinterpret_cast<const int8_t*>(blk + P->L.o_cells);
+          int lnz = 0;
+          for (int l = 0; l < n; ++l)
+            if (pos[static_cast<size_t>(l)] != 0) lnz = l;
+          if (h->state == kInit) {
+            resets.push_back({pos, 0, h->nrep, std::min<int>(h->nrep, lnz)});
+          } else if (C[tri_off(h->level, n) + V[h->level]] > 0) {  // not parked
+            resets.push_back({pos, lnz, std::max<int>(lnz, h->level), 0});
+          }
+        }
+        h->state = kEmpty;
+        h->level = -1;
+        idle.push_back(i);
+      }
+    }
+    kept = dnormalize(std::move(kept));
+    const std::vector<DInterval> to_place = dsubtract(incoming, kept);
+    if (to_place.size() > idle.size()) throw CapacityError("work update fragments exceed explorer capacity");
+    // a fragment re-seated exactly at a reset explorer's start replays the path nodes that
+    // explorer already counted: discount them (the same recount as pbbgpu_snapshot_ex); a
+    // partial replay not re-seated there keeps only its first-leaf-owned nodes
+    for (const Reset& r : resets) {
+      bool reseated = false;
+      for (const DInterval& f : to_place)
+        if (dcmp(f.a, r.start) == 0) reseated = true;
+      const int lo = reseated ? r.lo : 0, hi = reseated ? r.hi : r.lzcut;
+      for (int l = lo; l < hi; ++l) {
+        ++extra_dups;
+        ++extra[static_cast<size_t>(n - 1 - l)];
+      }
+    }
+    xfer(P, P->d_state, st.data(), st.size(), cudaMemcpyHostToDevice, "state copy");
+    if (extra_dups) {
+      read_counters(P);
+      const unsigned long long d = P->h_ctr->dups + extra_dups;
+      xfer(P, reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, dups), &d, sizeof(d), cudaMemcpyHostToDevice, "copy");
+      std::vector<unsigned long long> dh(static_cast<size_t>(n) + 1);
+      xfer(P, dh.data(), P->d_dhist, dh.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, "copy");
+      for (int f = 0; f <= n; ++f) dh[static_cast<size_t>(f)] += extra[static_cast<size_t>(f)];
+      xfer(P, P->d_dhist, dh.data(), dh.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, "copy");
+    }
+    std::sort(idle.begin(), idle.end());
+    std::vector<int> da, db, slots;
+    std::vector<uint8_t> dn;
+    for (size_t i = 0; i < to_place.size(); ++i) {
+      da.insert(da.end(), to_place[i].a.begin(), to_place[i].a.end());
+      if (to_place[i].b_nf) db.insert(db.end(), static_cast<size_t>(n), 0);
+      else db.insert(db.end(), to_place[i].b.begin(), to_place[i].b.end());
+      dn.push_back(to_place[i].b_nf ? 1 : 0);
+      slots.push_back(idle[i]);
+    }
+    assign_digits(P, da, db, dn, slots);
+    read_counters(P);
+    P->last_active = static_cast<int>(P->K - idle.size() + to_place.size());
+  });
+}
+
+int pbbgpu_improved_since_mark(pbbgpu_pool* P, int* improved) {
+  return guarded([&] {
+    std::scoped_lock lk(P->best_mu);
+    *improved = 0;
+    if (P->best_sched_value < P->improvement_mark) {
+      P->improvement_mark = P->best_sched_value;
+      *improved = 1;
+    }
+  });
+}
+
+int pbbgpu_steals_since_mark(pbbgpu_pool* P, uint64_t* steals) {
+  return guarded([&] {
+    if (P->batch_only) {
+      *steals = 0;
+      return;
+    }
+    read_counters(P);
+    *steals = P->h_ctr->steals - P->steal_mark;
+  });
+}
+
+int pbbgpu_reset_steal_mark(pbbgpu_pool* P) {
+  return guarded([&] {
+    if (P->batch_only) return;
+    read_counters(P);
+    P->steal_mark = P->h_ctr->steals;
+  });
+}
+
+int pbbgpu_take_census(pbbgpu_pool* P, uint64_t* out, int64_t cap, int64_t* count) {
+  return guarded([&] {
+    *count = 0;
+    if (!P->d_census) throw StateError("take_census: the pool was created without record_census");
+    read_counters(P);
+    const int64_t c = P->h_ctr->census_count;
+    if (c > P->census_cap) throw CapacityError("census buffer overflow: raise census_cap or take the census more often");
+    if (c > cap) throw CapacityError("take_census: output buffer too small");
+    if (c > 0) xfer(P, out, P->d_census, static_cast<size_t>(c) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, "census copy");
+    const unsigned zero = 0;
+    xfer(P, reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, census_count), &zero, sizeof(zero), cudaMemcpyHostToDevice, "copy");
+    *count = c;
+  });
+}
+
+int pbbgpu_flush_timeline(pbbgpu_pool* P) {
+  return guarded([&] {
+    if (!P->timeline) return;
+    sample_timeline(P, true);
+    std::fflush(P->timeline);
   });
 }
 

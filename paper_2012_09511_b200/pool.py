@@ -47,6 +47,10 @@ class PoolConfig:
     rounds_per_sync: int = 0    # device rounds per run_round() call; 0 = 3
     max_split: int = 0          # thieves per victim per steal phase (multi-way split); 0 = 4
     split_mode: int = 0         # 0 = factoradic (reference), 1 = live siblings, 2 = live else factoradic
+    steal_policy: int = 0       # 0 = B200 policy; 1 = the reference's steal_phase exactly (explorer.cpp:251-340)
+    record_census: bool = False  # PoolConfig.record_census: leaf positions (n <= 20), take_census()
+    census_cap: int = 0         # census entries held between take_census calls; 0 = 2^20
+    timeline_path: str = ""     # PoolConfig.timeline_path: activity CSV written by the pool
 
     def to_c(self) -> _lib.Config:
         c = _lib.Config()
@@ -64,7 +68,10 @@ class PoolConfig:
         c.rounds_per_sync = self.rounds_per_sync
         c.max_split = self.max_split
         c.split_mode = self.split_mode
-
+        c.steal_policy = self.steal_policy
+        c.record_census = int(self.record_census)
+        c.census_cap = self.census_cap
+        c.timeline_path = self.timeline_path.encode() if self.timeline_path else None
         return c
 
 
@@ -250,6 +257,48 @@ class GpuPool:
             return
         _lib.check(self._lib.pbbgpu_assign(self._h, a.ctypes.data_as(_u16p), b.ctypes.data_as(_u16p),
                                            nf.ctypes.data_as(_u8p), len(nf)))
+
+    def apply_work_update(self, intervals: Sequence[Interval]) -> None:
+        """apply_work_update (explorer.cpp:162-199): adopt a coordinator's interval set; explorers
+        whose remaining work starts the same keep their state (end shrunk), the rest go idle,
+        the new parts are seated on idle explorers."""
+        if len(intervals) > self.K():
+            raise ValueError("work update holds more intervals than explorers")
+        for lo, hi in intervals:
+            if lo > hi:
+                raise ValueError("interval with a > b")
+        ivs = [(a, b) for a, b in intervals if a < b]
+        a, b, inf = _digits(ivs, self.inst.n) if ivs else (np.zeros((0, self.inst.n), np.uint16),) * 2 + (
+            np.zeros(0, np.uint8),)
+        _lib.check(self._lib.pbbgpu_apply_work_update(self._h, a.ctypes.data_as(_u16p), b.ctypes.data_as(_u16p),
+                                                      inf.ctypes.data_as(_u8p), len(ivs)))
+
+    def improved_since_mark(self) -> bool:
+        """improved_since_mark (explorer.hpp:94): the best schedule improved; resets the mark."""
+        v = ctypes.c_int()
+        _lib.check(self._lib.pbbgpu_improved_since_mark(self._h, ctypes.byref(v)))
+        return bool(v.value)
+
+    def steals_since_mark(self) -> int:
+        v = ctypes.c_uint64()
+        _lib.check(self._lib.pbbgpu_steals_since_mark(self._h, ctypes.byref(v)))
+        return int(v.value)
+
+    def reset_steal_mark(self) -> None:
+        _lib.check(self._lib.pbbgpu_reset_steal_mark(self._h))
+
+    def take_census(self) -> List[int]:
+        """take_census (explorer.hpp:102): leaf positions recorded since the last call."""
+        cap = self.cfg.census_cap or (1 << 20)
+        buf = np.zeros(cap, dtype=np.uint64)
+        cnt = ctypes.c_int64()
+        _lib.check(self._lib.pbbgpu_take_census(self._h, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), cap,
+                                                ctypes.byref(cnt)))
+        return [int(x) for x in buf[:cnt.value]]
+
+    def flush_timeline(self) -> None:
+        """flush_timeline (explorer.hpp:103): forced sample + flush of the pool's timeline CSV."""
+        _lib.check(self._lib.pbbgpu_flush_timeline(self._h))
 
     def run_round(self) -> int:
         act = ctypes.c_int()

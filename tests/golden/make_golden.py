@@ -34,6 +34,14 @@ def main():
         counts[f"neh:{name}"] = json.loads(run("neh", name))
     for name, iters, seed in (("ta001", 2000, 7), ("ta021", 2000, 11), ("ta041", 500, 3), ("ta056", 300, 5)):
         counts[f"ils:{name}"] = json.loads(run("ils", name, iters, seed))
+    # every PoolStats field of pool_run (K explorers, batch_steps, fixed tree or pruning disabled):
+    # the reference steal policy on the GPU must reproduce these exactly
+    for inst, ub, K, bs, nopr in (("ta011", 1582, 16, 1024, 0), ("ta011", 1582, 64, 1024, 0),
+                                  ("ta011", 1582, 48, 1024, 0), ("ta011", 1582, 256, 1024, 0),
+                                  ("ta011", 1582, 20, 256, 0), ("ta001", 1278, 16, 1024, 0),
+                                  ("ta001", 1278, 4, 8, 0), ("gen:8:5:4242", 100000, 16, 64, 1),
+                                  ("gen:9:5:77", 100000, 64, 128, 1), ("gen:9:10:78", 100000, 12, 200, 1)):
+        counts[f"stats:{inst}@{ub}:K{K}:b{bs}:np{nopr}"] = json.loads(run("stats", inst, ub, K, 4, bs, nopr, nopr))
     with open(os.path.join(HERE, "ref_counts.json"), "w") as f:
         json.dump(counts, f, indent=1, sort_keys=True)
     # per-node decompose dumps (SURVEY.md §8(d) sampler): seed 42

@@ -2,7 +2,10 @@
 outputs and the C oracle. Bit-exact integer parity everywhere.
 """
 import itertools
+import json
 import math
+import os
+import subprocess
 
 import numpy as np
 import pytest
@@ -535,3 +538,221 @@ def test_gpu_lb2_optimal_under_ties(seed, m):
         fw, bw = prob.children_bounds_lb2_exact(perms[i], d1s[i], d2s[i])
         assert [int(x) for x in lf[i, :f]] == fw
         assert [int(x) for x in lbw[i, :f]] == bw
+
+
+# ---------------------------------------------------------------- the reference's own steal policy
+
+def _ref_instance(name):
+    if name.startswith("gen:"):
+        n, m, seed = (int(x) for x in name[4:].split(":"))
+        return pbb.generate_taillard(n, m, seed)
+    return pbb.taillard_named(name)
+
+
+_STATS_KEYS = sorted(k for k in golden_io.ref_counts() if k.startswith("stats:"))
+
+
+@pytest.mark.parametrize("key", _STATS_KEYS)
+def test_reference_steal_policy_reproduces_pool_stats(key):
+    """steal_policy = 1 (explorer.cpp:251-340 on the device) with the reference's round length
+    (batch_steps) reproduces EVERY PoolStats counter of the compiled reference's pool_run:
+    raw decomposed (replays included), leaves, local steals, steal phases, intervals
+    initialized -- for K = 4^c (hypercube matching) and other K (largest eligible)."""
+    g = golden_io.ref_counts()[key]
+    inst = _ref_instance(g["instance"])
+    nopr = bool(g["disable_pruning"])
+    cfg = pbb.PoolConfig(explorers=g["explorers"], batch_steps=g["batch_steps"], steal_policy=1,
+                         disable_pruning=nopr, record_census=nopr, rounds_per_sync=2)
+    with pbb.GpuPool(inst, cfg, bound="lb1") as pool:
+        pool.set_initial_bound(g["initial_ub"])
+        pool.assign_fresh([(0, math.factorial(inst.n))])          # pool_run's default interval
+        while pool.run_round():
+            pass
+        st = pool.stats()
+        assert (st.decomposed, st.leaves, st.local_steals, st.steal_phases, st.intervals_initialized) == (
+            g["decomposed"], g["leaves"], g["local_steals"], g["steal_phases"], g["intervals_initialized"])
+        assert pool.best_value() == g["best_value"]
+        if nopr:
+            census = pool.take_census()
+            assert len(census) == g["census_size"] and sorted(census) == list(range(math.factorial(inst.n)))
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+def test_census_covers_every_leaf_under_any_partition(policy):
+    """SPEC acceptance 4: pruning disabled, n <= 9, any partition into <= 16
+    intervals: the census holds each of the n! leaves exactly once."""
+    inst = pbb.generate_taillard(8, 5, 31337)
+    nf = math.factorial(8)
+    rng = np.random.default_rng(policy)
+    cuts = sorted(set(int(x) for x in rng.integers(1, nf, 15)))
+    ivs = list(zip([0] + cuts, cuts + [nf]))
+    cfg = pbb.PoolConfig(explorers=64, disable_pruning=True, record_census=True, steal_policy=policy,
+                         batch_steps=97 if policy else 0)
+    with pbb.GpuPool(inst, cfg, bound="lb1") as pool:
+        pool.set_initial_bound(10 ** 6)
+        pool.assign_fresh(ivs)
+        while pool.run_round():
+            pass
+        census = pool.take_census()
+        assert pool.take_census() == []                             # taken: cleared
+    assert sorted(census) == list(range(nf))
+
+
+def test_census_requires_small_n_and_the_flag():
+    with pytest.raises(ValueError):
+        pbb.GpuPool(pbb.taillard_named("ta041"), pbb.PoolConfig(record_census=True))
+    with pbb.GpuPool(pbb.taillard_named("ta001"), pbb.PoolConfig(explorers=32)) as pool:
+        with pytest.raises(_lib.PbbError):
+            pool.take_census()
+
+
+# ---------------------------------------------------------------- the rest of the worker-facing surface
+
+def _merged(ivs):
+    out = []
+    for a, b in sorted(ivs):
+        if out and a <= out[-1][1]:
+            out[-1] = (out[-1][0], max(out[-1][1], b))
+        else:
+            out.append((a, b))
+    return out
+
+
+def test_apply_work_update_keeps_splits_and_reseats():
+    """apply_work_update (explorer.cpp:162-199): echoing the snapshot keeps every explorer;
+    splitting every interval in two keeps the left parts (ends shrink) and seats the right
+    parts on idle explorers. The proof then completes with the reference's exact count."""
+    ref = golden_io.ref_counts()["ta011@1582"]
+    inst = pbb.taillard_named("ta011")
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=1024, batch_steps=64, rounds_per_sync=1)) as pool:
+        pool.set_initial_bound(1582)
+        pool.assign_split(200)
+        for _ in range(2):
+            pool.run_round()
+        snap = pool.snapshot_intervals()
+        act = pool.active_count()
+        pool.apply_work_update(snap)                                # echo: nothing moves
+        assert pool.snapshot_intervals() == snap and pool.active_count() == act
+        halves = []
+        for a, b in snap:
+            mid = (a + b) // 2
+            halves += [(a, mid), (mid, b)] if b - a >= 2 else [(a, b)]
+        pool.apply_work_update(halves)
+        assert _merged(pool.snapshot_intervals()) == _merged(snap)  # same remaining work
+        assert pool.active_count() == len([h for h in halves if h[0] < h[1]])
+        while pool.run_round():
+            pass
+        st = pool.stats()
+    assert st.unique == ref["decomposed"] and st.leaves == ref["leaves"]
+
+
+def test_apply_work_update_drops_work_and_errors():
+    inst = pbb.taillard_named("ta011")
+    nf = math.factorial(20)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=64, batch_steps=32, rounds_per_sync=1)) as pool:
+        pool.set_initial_bound(1582)
+        pool.assign_split(64)
+        pool.run_round()
+        snap = pool.snapshot_intervals()
+        keep = snap[: len(snap) // 2]
+        pool.apply_work_update(keep)                                # the other half goes idle
+        assert pool.snapshot_intervals() == keep
+        with pytest.raises(ValueError):                             # more intervals than explorers
+            pool.apply_work_update([(i, i + 1) for i in range(0, 2 * 65, 2)])
+        pool.apply_work_update([])
+        assert pool.active_count() == 0
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=8)) as pool:
+        pool.set_initial_bound(1582)
+        pool.assign_split(8)                                        # 8 explorers on [s_i, s_i+1)
+        starts = [a for a, _ in pool.snapshot_intervals()]
+        pool.apply_work_update([(a, a + 1024) for a in starts])     # all kept, ends shrink
+        assert pool.snapshot_intervals() == [(a, a + 1024) for a in starts]
+        with pytest.raises(_lib.PbbError):                          # 8 gaps, no idle explorer
+            pool.apply_work_update([(0, nf)])
+
+
+def test_marks_follow_the_reference():
+    inst = pbb.taillard_named("ta001")
+    neh = pbb.neh(inst)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=64, batch_steps=16, rounds_per_sync=1)) as pool:
+        pool.set_initial_bound(neh.cmax, neh.perm)
+        assert not pool.improved_since_mark()                       # the seed is the mark
+        pool.assign_split(4)
+        saw = False
+        while pool.run_round():
+            saw |= pool.improved_since_mark()
+        saw |= pool.improved_since_mark()
+        assert saw and not pool.improved_since_mark()
+        assert pool.best_schedule().cmax == pool.best_value() == 1278
+        assert pool.steals_since_mark() > 0
+        pool.reset_steal_mark()
+        assert pool.steals_since_mark() == 0
+
+
+def test_pool_timeline_csv(tmp_path):
+    """PoolConfig.timeline_path: rows written by the pool at run_round (>= 50 ms apart, forced
+    at exhaustion), exact floor(log2) remaining lengths, flush_timeline forces a sample."""
+    import csv
+
+    path = tmp_path / "pool_tl.csv"
+    inst = pbb.taillard_named("ta011")
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=96, rounds_per_sync=1, timeline_path=str(path))) as pool:
+        pool.set_initial_bound(1582)
+        pool.assign_fresh([(0, math.factorial(20))])
+        while pool.run_round():
+            pass
+        pool.flush_timeline()
+    rows = list(csv.reader(open(path)))
+    assert rows[0] == ["timestamp_ms", "explorer_id", "active", "interval_length_log2"]
+    body = rows[1:]
+    assert len(body) >= 2 * 96 and len(body) % 96 == 0
+    first = body[:96]
+    assert first[0][2] == "1" and int(first[0][3]) <= 61 and int(first[0][3]) >= 0   # log2(20!) = 61.07
+    assert all(r[2] == "0" and r[3] == "-1" for r in body[-96:])
+
+
+# ---------------------------------------------------------------- the reference's runtime driving GPU pools
+
+GPU_WORKER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "integration", "_build",
+                          "gpu_worker")
+
+
+def _gpu_worker(*args):
+    if not os.path.exists(GPU_WORKER):
+        pytest.skip("integration/_build/gpu_worker not built (make -C integration needs /root/reference)")
+    out = subprocess.run([GPU_WORKER, *map(str, args)], capture_output=True, text=True, timeout=600, check=True)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("K", [16, 64, 48])
+def test_reference_binding_pool_run_reproduces_pool_stats(K):
+    """integration/pbb/gpu_pool.hpp (GpuExplorerPool, compiled against the reference's own
+    headers) driven like pool_run with the reference steal policy: PoolStats equal the compiled
+    reference's (tests/golden/ref_counts.json, made by oracle/_ref/ref_driver)."""
+    g = golden_io.ref_counts()[f"stats:ta011@1582:K{K}:b1024:np0"]
+    r = _gpu_worker("pool", "ta011", 1582, K, "lb1", 1, 1024)
+    assert (r["decomposed"], r["leaves"], r["local_steals"], r["steal_phases"], r["intervals_initialized"]) == (
+        g["decomposed"], g["leaves"], g["local_steals"], g["steal_phases"], g["intervals_initialized"])
+    assert r["unique"] == golden_io.ref_counts()["ta011@1582"]["decomposed"]
+
+
+@pytest.mark.parametrize("name,ub,leaves,unique", [("ta011", 1582, 54, 158049), ("ta021", 2297, 1440, 462443491)])
+def test_reference_coordinator_drives_one_gpu_worker_exactly(name, ub, leaves, unique):
+    """Coordinator::run (src/coordinator.cpp) over the reference's in-process transport and
+    wire codec, one worker running worker_run's pool-role loop on a GpuExplorerPool
+    (apply_work_update, marks, snapshots): the proof's counts equal pool_run's exactly."""
+    r = _gpu_worker("cluster", name, ub, 1, "lb1")
+    assert r["unique"] == unique and r["leaves"] == leaves
+    assert r["coordinator_total_nodes"] == r["decomposed"]        # WORK checkpoints carried every node
+    assert r["updates_applied"] >= 1 and r["splits"] == 0
+
+
+def test_reference_coordinator_drives_several_gpu_workers():
+    """Three GPU workers under the reference coordinator: work units are split by the
+    coordinator (split_unit) and handed over with apply_work_update; every leaf is evaluated and
+    nothing is lost (the protocol may redo work a stale snapshot had already covered, as it does
+    with the reference's CPU workers)."""
+    r = _gpu_worker("cluster", "ta011", 1582, 3, "lb1")
+    assert r["splits"] > 0 and r["updates_applied"] > 3
+    assert r["leaves"] >= 54 and r["unique"] >= 158049
+    assert r["coordinator_total_nodes"] == r["decomposed"]
