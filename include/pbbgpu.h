@@ -34,6 +34,9 @@
  *   pbbgpu_promote                  <- ExplorerPool::promote_solutions  (explorer.hpp:99, explorer.cpp:397-424)
  *   pbbgpu_explorer_lengths         <- timeline sampling                (explorer.cpp:71-85, 448-464)
  *   pbbgpu_int32_peak               <- (new) integer-ALU roofline denominator
+ *   pbbgpu_group_*                  <- Coordinator/worker WORK+BEST exchange inside one box
+ *                                      (src/coordinator.cpp:170-306, src/workunit.cpp:59-74) over
+ *                                      NVLink peer memory
  *   pbbgpu_taillard / pbbgpu_makespan / pbbgpu_neh
  *                                   <- generate_taillard / taillard_named / makespan / neh
  *                                      (instance.hpp:42-48, heuristic.hpp:21)
@@ -222,6 +225,33 @@ int pbbgpu_explorer_lengths(pbbgpu_pool* pool, float* out, int cap);
  * measured integer-op throughput of the device, the roofline denominator of the bounding
  * kernels (MEASURED_PEAKS.json has no integer peak). */
 int pbbgpu_int32_peak(int device, double* ops_per_s);
+
+/* ---- multi-GPU group: one process per GPU, peer memory over NVLink.
+ * Replaces the coordinator / worker exchange inside one box (src/coordinator.cpp:170-306,
+ * src/workunit.cpp:59-74): each rank's pool owns a peer window (CUDA IPC); every round the
+ * device itself shares the incumbent (system-scope atomicMin), publishes its activity, requests
+ * work when below K/2 active explorers, and serves a less busy peer's request by splitting its
+ * longest intervals straight into that peer's inbox. The host only detects termination.
+ *   create -> exchange handles (any side channel, e.g. torch.distributed) -> open
+ *   per solve: reset -> barrier -> solve -> barrier ; close after a final barrier */
+typedef struct {
+  uint64_t syncs;       /* host synchronizations (run_round calls) */
+  uint64_t exchanges;   /* device exchange rounds */
+  uint64_t imported;    /* intervals seated from peers */
+  uint64_t exported;    /* intervals deposited into peers */
+  double wall_s;
+  double device_ms;     /* CUDA-event time of the solve loop */
+  int completed;        /* 0 when the time limit stopped it */
+} pbbgpu_group_stats_t;
+int pbbgpu_group_handle_size(void);
+int pbbgpu_group_create(pbbgpu_pool* pool, int world, int rank, void* handle_out);
+int pbbgpu_group_open(pbbgpu_pool* pool, const void* handles /* world * handle_size bytes, rank order */);
+int pbbgpu_group_reset(pbbgpu_pool* pool);
+/* this rank's share of [0,n!) (interleaved equal ranges, or breadth-first seeding when
+ * seed_div > 0), rounds until the group terminates (or the time limit); counters are local */
+int pbbgpu_group_solve(pbbgpu_pool* pool, int64_t initial_ub, int seed_div, double time_limit_s,
+                       pbbgpu_group_stats_t* out);
+int pbbgpu_group_close(pbbgpu_pool* pool);
 
 /* pool_run: assign [0,n!) (or the given intervals), run rounds to exhaustion or time limit */
 int pbbgpu_solve(pbbgpu_pool* pool, int64_t initial_ub, const uint16_t* a_digits,

@@ -30,6 +30,8 @@ EXPORTS = (
     "pbbgpu_insertion_ls", "pbbgpu_offer_schedule", "pbbgpu_promote", "pbbgpu_explorer_lengths",
     "pbbgpu_best_schedule", "pbbgpu_snapshot_ex", "pbbgpu_apply_work_update", "pbbgpu_improved_since_mark",
     "pbbgpu_steals_since_mark", "pbbgpu_reset_steal_mark", "pbbgpu_take_census", "pbbgpu_flush_timeline",
+    "pbbgpu_group_handle_size", "pbbgpu_group_create", "pbbgpu_group_open", "pbbgpu_group_reset",
+    "pbbgpu_group_solve", "pbbgpu_group_close",
 )
 
 
@@ -87,6 +89,21 @@ class Stats(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class GroupStats(ctypes.Structure):
+    _fields_ = [
+        ("syncs", ctypes.c_uint64),
+        ("exchanges", ctypes.c_uint64),
+        ("imported", ctypes.c_uint64),
+        ("exported", ctypes.c_uint64),
+        ("wall_s", ctypes.c_double),
+        ("device_ms", ctypes.c_double),
+        ("completed", ctypes.c_int),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 _lib = None
 
 
@@ -135,6 +152,13 @@ def load() -> ctypes.CDLL:
         "pbbgpu_reset_steal_mark": (ctypes.c_int, [P]),
         "pbbgpu_take_census": (ctypes.c_int, [P, u64p, ctypes.c_int64, i64p]),
         "pbbgpu_flush_timeline": (ctypes.c_int, [P]),
+        "pbbgpu_group_handle_size": (ctypes.c_int, []),
+        "pbbgpu_group_create": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
+        "pbbgpu_group_open": (ctypes.c_int, [P, ctypes.c_void_p]),
+        "pbbgpu_group_reset": (ctypes.c_int, [P]),
+        "pbbgpu_group_solve": (ctypes.c_int, [P, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                                              ctypes.POINTER(GroupStats)]),
+        "pbbgpu_group_close": (ctypes.c_int, [P]),
         "pbbgpu_offer_bound": (ctypes.c_int, [P, ctypes.c_int64]),
         "pbbgpu_stats": (ctypes.c_int, [P, ctypes.POINTER(Stats)]),
         "pbbgpu_histogram": (ctypes.c_int, [P, u64p, ctypes.c_int]),

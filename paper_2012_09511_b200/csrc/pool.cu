@@ -689,8 +689,9 @@ __global__ void __launch_bounds__(kStealThreads) steal_kernel(StealParams S) {
 // the coordinator's split_unit / steal_from_active, src/workunit.cpp:59-74,
 // src/coordinator.cpp:170-187): the `want` active explorers with the longest remaining
 // intervals keep [pos, mid) and hand [mid, end) out as factoradic digit vectors.
-__global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, int want, int* out_digits,
-                                                              uint8_t* out_nf, int* out_count) {
+// Block-wide body (kStealThreads threads): returns the number of exported intervals (all
+// threads), written as int digit pairs [a | b] (2n per interval) and end-is-n! flags.
+__device__ int export_body(const StealParams& S, int want, int* out_digits, uint8_t* out_nf) {
   __shared__ int bins[kBins];
   __shared__ int s_tot[2];
   const int t = threadIdx.x, K = S.K, n = S.L.n;
@@ -794,7 +795,191 @@ __global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, in
     }
   }
   __syncthreads();
-  if (t == 0) *out_count = min(s_tot[0], want);
+  const int cnt = min(s_tot[0], want);
+  __syncthreads();
+  return cnt;
+}
+
+__global__ void __launch_bounds__(kStealThreads) export_kernel(StealParams S, int want, int* out_digits,
+                                                              uint8_t* out_nf, int* out_count) {
+  const int cnt = export_body(S, want, out_digits, out_nf);
+  if (threadIdx.x == 0) *out_count = cnt;
+}
+
+// ---- multi-GPU group over NVLink peer memory (the intra-box analogue of the
+// coordinator's WORK / BEST exchange, src/coordinator.cpp:170-306, src/workunit.cpp:59-74)
+//
+// Every rank (one process per GPU) owns one PeerWindow in its device memory, exported with
+// cudaIpcGetMemHandle and mapped by every other rank. Per round, after the intra-GPU steal
+// pipeline, two small kernels run on each rank's own stream, with no host involvement:
+//   group_exchange_kernel  incumbent MIN (system-scope atomicMin into every window), import of
+//                          intervals a donor deposited into this rank's inbox (seated on idle
+//                          explorers), publication of the active count, a work request when
+//                          below `low` active explorers, and the choice of one requesting peer
+//                          to serve (claimed with a peer atomicCAS on its lock)
+//   group_export_kernel    the claimed request served: the longest remaining intervals are split
+//                          (export_body, right parts) and written straight into the peer's inbox
+//                          over NVLink, then published with a system fence + ready flag
+// The host only polls: termination = two consecutive identical waves of (active, sent, recv)
+// over all windows with every active == 0 and sum(sent) == sum(recv) (double counting; in-flight
+// deposits show as sent > recv).
+constexpr int kMaxGroup = 8;
+
+struct PeerWindow {
+  int best;                  // group incumbent (system-scope atomicMin by every rank)
+  int active;                // explorers not Empty after the owner's last round
+  int req;                   // intervals wanted by the owner (0 = none)
+  int lock;                  // 0 free, donor rank + 1 while a deposit is pending / being seated
+  int count;                 // intervals left in the inbox
+  int ready;                 // donor -> owner: inbox valid
+  int pad[2];
+  unsigned long long sent;   // intervals this rank deposited into peers
+  unsigned long long recv;   // intervals this rank seated from its inbox
+  // inbox: cap * 2n int digits, then cap uint8 end-is-n! flags
+};
+constexpr int kWindowHeader = 64;
+
+struct GroupState {
+  int serve, want;           // peer claimed this round (-1 none), intervals it asked for
+  int act[kMaxGroup];        // the last wave over all windows (host termination check)
+  unsigned long long sent[kMaxGroup], recv[kMaxGroup];
+  unsigned long long exchanges, imported, exported;
+};
+
+struct GroupParams {
+  unsigned char* win[kMaxGroup];  // mapped windows (own included, index = rank)
+  int world, rank, K, cap, low, share_best;
+  GroupState* gs;
+};
+
+__device__ __forceinline__ PeerWindow* pw(const GroupParams& G, int q) { return reinterpret_cast<PeerWindow*>(G.win[q]); }
+__device__ __forceinline__ int* inbox_digits(const GroupParams& G, int q) {
+  return reinterpret_cast<int*>(G.win[q] + kWindowHeader);
+}
+__device__ __forceinline__ uint8_t* inbox_nf(const GroupParams& G, int q, int n) {
+  return G.win[q] + kWindowHeader + static_cast<size_t>(G.cap) * 2 * n * sizeof(int);
+}
+__device__ __forceinline__ int vload(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+__device__ __forceinline__ unsigned long long vload64(const unsigned long long* p) {
+  return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__global__ void __launch_bounds__(kStealThreads) group_exchange_kernel(IvmLayout L, unsigned char* state, const int* ptot,
+                                                                      DevCounters* ctr, GroupParams G) {
+  __shared__ int s_idle[kStealThreads];
+  __shared__ int s_take, s_cnt;
+  const int t = threadIdx.x, K = G.K, n = L.n;
+  PeerWindow* me = pw(G, G.rank);
+  if (t == 0) {
+    G.gs->serve = -1;
+    G.gs->exchanges += 1ull;
+    if (G.share_best) {  // incumbent MIN over the group
+      const int b = vload(&ctr->best);
+      for (int q = 0; q < G.world; ++q) atomicMin_system(&pw(G, q)->best, b);
+      const int gb = vload(&me->best);
+      if (gb < b) atomicMin(&ctr->best, gb);
+    }
+    s_cnt = vload(&me->ready) ? vload(&me->count) : 0;
+    __threadfence_system();  // acquire: the inbox is read after the flag
+  }
+  __syncthreads();
+  const int cnt = s_cnt;
+  if (cnt > 0) {  // import: seat deposited intervals on idle explorers (list_idle_kernel's scan)
+    const int CH = (K + kStealThreads - 1) / kStealThreads;
+    const int lo = t * CH, hi = min(K, lo + CH);
+    int idle = 0;
+    for (int i = lo; i < hi; ++i) idle += reinterpret_cast<const IvmHdr*>(state + static_cast<size_t>(i) * L.gstride)->state == kEmpty;
+    s_idle[t] = idle;
+    __syncthreads();
+    for (int off = 1; off < kStealThreads; off <<= 1) {
+      const int v = t >= off ? s_idle[t - off] : 0;
+      __syncthreads();
+      s_idle[t] += v;
+      __syncthreads();
+    }
+    const int take = min(cnt, s_idle[kStealThreads - 1]);
+    int r = s_idle[t] - idle;
+    const int* dig = inbox_digits(G, G.rank);
+    const uint8_t* nf = inbox_nf(G, G.rank, n);
+    for (int i = lo; i < hi && r < take; ++i) {
+      unsigned char* blk = state + static_cast<size_t>(i) * L.gstride;
+      if (reinterpret_cast<const IvmHdr*>(blk)->state != kEmpty) continue;
+      const int e = cnt - 1 - r;  // consume the inbox from its end
+      int a[kMaxN], b[kMaxN];
+      for (int l = 0; l < n; ++l) {
+        a[l] = dig[static_cast<size_t>(e) * 2 * n + l];
+        b[l] = dig[static_cast<size_t>(e) * 2 * n + n + l];
+      }
+      seat_explorer(blk, L, ptot, a, b, !nf[e]);
+      ++r;
+    }
+    if (t == 0) s_take = take;
+    __syncthreads();
+    if (t == 0 && s_take > 0) {
+      me->recv += static_cast<unsigned long long>(s_take);
+      ctr->active += s_take;
+      ctr->inits += static_cast<unsigned long long>(s_take);
+      G.gs->imported += static_cast<unsigned long long>(s_take);
+      const int left = cnt - s_take;
+      me->count = left;
+      if (left == 0) {  // release: ready, request, then the lock (a donor claims only a free lock)
+        me->ready = 0;
+        me->req = 0;
+        __threadfence_system();
+        atomicExch_system(&me->lock, 0);
+      }
+    }
+  }
+  if (t == 0) {
+    const int act = vload(&ctr->active);
+    *reinterpret_cast<volatile int*>(&me->active) = act;
+    // request work when running low (and nothing is pending)
+    if (act < G.low && vload(&me->req) == 0 && vload(&me->lock) == 0 && !vload(&me->ready) && K - act > 0)
+      *reinterpret_cast<volatile int*>(&me->req) = min(K - act, G.cap);
+    // serve one requesting peer that is much less busy (round robin from the next rank)
+    if (act > 0) {
+      const unsigned long long rot = G.gs->exchanges;
+      for (int i = 1; i < G.world; ++i) {
+        const int q = static_cast<int>((static_cast<unsigned long long>(G.rank) + i + rot) % G.world);
+        if (q == G.rank) continue;
+        PeerWindow* w = pw(G, q);
+        const int rq = vload(&w->req);
+        if (rq <= 0 || vload(&w->lock) != 0 || 2 * vload(&w->active) + 1 >= act) continue;
+        if (atomicCAS_system(&w->lock, 0, G.rank + 1) != 0) continue;
+        __threadfence_system();
+        G.gs->serve = q;
+        G.gs->want = min(vload(&w->req), G.cap);
+        break;
+      }
+    }
+    // the wave the host checks for termination
+    for (int q = 0; q < G.world; ++q) {
+      PeerWindow* w = pw(G, q);
+      G.gs->act[q] = vload(&w->active);
+      G.gs->sent[q] = vload64(&w->sent);
+      G.gs->recv[q] = vload64(&w->recv);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kStealThreads) group_export_kernel(StealParams S, GroupParams G) {
+  const int q = G.gs->serve;
+  if (q < 0) return;
+  const int cnt = export_body(S, G.gs->want, inbox_digits(G, q), inbox_nf(G, q, S.L.n));
+  if (threadIdx.x == 0) {
+    PeerWindow* w = pw(G, q);
+    if (cnt > 0) {
+      pw(G, G.rank)->sent += static_cast<unsigned long long>(cnt);  // counted before it is visible
+      G.gs->exported += static_cast<unsigned long long>(cnt);
+      __threadfence_system();
+      *reinterpret_cast<volatile int*>(&w->count) = cnt;
+      __threadfence_system();
+      *reinterpret_cast<volatile int*>(&w->ready) = 1;
+    } else {
+      atomicExch_system(&w->lock, 0);  // nothing to give: release
+    }
+    G.gs->serve = -1;
+  }
 }
 
 // Idle explorers in index order (slots for assign / import) and their count.
@@ -1034,6 +1219,13 @@ struct pbbgpu_pool {
   FILE* timeline = nullptr;
   std::chrono::steady_clock::time_point t_start{}, t_last_sample{};
   bool sampled = false;
+  // multi-GPU group over peer memory (pbbgpu_group_*)
+  int g_world = 0, g_rank = 0, g_cap = 0;
+  unsigned char* d_window = nullptr;       // own PeerWindow (IPC-exported)
+  unsigned char* g_peer[kMaxGroup] = {};   // mapped windows (own at g_rank)
+  bool g_open = false;
+  GroupState* d_gs = nullptr;
+  GroupState* h_gs = nullptr;              // pinned
   // marks (explorer.hpp:94-96)
   int64_t improvement_mark = INT64_MAX;
   uint64_t steal_mark = 0;
@@ -1071,6 +1263,11 @@ struct pbbgpu_pool {
     cudaFree(d_ref_flags);
     cudaFree(d_ref_pairs);
     cudaFree(d_census);
+    for (int q = 0; q < g_world; ++q)
+      if (q != g_rank && g_peer[q]) cudaIpcCloseMemHandle(g_peer[q]);
+    cudaFree(d_window);
+    cudaFree(d_gs);
+    if (h_gs) cudaFreeHost(h_gs);
     if (timeline) std::fclose(timeline);
     if (h_ctr) cudaFreeHost(h_ctr);
     if (pin) cudaFreeHost(pin);
@@ -1557,6 +1754,19 @@ int count_active_host(pbbgpu_pool* P) {
   return P->K - cnt;
 }
 
+GroupParams group_params(const pbbgpu_pool* P) {
+  GroupParams G{};
+  for (int q = 0; q < P->g_world; ++q) G.win[q] = P->g_peer[q];
+  G.world = P->g_world;
+  G.rank = P->g_rank;
+  G.K = P->K;
+  G.cap = P->g_cap;
+  G.low = P->K / 2;
+  G.share_best = P->cfg.pinned || P->cfg.disable_pruning ? 0 : 1;
+  G.gs = P->d_gs;
+  return G;
+}
+
 // ---- host views of explorer blocks (snapshot, timeline, work updates)
 std::vector<unsigned char> download_state(pbbgpu_pool* P) {
   std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
@@ -1722,6 +1932,16 @@ int run_round(pbbgpu_pool* P) {
     ck(cudaGetLastError(), "split_thieves_kernel launch");
     split_victims_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, S.victim, S.plan, S.split_mode);
     ck(cudaGetLastError(), "split_victims_kernel launch");
+    if (P->g_open) {  // inter-GPU exchange over peer memory (no host involvement)
+      const GroupParams G = group_params(P);
+      group_exchange_kernel<<<1, kStealThreads, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, P->d_ctr, G);
+      ck(cudaGetLastError(), "group_exchange_kernel launch");
+      lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, S.split_mode);
+      ck(cudaGetLastError(), "lens_kernel launch");
+      group_export_kernel<<<1, kStealThreads, 0, P->stream>>>(S, G);
+      ck(cudaGetLastError(), "group_export_kernel launch");
+      P->launches += 3;
+    }
     ck(cudaEventRecord(P->evs[3 * r + 2], P->stream), "event");
     P->launches += 5;
   }
@@ -2839,6 +3059,142 @@ int pbbgpu_flush_timeline(pbbgpu_pool* P) {
     if (!P->timeline) return;
     sample_timeline(P, true);
     std::fflush(P->timeline);
+  });
+}
+
+// ---- multi-GPU group (one process per GPU; peer windows over CUDA IPC / NVLink)
+int pbbgpu_group_handle_size(void) { return static_cast<int>(sizeof(cudaIpcMemHandle_t)); }
+
+int pbbgpu_group_create(pbbgpu_pool* P, int world, int rank, void* handle_out) {
+  return guarded([&] {
+    if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
+    if (P->cfg.steal_policy == 1) throw std::invalid_argument("the reference steal policy is single-pool only");
+    if (world < 2 || world > kMaxGroup || rank < 0 || rank >= world) throw std::invalid_argument("bad group world / rank");
+    if (P->d_window) throw StateError("pbbgpu_group_create: the pool already has a group");
+    ck(cudaSetDevice(P->cfg.device), "cudaSetDevice");
+    P->g_cap = P->K;
+    const size_t bytes = kWindowHeader + static_cast<size_t>(P->g_cap) * (2 * P->n * sizeof(int) + 1);
+    ck(cudaMalloc(&P->d_window, bytes), "malloc window");
+    ck(cudaMemset(P->d_window, 0, bytes), "memset window");
+    ck(cudaMalloc(&P->d_gs, sizeof(GroupState)), "malloc");
+    ck(cudaMallocHost(&P->h_gs, sizeof(GroupState)), "malloc host");
+    P->g_world = world;
+    P->g_rank = rank;
+    P->g_peer[rank] = P->d_window;
+    ck(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out), P->d_window), "cudaIpcGetMemHandle");
+  });
+}
+
+int pbbgpu_group_open(pbbgpu_pool* P, const void* handles) {
+  return guarded([&] {
+    if (!P->d_window) throw StateError("pbbgpu_group_open before pbbgpu_group_create");
+    if (P->g_open) return;
+    ck(cudaSetDevice(P->cfg.device), "cudaSetDevice");
+    const auto* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+    for (int q = 0; q < P->g_world; ++q) {
+      if (q == P->g_rank) continue;
+      void* ptr = nullptr;
+      ck(cudaIpcOpenMemHandle(&ptr, h[q], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      P->g_peer[q] = static_cast<unsigned char*>(ptr);
+    }
+    P->g_open = true;
+  });
+}
+
+// Own window back to its initial state (call on every rank, then a group barrier, before a solve).
+int pbbgpu_group_reset(pbbgpu_pool* P) {
+  return guarded([&] {
+    if (!P->d_window) throw StateError("pbbgpu_group_reset: no group");
+    PeerWindow w{};
+    w.best = INT_MAX;
+    w.active = 1 << 20;  // "not started": never terminal, never served, until the first publish
+    xfer(P, P->d_window, &w, sizeof(w), cudaMemcpyHostToDevice, "window reset");
+    GroupState z{};
+    z.serve = -1;
+    xfer(P, P->d_gs, &z, sizeof(z), cudaMemcpyHostToDevice, "group state reset");
+  });
+}
+
+int pbbgpu_group_solve(pbbgpu_pool* P, int64_t initial_ub, int seed_div, double time_limit_s,
+                       pbbgpu_group_stats_t* out) {
+  return guarded([&] {
+    if (!P->g_open) throw StateError("pbbgpu_group_solve: open the group first");
+    std::memset(out, 0, sizeof(*out));
+    int rc = pbbgpu_set_initial_bound(P, initial_ub, nullptr, 0);
+    if (rc) throw std::runtime_error(g_last_error);
+    const int W = P->g_world, r = P->g_rank;
+    rc = seed_div > 0 ? pbbgpu_seed(P, initial_ub, r, W, std::max(W, W * P->K / seed_div))
+                      : pbbgpu_assign_split_strided(P, r, W, P->K, W * P->K);
+    if (rc) throw std::runtime_error(g_last_error);
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    ck(cudaEventRecord(e0, P->stream), "event");
+    bool completed = true, have_prev = false;
+    GroupState prev{};
+    uint64_t syncs = 0;
+    for (;;) {
+      run_round(P);
+      ++syncs;
+      xfer(P, P->h_gs, P->d_gs, sizeof(GroupState), cudaMemcpyDeviceToHost, "group state");
+      const GroupState& g = *P->h_gs;
+      bool terminal = true;
+      unsigned long long ss = 0, rr = 0;
+      for (int q = 0; q < W; ++q) {
+        terminal = terminal && g.act[q] == 0;
+        ss += g.sent[q];
+        rr += g.recv[q];
+      }
+      terminal = terminal && ss == rr;
+      if (terminal && have_prev) {
+        bool same = true;
+        for (int q = 0; q < W; ++q) same = same && prev.sent[q] == g.sent[q] && prev.recv[q] == g.recv[q];
+        if (same) break;
+      }
+      have_prev = terminal;
+      prev = g;
+      if (time_limit_s > 0) {
+        const std::chrono::duration<double> el = std::chrono::steady_clock::now() - t0;
+        if (el.count() >= time_limit_s) {
+          completed = false;
+          break;
+        }
+      }
+    }
+    ck(cudaEventRecord(e1, P->stream), "event");
+    ck(cudaEventSynchronize(e1), "event sync");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    xfer(P, P->h_gs, P->d_gs, sizeof(GroupState), cudaMemcpyDeviceToHost, "group state");
+    out->syncs = syncs;
+    out->exchanges = P->h_gs->exchanges;
+    out->imported = P->h_gs->imported;
+    out->exported = P->h_gs->exported;
+    out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    out->device_ms = ms;
+    out->completed = completed ? 1 : 0;
+  });
+}
+
+int pbbgpu_group_close(pbbgpu_pool* P) {
+  return guarded([&] {
+    if (!P->d_window) return;
+    ck(cudaStreamSynchronize(P->stream), "sync");
+    for (int q = 0; q < P->g_world; ++q) {
+      if (q != P->g_rank && P->g_peer[q]) cudaIpcCloseMemHandle(P->g_peer[q]);
+      P->g_peer[q] = nullptr;
+    }
+    cudaFree(P->d_window);
+    cudaFree(P->d_gs);
+    cudaFreeHost(P->h_gs);
+    P->d_window = nullptr;
+    P->d_gs = nullptr;
+    P->h_gs = nullptr;
+    P->g_open = false;
+    P->g_world = 0;
   });
 }
 

@@ -15,8 +15,17 @@
   termination all ranks report 0 active explorers in the same gathered snapshot
 Node counts stay exact: replays on the receiving GPU are discounted by the same
 unique = raw - min(L, lnz(a)) rule, which is partition invariant.
-The pool object only needs the GpuPool surface, so the orchestration logic is tested on CPU
-with a simulated pool and the gloo backend (tests/test_multi.py).
+Two data planes:
+  native      (GpuPool on CUDA, the default for world > 1) the pools exchange over NVLink peer
+              memory by themselves (pbbgpu_group_*, csrc/pool.cu): every round the device
+              shares the incumbent with system-scope atomicMin, requests work below K/2 active
+              explorers and serves a less busy peer by writing split intervals straight into its
+              inbox; torch.distributed only exchanges the CUDA IPC handles once, brackets each
+              solve with barriers and reduces the counters at the end
+  host-staged (any object with the GpuPool surface, e.g. the simulated pool of the CPU tests)
+              per sync one all_gather of (active, incumbent, stop) and of exported intervals
+The orchestration logic of the host-staged plane is tested on CPU with a simulated pool and
+the gloo backend (tests/test_multi.py); the native plane on GPUs (tests/test_gpu_multi.py).
 """
 from __future__ import annotations
 
@@ -45,8 +54,28 @@ class DistResult:
 _DELTA = ("unique", "decomposed", "leaves", "improvements", "local_steals")
 
 
+def _solve_native(pool, ub, group, device, time_limit_s, seed_div, world, rank) -> DistResult:
+    import torch.distributed as dist
+
+    st0 = pool.stats()
+    h0 = pool.histogram()
+    if not getattr(pool, "_group_ready", False):
+        handle = pool.group_create(world, rank)
+        handles = [None] * world
+        dist.all_gather_object(handles, handle, group=group)
+        pool.group_open(handles)
+        pool._group_ready = True
+    pool.group_reset()
+    dist.barrier(group=group)        # every window reset before any rank pushes into it
+    gst = pool.group_solve(ub, seed_div, time_limit_s)
+    dist.barrier(group=group)        # nobody reads or writes a peer window after this
+    return _finish(pool, st0, h0, group, device, world, rank, int(gst["imported"]), int(gst["syncs"]),
+                   int(gst["exchanges"]), bool(gst["completed"]))
+
+
 def solve_distributed(pool, ub: int, group=None, device=None, export_max: Optional[int] = None,
-                      low_fraction: float = 0.5, time_limit_s: float = 0.0, seed_div: int = 0) -> DistResult:
+                      low_fraction: float = 0.5, time_limit_s: float = 0.0, seed_div: int = 0,
+                      native: Optional[bool] = None) -> DistResult:
     """Run `pool` (a GpuPool, or any object with its surface) to exhaustion cooperatively with
     the other ranks of `group` (torch.distributed). world_size == 1 degenerates to pool_run.
 
@@ -60,6 +89,8 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world > 1 and native is not False and hasattr(pool, "group_solve"):
+        return _solve_native(pool, ub, group, device, time_limit_s, seed_div, world, rank)
     n = pool.inst.n
     K = pool.K()
     st0 = pool.stats()
@@ -164,6 +195,16 @@ def solve_distributed(pool, ub: int, group=None, device=None, export_max: Option
                 pool.import_work(mine[:, :n].astype(np.uint16), mine[:, n:2 * n].astype(np.uint16),
                                  mine[:, 2 * n].astype(np.uint8))
                 remote += len(mine)
+    return _finish(pool, st0, h0, group, device, world, rank, remote, rounds, exchanges, completed)
+
+
+def _finish(pool, st0, h0, group, device, world, rank, remote, rounds, exchanges, completed) -> DistResult:
+    """This solve's counters (the pool's are cumulative), summed over the ranks; the best
+    schedule broadcast from the rank that holds it."""
+    import torch
+    import torch.distributed as dist
+
+    n = pool.inst.n
     st1 = pool.stats()
     h1 = pool.histogram()
     # this solve only (the pool's counters are cumulative)

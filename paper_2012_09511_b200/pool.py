@@ -300,6 +300,30 @@ class GpuPool:
         """flush_timeline (explorer.hpp:103): forced sample + flush of the pool's timeline CSV."""
         _lib.check(self._lib.pbbgpu_flush_timeline(self._h))
 
+    # -- multi-GPU group over peer memory (pbbgpu_group_*; multi.solve_distributed drives it) -------
+    def group_create(self, world: int, rank: int) -> bytes:
+        """Create this rank's peer window; returns its CUDA IPC handle (to all_gather)."""
+        size = self._lib.pbbgpu_group_handle_size()
+        buf = ctypes.create_string_buffer(size)
+        _lib.check(self._lib.pbbgpu_group_create(self._h, world, rank, buf))
+        return buf.raw
+
+    def group_open(self, handles: Sequence[bytes]) -> None:
+        blob = b"".join(handles)
+        _lib.check(self._lib.pbbgpu_group_open(self._h, ctypes.c_char_p(blob)))
+
+    def group_reset(self) -> None:
+        _lib.check(self._lib.pbbgpu_group_reset(self._h))
+
+    def group_solve(self, ub: int, seed_div: int = 0, time_limit_s: float = 0.0) -> dict:
+        gs = _lib.GroupStats()
+        _lib.check(self._lib.pbbgpu_group_solve(self._h, int(min(ub, NO_INCUMBENT)), seed_div, time_limit_s,
+                                                ctypes.byref(gs)))
+        return gs.as_dict()
+
+    def group_close(self) -> None:
+        _lib.check(self._lib.pbbgpu_group_close(self._h))
+
     def run_round(self) -> int:
         act = ctypes.c_int()
         _lib.check(self._lib.pbbgpu_run_round(self._h, ctypes.byref(act)))
