@@ -407,11 +407,150 @@ __device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
 // byte permutes, one VIADD.16x2 and one VIADDMNMX.U16x2 for both directions. Each lane owns
 // a pair (32 pairs per round, the last round's spare lanes repeat pair P-1); per child the
 // 32 pair bounds are combined with REDUX.MAX.
+// Per-lane free-position masks of the current IVM row, one 32-bit word per pair round
+// (n <= 32, warp-per-explorer LB2): bit t of word r is set when the job at position t of pair
+// (32 r + lane)'s Johnson order is in the row. A node's free set is its row minus the selected
+// job, so the masks follow the explorer incrementally -- branch: the node's masks become the
+// next row's; backtrack: the job selected one level up is added back -- instead of being rebuilt
+// from the free jobs (f inverse-order lookups per pair round and node).
+template <int M, bool ON>
+struct RowMask {
+  static constexpr int P = M * (M - 1) / 2;
+  static constexpr int R = ON ? (P + 31) / 32 : 1;
+  uint32_t w[R];
+  __device__ __forceinline__ uint32_t bit(const InstView& in, int job, int r) const {
+    const int q = min(32 * r + static_cast<int>(threadIdx.x & 31), P - 1);
+    return 1u << in.invord[job * P + q];
+  }
+  __device__ __forceinline__ void build(const IvmView& iv, const InstView& in, int n, int level) {
+    if constexpr (ON) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r] = 0;
+      if (level < 0) return;
+      const int8_t* row = iv.cells + tri_off(level, n);
+      for (int c = 0; c < n - level; ++c) {
+        const int x = row[c];
+        const int job = (x < 0 ? -x : x) - 1;
+#pragma unroll
+        for (int r = 0; r < R; ++r) w[r] |= bit(in, job, r);
+      }
+    }
+  }
+  __device__ __forceinline__ void add(const InstView& in, int job) {
+    if constexpr (ON) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r] |= bit(in, job, r);
+    }
+  }
+};
+
+// One pair round of children_lb2_w: lane q's pair, the forward / backward passes over the set
+// bits of Fr (the node's free positions in the pair's order), then every child's bound for
+// the round's 32 pairs folded into acc (lane c holds child c).
 template <int M, bool SMALLN>
-__device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView& in, int n, int mp, int f,
-                                               unsigned long long fmask) {
+__device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in, int f, int q0, uint32_t Fr32,
+                                          unsigned long long Fq, uint32_t& acc0, uint32_t& acc1) {
   constexpr unsigned FULL = 0xffffffffu;
   constexpr int NEG = -30000;
+  const int lane = threadIdx.x & 31;
+  const uint32_t* H = reinterpret_cast<const uint32_t*>(iv.heads);  // [c][M] h' | t' << 16
+  const int P = in.npairs;
+  // packed rows are padded to a multiple of 32 pairs: lane q always reads bank q mod 32,
+  // whatever position t each lane is at (the set-bit passes diverge in t)
+  const int PS = round_up(P, 32);
+  int* Sl = reinterpret_cast<int*>(iv.pm) + lane;  // [j][32]: PM'_j (forward pass), then S_j
+  const int q = min(q0 + lane, P - 1);
+  const int k = in.pk[q], l = in.pl[q];
+  const int Atot = iv.rm[k], Btot = iv.rm[l];
+  const int qk = iv.tl[k], ql = iv.tl[l], rk = iv.fr[k], rl = iv.fr[l];
+  const int cAq = Atot + qk, cRB = rl + Btot;
+  // packed entries e = job << 7 | u << 13 | v << 24 (u = a + lag, v = a - b signed): e & 0x1f80 is
+  // the byte offset of row `job` of the per-lane [job][32] int32 table. With E = Btot + sum of
+  // v over the earlier free positions, X'_i = X_i + Btot = E + u_i (forward); going backward
+  // from G = Atot, G -= v_i gives X'_i = G + u_i. PM' and SM' carry the + Btot, so
+  //   I1 = max(PM'_i + v_i, SM'_i),  lo = max(A + q_k, I1 + q_l),  hi = max(r_l + B, I1 + r_k - v_i)
+  const unsigned char* pq = reinterpret_cast<const unsigned char*>(in.packed + q);
+  const int strideB = PS * 4;
+  unsigned char* Sb = reinterpret_cast<unsigned char*>(Sl);
+  if constexpr (SMALLN) {
+    // both passes walk exactly the f set bits with bfind: the backward pass on the mask, the
+    // forward pass on its bit reversal (position t = 31 - u, address pq31 - u * stride)
+    const unsigned char* pq31 = pq + 31 * strideB;
+    const int nstride = -strideB;
+    int E = Btot, pm = NEG;
+    for (uint32_t w = __brev(Fr32); w;) {
+      const int u = bfind_u32(w);
+      w ^= 1u << u;
+      const unsigned e = *reinterpret_cast<const unsigned*>(pq31 + u * nstride);
+      *reinterpret_cast<int*>(Sb + (e & 0x1f80u)) = pm;
+      pm = max(pm, E + static_cast<int>((e >> 13) & 0x7ffu));
+      E += static_cast<int>(e) >> 24;
+    }
+    int G = Atot, sm = NEG;
+    for (uint32_t w = Fr32; w;) {  // descending positions
+      const int t = bfind_u32(w);
+      w ^= 1u << t;
+      const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
+      int* slot = reinterpret_cast<int*>(Sb + (e & 0x1f80u));
+      const int v = static_cast<int>(e) >> 24;
+      const int I1 = max(*slot + v, sm);
+      const int lo = max(cAq, I1 + ql), hi = max(cRB, I1 + (rk - v));
+      *slot = static_cast<int>(__byte_perm(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi), 0x5410));
+      G -= v;
+      sm = max(sm, G + static_cast<int>((e >> 13) & 0x7ffu));
+    }
+  } else {
+    // n <= 64: same set-bit iteration over a 64-bit free-position mask
+    int E = Btot, pm = NEG;
+    for (unsigned long long w = Fq; w; w &= w - 1) {
+      const int t = __ffsll(static_cast<long long>(w)) - 1;
+      const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
+      *reinterpret_cast<int*>(Sb + (e & 0x1f80u)) = pm;
+      pm = max(pm, E + static_cast<int>((e >> 13) & 0x7ffu));
+      E += static_cast<int>(e) >> 24;
+    }
+    int G = Atot, sm = NEG;
+    for (unsigned long long w = Fq; w;) {
+      const int t = 63 - __clzll(static_cast<long long>(w));
+      w ^= 1ull << t;
+      const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
+      int* slot = reinterpret_cast<int*>(Sb + (e & 0x1f80u));
+      const int v = static_cast<int>(e) >> 24;
+      const int I1 = max(*slot + v, sm);
+      const int lo = max(cAq, I1 + ql), hi = max(cRB, I1 + (rk - v));
+      *slot = static_cast<int>(__byte_perm(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi), 0x5410));
+      G -= v;
+      sm = max(sm, G + static_cast<int>((e >> 13) & 0x7ffu));
+    }
+  }
+  const uint32_t C = static_cast<uint32_t>(Btot + ql) | static_cast<uint32_t>(rk + Atot) << 16;
+  const uint32_t* Hk = H + k;
+  const uint32_t* Hl = H + l;
+  for (int c = 0; c < f; ++c) {
+    const int j = iv.freej[c];
+    const uint32_t hk = Hk[c * M], hl = Hl[c * M];
+    const uint32_t S = static_cast<uint32_t>(Sl[j * 32]);
+    const uint32_t V = max_u16x2(add_u16x2(__byte_perm(hk, hl, 0x7610), S), add_u16x2(__byte_perm(hl, hk, 0x7610), C));
+    const uint32_t vF = __reduce_max_sync(FULL, V & 0xffffu);
+    const uint32_t vB = __reduce_max_sync(FULL, V) & 0xffff0000u;
+    if (SMALLN) {
+      if (lane == c) acc0 = max_u16x2(acc0, vF | vB);
+    } else if (lane == (c & 31)) {
+      if (c < 32) acc0 = max_u16x2(acc0, vF | vB);
+      else acc1 = max_u16x2(acc1, vF | vB);
+    }
+  }
+}
+
+// LB2, warp per explorer, lanes over machine pairs, exact max-plus prefix/suffix form.
+// (derivation above children_lb2_w's H tables; rounds in lb2_round). With RM (n <= 32 explorer
+// path) the node's free-position masks come from the explorer's row masks (RowMask) minus the
+// selected job, and become the next row's masks (the caller branches); otherwise they are built
+// from the free jobs through the static inverse order.
+template <int M, bool SMALLN, bool RM = false>
+__device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView& in, int n, int mp, int f,
+                                               unsigned long long fmask, RowMask<M, RM>* rowmask = nullptr,
+                                               int seljob = 0) {
   const int lane = threadIdx.x & 31;
   uint32_t* H = reinterpret_cast<uint32_t*>(iv.heads);  // [c][M] h' | t' << 16
   for (int c = lane; c < f; c += 32) {
@@ -435,98 +574,24 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
   __syncwarp();
   uint32_t acc0 = 0, acc1 = 0;
   const int P = in.npairs;
-  // packed rows are padded to a multiple of 32 pairs: lane q always reads bank q mod 32,
-  // whatever position t each lane is at (the set-bit passes diverge in t)
-  const int PS = round_up(P, 32);
-  int* Sl = reinterpret_cast<int*>(iv.pm) + lane;  // [j][32]: PM_j (forward pass), then S_j
-  for (int q0 = 0; q0 < P; q0 += 32) {
-    const int q = min(q0 + lane, P - 1);
-    const int k = in.pk[q], l = in.pl[q];
-    const int Atot = iv.rm[k], Btot = iv.rm[l];
-    const int qk = iv.tl[k], ql = iv.tl[l], rk = iv.fr[k], rl = iv.fr[l];
-    const int cAq = Atot + qk, cRB = rl + Btot;
-    // packed entries e = a | job << 7 | b << 13 | lag << 20 in rows of PS words; e & 0x1f80 is
-    // the byte offset of row `job` of the per-lane [job][32] int32 table
-    const unsigned char* pq = reinterpret_cast<const unsigned char*>(in.packed + q);
-    const int strideB = PS * 4;
-    unsigned char* Sb = reinterpret_cast<unsigned char*>(Sl);
-    if constexpr (SMALLN) {
-      // the pair's free positions as a bitmask (bit t = position t in the pair's order) from
-      // the static inverse order (f lookups); both passes walk exactly the f set bits with
-      // bfind: the backward pass on the mask, the forward pass on its bit reversal
-      uint32_t Fr = 0;
-      for (int c = 0; c < f; ++c) Fr |= 1u << in.invord[iv.freej[c] * P + q];
-      const unsigned char* pq31 = pq + 31 * strideB;
-      int A = 0, Bp = 0, pm = NEG;
-      for (uint32_t w = __brev(Fr); w;) {  // ascending positions t = 31 - u
-        const int u = bfind_u32(w);
-        w ^= 1u << u;
-        const unsigned e = *reinterpret_cast<const unsigned*>(pq31 - u * strideB);
-        A += e & 127;
-        const int X = A + static_cast<int>(e >> 20) - Bp;
-        *reinterpret_cast<int*>(Sb + (e & 0x1f80u)) = pm;
-        pm = max(pm, X);
-        Bp += (e >> 13) & 127;
-      }
-      int As = 0, Bs = Atot - Btot, sm = NEG;
-      for (uint32_t w = Fr; w;) {  // descending positions
-        const int t = bfind_u32(w);
-        w ^= 1u << t;
-        const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
-        int* slot = reinterpret_cast<int*>(Sb + (e & 0x1f80u));
-        const int a = e & 127, b = (e >> 13) & 127;
-        Bs += b;
-        const int X = static_cast<int>(e >> 20) + Bs - As;
-        const int I1 = max(*slot + a - b, sm) + Btot;
-        const int lo = max(cAq, I1 + ql), hi = max(cRB, rk + I1 + b - a);
-        *slot = static_cast<int>(static_cast<uint32_t>(lo) | static_cast<uint32_t>(hi) << 16);
-        sm = max(sm, X);
-        As += a;
-      }
-    } else {
-      // n <= 64: same set-bit iteration over a 64-bit free-position mask
-      unsigned long long Fq = 0;
-      for (int c = 0; c < f; ++c) Fq |= 1ull << in.invord[iv.freej[c] * P + q];
-      int A = 0, Bp = 0, pm = NEG;
-      for (unsigned long long w = Fq; w; w &= w - 1) {
-        const int t = __ffsll(static_cast<long long>(w)) - 1;
-        const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
-        A += e & 127;
-        const int X = A + static_cast<int>(e >> 20) - Bp;
-        *reinterpret_cast<int*>(Sb + (e & 0x1f80u)) = pm;
-        pm = max(pm, X);
-        Bp += (e >> 13) & 127;
-      }
-      int As = 0, Bs = Atot - Btot, sm = NEG;
-      for (unsigned long long w = Fq; w;) {
-        const int t = 63 - __clzll(static_cast<long long>(w));
-        w ^= 1ull << t;
-        const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
-        int* slot = reinterpret_cast<int*>(Sb + (e & 0x1f80u));
-        const int a = e & 127, b = (e >> 13) & 127;
-        Bs += b;
-        const int X = static_cast<int>(e >> 20) + Bs - As;
-        const int I1 = max(*slot + a - b, sm) + Btot;
-        const int lo = max(cAq, I1 + ql), hi = max(cRB, rk + I1 + b - a);
-        *slot = static_cast<int>(static_cast<uint32_t>(lo) | static_cast<uint32_t>(hi) << 16);
-        sm = max(sm, X);
-        As += a;
-      }
+  if constexpr (RM) {
+#pragma unroll
+    for (int r = 0; r < RowMask<M, RM>::R; ++r) {
+      const uint32_t Fr = rowmask->w[r] & ~rowmask->bit(in, seljob, r);
+      rowmask->w[r] = Fr;  // the caller branches: the node's free set is the next row
+      lb2_round<M, SMALLN>(iv, in, f, 32 * r, Fr, 0, acc0, acc1);
     }
-    const uint32_t C = static_cast<uint32_t>(Btot + ql) | static_cast<uint32_t>(rk + Atot) << 16;
-    const uint32_t* Hk = H + k;
-    const uint32_t* Hl = H + l;
-    for (int c = 0; c < f; ++c) {
-      const int j = iv.freej[c];
-      const uint32_t hk = Hk[c * M], hl = Hl[c * M];
-      const uint32_t S = static_cast<uint32_t>(Sl[j * 32]);
-      const uint32_t V = max_u16x2(add_u16x2(__byte_perm(hk, hl, 0x7610), S), add_u16x2(__byte_perm(hl, hk, 0x7610), C));
-      const uint32_t vF = __reduce_max_sync(FULL, V & 0xffffu);
-      const uint32_t vB = __reduce_max_sync(FULL, V) & 0xffff0000u;
-      if (lane == (c & 31)) {
-        if (SMALLN || c < 32) acc0 = max_u16x2(acc0, vF | vB);
-        else acc1 = max_u16x2(acc1, vF | vB);
+  } else {
+    for (int q0 = 0; q0 < P; q0 += 32) {
+      const int q = min(q0 + lane, P - 1);
+      uint32_t Fr = 0;
+      unsigned long long Fq = 0;
+      if constexpr (SMALLN) {
+        for (int c = 0; c < f; ++c) Fr |= 1u << in.invord[iv.freej[c] * P + q];
+      } else {
+        for (int c = 0; c < f; ++c) Fq |= 1ull << in.invord[iv.freej[c] * P + q];
       }
+      lb2_round<M, SMALLN>(iv, in, f, q0, Fr, Fq, acc0, acc1);
     }
   }
   if (lane < f) {
@@ -685,10 +750,10 @@ __device__ __forceinline__ bool reached_end(const Group<G>& grp, const IvmView& 
 
 // select_next (src/ivm.cpp:99-122) with the incremental R / d1 / d2 bookkeeping.
 // Returns the selected cell, or -1 when the explorer is exhausted.
-template <int M, int G>
+template <int M, int G, bool RM>
 __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& iv,
                                            const InstView& in, int n, int mp, bool has_end,
-                                           int& level, int& d1, int& d2) {
+                                           int& level, int& d1, int& d2, RowMask<M, RM>& rowmask) {
   for (;;) {
     if (level < 0) return -1;
     const int len = n - level;
@@ -716,6 +781,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
         const int job = (x < 0 ? -x : x) - 1;
         const int* pr = in.p32 + job * mp;
         for (int k = grp.g; k < M; k += G) iv.R[k] = static_cast<uint16_t>(iv.R[k] + pr[k]);
+        rowmask.add(in, job);  // the row one level up holds the job selected there
         grp.sync();
         if (grp.g == 0) iv.V[level] = static_cast<int8_t>(psel + 1);
       }
@@ -735,11 +801,11 @@ struct StepCounters {
 };
 
 // Decompose the node at (level, sel) and branch (bound.cpp:98-139 + ivm.cpp:124-145).
-template <int M, int G, int BOUND, bool SMALLN>
+template <int M, int G, int BOUND, bool SMALLN, bool RM>
 __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmView& iv,
                                                  const InstView& in, int n, int mp, int sel,
                                                  int prune, int& level, int& d1, int& d2,
-                                                 unsigned* shist) {
+                                                 unsigned* shist, RowMask<M, RM>& rowmask) {
   const int I = level;
   const int f = n - 1 - I;
   int8_t* row = iv.cells + tri_off(I, n);
@@ -754,7 +820,7 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
   if constexpr (BOUND == kLB1) {
     children_lb1<M, G>(grp, iv, in, mp, f);
   } else if constexpr (G == 32) {
-    children_lb2_w<M, SMALLN>(iv, in, n, mp, f, fm);
+    children_lb2_w<M, SMALLN, RM>(iv, in, n, mp, f, fm, &rowmask, job);
   } else {
     children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
   }
@@ -958,13 +1024,23 @@ __device__ __forceinline__ void stage_prefix_sums(unsigned char* smem, const Ins
   }
 }
 
+// incremental row masks (RowMask) for the warp-per-explorer LB2 path with n <= 32: 6 more
+// persistent registers per lane, hence at most 28 warps (explorers) per CTA. Measured on the
+// ta021 LB2 proof: 249 ms with, 227 ms without (the lost warps and a register spill cost more
+// than the f inverse-order lookups per pair round it saves), so it is compiled out.
+template <int BOUND, int G, bool SMALLN>
+constexpr bool kRowMask = false;
+template <int BOUND, int G, bool SMALLN>
+constexpr int kExploreThreads = (BOUND == kLB1 && G == 8) ? 768 : (kRowMask<BOUND, G, SMALLN> ? 896 : 1024);
+
 template <int M, int G, int BOUND, bool SMALLN = false>
-__global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explore_kernel(const ExploreParams P) {
+__global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_kernel(const ExploreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = P.L;
   const int n = L.n, mp = L.mp;
   const int NG = blockDim.x / G;  // explorers per CTA
   constexpr bool PACKED = BOUND == kLB2 && G == 32;
+  constexpr bool RM = kRowMask<BOUND, G, SMALLN>;
   const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? P.npairs : 0, PACKED);
 
   // ---- stage the instance (and LB2 pair tables) into shared memory
@@ -997,17 +1073,15 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
     unsigned* cnt = reinterpret_cast<unsigned*>(smem + IL.o_cnt);
     if (threadIdx.x < 16) cnt[threadIdx.x] = 0;
   }
-  // ---- stage this CTA's explorers
+  // ---- stage this CTA's explorers (a warp per explorer block, 16-byte words over the lanes)
   const int first = blockIdx.x * NG;
   unsigned char* ivbase = smem + IL.bytes;
   {
-    const int words = L.gstride / 16;
-    for (int idx = threadIdx.x; idx < NG * words; idx += blockDim.x) {
-      const int i = idx / words, w = idx % words;
-      if (first + i < P.K) {
-        reinterpret_cast<uint4*>(ivbase + i * L.sstride)[w] =
-            reinterpret_cast<const uint4*>(P.state + static_cast<size_t>(first + i) * L.gstride)[w];
-      }
+    const int words = L.gstride / 16, nw = blockDim.x >> 5;
+    for (int i = threadIdx.x >> 5; i < NG && first + i < P.K; i += nw) {
+      const uint4* src = reinterpret_cast<const uint4*>(P.state + static_cast<size_t>(first + i) * L.gstride);
+      uint4* dst = reinterpret_cast<uint4*>(ivbase + i * L.sstride);
+      for (int w = threadIdx.x & 31; w < words; w += 32) dst[w] = src[w];
     }
   }
   __syncthreads();
@@ -1034,6 +1108,8 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
     int level = iv.hdr->level, state = iv.hdr->state, d1 = iv.hdr->d1, d2 = iv.hdr->d2;
     int rlev = iv.hdr->rlev, nrep = iv.hdr->nrep;
     const bool has_end = iv.hdr->has_end != 0;
+    RowMask<M, RM> rowmask;
+    if (state != kEmpty) rowmask.build(iv, in, n, level);
     if (grp.g == 0 && state != kEmpty) atomicAdd(reinterpret_cast<unsigned*>(smem + IL.o_cnt) + 6, 1u);
     int best = grp.bcast(grp.g == 0 ? *reinterpret_cast<volatile int*>(&P.ctr->best) : 0, 0);
     int step = 0;
@@ -1079,13 +1155,13 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
           state = kActive;
           continue;
         }
-        decompose_branch<M, G, BOUND, SMALLN>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist);
+        decompose_branch<M, G, BOUND, SMALLN, RM>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist, rowmask);
         ++sc.decomposed;
         ++nrep;
         rlev = level;
         continue;
       }
-      const int sel = select_next<M, G>(grp, iv, in, n, mp, has_end, level, d1, d2);
+      const int sel = select_next<M, G, RM>(grp, iv, in, n, mp, has_end, level, d1, d2, rowmask);
       if (sel < 0) {
         state = kEmpty;
         break;
@@ -1094,7 +1170,7 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
         leaf<M, G>(grp, iv, in, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc, P.census, P.census_cap);
         continue;
       }
-      decompose_branch<M, G, BOUND, SMALLN>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist);
+      decompose_branch<M, G, BOUND, SMALLN, RM>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist, rowmask);
       ++sc.decomposed;
     }
     if (grp.g == 0) {
@@ -1117,13 +1193,11 @@ __global__ void __launch_bounds__((BOUND == kLB1 && G == 8) ? 768 : 1024) explor
   __syncthreads();
   // ---- write back explorers and counters
   {
-    const int words = L.gstride / 16;
-    for (int idx = threadIdx.x; idx < NG * words; idx += blockDim.x) {
-      const int i = idx / words, w = idx % words;
-      if (first + i < P.K) {
-        reinterpret_cast<uint4*>(P.state + static_cast<size_t>(first + i) * L.gstride)[w] =
-            reinterpret_cast<const uint4*>(ivbase + i * L.sstride)[w];
-      }
+    const int words = L.gstride / 16, nw = blockDim.x >> 5;
+    for (int i = threadIdx.x >> 5; i < NG && first + i < P.K; i += nw) {
+      uint4* dst = reinterpret_cast<uint4*>(P.state + static_cast<size_t>(first + i) * L.gstride);
+      const uint4* src = reinterpret_cast<const uint4*>(ivbase + i * L.sstride);
+      for (int w = threadIdx.x & 31; w < words; w += 32) dst[w] = src[w];
     }
     const unsigned* cnt = reinterpret_cast<const unsigned*>(smem + IL.o_cnt);
     if (threadIdx.x == 0) {

@@ -274,8 +274,9 @@ void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::v
       }
     }
   }
-  // transposed packed form [t][q] = a | job << 7 | b << 13 | lag << 20 (children_lb2_w; the
-  // job field is pre-shifted to the byte offset of its row in the per-lane [job][32] int32 table)
+  // transposed packed form [t][q] = job << 7 | u << 13 | v << 24 with u = a + lag (11 bits) and
+  // v = a - b (8 bits, signed) for children_lb2_w: the job field is pre-shifted to the byte
+  // offset of its row in the per-lane [job][32] int32 table
   const int PS = round_up(P, 32);  // row stride padded to 32 pairs (bank-conflict-free passes)
   packed.assign(static_cast<size_t>(PS) * n, 0);
   packable = n <= 64;
@@ -285,9 +286,10 @@ void lb2_tables(int n, int m, const int32_t* p, std::vector<uint8_t>& pk, std::v
       const int a = p[static_cast<size_t>(j) * m + pk[static_cast<size_t>(qq)]];
       const int b = p[static_cast<size_t>(j) * m + pl[static_cast<size_t>(qq)]];
       const int lg = lag[static_cast<size_t>(qq) * n + j];
-      if (a > 127 || b > 127 || lg > 2047) packable = false;
-      packed[static_cast<size_t>(t) * PS + qq] =
-          static_cast<uint32_t>(a) | static_cast<uint32_t>(j) << 7 | static_cast<uint32_t>(b) << 13 | static_cast<uint32_t>(lg) << 20;
+      const int u = a + lg, v = a - b;
+      if (u > 2047 || v < -128 || v > 127) packable = false;
+      packed[static_cast<size_t>(t) * PS + qq] = static_cast<uint32_t>(j) << 7 | static_cast<uint32_t>(u & 0x7ff) << 13 |
+                                                 static_cast<uint32_t>(v & 0xff) << 24;
     }
   }
 }
