@@ -444,6 +444,13 @@ struct RowMask {
   }
 };
 
+// Fold each S_j into child j's bounds inside the backward pass (shared atomicMax, no S table
+// pass and no per-child REDUX pair) instead of a separate child loop: measured faster for n > 32
+// (ta056 LB2 18.8 -> 22.0 M nodes/s, f ~ 30) and slower for n <= 32 (ta021 LB2 225 -> 275 ms,
+// f ~ 10: the lanes' Johnson orders collide on the same jobs and the atomics serialize).
+template <bool SMALLN>
+constexpr bool kFusedCombine = !SMALLN;
+
 // One pair round of children_lb2_w: lane q's pair, the forward / backward passes over the set
 // bits of Fr (the node's free positions in the pair's order), then every child's bound for
 // the round's 32 pairs folded into acc (lane c holds child c).
@@ -472,6 +479,24 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
   const unsigned char* pq = reinterpret_cast<const unsigned char*>(in.packed + q);
   const int strideB = PS * 4;
   unsigned char* Sb = reinterpret_cast<unsigned char*>(Sl);
+  const uint32_t C = static_cast<uint32_t>(Btot + ql) | static_cast<uint32_t>(rk + Atot) << 16;
+  // S_j of the backward pass: kept for the child loop below, or (kFusedCombine<SMALLN>) folded at once
+  // into child j's bounds: V = max(H'_k|H'_l + S_j, H'_l|H'_k + C) with job-indexed H' rows and
+  // shared-memory atomicMax into the job-indexed lbf / lbb
+  const uint32_t* Hk = H + k;
+  const int dkl = l - k;
+  auto fold = [&](unsigned e, uint32_t S, int* slot) {
+    if constexpr (kFusedCombine<SMALLN>) {
+      const int job = static_cast<int>((e >> 7) & 63u);
+      const uint32_t* hp = Hk + job * M;
+      const uint32_t hk = hp[0], hl = hp[dkl];
+      const uint32_t V = max_u16x2(add_u16x2(__byte_perm(hk, hl, 0x7610), S), add_u16x2(__byte_perm(hl, hk, 0x7610), C));
+      atomicMax(reinterpret_cast<unsigned*>(iv.lbf) + job, V & 0xffffu);
+      atomicMax(reinterpret_cast<unsigned*>(iv.lbb) + job, V >> 16);
+    } else {
+      *slot = static_cast<int>(S);
+    }
+  };
   if constexpr (SMALLN) {
     // both passes walk exactly the f set bits with bfind: the backward pass on the mask, the
     // forward pass on its bit reversal (position t = 31 - u, address pq31 - u * stride)
@@ -495,7 +520,7 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
       const int v = static_cast<int>(e) >> 24;
       const int I1 = max(*slot + v, sm);
       const int lo = max(cAq, I1 + ql), hi = max(cRB, I1 + (rk - v));
-      *slot = static_cast<int>(__byte_perm(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi), 0x5410));
+      fold(e, __byte_perm(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi), 0x5410), slot);
       G -= v;
       sm = max(sm, G + static_cast<int>((e >> 13) & 0x7ffu));
     }
@@ -518,13 +543,12 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
       const int v = static_cast<int>(e) >> 24;
       const int I1 = max(*slot + v, sm);
       const int lo = max(cAq, I1 + ql), hi = max(cRB, I1 + (rk - v));
-      *slot = static_cast<int>(__byte_perm(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi), 0x5410));
+      fold(e, __byte_perm(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi), 0x5410), slot);
       G -= v;
       sm = max(sm, G + static_cast<int>((e >> 13) & 0x7ffu));
     }
   }
-  const uint32_t C = static_cast<uint32_t>(Btot + ql) | static_cast<uint32_t>(rk + Atot) << 16;
-  const uint32_t* Hk = H + k;
+  if constexpr (kFusedCombine<SMALLN>) return;
   const uint32_t* Hl = H + l;
   for (int c = 0; c < f; ++c) {
     const int j = iv.freej[c];
@@ -552,10 +576,12 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
                                                unsigned long long fmask, RowMask<M, RM>* rowmask = nullptr,
                                                int seljob = 0) {
   const int lane = threadIdx.x & 31;
-  uint32_t* H = reinterpret_cast<uint32_t*>(iv.heads);  // [c][M] h' | t' << 16
+  uint32_t* H = reinterpret_cast<uint32_t*>(iv.heads);  // [c][M] (kFusedCombine: [job][M]) h' | t' << 16
   for (int c = lane; c < f; c += 32) {
     const int j = iv.freej[c];
     const int* pr = in.p32 + j * mp;
+    const int row = kFusedCombine<SMALLN> ? j : c;
+    if (kFusedCombine<SMALLN>) iv.lbf[j] = iv.lbb[j] = 0;
     int hp[M];
     int prev = 0;
 #pragma unroll
@@ -568,7 +594,7 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
     for (int k = M - 1; k >= 0; --k) {
       const int tp = max(prev, iv.tl[k]);
       prev = tp + pr[k];
-      H[c * M + k] = static_cast<uint32_t>(hp[k]) | static_cast<uint32_t>(tp) << 16;
+      H[row * M + k] = static_cast<uint32_t>(hp[k]) | static_cast<uint32_t>(tp) << 16;
     }
   }
   __syncwarp();
@@ -593,6 +619,21 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
       }
       lb2_round<M, SMALLN>(iv, in, f, q0, Fr, Fq, acc0, acc1);
     }
+  }
+  if constexpr (kFusedCombine<SMALLN>) {  // job-indexed -> child-indexed (lane c holds children c, c + 32)
+    __syncwarp();
+    int a0 = 0, b0 = 0, a1 = 0, b1 = 0;
+    if (lane < f) {
+      a0 = iv.lbf[iv.freej[lane]];
+      b0 = iv.lbb[iv.freej[lane]];
+    }
+    if (lane + 32 < f) {
+      a1 = iv.lbf[iv.freej[lane + 32]];
+      b1 = iv.lbb[iv.freej[lane + 32]];
+    }
+    acc0 = static_cast<uint32_t>(a0) | static_cast<uint32_t>(b0) << 16;
+    acc1 = static_cast<uint32_t>(a1) | static_cast<uint32_t>(b1) << 16;
+    __syncwarp();
   }
   if (lane < f) {
     iv.lbf[lane] = static_cast<int>(acc0 & 0xffffu);
