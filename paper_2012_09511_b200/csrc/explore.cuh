@@ -118,7 +118,9 @@ __host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound, int lan
     o += round_up(n * m * 2, 16);
     L.o_lst = o;
     if (lanes == 32) {
-      o += round_up(2 * n * 32 * 2, 16);  // int16 PM[j][lane], SM[j][lane]
+      // per-lane [job][32] table: int32 PM' then S_j (n <= 32), int16 PM' only (n > 32: S_j is
+      // folded into the child bounds in the backward pass)
+      o += round_up(n * 32 * (n <= 32 ? 4 : 2), 16);
       L.o_pos = 0;
     } else {
       o += n * 16;
@@ -525,12 +527,15 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
       sm = max(sm, G + static_cast<int>((e >> 13) & 0x7ffu));
     }
   } else {
-    // n <= 64: same set-bit iteration over a 64-bit free-position mask
+    // n <= 64: same set-bit iteration over a 64-bit free-position mask; S_j is folded at once
+    // (kFusedCombine), so the per-lane table only carries PM' and is int16 ([job][32] x 2 B)
+    static_assert(kFusedCombine<SMALLN>, "the n > 32 path keeps only PM' in its lane table");
+    unsigned char* Pb = reinterpret_cast<unsigned char*>(reinterpret_cast<int16_t*>(iv.pm) + lane);
     int E = Btot, pm = NEG;
     for (unsigned long long w = Fq; w; w &= w - 1) {
       const int t = __ffsll(static_cast<long long>(w)) - 1;
       const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
-      *reinterpret_cast<int*>(Sb + (e & 0x1f80u)) = pm;
+      *reinterpret_cast<int16_t*>(Pb + ((e & 0x1f80u) >> 1)) = static_cast<int16_t>(pm);
       pm = max(pm, E + static_cast<int>((e >> 13) & 0x7ffu));
       E += static_cast<int>(e) >> 24;
     }
@@ -539,9 +544,9 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
       const int t = 63 - __clzll(static_cast<long long>(w));
       w ^= 1ull << t;
       const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
-      int* slot = reinterpret_cast<int*>(Sb + (e & 0x1f80u));
+      int* slot = nullptr;
       const int v = static_cast<int>(e) >> 24;
-      const int I1 = max(*slot + v, sm);
+      const int I1 = max(static_cast<int>(*reinterpret_cast<const int16_t*>(Pb + ((e & 0x1f80u) >> 1))) + v, sm);
       const int lo = max(cAq, I1 + ql), hi = max(cRB, I1 + (rk - v));
       fold(e, __byte_perm(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi), 0x5410), slot);
       G -= v;
