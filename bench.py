@@ -156,6 +156,15 @@ def cpu_sample(wl, seconds, cores):
                       f"UB={ub}, {cores} threads, {seconds:.0f} s of the proof ({r['unique']} unique nodes)"}
 
 
+def base_config(args, wl, world):
+    """The `config` both arms print (identical keys and values for the same workload)."""
+    tlim = float(wl.get("time_limit", 0.0))
+    return {"workload": args.workload, "instance": wl["instance"], "bound": wl["bound"].upper(),
+            "initial_ub": wl["ub"], "pinned": bool(wl.get("pinned", False)),
+            "mode": (f"time-bounded ({tlim:g} s) per step" if tlim else "full proof (fixed tree) per step"),
+            "parallelism": f"dp{world}" if world > 1 else "single", "desc": wl["desc"]}
+
+
 def run_reference(args, wl, rank):
     if rank != 0:
         return 0
@@ -172,8 +181,7 @@ def run_reference(args, wl, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * args.ref_step_s,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (Taillard generator, published seed)",
-            "config": {"workload": args.workload, "instance": wl["instance"], "bound": wl["bound"].upper(),
-                       "initial_ub": wl["ub"], "desc": wl["desc"]},
+            "config": base_config(args, wl, args.gpus),
             "cpu_baseline": cb, "e2e": {"value": v, "unit": "nodes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -210,8 +218,13 @@ def run_extras(pbb, solve_distributed, dev, local, world, rank, peak, args):
         solve_distributed(pool, 2297, device=dev)
         r, ms = timed(lambda: solve_distributed(pool, 2297, device=dev))
     out["ta021_lb1_ub2297_full_proof"] = {
-        "ms": ms, "unique_nodes": r.unique, "leaves": r.leaves, "nodes_per_s": r.unique / (ms / 1e3),
-        "reference_1core_s": 534.8, "reference_note": "SURVEY.md Appendix C (reference K=1, this build container)"}
+        "ms": ms, "unique_nodes": r.unique, "leaves": r.leaves, "nodes_per_s": r.unique / (ms / 1e3)}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        # the compiled reference itself (oracle/_ref/ref_driver: pool_run, K = 8 x threads) on this
+        # box's host cores, same workload, time-bounded sample
+        cb = cpu_sample(WORKLOADS["ta021-lb1"], args.ref_lb1_s, cpu_cores())
+        out["ta021_lb1_ub2297_full_proof"]["cpu_baseline"] = cb
+        out["ta021_lb1_ub2297_full_proof"]["vs_cpu_reference"] = (r.unique / (ms / 1e3)) / cb["value"]
     for key, name, bound, ub, pinned, secs in (("ta056_lb2_ub3679_timebounded", "ta056", "lb2", 3679, False, 5.0),
                                                ("ta041_lb1_pinned3000_timebounded", "ta041", "lb1", 3000, True, 5.0)):
         inst = pbb.taillard_named(name)
@@ -269,6 +282,7 @@ def main():
     ap.add_argument("--cpu-sample-s", type=float, default=20.0)
     ap.add_argument("--ref-step-s", type=float, default=15.0)
     ap.add_argument("--ref-warmup-s", type=float, default=3.0)
+    ap.add_argument("--ref-lb1-s", type=float, default=30.0, help="reference LB1 CPU sample in the extras")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
@@ -363,12 +377,23 @@ def main():
     peak = pbb.int32_peak(local)
     tr = load_traffic()
     traffic = tr.get(f"{args.workload}:explore_kernel_dram_bytes_per_launch")
+    # executed work beside the algorithmic W: thread instructions per decomposed node of the
+    # explore kernel (ncu smsp__thread_inst_executed.sum of one launch / that launch's raw
+    # decomposed nodes, profiles/ncu_summary.json) x this step's raw decomposed nodes
+    tipn = tr.get(f"{args.workload}:explore_kernel_thread_inst_per_node")
+    raw_step = results[-1].decomposed
     roofline = {"bound": "int_alu", "achieved": ops / (kms / 1000.0) / 1e12, "peak": peak * world / 1e12,
                 "unit": "Tops/s", "frac": (ops / (kms / 1000.0)) / (peak * world), "traffic": traffic,
                 "kernel": "explore_kernel", "kernel_ms_per_step": kms,
                 "kernel_share_of_step": kms / statistics.mean(times),
                 "ops_per_step": ops, "ops_model": "SURVEY.md §8(d) W2(f)" if wl["bound"] == "lb2" else "SURVEY.md §8(d) W1(f)",
                 "peak_source": "pbbgpu_int32_peak microbenchmark, this run (add+max streams; MEASURED_PEAKS.json has no integer peak)"}
+    if tipn:
+        ex = tipn * raw_step
+        roofline.update({"executed_ops": ex, "executed_ops_source": "ncu thread instructions per decomposed node "
+                         "(profiles/ncu_summary.json) x raw decomposed nodes of the step",
+                         "executed_frac": ex / (kms / 1000.0) / (peak * world),
+                         "alg_ops_per_executed": ops / ex})
 
     # e2e: the C-ABI calls a user makes, HOST buffers in, results back to host, per step. A
     # serving loop keeps one pool per instance shape (created once, outside the timed region)
@@ -416,17 +441,13 @@ def main():
                 "warmup": args.warmup, "ms_per_step": statistics.mean(times), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "int32",
                 "data": "synthetic (Taillard instance regenerated from its published seed; exact benchmark matrix)",
-                "config": {"workload": args.workload, "instance": wl["instance"], "bound": wl["bound"].upper(),
-                           "initial_ub": wl["ub"],
-                           "mode": (f"time-bounded ({tlim:g} s) per step" if tlim else "full proof (fixed tree) per step"),
-                           "unique_nodes_per_step": unique, "leaves_per_step": results[-1].leaves,
+                "config": base_config(args, wl, world),
+                "details": {"unique_nodes_per_step": unique, "leaves_per_step": results[-1].leaves,
                            "time_to_proof_ms": statistics.mean(times), "explorers_per_gpu": pool.K(),
                            "work_split": "live siblings" if int(wl.get("split_mode", 0)) == 1 else "factoradic (reference)",
                            "initial_partition": (f"breadth-first seeding into world*K/{seed_div} intervals"
                                                  if seed_div else "world*K equal factoradic ranges, interleaved"),
-                           "parallelism": f"dp{world}" if world > 1 else "single",
-                           "l2": "256 MiB flush between steps, outside the per-step event brackets",
-                           "desc": wl["desc"]},
+                           "l2": "256 MiB flush between steps, outside the per-step event brackets"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks, "extra": extra}
         print(json.dumps(line), flush=True)

@@ -48,14 +48,23 @@ def w2(f, n, m):
 
 
 def cmd_explore(inst_name, bound, ub, rounds):
+    """One explore launch per round (rounds_per_sync = 1); prints the raw decomposed nodes of
+    every round, so an ncu capture of explore launch s + 1 (-s s -c 1) can be divided by its
+    round's node count (profiles/ncu_summary.json: thread instructions per decomposed node)."""
     import paper_2012_09511_b200 as pbb
     inst = pbb.taillard_named(inst_name)
-    with pbb.GpuPool(inst, pbb.PoolConfig(), bound=bound) as pool:
+    with pbb.GpuPool(inst, pbb.PoolConfig(rounds_per_sync=1), bound=bound) as pool:
         pool.set_initial_bound(int(ub))
         pool.assign_split()
+        per_round, last = [], 0
         for _ in range(int(rounds)):
-            if pool.run_round() == 0:
+            act = pool.run_round()
+            d = pool.stats().decomposed
+            per_round.append(d - last)
+            last = d
+            if act == 0:
                 break
+        print(json.dumps({"raw_decomposed_per_round": per_round}))
         print(pool.stats())
 
 
