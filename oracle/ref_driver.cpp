@@ -11,7 +11,7 @@
 //
 // Modes
 //   solve  <ta> <ub|neh> <K> <threads> [time_limit_s]      pool_run
-//   hist   <ta> <ub>                                      K=1 fixed tree + per-f histogram
+//   hist   <ta|gen:n:m:seed> <ub>                         K=1 fixed tree + per-f histogram
 //   nodes  <ta> <ub> <seed> <starts> <per_start>          per-node decompose dump
 //   pinned <ta> <ub> <threads> <seconds> <prefix_depth>   prune>=ub, never improve
 //   neh    <ta>                                           NEH makespan + perm
@@ -61,6 +61,16 @@ int lnz(const Factoradic& a) {
   return r;
 }
 
+Instance named_or_generated(const char* s) {
+  if (std::strncmp(s, "gen:", 4) == 0) {
+    int n = 0, m = 0;
+    long seed = 0;
+    if (std::sscanf(s + 4, "%d:%d:%ld", &n, &m, &seed) != 3) throw std::invalid_argument("gen:n:m:seed");
+    return generate_taillard(n, m, static_cast<std::int32_t>(seed));
+  }
+  return taillard_named(s);
+}
+
 int cmd_solve(int argc, char** argv) {
   if (argc < 6) return 2;
   Instance inst = taillard_named(argv[2]);
@@ -90,7 +100,7 @@ int cmd_solve(int argc, char** argv) {
 // explore loop), with a histogram of decomposed nodes by free-job count f.
 int cmd_hist(int argc, char** argv) {
   if (argc < 4) return 2;
-  Instance inst = taillard_named(argv[2]);
+  Instance inst = named_or_generated(argv[2]);
   const std::int64_t ub = parse_ub(inst, argv[3]);
   const int n = inst.n;
   Ivm ivm(n);
@@ -305,16 +315,6 @@ int cmd_ckptload(int argc, char** argv) {
   }
   std::printf("]}\n");
   return 0;
-}
-
-Instance named_or_generated(const char* s) {
-  if (std::strncmp(s, "gen:", 4) == 0) {
-    int n = 0, m = 0;
-    long seed = 0;
-    if (std::sscanf(s + 4, "%d:%d:%ld", &n, &m, &seed) != 3) throw std::invalid_argument("gen:n:m:seed");
-    return generate_taillard(n, m, static_cast<std::int32_t>(seed));
-  }
-  return taillard_named(s);
 }
 
 int cmd_stats(int argc, char** argv) {

@@ -1150,7 +1150,8 @@ struct TraceScope {
 };
 
 struct pbbgpu_pool {
-  int n = 0, m = 0, mp = 0, bound = 0;
+  int n = 0, m = 0, mp = 0, bound = 0;  // m: compiled machine count (5, 10, 20)
+  int m_real = 0;                        // the instance's machines (zero-time machines pad to m)
   pbbgpu_config_t cfg{};
   std::vector<int32_t> p;
   int K = 0, G = 0, steps = 0, grid = 0, block = 128;
@@ -1316,12 +1317,31 @@ void validate_times(int n, int m, const int32_t* p) {
   if (static_cast<int64_t>(n + m) * pmax >= 65536) throw std::invalid_argument("pbbgpu: (n+m)*max(p) must stay below 2^16");
 }
 
-HostTables build_tables(int n, int m, int bound, const int32_t* p, bool big) {
+// Compiled machine count for an instance with m machines: the instance is padded with
+// zero-time machines after the last one. A trailing zero machine changes no makespan, no
+// front / tail / remain of a real machine and no LB1 value (its chain term never exceeds the
+// last real machine's), and LB2 pairs are built over the real machines only, so every value
+// the reference defines is unchanged (tests/test_gpu.py::test_any_machine_count_*).
+int compiled_m(int m) {
+  if (m < 1 || m > 20) throw std::invalid_argument("pbbgpu: m must be in [1, 20] (padded to 5, 10 or 20 machines)");
+  return m <= 5 ? 5 : (m <= 10 ? 10 : 20);
+}
+
+std::vector<int32_t> pad_machines(int n, int m, int M, const int32_t* p) {
+  std::vector<int32_t> q(static_cast<size_t>(n) * M, 0);
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < m; ++k) q[static_cast<size_t>(j) * M + k] = p[static_cast<size_t>(j) * m + k];
+  return q;
+}
+
+// m: the instance's machines (p_real row stride, LB2 pairs); M: compiled (p32 / ptot width).
+HostTables build_tables(int n, int m, int M, int bound, const int32_t* p_real, bool big) {
   HostTables T;
-  const int mp = round_up(m, 4);
+  const int mp = round_up(M, 4);
   const int npairs = m * (m - 1) / 2;
+  const int32_t* p = p_real;
   T.p32.assign(static_cast<size_t>(n) * mp, 0);
-  T.ptot.assign(static_cast<size_t>(m), 0);
+  T.ptot.assign(static_cast<size_t>(M), 0);
   for (int j = 0; j < n; ++j)
     for (int k = 0; k < m; ++k) {
       T.p32[static_cast<size_t>(j) * mp + k] = p[static_cast<size_t>(j) * m + k];
@@ -1438,18 +1458,20 @@ void reset_search(pbbgpu_pool* P) {
   P->host_improvements = 0;
 }
 
-void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const pbbgpu_config_t* cfg) {
+void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bound, const pbbgpu_config_t* cfg) {
   if (n < 2 || n > kBigMaxN) throw std::invalid_argument("pbbgpu: n must be in [2, 512]");
-  if (m != 5 && m != 10 && m != 20) throw std::invalid_argument("pbbgpu: m must be 5, 10 or 20 (compiled machine counts)");
   if (bound != kLB1 && bound != kLB2) throw std::invalid_argument("pbbgpu: bound must be PBBGPU_LB1 or PBBGPU_LB2");
-  validate_times(n, m, p);
+  const int m = compiled_m(m_real);
+  if (bound == kLB2 && m_real < 2) bound = kLB1;  // no machine pair: LB2 is LB1
+  validate_times(n, m, pad_machines(n, m_real, m, p_real).data());
+  P->m_real = m_real;
   if (cfg && cfg->record_census && n > 20) throw std::invalid_argument("record_census needs n <= 20 (position_u64)");
   if (cfg && cfg->steal_policy == 1 && n > 30) throw std::invalid_argument("the reference steal policy needs n <= 30");
   if (cfg && (cfg->steal_policy < 0 || cfg->steal_policy > 1)) throw std::invalid_argument("steal_policy must be 0 or 1");
   P->n = n;
   P->m = m;
   P->bound = bound;
-  P->p.assign(p, p + static_cast<size_t>(n) * m);
+  P->p = pad_machines(n, m_real, m, p_real);  // host makespans on the padded matrix are the instance's
   if (cfg) P->cfg = *cfg;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw CudaError("pbbgpu: no CUDA device (the product path has no CPU fallback)");
@@ -1466,8 +1488,8 @@ void pool_init(pbbgpu_pool* P, int n, int m, const int32_t* p, int bound, const 
   }
   P->rounds_per_sync = P->cfg.rounds_per_sync > 0 ? std::min(P->cfg.rounds_per_sync, 8) : 3;
 
-  if (bound == kLB2) P->npairs = m * (m - 1) / 2;
-  const HostTables T = build_tables(n, m, bound, p, n > kMaxN);
+  if (bound == kLB2) P->npairs = m_real * (m_real - 1) / 2;
+  const HostTables T = build_tables(n, m_real, m, bound, p_real, n > kMaxN);
   const bool packable = T.packable;
   if (n > kMaxN) {  // batch-only pool: the large-n bounding kernel, no explorers
     P->batch_only = true;
@@ -2096,12 +2118,13 @@ void pbbgpu_destroy(pbbgpu_pool* P) {
 int pbbgpu_load_instance(pbbgpu_pool* P, const int32_t* p) {
   return guarded([&] {
     if (!P || !p) throw std::invalid_argument("pbbgpu_load_instance: null argument");
-    validate_times(P->n, P->m, p);
-    const HostTables T = build_tables(P->n, P->m, P->bound, p, P->batch_only);
+    std::vector<int32_t> padded = pad_machines(P->n, P->m_real, P->m, p);
+    validate_times(P->n, P->m, padded.data());
+    const HostTables T = build_tables(P->n, P->m_real, P->m, P->bound, p, P->batch_only);
     if (P->bound == kLB2 && !P->batch_only && P->G == 32 && !T.packable)
       throw CapacityError("pbbgpu_load_instance: this instance's LB2 tables do not pack into 31 bits; create a new pool");
     ck(cudaStreamSynchronize(P->stream), "sync");
-    P->p.assign(p, p + static_cast<size_t>(P->n) * P->m);
+    P->p = std::move(padded);
     upload_tables(P, T);
     reset_search(P);
   });

@@ -28,6 +28,10 @@ def main():
     # fixed trees (UB = optimum) and improving runs, K = 1 (pool_run semantics)
     for name, ub in (("ta001", 1278), ("ta011", 1582), ("ta031", 2724), ("ta041", 2991)):
         counts[f"{name}@{ub}"] = json.loads(run("hist", name, ub))
+    # machine counts the compiled kernels do not have (padded with zero-time machines), incl. a
+    # VFR-like 30 x 15 instance
+    for name, ub in (("gen:30:15:4242", 2490), ("gen:16:13:1234", 1512), ("gen:18:3:77", 926)):
+        counts[f"{name}@{ub}"] = json.loads(run("hist", name, ub))
     for name in ("ta001", "ta041"):
         counts[f"{name}@neh"] = json.loads(run("solve", name, "neh", 1, 1))
     for name in ("ta001", "ta011", "ta021", "ta031", "ta041", "ta056", "ta111"):

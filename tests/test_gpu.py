@@ -756,3 +756,38 @@ def test_reference_coordinator_drives_several_gpu_workers():
     assert r["splits"] > 0 and r["updates_applied"] > 3
     assert r["leaves"] >= 54 and r["unique"] >= 158049
     assert r["coordinator_total_nodes"] == r["decomposed"]
+
+
+# ---------------------------------------------------------------- any machine count (m <= 20)
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 7, 9, 13, 15, 17, 19])
+@pytest.mark.parametrize("bound", ["lb1", "lb2"])
+def test_any_machine_count_bounds_match_oracle(m, bound):
+    """m not in {5, 10, 20}: the pool pads the instance with zero-time machines; every child
+    bound (LB2 over the real machine pairs only; m = 1: LB1) equals the oracle's."""
+    n = 12
+    inst = pbb.generate_taillard(n, m, 500 + m)
+    perms, d1s, d2s = _random_nodes(n, 300, m)
+    prob = orc.Problem(inst.p, orc.LB1 if bound == "lb1" else orc.LB2)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=128), bound=bound) as pool:
+        lb, dr, pr, lf, lbw = pool.decompose_batch(perms, d1s, d2s, 10 ** 6)
+    for i in range(len(d1s)):
+        f = n - d1s[i] - d2s[i]
+        fw, bw = prob.children_bounds(perms[i], d1s[i], d2s[i])
+        assert [int(x) for x in lf[i, :f]] == fw and [int(x) for x in lbw[i, :f]] == bw
+        d, clb, _ = prob.decompose(perms[i], d1s[i], d2s[i], 10 ** 6)
+        assert int(dr[i]) == d and [int(x) for x in lb[i, :f]] == clb
+
+
+@pytest.mark.parametrize("key", ["gen:30:15:4242@2490", "gen:16:13:1234@1512", "gen:18:3:77@926"])
+def test_any_machine_count_fixed_trees_match_reference(key):
+    """Fixed trees of instances with 15 (VFR-like 30 x 15), 13 and 3 machines: unique node count,
+    leaves and the per-f histogram equal the compiled reference's (ref_driver hist)."""
+    g = golden_io.ref_counts()[key]
+    name, ub = key.split("@")
+    n, m, seed = (int(x) for x in name[4:].split(":"))
+    inst = pbb.generate_taillard(n, m, seed)
+    res = pbb.pool_run(inst, int(ub), cfg=pbb.PoolConfig())
+    assert res.stats.unique == g["decomposed"] and res.stats.leaves == g["leaves"]
+    assert res.best_value == int(ub)
+    assert {str(k): v for k, v in res.hist.items()} == g["hist"]
