@@ -34,6 +34,9 @@
  *   pbbgpu_promote                  <- ExplorerPool::promote_solutions  (explorer.hpp:99, explorer.cpp:397-424)
  *   pbbgpu_explorer_lengths         <- timeline sampling                (explorer.cpp:71-85, 448-464)
  *   pbbgpu_int32_peak               <- (new) integer-ALU roofline denominator
+ *   pbbgpu_worker_run               <- worker_run's pool role over the reference's TCP protocol
+ *                                      (src/worker.cpp:138-296, src/protocol.cpp, src/transport.cpp)
+ *   pbbgpu_wire_reencode            <- encode / decode (src/protocol.cpp:104-177)
  *   pbbgpu_group_*                  <- Coordinator/worker WORK+BEST exchange inside one box
  *                                      (src/coordinator.cpp:170-306, src/workunit.cpp:59-74) over
  *                                      NVLink peer memory
@@ -62,6 +65,7 @@ extern "C" {
 #define PBBGPU_ERR_STATE -2    /* std::logic_error */
 #define PBBGPU_ERR_CUDA -3     /* device / driver failure, no GPU */
 #define PBBGPU_ERR_CAPACITY -4 /* std::runtime_error (capacity) */
+#define PBBGPU_ERR_TRANSPORT -5 /* TransportError (transport.hpp:15-17): peer loss, malformed frames */
 
 #define PBBGPU_LB1 1
 #define PBBGPU_LB2 2
@@ -252,6 +256,36 @@ int pbbgpu_group_reset(pbbgpu_pool* pool);
 int pbbgpu_group_solve(pbbgpu_pool* pool, int64_t initial_ub, int seed_div, double time_limit_s,
                        pbbgpu_group_stats_t* out);
 int pbbgpu_group_close(pbbgpu_pool* pool);
+
+/* the pool's instance as given to pbbgpu_create: n, m and the job-major n*m matrix */
+int pbbgpu_pool_shape(const pbbgpu_pool* pool, int* n, int* m);
+int pbbgpu_pool_times(const pbbgpu_pool* pool, int32_t* p_out);
+
+/* ---- the reference's wire protocol and a GPU worker speaking it
+ * Frames of src/protocol.cpp:104-177 over blocking TCP (src/transport.cpp:108-341), so a pool
+ * joins the reference's own Coordinator (src/coordinator.cpp) as a worker process. */
+typedef struct {
+  uint32_t worker_id;          /* WorkerConfig.worker_id (worker.hpp:15) */
+  double checkpoint_period_s;  /* WORK checkpoint timer; 0 = 30 s */
+  int64_t initial_ub;          /* offered after the seed; <= 0 = none */
+  uint64_t rng_seed;           /* insertion_local_search seed; 0 = 1 */
+  int ils_iterations;          /* seed descent budget; 0 = 2000 (worker.cpp:146-149) */
+  int send_initial_best;       /* WorkerConfig.send_initial_best; set -1 for false (0 = default true) */
+} pbbgpu_worker_config_t;
+typedef struct {
+  int64_t local_best;          /* makespan of the pool's best schedule (INT64_MAX = none) */
+  int has_schedule;
+  uint64_t checkpoints_sent, bests_sent, updates_applied, messages;
+} pbbgpu_worker_result_t;
+/* worker_run's pool role (src/worker.cpp:138-296) on `pool`, connected to a coordinator at
+ * host:port; returns after END. PBBGPU_ERR_TRANSPORT on peer loss / protocol violations. */
+int pbbgpu_worker_run(pbbgpu_pool* pool, const char* host, int port, const pbbgpu_worker_config_t* cfg,
+                      pbbgpu_worker_result_t* out);
+/* decode one frame (sender_is_worker selects the WORK layout) and encode it again, intervals
+ * passed through factoradic digits when n > 0: byte-identical to the input for every frame the
+ * reference's encode() produces (the codec's parity hook; no GPU needed) */
+int pbbgpu_wire_reencode(const uint8_t* frame, int64_t len, int sender_is_worker, int n, uint8_t* out,
+                         int64_t cap, int64_t* out_len);
 
 /* pool_run: assign [0,n!) (or the given intervals), run rounds to exhaustion or time limit */
 int pbbgpu_solve(pbbgpu_pool* pool, int64_t initial_ub, const uint16_t* a_digits,

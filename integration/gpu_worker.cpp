@@ -6,6 +6,10 @@
 //
 //   gpu_worker pool <ta> <ub> <K> <lb1|lb2> <steal_policy> <batch_steps>
 //       pool_run's loop (src/explorer.cpp:473-507) over GpuExplorerPool
+//   gpu_worker tcp <ta> <ub> <workers> <lb1|lb2>
+//       Coordinator::run over the reference's TcpListener (src/transport.cpp) on 127.0.0.1,
+//       workers = libpbbgpu's own worker role and wire codec (pbbgpu_worker_run,
+//       csrc/wire.cpp), one GPU pool each: the product speaking the reference's protocol
 //   gpu_worker cluster <ta> <ub> <workers> <lb1|lb2>
 //       Coordinator::run (src/coordinator.cpp:241-306) over make_inproc_cluster (every message
 //       encoded / decoded by src/protocol.cpp), one GPU worker thread per transport endpoint,
@@ -214,6 +218,63 @@ int cmd_cluster(int argc, char** argv) {
   return 0;
 }
 
+int cmd_tcp(int argc, char** argv) {
+  if (argc < 6) return 2;
+  const Instance inst = taillard_named(argv[2]);
+  const std::int64_t ub = parse_ub(inst, argv[3]);
+  const int W = std::atoi(argv[4]);
+  const int bound = bound_of(argv[5]);
+  TcpListener listener("127.0.0.1", 0);
+  const int port = listener.port();
+  std::vector<pbbgpu_worker_result_t> res(static_cast<std::size_t>(W));
+  std::vector<pbbgpu_stats_t> st(static_cast<std::size_t>(W));
+  std::vector<std::string> errors(static_cast<std::size_t>(W));
+  std::vector<std::thread> workers;
+  for (int w = 0; w < W; ++w) {
+    workers.emplace_back([&, w] {
+      pbbgpu_pool* pool = nullptr;
+      pbbgpu_config_t c{};
+      int rc = pbbgpu_create(inst.n, inst.m, inst.p.data(), bound, &c, &pool);
+      if (rc == PBBGPU_OK) {
+        pbbgpu_worker_config_t wc{};
+        wc.worker_id = static_cast<std::uint32_t>(w);
+        wc.initial_ub = ub;
+        wc.checkpoint_period_s = 0.05;
+        wc.rng_seed = 1 + static_cast<std::uint64_t>(w);
+        rc = pbbgpu_worker_run(pool, "127.0.0.1", port, &wc, &res[static_cast<std::size_t>(w)]);
+        if (rc == PBBGPU_OK) rc = pbbgpu_stats(pool, &st[static_cast<std::size_t>(w)]);
+      }
+      if (rc != PBBGPU_OK) errors[static_cast<std::size_t>(w)] = pbbgpu_last_error();
+      pbbgpu_destroy(pool);
+    });
+  }
+  CoordinatorConfig ccfg;
+  Coordinator coord(inst, ccfg);
+  coord.add_initial_interval();
+  const std::shared_ptr<CoordinatorTransport> transport = listener.accept_workers(W);
+  const CoordinatorResult cr = coord.run(*transport);
+  for (auto& t : workers) t.join();
+  for (const std::string& e : errors)
+    if (!e.empty()) throw std::runtime_error("worker failed: " + e);
+  std::uint64_t unique = 0, raw = 0, leaves = 0, updates = 0, msgs = 0;
+  for (int w = 0; w < W; ++w) {
+    unique += st[static_cast<std::size_t>(w)].unique;
+    raw += st[static_cast<std::size_t>(w)].decomposed;
+    leaves += st[static_cast<std::size_t>(w)].leaves;
+    updates += res[static_cast<std::size_t>(w)].updates_applied;
+    msgs += res[static_cast<std::size_t>(w)].messages;
+  }
+  std::printf(
+      "{\"mode\":\"tcp\",\"instance\":\"%s\",\"initial_ub\":%lld,\"workers\":%d,\"best_value\":%lld,"
+      "\"coordinator_total_nodes\":%llu,\"splits\":%llu,\"messages\":%llu,\"worker_messages\":%llu,"
+      "\"decomposed\":%llu,\"unique\":%llu,\"leaves\":%llu,\"updates_applied\":%llu,\"wall_s\":%.3f}\n",
+      argv[2], (long long)ub, W, (long long)cr.best_value, (unsigned long long)cr.total_nodes,
+      (unsigned long long)cr.splits, (unsigned long long)cr.messages, (unsigned long long)msgs,
+      (unsigned long long)raw, (unsigned long long)unique, (unsigned long long)leaves, (unsigned long long)updates,
+      cr.wall_s);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -225,6 +286,7 @@ int main(int argc, char** argv) {
   try {
     if (std::strcmp(argv[1], "pool") == 0) rc = cmd_pool(argc, argv);
     else if (std::strcmp(argv[1], "cluster") == 0) rc = cmd_cluster(argc, argv);
+    else if (std::strcmp(argv[1], "tcp") == 0) rc = cmd_tcp(argc, argv);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "gpu_worker: %s\n", e.what());
     return 1;

@@ -40,6 +40,7 @@
 #include "pbb/heuristic.hpp"
 #include "pbb/instance.hpp"
 #include "pbb/ivm.hpp"
+#include "pbb/protocol.hpp"
 
 using namespace pbb;
 
@@ -343,6 +344,51 @@ int cmd_stats(int argc, char** argv) {
   return 0;
 }
 
+// Wire frames encoded by the reference (src/protocol.cpp) for the codec golden file: one line
+// per frame, "<sender> <n> <hex>" (sender W = worker, C = coordinator; n = the instance size the
+// intervals belong to).
+int cmd_frames(int, char**) {
+  std::mt19937_64 rng(2012);
+  auto emit = [](const char* who, int n, const Message& m) {
+    const std::vector<std::uint8_t> fr = encode(m);
+    std::printf("%s %d ", who, n);
+    for (std::uint8_t b : fr) std::printf("%02x", b);
+    std::printf("\n");
+  };
+  for (int n : {5, 20, 50, 500}) {
+    const BigCount nf = BigCount::factorial(n);
+    std::vector<BigCount> pts;  // random points from random digit vectors, cut into pieces
+    for (int t = 0; t < 12; ++t) {
+      Factoradic x = Factoradic::zero(n);
+      for (int l = 0; l < n; ++l) x.digits[l] = static_cast<int>(rng() % static_cast<std::uint64_t>(n - l));
+      pts.push_back(to_decimal(x));
+    }
+    std::sort(pts.begin(), pts.end());
+    std::vector<Interval> ivs;
+    for (std::size_t t = 0; t + 1 < pts.size(); t += 2)
+      if (pts[t] < pts[t + 1]) ivs.emplace_back(pts[t], pts[t + 1]);
+    ivs.emplace_back(pts.back(), nf);
+    std::vector<Interval> norm = normalize(ivs);
+    WorkRequest req;
+    req.worker_id = static_cast<std::uint32_t>(n);
+    req.nodes_since_checkpoint = 1234567890123ull + static_cast<std::uint64_t>(n);
+    req.kmax = 4736;
+    req.intervals = norm;
+    emit("W", n, req);
+    emit("W", n, WorkRequest{7, 0, 16, {}});
+    emit("C", n, WorkReply{norm});
+    emit("C", n, WorkReply{{Interval(BigCount(1), BigCount(2))}});
+  }
+  std::vector<std::uint32_t> sched;
+  for (std::uint32_t j = 0; j < 20; ++j) sched.push_back((j * 7) % 20);
+  emit("W", 20, BestMsg{2297, sched});
+  emit("C", 20, BestMsg{2297, {}});
+  emit("C", 20, BestMsg{kNoMakespan, {}});
+  emit("W", 20, EndMsg{1278, sched});
+  emit("C", 20, EndMsg{kNoMakespan, {}});
+  return 0;
+}
+
 int cmd_inst(int argc, char** argv) {
   if (argc < 3) return 2;
   Instance inst = taillard_named(argv[2]);
@@ -374,6 +420,7 @@ int main(int argc, char** argv) {
     else if (mode == "ckpt") rc = cmd_ckpt(argc, argv);
     else if (mode == "ckptload") rc = cmd_ckptload(argc, argv);
     else if (mode == "stats") rc = cmd_stats(argc, argv);
+    else if (mode == "frames") rc = cmd_frames(argc, argv);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "ref_driver: %s\n", e.what());
     return 1;

@@ -8,7 +8,7 @@ from .factoradic import compare, from_decimal, midpoint, to_decimal
 from .instance import (Instance, Schedule, generate_taillard, insertion_local_search, makespan, neh, parse_instance,
                        taillard_named)
 from .pool import (BACKWARD, FORWARD, NO_INCUMBENT, Decomposition, GpuPool, PoolConfig, PoolResult,
-                   PoolStats, Subproblem, Timeline, int32_peak, normalize, pool_run, solve_pool)
+                   PoolStats, Subproblem, Timeline, int32_peak, normalize, pool_run, solve_pool, wire_reencode)
 
 from .coop import CoopResult, solve_cooperative
 
@@ -17,5 +17,5 @@ __all__ = [
     "Instance", "Schedule", "generate_taillard", "taillard_named", "makespan", "neh", "parse_instance",
     "insertion_local_search",
     "GpuPool", "PoolConfig", "PoolStats", "PoolResult", "Subproblem", "Decomposition", "pool_run", "solve_pool",
-    "normalize", "int32_peak", "Timeline", "to_decimal", "from_decimal", "compare", "midpoint", "FORWARD", "BACKWARD", "NO_INCUMBENT",
+    "normalize", "int32_peak", "wire_reencode", "Timeline", "to_decimal", "from_decimal", "compare", "midpoint", "FORWARD", "BACKWARD", "NO_INCUMBENT",
 ]

@@ -16,6 +16,7 @@ PBBGPU_ERR_ARG = -1
 PBBGPU_ERR_STATE = -2
 PBBGPU_ERR_CUDA = -3
 PBBGPU_ERR_CAPACITY = -4
+PBBGPU_ERR_TRANSPORT = -5
 LB1 = 1
 LB2 = 2
 
@@ -31,7 +32,8 @@ EXPORTS = (
     "pbbgpu_best_schedule", "pbbgpu_snapshot_ex", "pbbgpu_apply_work_update", "pbbgpu_improved_since_mark",
     "pbbgpu_steals_since_mark", "pbbgpu_reset_steal_mark", "pbbgpu_take_census", "pbbgpu_flush_timeline",
     "pbbgpu_group_handle_size", "pbbgpu_group_create", "pbbgpu_group_open", "pbbgpu_group_reset",
-    "pbbgpu_group_solve", "pbbgpu_group_close",
+    "pbbgpu_group_solve", "pbbgpu_group_close", "pbbgpu_pool_shape", "pbbgpu_pool_times", "pbbgpu_worker_run",
+    "pbbgpu_wire_reencode",
 )
 
 
@@ -104,6 +106,31 @@ class GroupStats(ctypes.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_}
 
 
+class WorkerConfig(ctypes.Structure):
+    _fields_ = [
+        ("worker_id", ctypes.c_uint32),
+        ("checkpoint_period_s", ctypes.c_double),
+        ("initial_ub", ctypes.c_int64),
+        ("rng_seed", ctypes.c_uint64),
+        ("ils_iterations", ctypes.c_int),
+        ("send_initial_best", ctypes.c_int),
+    ]
+
+
+class WorkerResult(ctypes.Structure):
+    _fields_ = [
+        ("local_best", ctypes.c_int64),
+        ("has_schedule", ctypes.c_int),
+        ("checkpoints_sent", ctypes.c_uint64),
+        ("bests_sent", ctypes.c_uint64),
+        ("updates_applied", ctypes.c_uint64),
+        ("messages", ctypes.c_uint64),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
 _lib = None
 
 
@@ -159,6 +186,12 @@ def load() -> ctypes.CDLL:
         "pbbgpu_group_solve": (ctypes.c_int, [P, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
                                               ctypes.POINTER(GroupStats)]),
         "pbbgpu_group_close": (ctypes.c_int, [P]),
+        "pbbgpu_pool_shape": (ctypes.c_int, [P, ip, ip]),
+        "pbbgpu_pool_times": (ctypes.c_int, [P, i32p]),
+        "pbbgpu_worker_run": (ctypes.c_int, [P, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(WorkerConfig),
+                                             ctypes.POINTER(WorkerResult)]),
+        "pbbgpu_wire_reencode": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_void_p, ctypes.c_int64, i64p]),
         "pbbgpu_offer_bound": (ctypes.c_int, [P, ctypes.c_int64]),
         "pbbgpu_stats": (ctypes.c_int, [P, ctypes.POINTER(Stats)]),
         "pbbgpu_histogram": (ctypes.c_int, [P, u64p, ctypes.c_int]),

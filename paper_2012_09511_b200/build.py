@@ -12,8 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpbbgpu.so")
-SOURCES = [os.path.join(CSRC, "pool.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("explore.cuh", "bound_big.cuh", "pbb_layout.h")] + [
+SOURCES = [os.path.join(CSRC, "pool.cu"), os.path.join(CSRC, "wire.cpp")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("explore.cuh", "bound_big.cuh", "pbb_layout.h", "steal_ref.cuh")] + [
     os.path.join(ROOT, "include", "pbbgpu.h")]
 
 NVCC_FLAGS = [

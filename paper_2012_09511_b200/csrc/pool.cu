@@ -2012,6 +2012,8 @@ void check_digits(int n, const uint16_t* d) {
 
 // ------------------------------------------------------------------ C-ABI
 
+void pbbgpu_internal_set_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
 extern "C" {
 
 const char* pbbgpu_last_error(void) { return g_last_error.c_str(); }
@@ -2131,6 +2133,22 @@ int pbbgpu_load_instance(pbbgpu_pool* P, const int32_t* p) {
 }
 
 int pbbgpu_K(const pbbgpu_pool* P) { return P ? P->K : 0; }
+
+int pbbgpu_pool_shape(const pbbgpu_pool* P, int* n, int* m) {
+  return guarded([&] {
+    if (!P) throw std::invalid_argument("null pool");
+    *n = P->n;
+    *m = P->m_real;
+  });
+}
+
+int pbbgpu_pool_times(const pbbgpu_pool* P, int32_t* p) {
+  return guarded([&] {
+    if (!P) throw std::invalid_argument("null pool");
+    for (int j = 0; j < P->n; ++j)
+      for (int k = 0; k < P->m_real; ++k) p[static_cast<size_t>(j) * P->m_real + k] = P->p[static_cast<size_t>(j) * P->m + k];
+  });
+}
 
 int pbbgpu_set_initial_bound(pbbgpu_pool* P, int64_t ub, const int32_t* sched, int len) {
   return guarded([&] {

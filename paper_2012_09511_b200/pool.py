@@ -324,6 +324,19 @@ class GpuPool:
     def group_close(self) -> None:
         _lib.check(self._lib.pbbgpu_group_close(self._h))
 
+    def worker_run(self, host: str, port: int, worker_id: int = 0, initial_ub: int = 0,
+                   checkpoint_period_s: float = 30.0, rng_seed: int = 1) -> dict:
+        """worker_run's pool role (src/worker.cpp:138-296) against a coordinator speaking the
+        reference's wire protocol over TCP (pbbgpu_worker_run); returns after END."""
+        c = _lib.WorkerConfig()
+        c.worker_id = worker_id
+        c.checkpoint_period_s = checkpoint_period_s
+        c.initial_ub = initial_ub
+        c.rng_seed = rng_seed
+        r = _lib.WorkerResult()
+        _lib.check(self._lib.pbbgpu_worker_run(self._h, host.encode(), port, ctypes.byref(c), ctypes.byref(r)))
+        return r.as_dict()
+
     def run_round(self) -> int:
         act = ctypes.c_int()
         _lib.check(self._lib.pbbgpu_run_round(self._h, ctypes.byref(act)))
@@ -507,3 +520,14 @@ class Timeline:
 
     def close(self):
         self.f.close()
+
+
+def wire_reencode(frame: bytes, sender_is_worker: bool, n: int = 0) -> bytes:
+    """Decode one frame of the reference's wire protocol (src/protocol.cpp) and encode it again,
+    interval endpoints passed through factoradic digits when n > 0 (pbbgpu_wire_reencode)."""
+    lib = _lib.load()
+    cap = 2 * len(frame) + 64
+    out = ctypes.create_string_buffer(cap)
+    ln = ctypes.c_int64()
+    _lib.check(lib.pbbgpu_wire_reencode(frame, len(frame), int(sender_is_worker), n, out, cap, ctypes.byref(ln)))
+    return out.raw[:ln.value]

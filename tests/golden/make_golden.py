@@ -53,6 +53,9 @@ def main():
                                   ("ta041", 2991, 30, 10), ("ta056", 3679, 30, 10)):
         with open(os.path.join(HERE, f"ref_nodes_{name}.txt"), "w") as f:
             f.write(run("nodes", name, ub, 42, starts, per))
+    # wire frames encoded by the reference (src/protocol.cpp encode)
+    with open(os.path.join(HERE, "ref_frames.txt"), "w") as f:
+        f.write(run("frames"))
     # coordinator checkpoint file written by the reference (checkpoint_save)
     subprocess.run([DRIVER, "ckpt", "ta021", os.path.join(HERE, "ref_checkpoint_ta021.ckpt")], check=True)
     # instance matrices as the reference generates them

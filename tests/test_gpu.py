@@ -791,3 +791,18 @@ def test_any_machine_count_fixed_trees_match_reference(key):
     assert res.stats.unique == g["decomposed"] and res.stats.leaves == g["leaves"]
     assert res.best_value == int(ub)
     assert {str(k): v for k, v in res.hist.items()} == g["hist"]
+
+
+@pytest.mark.parametrize("workers", [1, 2])
+def test_product_worker_speaks_the_reference_protocol_over_tcp(workers):
+    """libpbbgpu's own worker role and wire codec (pbbgpu_worker_run) connected over TCP to the
+    reference's Coordinator and TcpListener: the proof completes; with one worker its counts
+    are exactly pool_run's, and the coordinator's node total is the workers' WORK checkpoints."""
+    r = _gpu_worker("tcp", "ta011", 1582, workers, "lb1")
+    assert r["leaves"] >= 54 and r["unique"] >= 158049
+    assert r["coordinator_total_nodes"] == r["decomposed"]
+    assert r["messages"] == r["worker_messages"]               # every frame decoded by the reference
+    if workers == 1:
+        assert r["unique"] == 158049 and r["leaves"] == 54 and r["splits"] == 0
+    else:
+        assert r["splits"] > 0

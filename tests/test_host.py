@@ -168,3 +168,44 @@ def test_instance_fingerprint():
     from paper_2012_09511_b200 import checkpoint as ck
 
     assert f"{ck.instance_fingerprint(pbb.taillard_named('ta021')):016x}" == "23f4aba7591455ec"
+
+
+# ---------------------------------------------------------------- wire protocol
+
+def _ref_frames():
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_frames.txt")
+    out = []
+    for line in open(path):
+        who, n, hx = line.split()
+        out.append((who == "W", int(n), bytes.fromhex(hx)))
+    return out
+
+
+def test_wire_codec_reencodes_reference_frames_byte_for_byte():
+    """Every frame the reference's encode() produced (tests/golden/ref_frames.txt: WORK requests
+    and replies with intervals of [0, n!) for n = 5 .. 500, BEST / END with and without
+    schedules) decodes and re-encodes to the same bytes, also with the interval endpoints passed
+    through the pool boundary's factoradic digit vectors."""
+    frames = _ref_frames()
+    assert len(frames) >= 20
+    for worker, n, fr in frames:
+        assert pbb.wire_reencode(fr, worker) == fr
+        assert pbb.wire_reencode(fr, worker, n) == fr
+
+
+def test_wire_codec_rejects_malformed_frames():
+    from paper_2012_09511_b200 import _lib
+
+    worker, n, fr = _ref_frames()[0]
+    with pytest.raises(_lib.PbbError):
+        pbb.wire_reencode(fr[:-1], worker)                        # truncated
+    with pytest.raises(_lib.PbbError):
+        pbb.wire_reencode(fr + b"\x00", worker)                   # length mismatch
+    bad = bytearray(fr)
+    bad[4] = 9
+    with pytest.raises(_lib.PbbError):
+        pbb.wire_reencode(bytes(bad), worker)                     # unknown tag
+    one = bytes.fromhex("0000000b0100000001000101000101")           # WORK reply [1, 1): a >= b
+    with pytest.raises(_lib.PbbError):
+        pbb.wire_reencode(one, False)
