@@ -43,6 +43,10 @@ WORKLOADS = {
                              desc="Taillard ta041 (50x10), LB1, pinned UB 3000 (prune >= 3000, never improve): "
                                   "fixed tree of 520,458,272 nodes per step; live-sibling work splitting, "
                                   "breadth-first seeding"),
+    "ta041-lb1-pinned3135": dict(instance="ta041", bound="lb1", ub=3135, pinned=True, split_mode=1, time_limit=10.0,
+                                 desc="Taillard ta041 (50x10), LB1, pinned UB = NEH 3135 (prune >= 3135, never "
+                                      "improve): 10 s time-bounded exploration per step of a > 10^10-node fixed "
+                                      "tree (SURVEY.md §8(d) fixed node budget); live-sibling work splitting"),
     "ta056-lb2": dict(instance="ta056", bound="lb2", ub=3679, time_limit=10.0,
                       desc="Taillard ta056 (50x20), LB2, initial UB = best-known 3679, 10 s time-bounded "
                            "exploration per step"),

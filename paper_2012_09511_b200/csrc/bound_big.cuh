@@ -56,8 +56,8 @@ __host__ __device__ inline int big_smem_bytes(int n, int mp, int m) {
 // job s - wp on machine k. The loads are independent of the chain, so they run two steps
 // ahead (indices clamped into range; out-of-range steps leave C unchanged and add 0).
 // MP = 0: row stride passed at run time.
-template <int MP>
-__device__ __forceinline__ void big_wave(const int* sp, const uint16_t* spm, int n, int len, bool rev, int k,
+template <int MP, typename PT = int>
+__device__ __forceinline__ void big_wave(const PT* sp, const uint16_t* spm, int n, int len, bool rev, int k,
                                          int wp, bool act, int steps, int& C, int& sum, int mp = MP) {
   const int hi = max(len - 1, 0);
   auto at = [&](int s) {
@@ -65,10 +65,10 @@ __device__ __forceinline__ void big_wave(const int* sp, const uint16_t* spm, int
     return static_cast<int>(spm[rev ? n - 1 - i : i]);
   };
   int jn = at(1);
-  int pn = sp[at(0) * mp + k];
+  int pn = static_cast<int>(sp[at(0) * mp + k]);
   for (int s = 0; s < steps; ++s) {
     const int pv = pn;
-    pn = sp[jn * mp + k];
+    pn = static_cast<int>(sp[jn * mp + k]);
     jn = at(s + 2);
     int left = __shfl_up_sync(0xffffffffu, C, 1);
     if (wp == 0) left = 0;
@@ -469,6 +469,232 @@ __global__ void __launch_bounds__(kBig1Warps * 32, M > 16 ? 1 : 2) decompose_big
   }
 }
 
+
+// LB2 for large n, one WARP per node (batches whose nodes have f <= kBig2wFmax free jobs; the
+// CTA-per-node decompose_big_kernel keeps the rest). A CTA stages the instance once and runs
+// up to 20 nodes at a time (one per warp), so the serial parts of a node (its wavefront
+// tables) overlap other warps' pair passes instead of idling a whole CTA at a barrier:
+//   tables     front / tail as lane-per-machine wavefronts (as decompose_big_lb1_kernel),
+//              remain = ptot - fixed sums (no pass over the free jobs)
+//   heads      lane per child: H'[c][k] = h'_k | t'_k << 16 (explore.cuh children_lb2_w)
+//   pairs      lane per machine pair, 32 pairs per round: the free positions of the pair's
+//              Johnson order as a lane-private bitmask in shared memory (from the inverse
+//              order, coalesced over the lanes), then the forward / backward passes of the
+//              O(P (n + f)) max-plus form over exactly the f set bits, order entries
+//              (job | u << 9 | v << 24, u = a + lag, v = a - b) streamed from L2 kPf per lane
+//              in flight, PM'_i kept per rank in a per-warp global scratch (all lanes are at
+//              the same rank at every step: coalesced), every S_j folded into child j's bounds
+//              at once with shared-memory atomicMax (as explore.cuh lb2_round, n > 32)
+//   MinMin     lanes over children, REDUX (src/bound.cpp:109-131)
+constexpr int kBig2wFmax = 128;
+constexpr int kBig2wMaxWarps = 20;
+
+__host__ __device__ inline int big2w_warp_bytes(int n, int m, int fmax) {
+  const int mw = (n + 31) / 32;
+  return round_up(round_up(n, 8) * 2 * 2 + 3 * round_up(m, 4) * 4 + mw * 32 * 4 + 2 * round_up(fmax, 4) * 4 +
+                      fmax * m * 4 + fmax * 32 * (4 + 2),
+                  16);
+}
+
+__host__ __device__ inline int big2w_smem_bytes(int n, int mp, int m, int fmax, int warps) {
+  return round_up(n * mp * 2, 16) + warps * big2w_warp_bytes(n, m, fmax);  // p as uint16
+}
+
+#ifdef __CUDACC__
+
+template <int M>
+__global__ void __launch_bounds__(kBig2wMaxWarps * 32) decompose_big_lb2w_kernel(const BigBatchParams B, const int* ptot,
+                                                                              const uint32_t* packed32, int fmax,
+                                                                              int* pm_scratch) {
+  constexpr int MP = (M + 3) / 4 * 4;
+  constexpr int NEG = -30000;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = B.n, P = B.npairs, PS = round_up(P, 32), MW = (n + 31) >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  uint16_t* sp = reinterpret_cast<uint16_t*>(smem);  // [n][MP] (p < 2^16: validate_times)
+  unsigned char* wb = smem + round_up(n * MP * 2, 16) + warp * big2w_warp_bytes(n, M, fmax);
+  uint16_t* spm = reinterpret_cast<uint16_t*>(wb);                  // the node's perm
+  uint16_t* cidx = spm + round_up(n, 8);                             // job -> child (0xffff: fixed)
+  int* fr = reinterpret_cast<int*>(cidx + round_up(n, 8));
+  int* tl = fr + MP;
+  int* rm = tl + MP;
+  uint32_t* mask = reinterpret_cast<uint32_t*>(rm + MP);             // [MW][32] lane-private words
+  int* accf = reinterpret_cast<int*>(mask + MW * 32);                // [fmax] child-indexed
+  int* accb = accf + round_up(fmax, 4);
+  uint32_t* H = reinterpret_cast<uint32_t*>(accb + round_up(fmax, 4));  // [fmax][M] h' | t' << 16
+  uint32_t* ent = H + fmax * M + lane;                                 // [rank][32]: the walk's order entries
+  int16_t* pml = reinterpret_cast<int16_t*>(H + fmax * M + fmax * 32) + lane;  // [rank][32]: PM'
+  (void)pm_scratch;
+  for (int i = tid; i < n * MP; i += blockDim.x) sp[i] = static_cast<uint16_t>(B.p32[i]);
+  __syncthreads();
+  for (int node = blockIdx.x * nwarps + warp; node < B.count; node += gridDim.x * nwarps) {
+    const int* perm = B.perms + static_cast<size_t>(node) * n;
+    const int d1 = B.d1[node], d2 = B.d2[node], f = n - d1 - d2;
+    for (int i = lane; i < n; i += 32) {
+      spm[i] = static_cast<uint16_t>(perm[i]);
+      cidx[i] = 0xffff;
+    }
+    __syncwarp();
+    for (int c = lane; c < f; c += 32) cidx[spm[d1 + c]] = static_cast<uint16_t>(c);
+    {  // node tables (bound_tables, src/bound.cpp:20-46)
+      int C = 0, sum = 0, tsum = 0;
+      big_wave<MP, uint16_t>(sp, spm, n, d1, false, lane < M ? lane : 0, lane, lane < M, d1 + M - 1, C, sum);
+      if (lane < M) fr[lane] = C;
+      C = 0;
+      const int k = M - 1 - lane;
+      big_wave<MP, uint16_t>(sp, spm, n, d2, true, lane < M ? k : 0, lane, lane < M, d2 + M - 1, C, tsum);
+      if (lane < M) tl[k] = C;
+      const int ts = __shfl_sync(0xffffffffu, tsum, (M - 1 - lane) & 31);
+      if (lane < M) rm[lane] = ptot[lane] - sum - ts;
+    }
+    __syncwarp();
+    for (int c = lane; c < f; c += 32) {  // child heads / tails without the job's own time
+      const uint16_t* pr = sp + spm[d1 + c] * MP;
+      int hp[M];
+      int prev = 0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        hp[k] = max(prev, fr[k]);
+        prev = hp[k] + pr[k];
+      }
+      prev = 0;
+#pragma unroll
+      for (int k = M - 1; k >= 0; --k) {
+        const int tp = max(prev, tl[k]);
+        prev = tp + pr[k];
+        H[c * M + k] = static_cast<uint32_t>(hp[k]) | static_cast<uint32_t>(tp) << 16;
+      }
+      accf[c] = 0;
+      accb[c] = 0;
+    }
+    __syncwarp();
+    for (int q0 = 0; q0 < P; q0 += 32) {
+      const int q = min(q0 + lane, P - 1);
+      const int k = B.pk[q], l = B.pl[q];
+      const int Atot = rm[k], Btot = rm[l];
+      const int qk = tl[k], ql = tl[l], rk = fr[k], rl = fr[l];
+      const int cAq = Atot + qk, cRB = rl + Btot;
+      const uint32_t Cc = static_cast<uint32_t>(Btot + ql) | static_cast<uint32_t>(rk + Atot) << 16;
+      // free positions of the pair's order: lane-private mask words (inverse order, coalesced
+      // loads; shared-memory atomicOr so the updates pipeline instead of chaining through
+      // load-modify-store) and a summary of the non-empty words (n <= 512: 16 words)
+      for (int w = 0; w < MW; ++w) mask[w * 32 + lane] = 0;
+      uint32_t nonempty = 0;
+      __syncwarp();
+      {
+        const uint16_t* iq = B.inv16 + q;
+        int c = 0;
+        for (; c + 16 <= f; c += 16) {  // 16 inverse-order loads in flight per lane
+          int pos[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) pos[u] = iq[static_cast<size_t>(spm[d1 + c + u]) * P];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            atomicOr(&mask[(pos[u] >> 5) * 32 + lane], 1u << (pos[u] & 31));
+            nonempty |= 1u << (pos[u] >> 5);
+          }
+        }
+        for (; c < f; ++c) {
+          const int pos = iq[static_cast<size_t>(spm[d1 + c]) * P];
+          atomicOr(&mask[(pos >> 5) * 32 + lane], 1u << (pos & 31));
+          nonempty |= 1u << (pos >> 5);
+        }
+      }
+      __syncwarp();
+      const uint32_t* col = packed32 + q;
+      // every lane walks exactly f positions (its pair's free jobs): the forward pass gathers the
+      // order entries from L2 in position order (4 in flight) and keeps them with PM'_i in the
+      // warp's shared lists by rank; the backward pass reads both back in reverse
+      uint32_t words = nonempty, bits = 0;
+      int w = 0;
+      auto next_up = [&]() {  // ascending set bits over the non-empty words
+        if (bits == 0) {
+          w = __ffs(words) - 1;
+          words &= words - 1;
+          bits = mask[w * 32 + lane];
+        }
+        const int t = w * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
+        return t;
+      };
+      int E = Btot, pm = NEG, rank = 0;
+      auto fwd = [&](uint32_t e) {  // PM'_i = prefix max of X' over the earlier free positions
+        ent[rank * 32] = e;
+        pml[rank * 32] = static_cast<int16_t>(pm);
+        ++rank;
+        pm = max(pm, E + static_cast<int>((e >> 9) & 0x7ffu));
+        E += static_cast<int>(e) >> 24;
+      };
+      int i = 0;
+      for (; i + 16 <= f; i += 16) {  // 16 order entries in flight per lane
+        uint32_t e[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) e[u] = col[static_cast<size_t>(next_up()) * PS];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) fwd(e[u]);
+      }
+      for (; i + 4 <= f; i += 4) {
+        uint32_t e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) e[u] = col[static_cast<size_t>(next_up()) * PS];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) fwd(e[u]);
+      }
+      for (; i < f; ++i) fwd(col[static_cast<size_t>(next_up()) * PS]);
+      int G = Atot, sm = NEG;
+      for (int r = f - 1; r >= 0; --r) {  // S_j folded into child j's bounds
+        const uint32_t e = ent[r * 32];
+        const int v = static_cast<int>(e) >> 24;
+        const int c = cidx[e & 0x1ffu];
+        const int I1 = max(static_cast<int>(pml[r * 32]) + v, sm);
+        const int lo = max(cAq, I1 + ql), hi = max(cRB, I1 + (rk - v));
+        const uint32_t S = __byte_perm(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi), 0x5410);
+        const uint32_t hk = H[c * M + k], hl = H[c * M + l];
+        const uint32_t V = max_u16x2(add_u16x2(__byte_perm(hk, hl, 0x7610), S), add_u16x2(__byte_perm(hl, hk, 0x7610), Cc));
+        atomicMax(reinterpret_cast<unsigned*>(accf) + c, V & 0xffffu);
+        atomicMax(reinterpret_cast<unsigned*>(accb) + c, V >> 16);
+        G -= v;
+        sm = max(sm, G + static_cast<int>((e >> 9) & 0x7ffu));
+      }
+    }
+    __syncwarp();
+    // MinMin over children in decode order (src/bound.cpp:109-131) and the outputs
+    int lo = INT_MAX, cf = 0, cb = 0, sf = 0, sb = 0;
+    for (int c = lane; c < f; c += 32) {
+      const int vf = accf[c], vb = accb[c];
+      const int v = min(vf, vb);
+      if (v < lo) {
+        lo = v;
+        cf = cb = 0;
+      }
+      cf += vf == lo;
+      cb += vb == lo;
+      sf += vf;
+      sb += vb;
+    }
+    const int glo = __reduce_min_sync(0xffffffffu, lo);
+    cf = __reduce_add_sync(0xffffffffu, lo == glo ? cf : 0);
+    cb = __reduce_add_sync(0xffffffffu, lo == glo ? cb : 0);
+    sf = __reduce_add_sync(0xffffffffu, sf);
+    sb = __reduce_add_sync(0xffffffffu, sb);
+    int d = kFwd;
+    if (cf != cb) d = cf < cb ? kFwd : kBwd;
+    else if (sf != sb) d = sf > sb ? kFwd : kBwd;
+    const size_t ob = static_cast<size_t>(node) * n;
+    for (int c = lane; c < f; c += 32) {
+      const int vf = accf[c], vb = accb[c];
+      const int lb = d == kFwd ? vf : vb;
+      B.lb_fwd[ob + c] = vf;
+      B.lb_bwd[ob + c] = vb;
+      B.child_lb[ob + c] = lb;
+      B.pruned[ob + c] = lb >= B.incumbent;
+    }
+    if (lane == 0) B.dir[node] = static_cast<uint8_t>(d);
+    __syncwarp();
+  }
+}
+
+#endif  // __CUDACC__
 
 // LB1 for large n, node tables lane-per-node: a warp takes 32 nodes at a time; each lane runs
 // its node's front over sigma1 and then its tail over reversed sigma2 as one sequence of

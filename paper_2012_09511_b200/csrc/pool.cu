@@ -1092,6 +1092,16 @@ Big1Fn big1g_fn(int m) {
   return nullptr;
 }
 
+using Big2wFn = void (*)(BigBatchParams, const int*, const uint32_t*, int, int*);
+Big2wFn big2w_fn(int m) {
+  switch (m) {
+    case 5: return decompose_big_lb2w_kernel<5>;
+    case 10: return decompose_big_lb2w_kernel<10>;
+    case 20: return decompose_big_lb2w_kernel<20>;
+  }
+  return nullptr;
+}
+
 BigFn big_fn(int m, int bound) {
   if (bound == kLB1) {
     switch (m) {
@@ -1169,6 +1179,12 @@ struct pbbgpu_pool {
   int big1g_grid = 0;
   size_t big1g_smem = 0;
   uint2* d_packed64 = nullptr;
+  uint32_t* d_packed32big = nullptr;   // LB2 warp-per-node order entries [n][PS]: job | u << 9 | v << 24
+  bool packed32big = false;
+  Big2wFn big2w = nullptr;
+  int* d_pm_scratch = nullptr;         // per warp [kBig2wFmax][32] PM' ranks
+  int big2w_grid = 0, big2w_warps = 0;
+  size_t smem_optin = 0;               // cudaDevAttrMaxSharedMemoryPerBlockOptin
   uint16_t* d_inv16 = nullptr;
   int* d_big_scratch = nullptr;
   int big_grid = 0;
@@ -1253,6 +1269,8 @@ struct pbbgpu_pool {
     cudaFree(d_packed);
     cudaFree(d_invord);
     cudaFree(d_packed64);
+    cudaFree(d_packed32big);
+    cudaFree(d_pm_scratch);
     cudaFree(d_inv16);
     cudaFree(d_big_scratch);
 
@@ -1305,6 +1323,8 @@ struct HostTables {
   std::vector<uint16_t> lag, ord16, inv16;
   std::vector<uint32_t> packed;
   std::vector<uint2> pk64;
+  std::vector<uint32_t> pk32big;  // [n][PS] job | u << 9 | v << 24 (decompose_big_lb2w_kernel)
+  bool packable32big = false;
   bool packable = false;
 };
 
@@ -1361,6 +1381,21 @@ HostTables build_tables(int n, int m, int M, int bound, const int32_t* p_real, b
         T.pk64[static_cast<size_t>(t) * npairs + q] =
             make_uint2(static_cast<unsigned>(j) | static_cast<unsigned>(a) << 16, static_cast<unsigned>(bb) | static_cast<unsigned>(lg) << 16);
       }
+    {  // warp-per-node entries: u = a + lag (11 bits), v = a - b (8 bits, signed), job (9 bits)
+      const int PS = round_up(npairs, 32);
+      T.pk32big.assign(static_cast<size_t>(n) * PS, 0);
+      T.packable32big = n <= 512;
+      for (int q = 0; q < npairs; ++q)
+        for (int t = 0; t < n; ++t) {
+          const int j = T.ord16[static_cast<size_t>(q) * n + t];
+          const int a = p[static_cast<size_t>(j) * m + T.pk[static_cast<size_t>(q)]];
+          const int bb = p[static_cast<size_t>(j) * m + T.pl[static_cast<size_t>(q)]];
+          const int u = a + T.lag[static_cast<size_t>(q) * n + j], v = a - bb;
+          if (u > 2047 || v < -128 || v > 127) T.packable32big = false;
+          T.pk32big[static_cast<size_t>(t) * PS + q] =
+              static_cast<uint32_t>(j) | static_cast<uint32_t>(u & 0x7ff) << 9 | static_cast<uint32_t>(v & 0xff) << 24;
+        }
+    }
     T.inv16.assign(static_cast<size_t>(n) * npairs, 0);  // [job][pair] -> position
     for (int q = 0; q < npairs; ++q)
       for (int t = 0; t < n; ++t)
@@ -1423,6 +1458,7 @@ void upload_tables(pbbgpu_pool* P, const HostTables& T) {
     u.put(P->d_pl, T.pl);
     if (P->batch_only) {
       u.put(P->d_packed64, T.pk64);
+      u.put(P->d_packed32big, T.pk32big);
       u.put(P->d_inv16, T.inv16);
     } else {
       u.put(P->d_ord, T.ord);
@@ -1519,8 +1555,23 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, threads, P->big_smem), "occupancy");
     if (per_sm < 1) throw CapacityError("pbbgpu: large-n bounding kernel cannot be resident");
     P->big_grid = per_sm * prop.multiProcessorCount;
-    if (bound == kLB2)
+    if (bound == kLB2) {
       ck(cudaMalloc(&P->d_big_scratch, static_cast<size_t>(P->big_grid) * n * kBigThreads * sizeof(int)), "malloc scratch");
+      // warp per node for batches of nodes with f <= kBig2wFmax: as many warps per SM as the
+      // shared memory holds at the largest f (the launch sizes its dynamic smem per batch)
+      P->packed32big = T.packable32big;
+      P->big2w = big2w_fn(m);
+      const void* wfn = reinterpret_cast<const void*>(P->big2w);
+      const size_t cap = static_cast<size_t>(prop.sharedMemPerBlockOptin);
+      P->smem_optin = cap;
+      ck(cudaFuncSetAttribute(wfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cap)), "smem attr");
+      int w = kBig2wMaxWarps;
+      while (w > 1 && static_cast<size_t>(big2w_smem_bytes(n, P->mp, m, kBig2wFmax, w)) > cap) --w;
+      P->big2w_warps = w;
+      P->big2w_grid = prop.multiProcessorCount;
+      ck(cudaMalloc(&P->d_pm_scratch, static_cast<size_t>(P->big2w_grid) * kBig2wMaxWarps * kBig2wFmax * 32 * sizeof(int)),
+         "malloc scratch");
+    }
     P->K = 0;
     return;
   }
@@ -2809,7 +2860,22 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
       else if (P->big1)
         P->big1<<<std::min((count + kBig1Warps - 1) / kBig1Warps, P->big_grid), kBig1Warps * 32, P->big_smem, P->stream>>>(
             G, P->d_ptot);
-      else
+      else if (P->big2w && P->packed32big && [&] {
+                 for (int i = 0; i < count; ++i)
+                   if (n - d1[i] - d2[i] > kBig2wFmax) return false;
+                 return true;
+               }()) {
+        // LB2 warp per node: smem sized for the batch's largest f
+        int fmax = 4;
+        for (int i = 0; i < count; ++i) fmax = std::max(fmax, n - d1[i] - d2[i]);
+        fmax = round_up(fmax, 4);
+        int w = kBig2wMaxWarps;
+        const size_t cap = P->smem_optin;
+        while (w > 1 && static_cast<size_t>(big2w_smem_bytes(n, P->mp, P->m, fmax, w)) > cap) --w;
+        const int grid = std::min(P->big2w_grid, (count + w - 1) / w);
+        P->big2w<<<grid, w * 32, big2w_smem_bytes(n, P->mp, P->m, fmax, w), P->stream>>>(G, P->d_ptot, P->d_packed32big, fmax,
+                                                                                         P->d_pm_scratch);
+      } else
         P->big<<<std::min(count, P->big_grid), kBigThreads, P->big_smem, P->stream>>>(G);
       ck(cudaGetLastError(), "decompose_big launch");
       ck(cudaEventRecord(P->ev1, P->stream), "event");
