@@ -91,7 +91,7 @@ def cmd_sweep(name, bounds="lb1,lb2"):
     for bound in bounds.split(","):
         with pbb.GpuPool(inst, bound=bound) as pool:
             for f in ((10, 50, 100, 200, 300, 400, 499) if n >= 500 else (10, 50, n - 1)):
-                cnt = 32768 if bound == "lb1" else (2048 if f <= 100 else 1024)
+                cnt = 32768 if bound == "lb1" else (8192 if f <= 128 else 1024)
                 perms = rng.random((cnt, n)).argsort(axis=1).astype(np.int32)
                 d1 = rng.integers(0, n - f + 1, cnt)
                 d2 = n - f - d1
