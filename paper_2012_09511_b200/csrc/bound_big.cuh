@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
   for (int node = blockIdx.x; node < B.count; node += gridDim.x) {
     const int* perm = B.perms + static_cast<size_t>(node) * n;
     const int d1 = B.d1[node], d2 = B.d2[node], f = n - d1 - d2;
+    if (d1 < 0) continue;  // no node in this slot (big explorer pool steps)
     for (int j = tid; j < n; j += blockDim.x) {
       isfree[j] = 0;
       accf[j] = 0;
@@ -430,6 +431,7 @@ __global__ void __launch_bounds__(kBig1Warps * 32, M > 16 ? 1 : 2) decompose_big
   for (int node = blockIdx.x * kBig1Warps + warp; node < B.count; node += gridDim.x * kBig1Warps) {
     const int* perm = B.perms + static_cast<size_t>(node) * n;
     const int d1 = B.d1[node], d2 = B.d2[node], f = n - d1 - d2;
+    if (d1 < 0) continue;  // no node in this slot
     for (int i = lane; i < n; i += 32) spm[i] = static_cast<uint16_t>(perm[i]);
     __syncwarp();
     int sum = 0;  // fixed jobs' processing times on this lane's machine
@@ -530,6 +532,7 @@ __global__ void __launch_bounds__(kBig2wMaxWarps * 32) decompose_big_lb2w_kernel
   for (int node = blockIdx.x * nwarps + warp; node < B.count; node += gridDim.x * nwarps) {
     const int* perm = B.perms + static_cast<size_t>(node) * n;
     const int d1 = B.d1[node], d2 = B.d2[node], f = n - d1 - d2;
+    if (d1 < 0) continue;  // no node in this slot
     for (int i = lane; i < n; i += 32) {
       spm[i] = static_cast<uint16_t>(perm[i]);
       cidx[i] = 0xffff;
@@ -727,8 +730,9 @@ __global__ void __launch_bounds__(kBig1gWarps * 32, 1) decompose_big_lb1g_kernel
   // still spreads over every SM
   for (int g = warp * gridDim.x + blockIdx.x; g < groups; g += gridDim.x * kBig1gWarps) {
     const int node = g * 32 + lane;
-    const bool live = node < B.count;
-    const int d1 = live ? B.d1[node] : 0, d2 = live ? B.d2[node] : 0;
+    const int rd1 = node < B.count ? B.d1[node] : -1;  // -1: no node in this slot
+    const bool live = rd1 >= 0;
+    const int d1 = live ? rd1 : 0, d2 = live ? B.d2[node] : 0;
     const int len = d1 + d2;
     const int steps = __reduce_max_sync(0xffffffffu, len);
     const int* perm = B.perms + static_cast<size_t>(live ? node : 0) * n;
@@ -797,6 +801,7 @@ __global__ void __launch_bounds__(kBig1gWarps * 32, 1) decompose_big_lb1g_kernel
       const int nd = g * 32 + q;
       const int* sq = stage + q * 4 * MP;
       const int qd1 = __shfl_sync(0xffffffffu, d1, q), qd2 = __shfl_sync(0xffffffffu, d2, q);
+      if (!__shfl_sync(0xffffffffu, static_cast<int>(live), q)) continue;
       big1_children<M, MP>(B, sp, B.perms + static_cast<size_t>(nd) * n, qd1, n - qd1 - qd2, nd, sq, sq + MP,
                            sq + 2 * MP, sq + 3 * MP, lane);
     }

@@ -972,7 +972,8 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // cell's subtree when that cell is pruned/consumed (an explorer parked on a pruned cell
 // after a replay, or on an evaluated leaf, has already covered the whole subtree; its
 // padded V lies *before* its actual progress). Returns false when nothing remains (>= n!).
-__device__ __forceinline__ bool effective_pos(const int8_t* V, int level, const int8_t* cells, int n, int* pos) {
+template <typename T>
+__device__ __forceinline__ bool effective_pos(const T* V, int level, const T* cells, int n, int* pos) {
   for (int l = 0; l < n; ++l) pos[l] = l <= level ? V[l] : 0;
   if (cells[tri_off(level, n) + V[level]] > 0) return true;
   for (int l = level; l >= 0; --l) {  // + (n-1-level)!: increment digit `level` with carry
@@ -985,7 +986,8 @@ __device__ __forceinline__ bool effective_pos(const int8_t* V, int level, const 
 // log2 of end - pos: exact factoradic subtraction (borrows from the least significant digit;
 // end = n! when !has_end), then the leading non-zero digit (+ the next one) gives the
 // magnitude. -1 when nothing remains.
-__device__ __forceinline__ float remaining_log2_pos(const int* pos, const int8_t* E, bool has_end, int n,
+template <typename T>
+__device__ __forceinline__ float remaining_log2_pos(const int* pos, const T* E, bool has_end, int n,
                                                     const float* lgfact) {
   int lead = -1, d0 = 0, d1 = 0;
   if (has_end) {

@@ -452,7 +452,8 @@ __global__ void lens_kernel(IvmLayout L, const unsigned char* state, int K, cons
 
 // ---- multi-way interval splitting (exact mixed-radix arithmetic, no big integers)
 // D = end - pos as digits plus a top unit of weight n! (end = n! when !has_end).
-__device__ bool diff_digits(const int* pos, const int8_t* E, bool has_end, int n, int* D, int& top) {
+template <typename T>
+__device__ bool diff_digits(const int* pos, const T* E, bool has_end, int n, int* D, int& top) {
   top = 0;
   if (has_end) {
     int borrow = 0;
@@ -613,6 +614,7 @@ __global__ void split_victims_kernel(IvmLayout L, unsigned char* state, const in
 }
 
 #include "steal_ref.cuh"
+#include "explore_big.cuh"
 
 // Steal phase (src/explorer.cpp:283-340, B200 form). The explore kernel leaves one float per
 // explorer in S.lens (log2 of its remaining leaves from the effective position, -2 busy /
@@ -985,7 +987,7 @@ __global__ void __launch_bounds__(kStealThreads) group_export_kernel(StealParams
 }
 
 // Idle explorers in index order (slots for assign / import) and their count.
-__global__ void __launch_bounds__(kStealThreads) list_idle_kernel(IvmLayout L, const unsigned char* state, int K,
+__global__ void __launch_bounds__(kStealThreads) list_idle_kernel(size_t stride, int soff, const unsigned char* state, int K,
                                                                  int* slots, int* count) {
   __shared__ int s_idle[kStealThreads];
   const int t = threadIdx.x;
@@ -993,7 +995,7 @@ __global__ void __launch_bounds__(kStealThreads) list_idle_kernel(IvmLayout L, c
   const int lo = t * CH, hi = min(K, lo + CH);
   int idle = 0;
   for (int i = lo; i < hi; ++i)
-    idle += reinterpret_cast<const IvmHdr*>(state + static_cast<size_t>(i) * L.gstride)->state == kEmpty;
+    idle += state[static_cast<size_t>(i) * stride + soff] == kEmpty;
   s_idle[t] = idle;
   __syncthreads();
   for (int off = 1; off < kStealThreads; off <<= 1) {
@@ -1004,7 +1006,7 @@ __global__ void __launch_bounds__(kStealThreads) list_idle_kernel(IvmLayout L, c
   }
   int r = s_idle[t] - idle;
   for (int i = lo; i < hi; ++i)
-    if (reinterpret_cast<const IvmHdr*>(state + static_cast<size_t>(i) * L.gstride)->state == kEmpty) slots[r++] = i;
+    if (state[static_cast<size_t>(i) * stride + soff] == kEmpty) slots[r++] = i;
   if (t == kStealThreads - 1) *count = s_idle[t];
 }
 
@@ -1238,6 +1240,15 @@ struct pbbgpu_pool {
   FILE* timeline = nullptr;
   std::chrono::steady_clock::time_point t_start{}, t_last_sample{};
   bool sampled = false;
+  // explorer pool for n > 64 (explore_big.cuh): IVMs in HBM, bounded by the large-n kernels
+  bool big_explore = false;
+  BigIvmLayout BL{};
+  int big_steps = 8;
+  int *d_bperm = nullptr, *d_bd1 = nullptr, *d_bd2 = nullptr, *d_bfstat = nullptr;
+  uint8_t *d_bkind = nullptr, *d_bdir = nullptr, *d_bpr = nullptr;
+  int *d_blb = nullptr, *d_blf = nullptr, *d_blbw = nullptr;
+  BigImp* d_bimp = nullptr;
+  int* h_bfstat = nullptr;  // pinned
   // multi-GPU group over peer memory (pbbgpu_group_*)
   int g_world = 0, g_rank = 0, g_cap = 0;
   unsigned char* d_window = nullptr;       // own PeerWindow (IPC-exported)
@@ -1284,6 +1295,12 @@ struct pbbgpu_pool {
     cudaFree(d_ref_flags);
     cudaFree(d_ref_pairs);
     cudaFree(d_census);
+    for (void* q : {static_cast<void*>(d_bperm), static_cast<void*>(d_bd1), static_cast<void*>(d_bd2),
+                    static_cast<void*>(d_bfstat), static_cast<void*>(d_bkind), static_cast<void*>(d_bdir),
+                    static_cast<void*>(d_bpr), static_cast<void*>(d_blb), static_cast<void*>(d_blf),
+                    static_cast<void*>(d_blbw), static_cast<void*>(d_bimp)})
+      cudaFree(q);
+    if (h_bfstat) cudaFreeHost(h_bfstat);
     for (int q = 0; q < g_world; ++q)
       if (q != g_rank && g_peer[q]) cudaIpcCloseMemHandle(g_peer[q]);
     cudaFree(d_window);
@@ -1472,13 +1489,14 @@ void upload_tables(pbbgpu_pool* P, const HostTables& T) {
 
 // counters, histograms, incumbent and explorer states back to a fresh pool's
 void reset_search(pbbgpu_pool* P) {
-  if (P->batch_only) return;  // bounding-only pools keep no search state
+  if (P->batch_only && !P->big_explore) return;  // bounding-only pools keep no search state
   DevCounters z{};
   z.best = INT_MAX;
   xfer(P, P->d_ctr, &z, sizeof(z), cudaMemcpyHostToDevice, "copy");
   ck(cudaMemsetAsync(P->d_hist, 0, (static_cast<size_t>(P->n) + 1) * sizeof(unsigned long long), P->stream), "memset");
   ck(cudaMemsetAsync(P->d_dhist, 0, (static_cast<size_t>(P->n) + 1) * sizeof(unsigned long long), P->stream), "memset");
-  clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
+  if (P->big_explore) big_clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->BL, P->d_state, P->K);
+  else clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
   ck(cudaGetLastError(), "clear_kernel");
   P->launches += 1;
   ck(cudaStreamSynchronize(P->stream), "sync");
@@ -1573,6 +1591,38 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
          "malloc scratch");
     }
     P->K = 0;
+    if (P->cfg.explorers > 0) {  // explorer pool (explore_big.cuh)
+      if (P->cfg.steal_policy == 1 || P->cfg.record_census || (P->cfg.timeline_path && *P->cfg.timeline_path))
+        throw std::invalid_argument("pbbgpu: steal_policy 1, census and timeline need n <= 64");
+      P->big_explore = true;
+      P->K = P->cfg.explorers;
+      P->BL = big_ivm_layout(n);
+      P->big_steps = P->cfg.steps_per_round > 0 ? P->cfg.steps_per_round : 8;
+      const size_t K = static_cast<size_t>(P->K);
+      ck(cudaMalloc(&P->d_state, K * P->BL.stride), "malloc explorers");
+      ck(cudaMalloc(&P->d_bperm, K * n * sizeof(int)), "malloc");
+      ck(cudaMalloc(&P->d_bd1, K * sizeof(int)), "malloc");
+      ck(cudaMalloc(&P->d_bd2, K * sizeof(int)), "malloc");
+      ck(cudaMalloc(&P->d_bkind, K), "malloc");
+      ck(cudaMalloc(&P->d_bfstat, 4 * sizeof(int)), "malloc");
+      ck(cudaMallocHost(&P->h_bfstat, 4 * sizeof(int)), "malloc host");
+      ck(cudaMalloc(&P->d_blb, K * n * sizeof(int)), "malloc");
+      ck(cudaMalloc(&P->d_blf, K * n * sizeof(int)), "malloc");
+      ck(cudaMalloc(&P->d_blbw, K * n * sizeof(int)), "malloc");
+      ck(cudaMalloc(&P->d_bdir, K), "malloc");
+      ck(cudaMalloc(&P->d_bpr, K * n), "malloc");
+      ck(cudaMalloc(&P->d_bimp, kBigImpCap * sizeof(BigImp)), "malloc");
+      ck(cudaMalloc(&P->d_wrk, (K * 2 + 4) * sizeof(int)), "malloc");
+      ck(cudaMalloc(&P->d_lens, K * sizeof(float)), "malloc");
+      ck(cudaMalloc(&P->d_ctr, sizeof(DevCounters)), "malloc");
+      ck(cudaMallocHost(&P->h_ctr, sizeof(DevCounters)), "malloc host");
+      ck(cudaMalloc(&P->d_hist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
+      ck(cudaMalloc(&P->d_dhist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
+      std::vector<float> lgf(static_cast<size_t>(n) + 1, 0.f);
+      for (int k = 2; k <= n; ++k) lgf[static_cast<size_t>(k)] = lgf[static_cast<size_t>(k - 1)] + std::log2(static_cast<float>(k));
+      put(P, P->d_lgfact, lgf);
+      reset_search(P);
+    }
     return;
   }
   P->G = P->cfg.group > 0 ? P->cfg.group : pick_group(n, bound);
@@ -1701,6 +1751,30 @@ int split_kind(int cfg_mode) {
   }
 }
 
+// Large-n bounding launch over `count` batch slots (dead slots have d1 < 0): LB1 lane-per-node
+// tables when the fixed jobs dominate (measured crossover on ta111 near f = n/2), else warp per
+// node; LB2 warp per node when every node has f <= kBig2wFmax (shared memory sized for the
+// largest f), else CTA per node. nodes = live slots, fsum their free jobs.
+void launch_big_bounding(pbbgpu_pool* P, const BigBatchParams& G, int count, int fmax, long long fsum, int nodes) {
+  const int n = P->n;
+  if (P->big1 && fsum * 2 < static_cast<long long>(nodes) * n)
+    P->big1g<<<std::min((count + 31) / 32, P->big1g_grid), kBig1gWarps * 32, P->big1g_smem, P->stream>>>(G, P->d_ptot);
+  else if (P->big1)
+    P->big1<<<std::min((count + kBig1Warps - 1) / kBig1Warps, P->big_grid), kBig1Warps * 32, P->big_smem, P->stream>>>(
+        G, P->d_ptot);
+  else if (P->big2w && P->packed32big && fmax <= kBig2wFmax) {
+    const int fm = round_up(std::max(fmax, 4), 4);
+    int w = kBig2wMaxWarps;
+    while (w > 1 && static_cast<size_t>(big2w_smem_bytes(n, P->mp, P->m, fm, w)) > P->smem_optin) --w;
+    const int grid = std::min(P->big2w_grid, (count + w - 1) / w);
+    P->big2w<<<grid, w * 32, big2w_smem_bytes(n, P->mp, P->m, fm, w), P->stream>>>(G, P->d_ptot, P->d_packed32big, fm,
+                                                                                   P->d_pm_scratch);
+  } else {
+    P->big<<<std::min(count, P->big_grid), kBigThreads, P->big_smem, P->stream>>>(G);
+  }
+  ck(cudaGetLastError(), "decompose_big launch");
+}
+
 void read_counters(pbbgpu_pool* P) {
   xfer(P, P->h_ctr, P->d_ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, "ctr copy");
 }
@@ -1786,8 +1860,18 @@ T* scratch(pbbgpu_pool* P, int slot, size_t count) {
   return static_cast<T*>(P->scr[slot]);
 }
 
+void clear_explorers(pbbgpu_pool* P) {
+  if (P->big_explore) big_clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->BL, P->d_state, P->K);
+  else clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
+  ck(cudaGetLastError(), "clear_kernel");
+}
+
+size_t state_stride(const pbbgpu_pool* P) { return P->big_explore ? static_cast<size_t>(P->BL.stride) : static_cast<size_t>(P->L.gstride); }
+int state_off(const pbbgpu_pool* P) { return P->big_explore ? static_cast<int>(offsetof(BigHdr, state)) : static_cast<int>(offsetof(IvmHdr, state)); }
+
 void assign_digits(pbbgpu_pool* P, const std::vector<int>& a, const std::vector<int>& b, const std::vector<uint8_t>& nf, const std::vector<int>& slots) {
-  if (P->batch_only) throw StateError("pbbgpu: n > 64 pools are bounding-only (decompose_batch); exploration needs n <= 64");
+  if (P->batch_only && !P->big_explore)
+    throw StateError("pbbgpu: this n > 64 pool is bounding-only (decompose_batch); create it with explorers > 0 to explore");
   const int cnt = static_cast<int>(slots.size());
   if (cnt == 0) return;
   int* da = scratch<int>(P, 0, a.size());
@@ -1798,7 +1882,8 @@ void assign_digits(pbbgpu_pool* P, const std::vector<int>& a, const std::vector<
   xfer(P, db, b.data(), b.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
   xfer(P, ds, slots.data(), slots.size() * sizeof(int), cudaMemcpyHostToDevice, "copy");
   xfer(P, dn, nf.data(), nf.size(), cudaMemcpyHostToDevice, "copy");
-  init_kernel<<<(cnt + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, da, db, dn, ds, cnt);
+  if (P->big_explore) big_init_kernel<<<(cnt + 7) / 8, 256, 0, P->stream>>>(P->BL, P->d_state, da, db, dn, ds, cnt);
+  else init_kernel<<<(cnt + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, da, db, dn, ds, cnt);
   ck(cudaGetLastError(), "init_kernel");
   P->launches += 1;
   read_counters(P);
@@ -1809,7 +1894,7 @@ void assign_digits(pbbgpu_pool* P, const std::vector<int>& a, const std::vector<
 
 std::vector<int> idle_slots(pbbgpu_pool* P) {
   int* d_cnt = P->d_wrk + 2 * P->K;
-  list_idle_kernel<<<1, kStealThreads, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_wrk, d_cnt);
+  list_idle_kernel<<<1, kStealThreads, 0, P->stream>>>(state_stride(P), state_off(P), P->d_state, P->K, P->d_wrk, d_cnt);
   ck(cudaGetLastError(), "list_idle_kernel");
   P->launches += 1;
   int cnt = 0;
@@ -1821,7 +1906,7 @@ std::vector<int> idle_slots(pbbgpu_pool* P) {
 
 int count_active_host(pbbgpu_pool* P) {
   int* d_cnt = P->d_wrk + 2 * P->K;
-  list_idle_kernel<<<1, kStealThreads, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_wrk, d_cnt);
+  list_idle_kernel<<<1, kStealThreads, 0, P->stream>>>(state_stride(P), state_off(P), P->d_state, P->K, P->d_wrk, d_cnt);
   ck(cudaGetLastError(), "list_idle_kernel");
   P->launches += 1;
   int cnt = 0;
@@ -1939,8 +2024,145 @@ void sample_timeline(pbbgpu_pool* P, bool force) {
   }
 }
 
+// Leaf improvements of the large-n explorers (BigImp ring), validated by makespan.
+void harvest_big(pbbgpu_pool* P) {
+  const int cnt = std::min(P->h_ctr->imp_count, kBigImpCap);
+  if (cnt > 0) {
+    std::vector<BigImp> recs(static_cast<size_t>(cnt));
+    xfer(P, recs.data(), P->d_bimp, recs.size() * sizeof(BigImp), cudaMemcpyDeviceToHost, "imp copy");
+    std::scoped_lock lk(P->best_mu);
+    std::vector<int32_t> perm(static_cast<size_t>(P->n));
+    for (const BigImp& r : recs) {
+      if (r.mk >= P->best_sched_value) continue;
+      for (int i = 0; i < P->n; ++i) perm[static_cast<size_t>(i)] = r.perm[i];
+      int64_t mk = -1;
+      try {
+        mk = makespan_host(P->n, P->m, P->p.data(), perm.data());
+      } catch (const std::exception&) {
+        continue;  // torn record
+      }
+      if (mk != r.mk) continue;
+      P->best_sched_value = r.mk;
+      P->best_sched = perm;
+    }
+    const int zero = 0;
+    xfer(P, reinterpret_cast<char*>(P->d_ctr) + offsetof(DevCounters, imp_count), &zero, sizeof(int), cudaMemcpyHostToDevice, "imp reset");
+  }
+  std::scoped_lock lk(P->best_mu);
+  P->best_value = std::min<int64_t>(P->best_value, P->h_ctr->best);
+}
+
+// run_round of the n > 64 explorer pool: rounds of big_steps select -> bound -> branch steps,
+// then the steal pipeline (explore_big.cuh). Each step reads back 16 bytes (the batch's largest
+// and total free-job counts) to pick the bounding kernel.
+int big_run_round(pbbgpu_pool* P) {
+  const int64_t offer = P->pending_offer.exchange(INT64_MAX);
+  if (offer < P->best_value) {
+    {
+      std::scoped_lock lk(P->best_mu);
+      P->best_value = offer;
+    }
+    if (!P->cfg.pinned) set_device_best(P, offer);
+  }
+  const int n = P->n;
+  const int prune_mode = P->cfg.disable_pruning ? 2 : (P->cfg.pinned ? 1 : 0);
+  BigStepParams BS{};
+  BS.L = P->BL;
+  BS.state = P->d_state;
+  BS.K = P->K;
+  BS.perms = P->d_bperm;
+  BS.d1 = P->d_bd1;
+  BS.d2 = P->d_bd2;
+  BS.kind = P->d_bkind;
+  BS.fstat = P->d_bfstat;
+  BS.ctr = P->d_ctr;
+  BS.hist = P->d_hist;
+  BS.dhist = P->d_dhist;
+  BS.dir = P->d_bdir;
+  BS.pruned = P->d_bpr;
+  BS.lb_fwd = P->d_blf;
+  BS.prune_mode = prune_mode;
+  BS.imp = P->d_bimp;
+  BigBatchParams G{};
+  G.n = n;
+  G.m = P->m;
+  G.mp = P->mp;
+  G.npairs = P->npairs;
+  G.perms = P->d_bperm;
+  G.d1 = P->d_bd1;
+  G.d2 = P->d_bd2;
+  G.count = P->K;
+  G.p32 = P->d_p32;
+  G.pk = P->d_pk;
+  G.pl = P->d_pl;
+  G.packed = P->d_packed64;
+  G.inv16 = P->d_inv16;
+  G.scratch = P->d_big_scratch;
+  G.child_lb = P->d_blb;
+  G.lb_fwd = P->d_blf;
+  G.lb_bwd = P->d_blbw;
+  G.dir = P->d_bdir;
+  G.pruned = P->d_bpr;
+  StealParams S{};
+  S.K = P->K;
+  S.ctr = P->d_ctr;
+  S.thief = P->d_wrk;
+  S.victim = P->d_wrk + P->K;
+  S.plan = P->d_wrk + 2 * P->K + 2;
+  S.min_log2 = static_cast<float>(P->cfg.min_steal_log2 > 0 ? P->cfg.min_steal_log2 : std::log2(40320.0));
+  S.lgfact = P->d_lgfact;
+  S.trigger = static_cast<float>(P->cfg.steal_trigger > 0 ? P->cfg.steal_trigger : 1.0);
+  S.lens = P->d_lens;
+  S.max_split = P->cfg.max_split > 0 ? std::min(P->cfg.max_split, 63) : 4;
+  const int blocks = (P->K + 7) / 8;
+  for (int r = 0; r < P->rounds_per_sync; ++r) {
+    ck(cudaEventRecord(P->evs[3 * r], P->stream), "event");
+    for (int st = 0; st < P->big_steps; ++st) {
+      // the pruning bound of this step: the host's best (device improvements of this round
+      // reach it at the next synchronization; a higher bound only prunes less)
+      int64_t inc = P->cfg.disable_pruning ? INT_MAX : (P->cfg.pinned ? P->pinned_ub : P->best_value);
+      G.incumbent = static_cast<int>(std::min<int64_t>(inc, INT_MAX));
+      ck(cudaMemsetAsync(P->d_bfstat, 0, 4 * sizeof(int), P->stream), "memset");
+      big_select_kernel<8><<<blocks, 256, 0, P->stream>>>(BS);
+      ck(cudaGetLastError(), "big_select_kernel");
+      ck(cudaMemcpyAsync(P->h_bfstat, P->d_bfstat, 4 * sizeof(int), cudaMemcpyDeviceToHost, P->stream), "fstat");
+      ck(cudaStreamSynchronize(P->stream), "sync");
+      P->d2h_bytes += 4 * sizeof(int);
+      P->launches += 1;
+      if (P->h_bfstat[1] == 0) break;
+      launch_big_bounding(P, G, P->K, P->h_bfstat[0], P->h_bfstat[2], P->h_bfstat[1]);
+      big_branch_kernel<8><<<blocks, 256, 0, P->stream>>>(BS);
+      ck(cudaGetLastError(), "big_branch_kernel");
+      P->launches += 2;
+    }
+    ck(cudaEventRecord(P->evs[3 * r + 1], P->stream), "event");
+    big_lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->BL, P->d_state, P->K, P->d_lgfact, P->d_lens);
+    steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
+    big_split_thieves_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->BL, P->d_state, S.thief, S.victim, S.plan,
+                                                                         P->d_ctr);
+    big_split_victims_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->BL, P->d_state, S.victim, S.plan);
+    ck(cudaGetLastError(), "big steal pipeline");
+    ck(cudaEventRecord(P->evs[3 * r + 2], P->stream), "event");
+    P->launches += 4;
+  }
+  read_counters(P);
+  for (int r = 0; r < P->rounds_per_sync; ++r) {
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, P->evs[3 * r], P->evs[3 * r + 1]), "elapsed");
+    P->kernel_ms += ms;
+    ck(cudaEventElapsedTime(&ms, P->evs[3 * r + 1], P->evs[3 * r + 2]), "elapsed");
+    P->steal_ms += ms;
+  }
+  P->rounds += static_cast<uint64_t>(P->rounds_per_sync);
+  harvest_big(P);
+  P->last_active = P->h_ctr->active;
+  return P->h_ctr->active;
+}
+
 int run_round(pbbgpu_pool* P) {
-  if (P->batch_only) throw StateError("pbbgpu: n > 64 pools are bounding-only (decompose_batch); exploration needs n <= 64");
+  if (P->big_explore) return big_run_round(P);
+  if (P->batch_only)
+    throw StateError("pbbgpu: this n > 64 pool is bounding-only (decompose_batch); create it with explorers > 0 to explore");
   const int64_t offer = P->pending_offer.exchange(INT64_MAX);
   if (offer < P->best_value) {
     {
@@ -2421,8 +2643,7 @@ int pbbgpu_seed(pbbgpu_pool* P, int64_t bound, int first, int stride, int total)
       nf.push_back(last ? 1 : 0);
       slots.push_back(static_cast<int>(slots.size()));
     }
-    clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
-    ck(cudaGetLastError(), "clear_kernel");
+    clear_explorers(P);
     P->launches += 1;
     assign_digits(P, a, b, nf, slots);
   });
@@ -2459,8 +2680,7 @@ int pbbgpu_assign_split_strided(pbbgpu_pool* P, int first, int stride, int count
       else nf[static_cast<size_t>(c)] = 1;
       slots[static_cast<size_t>(c)] = c;
     }
-    clear_kernel<<<(P->K + 255) / 256, 256, 0, P->stream>>>(P->L, P->d_state, P->K);
-    ck(cudaGetLastError(), "clear_kernel");
+    clear_explorers(P);
     P->launches += 1;
     assign_digits(P, a, b, nf, slots);
   });
@@ -2753,7 +2973,7 @@ int pbbgpu_explorer_lengths(pbbgpu_pool* P, float* out, int cap) {
 
 int pbbgpu_stats(pbbgpu_pool* P, pbbgpu_stats_t* out) {
   return guarded([&] {
-    if (P->batch_only) {
+    if (P->batch_only && !P->big_explore) {
       std::memset(out, 0, sizeof(*out));
       out->kernel_launches = P->launches;
       out->batch_kernel_ms = P->batch_ms;
@@ -2850,34 +3070,13 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
       G.dir = ddir;
       G.pruned = dpr;
       ck(cudaEventRecord(P->ev0, P->stream), "event");
-      // LB1: the node tables cost ~(d1 + d2) steps, the children ~f; lane-per-node tables win
-      // when the fixed part dominates (measured crossover on ta111 near f = n/2)
+      int fmax = 0;
       long long fsum = 0;
-      for (int i = 0; i < count; ++i) fsum += n - d1[i] - d2[i];
-      if (P->big1 && fsum * 2 < static_cast<long long>(count) * n)
-        P->big1g<<<std::min((count + 31) / 32, P->big1g_grid), kBig1gWarps * 32,
-                    P->big1g_smem, P->stream>>>(G, P->d_ptot);
-      else if (P->big1)
-        P->big1<<<std::min((count + kBig1Warps - 1) / kBig1Warps, P->big_grid), kBig1Warps * 32, P->big_smem, P->stream>>>(
-            G, P->d_ptot);
-      else if (P->big2w && P->packed32big && [&] {
-                 for (int i = 0; i < count; ++i)
-                   if (n - d1[i] - d2[i] > kBig2wFmax) return false;
-                 return true;
-               }()) {
-        // LB2 warp per node: smem sized for the batch's largest f
-        int fmax = 4;
-        for (int i = 0; i < count; ++i) fmax = std::max(fmax, n - d1[i] - d2[i]);
-        fmax = round_up(fmax, 4);
-        int w = kBig2wMaxWarps;
-        const size_t cap = P->smem_optin;
-        while (w > 1 && static_cast<size_t>(big2w_smem_bytes(n, P->mp, P->m, fmax, w)) > cap) --w;
-        const int grid = std::min(P->big2w_grid, (count + w - 1) / w);
-        P->big2w<<<grid, w * 32, big2w_smem_bytes(n, P->mp, P->m, fmax, w), P->stream>>>(G, P->d_ptot, P->d_packed32big, fmax,
-                                                                                         P->d_pm_scratch);
-      } else
-        P->big<<<std::min(count, P->big_grid), kBigThreads, P->big_smem, P->stream>>>(G);
-      ck(cudaGetLastError(), "decompose_big launch");
+      for (int i = 0; i < count; ++i) {
+        fmax = std::max(fmax, n - d1[i] - d2[i]);
+        fsum += n - d1[i] - d2[i];
+      }
+      launch_big_bounding(P, G, count, fmax, fsum, count);
       ck(cudaEventRecord(P->ev1, P->stream), "event");
     }
     BatchParams B{};

@@ -32,6 +32,9 @@ def main():
     # VFR-like 30 x 15 instance
     for name, ub in (("gen:30:15:4242", 2490), ("gen:16:13:1234", 1512), ("gen:18:3:77", 926)):
         counts[f"{name}@{ub}"] = json.loads(run("hist", name, ub))
+    # n > 64 fixed trees (explorer pools with IVM state in HBM)
+    for name, ub in (("ta061", 5493), ("ta081", 6070), ("ta101", 11150), ("ta111", 26000)):
+        counts[f"{name}@{ub}"] = json.loads(run("hist", name, ub))
     for name in ("ta001", "ta041"):
         counts[f"{name}@neh"] = json.loads(run("solve", name, "neh", 1, 1))
     for name in ("ta001", "ta011", "ta021", "ta031", "ta041", "ta056", "ta111"):

@@ -806,3 +806,35 @@ def test_product_worker_speaks_the_reference_protocol_over_tcp(workers):
         assert r["unique"] == 158049 and r["leaves"] == 54 and r["splits"] == 0
     else:
         assert r["splits"] > 0
+
+
+# ---------------------------------------------------------------- explorer pools for n > 64
+
+@pytest.mark.parametrize("key,bound,K", [("ta061@5493", "lb1", 1024), ("ta081@6070", "lb1", 4096),
+                                         ("ta101@11150", "lb1", 8192), ("ta111@26000", "lb1", 2048),
+                                         ("ta081@6070", "lb2", 4096), ("ta111@26000", "lb2", 1024)])
+def test_large_n_explorer_pool_fixed_trees(key, bound, K):
+    """64 < n <= 512: IVM explorers in HBM (int16 cells), one select -> bound (the large-n
+    kernels) -> branch step at a time, log2-bucket interval stealing: unique counts, leaves and
+    per-f histograms equal the reference's K = 1 fixed trees (LB1) / the oracle's (LB2)."""
+    gold = golden_io.ref_counts()[key] if bound == "lb1" else golden_io.lb2_counts()[key]
+    want = gold["decomposed"] if bound == "lb1" else gold["unique"]
+    name, ub = key.split("@")
+    inst = pbb.taillard_named(name)
+    res = pbb.pool_run(inst, int(ub), cfg=pbb.PoolConfig(explorers=K), bound=bound)
+    assert res.stats.K == K and res.stats.completed
+    assert res.stats.unique == want and res.stats.leaves == gold["leaves"]
+    assert res.best_value == int(ub)
+    assert {str(k): v for k, v in res.hist.items()} == {str(k): v for k, v in gold["hist"].items()}
+
+
+def test_large_n_explorer_pool_finds_optimum_and_partitions():
+    """An improving run from NEH on ta061 (100 x 5) proves the optimum 5493 with a verified
+    schedule; a user partition of [0, n!) gives the same fixed-tree count."""
+    inst = pbb.taillard_named("ta061")
+    res = pbb.pool_run(inst, pbb.neh(inst).cmax, cfg=pbb.PoolConfig(explorers=1024))
+    assert res.best_value == 5493 and pbb.makespan(inst, res.best.perm) == 5493
+    nf = math.factorial(100)
+    cuts = [0, nf // 7, nf // 3, nf // 2 + 12345, nf]
+    res2 = pbb.pool_run(inst, 5493, intervals=list(zip(cuts[:-1], cuts[1:])), cfg=pbb.PoolConfig(explorers=1024))
+    assert res2.stats.unique == golden_io.ref_counts()["ta061@5493"]["decomposed"]
