@@ -237,6 +237,26 @@ def run_extras(pbb, solve_distributed, dev, local, world, rank, peak, args):
             r, ms = timed(lambda: solve_distributed(pool, ub, device=dev, time_limit_s=secs))
         out[key] = {"ms": ms, "unique_nodes": r.unique, "leaves": r.leaves, "best": r.best_value,
                     "nodes_per_s": r.unique / (ms / 1e3), "completed": r.completed}
+    # ta111 (500 x 20) exploration: the n > 64 explorer pool (IVMs in HBM) from the NEH bound
+    inst = pbb.taillard_named("ta111")
+    row = {"note": "single-GPU only (the n > 64 pools have no peer-memory exchange)"}
+    if world == 1:
+        with pbb.GpuPool(inst, pbb.PoolConfig(device=local, explorers=32768), bound="lb1") as pool:
+            r, ms = timed(lambda: solve_distributed(pool, 26670, device=dev, time_limit_s=5.0))
+        row = {"ms": ms, "unique_nodes": r.unique, "best": r.best_value, "nodes_per_s": r.unique / (ms / 1e3),
+               "explorers_per_gpu": 32768}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+        if os.path.exists(drv):
+            cores = cpu_cores()
+            o = subprocess.run([drv, "solve", "ta111", "neh", str(8 * cores), str(cores), "10"], capture_output=True,
+                               text=True, check=True).stdout
+            ref = json.loads(o.strip().splitlines()[-1])
+            row["cpu_baseline"] = {"value": ref["decomposed"] / ref["wall_s"], "unit": "nodes/s", "cores": cores,
+                                   "kind": "reference", "sample": f"oracle/_ref/ref_driver pool_run ta111 LB1 UB=NEH "
+                                   f"26670, K={8 * cores}, {cores} threads, 10 s"}
+            row["vs_cpu_reference"] = row["nodes_per_s"] / row["cpu_baseline"]["value"]
+    out["ta111_lb1_explore_neh_5s"] = row
     # ta111 bounding sweep on every rank: each GPU bounds its own batch (weak scaling, no
     # collective on the data path); rate = world x batch / max-over-ranks kernel time
     inst = pbb.taillard_named("ta111")

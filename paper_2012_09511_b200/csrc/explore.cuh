@@ -1026,29 +1026,6 @@ __device__ __forceinline__ float remaining_log2_pos(const int* pos, const T* E, 
   return lgfact[n - 1 - lead] + __log2f(d);
 }
 
-// mid = floor((pos + end) / 2) (src/factoradic.cpp:59-93); true when mid > pos.
-__device__ __forceinline__ bool midpoint_pos(const int* pos, const int8_t* E, bool has_end, int n, int* mid) {
-  int carry = 0;
-  if (has_end) {
-    for (int l = n - 1; l >= 0; --l) {
-      const int s = pos[l] + E[l] + carry, radix = n - l;
-      mid[l] = s % radix;
-      carry = s / radix;
-    }
-  } else {
-    for (int l = 0; l < n; ++l) mid[l] = pos[l];
-    carry = 1;
-  }
-  int rem = carry, cmp = 0;
-  for (int l = 0; l < n; ++l) {
-    const int cur = rem * (n - l) + mid[l];
-    mid[l] = cur / 2;
-    rem = cur % 2;
-    if (!cmp) cmp = mid[l] < pos[l] ? -1 : (mid[l] > pos[l] ? 1 : 0);
-  }
-  return cmp > 0;
-}
-
 // Prefix / suffix sums of every job's row (node_tables' max-plus scans), built from the
 // global p32 table while the CTA stages the instance.
 __device__ __forceinline__ void stage_prefix_sums(unsigned char* smem, const InstLayout& IL, const int* p32, int n,

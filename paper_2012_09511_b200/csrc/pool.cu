@@ -1187,6 +1187,7 @@ struct pbbgpu_pool {
   int* d_pm_scratch = nullptr;         // per warp [kBig2wFmax][32] PM' ranks
   int big2w_grid = 0, big2w_warps = 0;
   size_t smem_optin = 0;               // cudaDevAttrMaxSharedMemoryPerBlockOptin
+  int num_sms = 148;                   // cudaDeviceProp::multiProcessorCount
   uint16_t* d_inv16 = nullptr;
   int* d_big_scratch = nullptr;
   int big_grid = 0;
@@ -1535,6 +1536,7 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
     ck(cudaSetDevice(P->cfg.device), "cudaSetDevice");
     ck(cudaGetDeviceProperties(&prop, P->cfg.device), "cudaGetDeviceProperties");
     if (prop.major < 10) throw CudaError("pbbgpu: kernels are built for sm_100a only");
+    P->num_sms = prop.multiProcessorCount;
     ck(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&P->ev0), "event");
     ck(cudaEventCreate(&P->ev1), "event");
@@ -2516,7 +2518,7 @@ void batch_bound(pbbgpu_pool* P, const std::vector<int>& perms, const std::vecto
   B.dir = ddir;
   B.pruned = dpr;
   const int NG = P->block / P->G;
-  const int grid = std::min((count + NG - 1) / NG, 148 * 8);
+  const int grid = std::min((count + NG - 1) / NG, P->num_sms * 8);
   P->bfn<<<grid, P->block, P->smem, P->stream>>>(B);
   ck(cudaGetLastError(), "decompose_batch launch");
   P->launches += 1;
@@ -3101,7 +3103,7 @@ int pbbgpu_decompose_batch(pbbgpu_pool* P, const int32_t* perms, const int32_t* 
     B.pruned = dpr;
     if (!P->batch_only) {
       const int NG = P->block / P->G;
-      const int grid = std::min((count + NG - 1) / NG, 148 * 8);
+      const int grid = std::min((count + NG - 1) / NG, P->num_sms * 8);
       ck(cudaEventRecord(P->ev0, P->stream), "event");
       P->bfn<<<grid, P->block, P->smem, P->stream>>>(B);
       ck(cudaGetLastError(), "decompose_batch launch");
