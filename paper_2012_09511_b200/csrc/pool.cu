@@ -1063,6 +1063,8 @@ ExploreFn explore_fn(int m, int bound, int G, bool small) {
       case 5: return explore_for_group<5, kLB1>(G, false);
       case 10: return explore_for_group<10, kLB1>(G, false);
       case 20: return explore_for_group<20, kLB1>(G, false);
+      case 40: return explore_for_group<40, kLB1>(G, false);
+      case 60: return explore_for_group<60, kLB1>(G, false);
     }
   } else {
     switch (m) {
@@ -1127,6 +1129,8 @@ BatchFn batch_fn(int m, int bound, int G, bool small) {
       case 5: return batch_for_group<5, kLB1>(G, false);
       case 10: return batch_for_group<10, kLB1>(G, false);
       case 20: return batch_for_group<20, kLB1>(G, false);
+      case 40: return batch_for_group<40, kLB1>(G, false);
+      case 60: return batch_for_group<60, kLB1>(G, false);
     }
   } else {
     switch (m) {
@@ -1361,8 +1365,8 @@ void validate_times(int n, int m, const int32_t* p) {
 // last real machine's), and LB2 pairs are built over the real machines only, so every value
 // the reference defines is unchanged (tests/test_gpu.py::test_any_machine_count_*).
 int compiled_m(int m) {
-  if (m < 1 || m > 20) throw std::invalid_argument("pbbgpu: m must be in [1, 20] (padded to 5, 10 or 20 machines)");
-  return m <= 5 ? 5 : (m <= 10 ? 10 : 20);
+  if (m < 1 || m > 60) throw std::invalid_argument("pbbgpu: m must be in [1, 60] (padded to 5, 10, 20, 40 or 60 machines)");
+  return m <= 5 ? 5 : (m <= 10 ? 10 : (m <= 20 ? 20 : (m <= 40 ? 40 : 60)));
 }
 
 std::vector<int32_t> pad_machines(int n, int m, int M, const int32_t* p) {
@@ -1518,6 +1522,9 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
   if (bound != kLB1 && bound != kLB2) throw std::invalid_argument("pbbgpu: bound must be PBBGPU_LB1 or PBBGPU_LB2");
   const int m = compiled_m(m_real);
   if (bound == kLB2 && m_real < 2) bound = kLB1;  // no machine pair: LB2 is LB1
+  if (m > 20 && (bound == kLB2 || n > kMaxN))
+    throw std::invalid_argument("pbbgpu: m > 20 is supported for LB1 with n <= 64 (LB2 pair tables and the n > 64 "
+                                "kernels are compiled for m <= 20)");
   validate_times(n, m, pad_machines(n, m_real, m, p_real).data());
   P->m_real = m_real;
   if (cfg && cfg->record_census && n > 20) throw std::invalid_argument("record_census needs n <= 20 (position_u64)");

@@ -30,7 +30,8 @@ def main():
         counts[f"{name}@{ub}"] = json.loads(run("hist", name, ub))
     # machine counts the compiled kernels do not have (padded with zero-time machines), incl. a
     # VFR-like 30 x 15 instance
-    for name, ub in (("gen:30:15:4242", 2490), ("gen:16:13:1234", 1512), ("gen:18:3:77", 926)):
+    for name, ub in (("gen:30:15:4242", 2490), ("gen:16:13:1234", 1512), ("gen:18:3:77", 926),
+                     ("gen:14:40:2024", 3124), ("gen:12:60:606", 4417), ("gen:16:25:99", 2282)):
         counts[f"{name}@{ub}"] = json.loads(run("hist", name, ub))
     # n > 64 fixed trees (explorer pools with IVM state in HBM)
     for name, ub in (("ta061", 5493), ("ta081", 6070), ("ta101", 11150), ("ta111", 26000)):

@@ -760,9 +760,13 @@ def test_reference_coordinator_drives_several_gpu_workers():
 
 # ---------------------------------------------------------------- any machine count (m <= 20)
 
-@pytest.mark.parametrize("m", [1, 2, 3, 4, 7, 9, 13, 15, 17, 19])
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 7, 9, 13, 15, 17, 19, 23, 40, 47, 60])
 @pytest.mark.parametrize("bound", ["lb1", "lb2"])
 def test_any_machine_count_bounds_match_oracle(m, bound):
+    if m > 20 and bound == "lb2":
+        with pytest.raises(ValueError):
+            pbb.GpuPool(pbb.generate_taillard(12, m, 1), bound="lb2")
+        return
     """m not in {5, 10, 20}: the pool pads the instance with zero-time machines; every child
     bound (LB2 over the real machine pairs only; m = 1: LB1) equals the oracle's."""
     n = 12
@@ -779,10 +783,12 @@ def test_any_machine_count_bounds_match_oracle(m, bound):
         assert int(dr[i]) == d and [int(x) for x in lb[i, :f]] == clb
 
 
-@pytest.mark.parametrize("key", ["gen:30:15:4242@2490", "gen:16:13:1234@1512", "gen:18:3:77@926"])
+@pytest.mark.parametrize("key", ["gen:30:15:4242@2490", "gen:16:13:1234@1512", "gen:18:3:77@926",
+                                 "gen:14:40:2024@3124", "gen:12:60:606@4417", "gen:16:25:99@2282"])
 def test_any_machine_count_fixed_trees_match_reference(key):
-    """Fixed trees of instances with 15 (VFR-like 30 x 15), 13 and 3 machines: unique node count,
-    leaves and the per-f histogram equal the compiled reference's (ref_driver hist)."""
+    """Fixed trees of instances with 15 (VFR-like 30 x 15), 13, 3, 25, 40 and 60 machines (LB1; m > 20
+    runs the M = 40 / 60 kernels): unique node count, leaves and the per-f histogram equal the
+    compiled reference's (ref_driver hist)."""
     g = golden_io.ref_counts()[key]
     name, ub = key.split("@")
     n, m, seed = (int(x) for x in name[4:].split(":"))
