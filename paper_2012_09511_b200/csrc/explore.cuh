@@ -531,18 +531,28 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
     // (kFusedCombine), so the per-lane table only carries PM' and is int16 ([job][32] x 2 B)
     static_assert(kFusedCombine<SMALLN>, "the n > 32 path keeps only PM' in its lane table");
     unsigned char* Pb = reinterpret_cast<unsigned char*>(reinterpret_cast<int16_t*>(iv.pm) + lane);
+    // the 64-bit mask walked as two 32-bit words (one FLO per set bit instead of the 64-bit
+    // find-first / count-leading sequences)
     int E = Btot, pm = NEG;
-    for (unsigned long long w = Fq; w; w &= w - 1) {
-      const int t = __ffsll(static_cast<long long>(w)) - 1;
+    auto fwd = [&](int t) {
       const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
       *reinterpret_cast<int16_t*>(Pb + ((e & 0x1f80u) >> 1)) = static_cast<int16_t>(pm);
       pm = max(pm, E + static_cast<int>((e >> 13) & 0x7ffu));
       E += static_cast<int>(e) >> 24;
+    };
+    const uint32_t lo32 = static_cast<uint32_t>(Fq), hi32 = static_cast<uint32_t>(Fq >> 32);
+    for (uint32_t w = __brev(lo32); w;) {  // ascending: positions 31 - u, then 63 - u
+      const int u = bfind_u32(w);
+      w ^= 1u << u;
+      fwd(31 - u);
+    }
+    for (uint32_t w = __brev(hi32); w;) {
+      const int u = bfind_u32(w);
+      w ^= 1u << u;
+      fwd(63 - u);
     }
     int G = Atot, sm = NEG;
-    for (unsigned long long w = Fq; w;) {
-      const int t = 63 - __clzll(static_cast<long long>(w));
-      w ^= 1ull << t;
+    auto bwd = [&](int t) {
       const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
       int* slot = nullptr;
       const int v = static_cast<int>(e) >> 24;
@@ -551,6 +561,16 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
       fold(e, __byte_perm(static_cast<uint32_t>(lo), static_cast<uint32_t>(hi), 0x5410), slot);
       G -= v;
       sm = max(sm, G + static_cast<int>((e >> 13) & 0x7ffu));
+    };
+    for (uint32_t w = hi32; w;) {  // descending
+      const int t = bfind_u32(w);
+      w ^= 1u << t;
+      bwd(32 + t);
+    }
+    for (uint32_t w = lo32; w;) {
+      const int t = bfind_u32(w);
+      w ^= 1u << t;
+      bwd(t);
     }
   }
   if constexpr (kFusedCombine<SMALLN>) return;
