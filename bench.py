@@ -476,7 +476,9 @@ def main():
                            "work_split": "live siblings" if int(wl.get("split_mode", 0)) == 1 else "factoradic (reference)",
                            "initial_partition": (f"breadth-first seeding into world*K/{seed_div} intervals"
                                                  if seed_div else "world*K equal factoradic ranges, interleaved"),
-                           "l2": "256 MiB flush between steps, outside the per-step event brackets"},
+                           "l2": "256 MiB flush between steps, outside the per-step event brackets",
+                           "exchange_us_per_round": getattr(results[-1], "exchange_us_per_round", 0.0),
+                           "inter_gpu_intervals_per_step": results[-1].remote_intervals},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clocks, "extra": extra}
         print(json.dumps(line), flush=True)

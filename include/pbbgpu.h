@@ -246,6 +246,8 @@ typedef struct {
   double wall_s;
   double device_ms;     /* CUDA-event time of the solve loop */
   int completed;        /* 0 when the time limit stopped it */
+  double exchange_us_per_round; /* device time of the exchange kernels (incumbent MIN, import,
+                                   request / claim, export into the peer) per round */
 } pbbgpu_group_stats_t;
 int pbbgpu_group_handle_size(void);
 int pbbgpu_group_create(pbbgpu_pool* pool, int world, int rank, void* handle_out);

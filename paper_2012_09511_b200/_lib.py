@@ -100,6 +100,7 @@ class GroupStats(ctypes.Structure):
         ("wall_s", ctypes.c_double),
         ("device_ms", ctypes.c_double),
         ("completed", ctypes.c_int),
+        ("exchange_us_per_round", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:

@@ -1261,6 +1261,9 @@ struct pbbgpu_pool {
   bool g_open = false;
   GroupState* d_gs = nullptr;
   GroupState* h_gs = nullptr;              // pinned
+  cudaEvent_t gev[8] = {};                 // per round: start of the exchange kernels
+  double group_ms = 0;                     // device time of the exchange kernels
+  uint64_t group_rounds = 0;
   // marks (explorer.hpp:94-96)
   int64_t improvement_mark = INT64_MAX;
   uint64_t steal_mark = 0;
@@ -1315,6 +1318,8 @@ struct pbbgpu_pool {
     if (h_ctr) cudaFreeHost(h_ctr);
     if (pin) cudaFreeHost(pin);
     for (cudaEvent_t e : evs)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : gev)
       if (e) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -2239,6 +2244,7 @@ int run_round(pbbgpu_pool* P) {
     split_victims_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, S.victim, S.plan, S.split_mode);
     ck(cudaGetLastError(), "split_victims_kernel launch");
     if (P->g_open) {  // inter-GPU exchange over peer memory (no host involvement)
+      ck(cudaEventRecord(P->gev[r], P->stream), "event");
       const GroupParams G = group_params(P);
       group_exchange_kernel<<<1, kStealThreads, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, P->d_ctr, G);
       ck(cudaGetLastError(), "group_exchange_kernel launch");
@@ -2258,6 +2264,11 @@ int run_round(pbbgpu_pool* P) {
     P->kernel_ms += ms;
     ck(cudaEventElapsedTime(&ms, P->evs[3 * r + 1], P->evs[3 * r + 2]), "elapsed");
     P->steal_ms += ms;
+    if (P->g_open) {
+      ck(cudaEventElapsedTime(&ms, P->gev[r], P->evs[3 * r + 2]), "elapsed");
+      P->group_ms += ms;
+      P->group_rounds += 1;
+    }
   }
   P->rounds += static_cast<uint64_t>(R);
   harvest(P);
@@ -3398,6 +3409,8 @@ int pbbgpu_group_create(pbbgpu_pool* P, int world, int rank, void* handle_out) {
     P->g_world = world;
     P->g_rank = rank;
     P->g_peer[rank] = P->d_window;
+    for (cudaEvent_t& e : P->gev)
+      if (!e) ck(cudaEventCreate(&e), "event");
     ck(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out), P->d_window), "cudaIpcGetMemHandle");
   });
 }
@@ -3451,6 +3464,8 @@ int pbbgpu_group_solve(pbbgpu_pool* P, int64_t initial_ub, int seed_div, double 
     bool completed = true, have_prev = false;
     GroupState prev{};
     uint64_t syncs = 0;
+    const double g0 = P->group_ms;
+    const uint64_t gr0 = P->group_rounds;
     for (;;) {
       run_round(P);
       ++syncs;
@@ -3493,6 +3508,7 @@ int pbbgpu_group_solve(pbbgpu_pool* P, int64_t initial_ub, int seed_div, double 
     out->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     out->device_ms = ms;
     out->completed = completed ? 1 : 0;
+    out->exchange_us_per_round = P->group_rounds > gr0 ? 1000.0 * (P->group_ms - g0) / static_cast<double>(P->group_rounds - gr0) : 0.0;
   });
 }
 

@@ -49,6 +49,7 @@ class DistResult:
     exchanges: int
     hist: Dict[int, int]
     completed: bool
+    exchange_us_per_round: float = 0.0  # native plane: device time of the exchange kernels per round
 
 
 _DELTA = ("unique", "decomposed", "leaves", "improvements", "local_steals")
@@ -69,8 +70,10 @@ def _solve_native(pool, ub, group, device, time_limit_s, seed_div, world, rank) 
     dist.barrier(group=group)        # every window reset before any rank pushes into it
     gst = pool.group_solve(ub, seed_div, time_limit_s)
     dist.barrier(group=group)        # nobody reads or writes a peer window after this
-    return _finish(pool, st0, h0, group, device, world, rank, int(gst["imported"]), int(gst["syncs"]),
-                   int(gst["exchanges"]), bool(gst["completed"]))
+    res = _finish(pool, st0, h0, group, device, world, rank, int(gst["imported"]), int(gst["syncs"]),
+                  int(gst["exchanges"]), bool(gst["completed"]))
+    res.exchange_us_per_round = float(gst["exchange_us_per_round"])
+    return res
 
 
 def solve_distributed(pool, ub: int, group=None, device=None, export_max: Optional[int] = None,
