@@ -27,6 +27,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "pbb_layout.h"
 
@@ -42,15 +43,16 @@ struct InstLayout {
 
 // packed = warp-per-explorer LB2 (children_lb2_w): one uint32 per (position, pair),
 // transposed [t][q]; otherwise the group LB2 tables (order [q][t], lag [q][j]).
-__host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs, bool packed = false) {
+// wide = 32-bit times: the exclusive and inclusive sums are two int32 [n][mp] arrays.
+__host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs, bool packed = false, bool wide = false) {
   InstLayout s;
   int o = 0;
   s.o_p32 = o;
   o += n * mp * 4;
   s.o_psf = o;  // [n][mp] prefix sums of p: exclusive | inclusive << 16
-  o += n * mp * 4;
+  o += n * mp * (wide ? 8 : 4);
   s.o_psb = o;  // [n][mp] suffix sums of p: exclusive | inclusive << 16
-  o += n * mp * 4;
+  o += n * mp * (wide ? 8 : 4);
   s.o_lag = o;
   o += packed ? 0 : round_up(npairs * n * 2, 16);
   s.o_pk32 = o;
@@ -74,11 +76,12 @@ __host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs, boo
   return s;
 }
 
-__host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound, int lanes) {
+__host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound, int lanes, bool wide = false) {
   IvmLayout L;
   L.n = n;
   L.m = m;
   L.mp = round_up(m, 4);
+  L.ftb = wide ? 4 : 2;
   int o = 8;  // IvmHdr
   L.o_cells = o;
   o += n * (n + 1) / 2;
@@ -92,9 +95,9 @@ __host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound, int lan
   o += n;
   o = round_up(o, 4);
   L.o_ft = o;
-  o += (n + 1) * m * 2;
+  o += (n + 1) * m * L.ftb;
   L.o_r = o;
-  o += m * 2;
+  o += m * L.ftb;
   L.gstride = round_up(o, 16);
   o = L.gstride;
   L.o_fr = o;
@@ -166,6 +169,10 @@ struct Group {
   }
 };
 
+// FT / R entry type: uint16 unless the instance needs wide times (IvmLayout::ftb == 4)
+template <bool W>
+using FtT = typename std::conditional<W, uint32_t, uint16_t>::type;
+
 // Shared-memory view of one explorer.
 struct IvmView {
   IvmHdr* hdr;
@@ -214,6 +221,10 @@ struct IvmView {
     pm = reinterpret_cast<int16_t*>(b + L.o_lst);
     sm = pm + L.n * 32;
   }
+  template <bool W>
+  __device__ __forceinline__ FtT<W>* ftw() const { return reinterpret_cast<FtT<W>*>(ft); }
+  template <bool W>
+  __device__ __forceinline__ FtT<W>* Rw() const { return reinterpret_cast<FtT<W>*>(R); }
 };
 
 struct InstView {
@@ -672,7 +683,9 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
 
 // MinMin (src/bound.cpp:109-131): lo over the union, fewer occurrences of lo wins, then the
 // larger sum, then Forward.
-template <int G>
+// Wide times (W): the count and sum differences are reduced separately (the sum of n bounds
+// stays below 2^31, validate_times).
+template <int G, bool W = false>
 __device__ __forceinline__ int minmin(const Group<G>& grp, const IvmView& iv, int f) {
   // one pass: per-lane minimum with its fwd/bwd occurrence counts and the running
   // sum difference; lanes whose minimum is the group's contribute their count difference.
@@ -692,6 +705,13 @@ __device__ __forceinline__ int minmin(const Group<G>& grp, const IvmView& iv, in
     sd += a - b;
   }
   const int glo = grp.rmin(lo);
+  if constexpr (W) {
+    const int cd = grp.rsum(lo == glo ? cf - cb : 0);
+    if (cd) return cd < 0 ? kFwd : kBwd;
+    const int v = grp.rsum(sd);
+    if (v) return v > 0 ? kFwd : kBwd;
+    return kFwd;
+  }
   const int v = grp.rsum(((lo == glo ? cf - cb : 0) << 24) + sd);
   const int cd = (v + (1 << 23)) >> 24;
   if (cd) return cd < 0 ? kFwd : kBwd;  // fewer occurrences of lo wins
@@ -701,7 +721,7 @@ __device__ __forceinline__ int minmin(const Group<G>& grp, const IvmView& iv, in
 
 // Node tables from the incremental stacks: node at `level` with selected job `job` placed
 // by dir[level]; d1/d2 include it.
-template <int M, int G>
+template <int M, int G, bool W = false>
 __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& iv,
                                             const InstView& in, int n, int mp, int job, int dI,
                                             int d1, int d2) {
@@ -712,8 +732,8 @@ __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& 
   // chunks with log2(G) shuffles instead of one lane walking all M machines.
   constexpr int C = (M + G - 1) / G;
   constexpr int NEG = -(1 << 30);
-  const uint16_t* fsrc = iv.ft + (dI == kFwd ? d1 - 1 : d1) * M;
-  const uint16_t* tsrc = iv.ft + (n - (dI == kBwd ? d2 - 1 : d2)) * M;
+  const FtT<W>* fsrc = iv.ftw<W>() + (dI == kFwd ? d1 - 1 : d1) * M;
+  const FtT<W>* tsrc = iv.ftw<W>() + (n - (dI == kBwd ? d2 - 1 : d2)) * M;
   const int* pr = in.p32 + job * mp;
   const int k0 = grp.g * C;
   int loc[C], inc[C];
@@ -725,8 +745,8 @@ __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& 
       const int k = k0 + c;
       if (k < M) {
         const uint32_t u = ps[k];
-        run = max(run, static_cast<int>(fsrc[k]) - static_cast<int>(u & 0xffffu));
-        inc[c] = static_cast<int>(u >> 16);
+        run = max(run, static_cast<int>(fsrc[k]) - static_cast<int>(W ? u : u & 0xffffu));
+        inc[c] = static_cast<int>(W ? ps[n * mp + k] : u >> 16);
       }
       loc[c] = run;
     }
@@ -746,8 +766,8 @@ __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& 
       const int k = k0 + c;
       if (k < M) {
         const uint32_t u = ps[k];
-        run = max(run, static_cast<int>(tsrc[k]) - static_cast<int>(u & 0xffffu));
-        inc[c] = static_cast<int>(u >> 16);
+        run = max(run, static_cast<int>(tsrc[k]) - static_cast<int>(W ? u : u & 0xffffu));
+        inc[c] = static_cast<int>(W ? ps[n * mp + k] : u >> 16);
       }
       loc[c] = run;
     }
@@ -766,7 +786,7 @@ __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& 
     const int k = k0 + c;
     if (k < M) {
       const int e = inc[c] + loc[c];
-      const int rmk = static_cast<int>(iv.R[k]) - pr[k];
+      const int rmk = static_cast<int>(iv.Rw<W>()[k]) - pr[k];
       const int frk = dI == kFwd ? e : static_cast<int>(fsrc[k]);
       const int tlk = dI == kFwd ? static_cast<int>(tsrc[k]) : e;
       iv.rm[k] = rmk;
@@ -816,7 +836,7 @@ __device__ __forceinline__ bool reached_end(const Group<G>& grp, const IvmView& 
 
 // select_next (src/ivm.cpp:99-122) with the incremental R / d1 / d2 bookkeeping.
 // Returns the selected cell, or -1 when the explorer is exhausted.
-template <int M, int G, bool RM>
+template <int M, int G, bool RM, bool W = false>
 __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& iv,
                                            const InstView& in, int n, int mp, bool has_end,
                                            int& level, int& d1, int& d2, RowMask<M, RM>& rowmask) {
@@ -846,7 +866,8 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
         const int x = iv.cells[tri_off(level, n) + psel];
         const int job = (x < 0 ? -x : x) - 1;
         const int* pr = in.p32 + job * mp;
-        for (int k = grp.g; k < M; k += G) iv.R[k] = static_cast<uint16_t>(iv.R[k] + pr[k]);
+        FtT<W>* R = iv.Rw<W>();
+        for (int k = grp.g; k < M; k += G) R[k] = static_cast<FtT<W>>(R[k] + pr[k]);
         rowmask.add(in, job);  // the row one level up holds the job selected there
         grp.sync();
         if (grp.g == 0) iv.V[level] = static_cast<int8_t>(psel + 1);
@@ -867,7 +888,7 @@ struct StepCounters {
 };
 
 // Decompose the node at (level, sel) and branch (bound.cpp:98-139 + ivm.cpp:124-145).
-template <int M, int G, int BOUND, bool SMALLN, bool RM>
+template <int M, int G, int BOUND, bool SMALLN, bool RM, bool W = false>
 __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmView& iv,
                                                  const InstView& in, int n, int mp, int sel,
                                                  int prune, int& level, int& d1, int& d2,
@@ -878,7 +899,7 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
   const int x = row[sel];
   const int job = (x < 0 ? -x : x) - 1;
   const int dI = iv.dir[I];
-  node_tables<M, G>(grp, iv, in, n, mp, job, dI, d1, d2);
+  node_tables<M, G, W>(grp, iv, in, n, mp, job, dI, d1, d2);
   const unsigned long long fm0 = gather_free<G>(grp, iv, row, sel, f);
   unsigned long long fm = 0;
   if constexpr (BOUND == kLB2) fm = grp.ror64(fm0);  // LB1 does not use the free set mask
@@ -891,17 +912,18 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
     children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
   }
   grp.sync();
-  const int dir = minmin<G>(grp, iv, f);
+  const int dir = minmin<G, W>(grp, iv, f);
   int8_t* nrow = iv.cells + tri_off(I + 1, n);
   for (int c = grp.g; c < f; c += G) {
     const int lb = dir == kFwd ? iv.lbf[c] : iv.lbb[c];
     const int j1 = iv.freej[c] + 1;
     nrow[c] = static_cast<int8_t>(lb >= prune ? -j1 : j1);
   }
+  FtT<W>* ft = iv.ftw<W>();
   for (int k = grp.g; k < M; k += G) {
-    if (dI == kFwd) iv.ft[d1 * M + k] = static_cast<uint16_t>(iv.fr[k]);
-    else iv.ft[(n - d2) * M + k] = static_cast<uint16_t>(iv.tl[k]);
-    iv.R[k] = static_cast<uint16_t>(iv.rm[k]);
+    if (dI == kFwd) ft[d1 * M + k] = static_cast<FtT<W>>(iv.fr[k]);
+    else ft[(n - d2) * M + k] = static_cast<FtT<W>>(iv.tl[k]);
+    iv.Rw<W>()[k] = static_cast<FtT<W>>(iv.rm[k]);
   }
   if (grp.g == 0) {
     iv.dir[I + 1] = static_cast<uint8_t>(dir);
@@ -916,7 +938,7 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
 
 // Leaf: one free job (explorer.cpp:42-57). Makespan of sigma1.j.sigma2 from the node
 // tables: C = max_k (front_{sigma1.j}[k] + tail_{sigma2}[k]).
-template <int M, int G>
+template <int M, int G, bool W = false>
 __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, const InstView& in,
                                      int n, int mp, int sel, int level, int d1, int d2,
                                      int improve, DevCounters* ctr, ImpRecord* imp,
@@ -926,7 +948,7 @@ __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, con
   const int x = row[sel];
   const int job = (x < 0 ? -x : x) - 1;
   const int dI = iv.dir[level];
-  node_tables<M, G>(grp, iv, in, n, mp, job, dI, d1, d2);
+  node_tables<M, G, W>(grp, iv, in, n, mp, job, dI, d1, d2);
   grp.sync();
   if (grp.g == 0) {
     const int len = n - level;
@@ -1049,21 +1071,32 @@ __device__ __forceinline__ float remaining_log2_pos(const int* pos, const T* E, 
 // Prefix / suffix sums of every job's row (node_tables' max-plus scans), built from the
 // global p32 table while the CTA stages the instance.
 __device__ __forceinline__ void stage_prefix_sums(unsigned char* smem, const InstLayout& IL, const int* p32, int n,
-                                                  int mp) {
+                                                  int mp, bool wide) {
   uint32_t* pf = reinterpret_cast<uint32_t*>(smem + IL.o_psf);
   uint32_t* pb = reinterpret_cast<uint32_t*>(smem + IL.o_psb);
+  const int nm = n * mp;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     const int* pr = p32 + j * mp;
     uint32_t acc = 0;
     for (int k = 0; k < mp; ++k) {
       const uint32_t v = static_cast<uint32_t>(pr[k]);
-      pf[j * mp + k] = acc | ((acc + v) << 16);
+      if (wide) {
+        pf[j * mp + k] = acc;
+        pf[nm + j * mp + k] = acc + v;
+      } else {
+        pf[j * mp + k] = acc | ((acc + v) << 16);
+      }
       acc += v;
     }
     acc = 0;
     for (int k = mp - 1; k >= 0; --k) {
       const uint32_t v = static_cast<uint32_t>(pr[k]);
-      pb[j * mp + k] = acc | ((acc + v) << 16);
+      if (wide) {
+        pb[j * mp + k] = acc;
+        pb[nm + j * mp + k] = acc + v;
+      } else {
+        pb[j * mp + k] = acc | ((acc + v) << 16);
+      }
       acc += v;
     }
   }
@@ -1078,7 +1111,8 @@ constexpr bool kRowMask = false;
 template <int BOUND, int G, bool SMALLN>
 constexpr int kExploreThreads = (BOUND == kLB1 && G == 8) ? 768 : (kRowMask<BOUND, G, SMALLN> ? 896 : 1024);
 
-template <int M, int G, int BOUND, bool SMALLN = false>
+// W: wide (32-bit) FT / R / prefix sums, LB1 only (pool_init)
+template <int M, int G, int BOUND, bool SMALLN = false, bool W = false>
 __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_kernel(const ExploreParams P) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = P.L;
@@ -1086,13 +1120,13 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
   const int NG = blockDim.x / G;  // explorers per CTA
   constexpr bool PACKED = BOUND == kLB2 && G == 32;
   constexpr bool RM = kRowMask<BOUND, G, SMALLN>;
-  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? P.npairs : 0, PACKED);
+  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? P.npairs : 0, PACKED, W);
 
   // ---- stage the instance (and LB2 pair tables) into shared memory
   {
     int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = P.p32[i];
-    stage_prefix_sums(smem, IL, P.p32, n, mp);
+    stage_prefix_sums(smem, IL, P.p32, n, mp, W);
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
       for (int i = threadIdx.x; i < round_up(P.npairs, 32) * n; i += blockDim.x) sk[i] = P.packed[i];
@@ -1200,22 +1234,22 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
           state = kActive;
           continue;
         }
-        decompose_branch<M, G, BOUND, SMALLN, RM>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist, rowmask);
+        decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist, rowmask);
         ++sc.decomposed;
         ++nrep;
         rlev = level;
         continue;
       }
-      const int sel = select_next<M, G, RM>(grp, iv, in, n, mp, has_end, level, d1, d2, rowmask);
+      const int sel = select_next<M, G, RM, W>(grp, iv, in, n, mp, has_end, level, d1, d2, rowmask);
       if (sel < 0) {
         state = kEmpty;
         break;
       }
       if (n - 1 - level <= 1) {
-        leaf<M, G>(grp, iv, in, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc, P.census, P.census_cap);
+        leaf<M, G, W>(grp, iv, in, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc, P.census, P.census_cap);
         continue;
       }
-      decompose_branch<M, G, BOUND, SMALLN, RM>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist, rowmask);
+      decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist, rowmask);
       ++sc.decomposed;
     }
     if (grp.g == 0) {
@@ -1289,18 +1323,18 @@ struct BatchParams {
   uint8_t* pruned; // [count*n]
 };
 
-template <int M, int G, int BOUND, bool SMALLN = false>
+template <int M, int G, int BOUND, bool SMALLN = false, bool W = false>
 __global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams B) {
   extern __shared__ __align__(128) unsigned char smem[];
   const IvmLayout& L = B.L;
   const int n = L.n, mp = L.mp;
   const int NG = blockDim.x / G;
   constexpr bool PACKED = BOUND == kLB2 && G == 32;
-  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? B.npairs : 0, PACKED);
+  const InstLayout IL = inst_layout(n, mp, BOUND == kLB2 ? B.npairs : 0, PACKED, W);
   {
     int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
-    stage_prefix_sums(smem, IL, B.p32, n, mp);
+    stage_prefix_sums(smem, IL, B.p32, n, mp, W);
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
       for (int i = threadIdx.x; i < round_up(B.npairs, 32) * n; i += blockDim.x) sk[i] = B.packed[i];
@@ -1379,7 +1413,7 @@ __global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams
     else if constexpr (G == 32) children_lb2_w<M, SMALLN>(iv, in, n, mp, f, fm);
     else children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
     grp.sync();
-    const int dir = minmin<G>(grp, iv, f);
+    const int dir = minmin<G, W>(grp, iv, f);
     for (int c = grp.g; c < f; c += G) {
       const int lb = dir == kFwd ? iv.lbf[c] : iv.lbb[c];
       B.child_lb[static_cast<size_t>(node) * n + c] = lb;

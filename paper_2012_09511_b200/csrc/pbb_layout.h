@@ -33,6 +33,7 @@ struct IvmLayout {
   int o_v, o_dir, o_end, o_tgt;  // int8 [n] each
   int o_ft;            // uint16 [(n+1)*m]: FS[d] at slot d, TS[d] at slot n-d
   int o_r;             // uint16 [m]: per-machine sum of the jobs of row `level`
+  int ftb;             // bytes per FT / R entry: 2, or 4 for wide times ((n+m)*max p >= 2^16, LB1)
   int gstride;         // persistent bytes per explorer (multiple of 16)
   // shared-memory scratch (per explorer)
   int o_fr, o_tl, o_rm, o_rt, o_frm;  // int32 [m]: front, tail, remain, remain+tail, front+remain

@@ -307,6 +307,8 @@ __device__ void seat_explorer(unsigned char* blk, const IvmLayout& L, const int*
   int8_t* tgt = reinterpret_cast<int8_t*>(blk + L.o_tgt);
   uint16_t* ft = reinterpret_cast<uint16_t*>(blk + L.o_ft);
   uint16_t* R = reinterpret_cast<uint16_t*>(blk + L.o_r);
+  uint32_t* ftw = reinterpret_cast<uint32_t*>(ft);
+  uint32_t* Rw = reinterpret_cast<uint32_t*>(R);
   bool empty = false;
   if (has_end) {  // to_decimal(a) >= b -> Empty (src/ivm.cpp:61-64)
     int cmp = 0;
@@ -321,9 +323,15 @@ __device__ void seat_explorer(unsigned char* blk, const IvmLayout& L, const int*
     endd[l] = static_cast<int8_t>(has_end ? b[l] : 0);
   }
   for (int k = 0; k < m; ++k) {
-    ft[k] = 0;                 // FS[0]
-    ft[n * m + k] = 0;         // TS[0]
-    R[k] = static_cast<uint16_t>(ptot[k]);
+    if (L.ftb == 4) {
+      ftw[k] = 0;
+      ftw[n * m + k] = 0;
+      Rw[k] = static_cast<uint32_t>(ptot[k]);
+    } else {
+      ft[k] = 0;                 // FS[0]
+      ft[n * m + k] = 0;         // TS[0]
+      R[k] = static_cast<uint16_t>(ptot[k]);
+    }
   }
   h->level = 0;
   h->state = empty ? kEmpty : kInit;
@@ -1035,30 +1043,39 @@ __global__ void __launch_bounds__(256) int32_peak_kernel(const int* in, int* out
 using ExploreFn = void (*)(ExploreParams);
 using BatchFn = void (*)(BatchParams);
 
-template <int M, int B>
+template <int M, int B, bool W = false>
 ExploreFn explore_for_group(int G, bool small) {
   switch (G) {
-    case 4: return explore_kernel<M, 4, B>;
-    case 8: return explore_kernel<M, 8, B>;
-    case 16: return explore_kernel<M, 16, B>;
-    case 32: return (B == kLB2 && small) ? explore_kernel<M, 32, B, true> : explore_kernel<M, 32, B>;
+    case 4: return explore_kernel<M, 4, B, false, W>;
+    case 8: return explore_kernel<M, 8, B, false, W>;
+    case 16: return explore_kernel<M, 16, B, false, W>;
+    case 32: return (B == kLB2 && small) ? explore_kernel<M, 32, B, true> : explore_kernel<M, 32, B, false, W>;
   }
   return nullptr;
 }
-template <int M, int B>
+template <int M, int B, bool W = false>
 BatchFn batch_for_group(int G, bool small) {
   switch (G) {
-    case 4: return decompose_batch_kernel<M, 4, B>;
-    case 8: return decompose_batch_kernel<M, 8, B>;
-    case 16: return decompose_batch_kernel<M, 16, B>;
-    case 32: return (B == kLB2 && small) ? decompose_batch_kernel<M, 32, B, true> : decompose_batch_kernel<M, 32, B>;
+    case 4: return decompose_batch_kernel<M, 4, B, false, W>;
+    case 8: return decompose_batch_kernel<M, 8, B, false, W>;
+    case 16: return decompose_batch_kernel<M, 16, B, false, W>;
+    case 32: return (B == kLB2 && small) ? decompose_batch_kernel<M, 32, B, true> : decompose_batch_kernel<M, 32, B, false, W>;
   }
   return nullptr;
 }
 
 // SMALLN (n <= 32): LB2 passes iterate the set bits of a 32-bit free-position mask
-ExploreFn explore_fn(int m, int bound, int G, bool small) {
-  if (bound == kLB1) {
+// wide: 32-bit FT / R tables (LB1 only)
+ExploreFn explore_fn(int m, int bound, int G, bool small, bool wide) {
+  if (bound == kLB1 && wide) {
+    switch (m) {
+      case 5: return explore_for_group<5, kLB1, true>(G, false);
+      case 10: return explore_for_group<10, kLB1, true>(G, false);
+      case 20: return explore_for_group<20, kLB1, true>(G, false);
+      case 40: return explore_for_group<40, kLB1, true>(G, false);
+      case 60: return explore_for_group<60, kLB1, true>(G, false);
+    }
+  } else if (bound == kLB1) {
     switch (m) {
       case 5: return explore_for_group<5, kLB1>(G, false);
       case 10: return explore_for_group<10, kLB1>(G, false);
@@ -1123,8 +1140,16 @@ BigFn big_fn(int m, int bound) {
   return nullptr;
 }
 
-BatchFn batch_fn(int m, int bound, int G, bool small) {
-  if (bound == kLB1) {
+BatchFn batch_fn(int m, int bound, int G, bool small, bool wide) {
+  if (bound == kLB1 && wide) {
+    switch (m) {
+      case 5: return batch_for_group<5, kLB1, true>(G, false);
+      case 10: return batch_for_group<10, kLB1, true>(G, false);
+      case 20: return batch_for_group<20, kLB1, true>(G, false);
+      case 40: return batch_for_group<40, kLB1, true>(G, false);
+      case 60: return batch_for_group<60, kLB1, true>(G, false);
+    }
+  } else if (bound == kLB1) {
     switch (m) {
       case 5: return batch_for_group<5, kLB1>(G, false);
       case 10: return batch_for_group<10, kLB1>(G, false);
@@ -1168,6 +1193,7 @@ struct TraceScope {
 struct pbbgpu_pool {
   int n = 0, m = 0, mp = 0, bound = 0;  // m: compiled machine count (5, 10, 20)
   int m_real = 0;                        // the instance's machines (zero-time machines pad to m)
+  bool wide = false;                     // 32-bit FT / R / prefix sums ((n+m)*max p >= 2^16, LB1)
   pbbgpu_config_t cfg{};
   std::vector<int32_t> p;
   int K = 0, G = 0, steps = 0, grid = 0, block = 128;
@@ -1355,13 +1381,21 @@ struct HostTables {
   bool packable = false;
 };
 
-void validate_times(int n, int m, const int32_t* p) {
+// Returns whether the instance needs wide (32-bit) explorer tables: every front / tail /
+// remain / bound is below (n+m)*max p, the 16-bit tables hold it when that is < 2^16. LB2's
+// pair tables and SIMD combine stay 16-bit; LB1 goes up to n*(n+m)*max p < 2^31 (MinMin's sum
+// of the children's bounds fits int32).
+bool validate_times(int n, int m, const int32_t* p, int bound) {
   int pmax = 0;
   for (int i = 0; i < n * m; ++i) {
     if (p[i] < 0) throw std::invalid_argument("negative processing time");
     pmax = std::max(pmax, p[i]);
   }
-  if (static_cast<int64_t>(n + m) * pmax >= 65536) throw std::invalid_argument("pbbgpu: (n+m)*max(p) must stay below 2^16");
+  const int64_t span = static_cast<int64_t>(n + m) * pmax;
+  if (span < 65536) return false;
+  if (bound == kLB2) throw std::invalid_argument("pbbgpu: LB2 needs (n+m)*max(p) below 2^16 (use LB1 for wider times)");
+  if (span * n >= (int64_t{1} << 31)) throw std::invalid_argument("pbbgpu: n*(n+m)*max(p) must stay below 2^31");
+  return true;
 }
 
 // Compiled machine count for an instance with m machines: the instance is padded with
@@ -1530,7 +1564,7 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
   if (m > 20 && (bound == kLB2 || n > kMaxN))
     throw std::invalid_argument("pbbgpu: m > 20 is supported for LB1 with n <= 64 (LB2 pair tables and the n > 64 "
                                 "kernels are compiled for m <= 20)");
-  validate_times(n, m, pad_machines(n, m_real, m, p_real).data());
+  P->wide = validate_times(n, m, pad_machines(n, m_real, m, p_real).data(), bound);
   P->m_real = m_real;
   if (cfg && cfg->record_census && n > 20) throw std::invalid_argument("record_census needs n <= 20 (position_u64)");
   if (cfg && cfg->steal_policy == 1 && n > 30) throw std::invalid_argument("the reference steal policy needs n <= 30");
@@ -1645,8 +1679,8 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
   // CTA size: the instance tables are staged once per CTA, so larger CTAs amortize them;
   // pick the block size that keeps the most explorers resident per SM.
   auto size_for = [&](int G, int BS) {
-    const IvmLayout L = ivm_layout(n, m, bound, G);
-    const InstLayout IL = inst_layout(n, L.mp, P->npairs, bound == kLB2 && G == 32);
+    const IvmLayout L = ivm_layout(n, m, bound, G, P->wide);
+    const InstLayout IL = inst_layout(n, L.mp, P->npairs, bound == kLB2 && G == 32, P->wide);
     return std::make_pair(static_cast<size_t>(IL.bytes) + static_cast<size_t>(BS / G) * L.sstride, std::make_pair(L, IL));
   };
   const size_t smem_cap = static_cast<size_t>(prop.sharedMemPerBlockOptin);
@@ -1656,7 +1690,7 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
     // every warp-multiple block size: the most explorers resident per SM wins
     int bs = 0;
     long res = -1;
-    const void* fn = reinterpret_cast<const void*>(explore_fn(m, bound, G, n <= 32));
+    const void* fn = reinterpret_cast<const void*>(explore_fn(m, bound, G, n <= 32, P->wide));
     cudaFuncAttributes fa{};
     ck(cudaFuncGetAttributes(&fa, fn), "func attrs");
     ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_cap)), "smem attr");
@@ -1697,8 +1731,8 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
   P->L = sz.second.first;
   P->IL = sz.second.second;
   P->mp = P->L.mp;
-  P->efn = explore_fn(m, bound, P->G, n <= 32);
-  P->bfn = batch_fn(m, bound, P->G, n <= 32);
+  P->efn = explore_fn(m, bound, P->G, n <= 32, P->wide);
+  P->bfn = batch_fn(m, bound, P->G, n <= 32, P->wide);
   ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->efn), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
   ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(P->bfn), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P->smem)), "smem attr");
   int per_sm = 0;
@@ -2414,7 +2448,8 @@ int pbbgpu_load_instance(pbbgpu_pool* P, const int32_t* p) {
   return guarded([&] {
     if (!P || !p) throw std::invalid_argument("pbbgpu_load_instance: null argument");
     std::vector<int32_t> padded = pad_machines(P->n, P->m_real, P->m, p);
-    validate_times(P->n, P->m, padded.data());
+    if (validate_times(P->n, P->m, padded.data(), P->bound) && !P->wide && !P->batch_only)
+      throw CapacityError("pbbgpu_load_instance: this instance needs 32-bit explorer tables ((n+m)*max p >= 2^16); create a new pool");
     const HostTables T = build_tables(P->n, P->m_real, P->m, P->bound, p, P->batch_only);
     if (P->bound == kLB2 && !P->batch_only && P->G == 32 && !T.packable)
       throw CapacityError("pbbgpu_load_instance: this instance's LB2 tables do not pack into 31 bits; create a new pool");

@@ -799,6 +799,77 @@ def test_any_machine_count_fixed_trees_match_reference(key):
     assert {str(k): v for k, v in res.hist.items()} == g["hist"]
 
 
+# ---------------------------------------------------------------- wide processing times (LB1)
+
+@pytest.mark.parametrize("n,m,pmax", [(12, 5, 50000), (12, 20, 9000), (14, 40, 20000), (40, 10, 30000),
+                                      (64, 20, 300000)])
+def test_wide_times_bounds_match_oracle(n, m, pmax):
+    """(n+m)*max p >= 2^16: the explorers keep 32-bit front / tail / remain tables and the
+    MinMin sums are reduced separately; every child bound, direction and prune flag equals the
+    oracle's (int64, bound.cpp's types)."""
+    rng = np.random.default_rng(n * 1000 + m)
+    inst = pbb.Instance(n, m, rng.integers(1, pmax + 1, size=(n, m), dtype=np.int32))
+    perms, d1s, d2s = _random_nodes(n, 300, m)
+    prob = orc.Problem(inst.p, orc.LB1)
+    inc = (n + m) * pmax // 3
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=128), bound="lb1") as pool:
+        lb, dr, pr, lf, lbw = pool.decompose_batch(perms, d1s, d2s, inc)
+    for i in range(len(d1s)):
+        f = n - d1s[i] - d2s[i]
+        fw, bw = prob.children_bounds(perms[i], d1s[i], d2s[i])
+        assert [int(x) for x in lf[i, :f]] == fw and [int(x) for x in lbw[i, :f]] == bw
+        d, clb, prn = prob.decompose(perms[i], d1s[i], d2s[i], inc)
+        assert int(dr[i]) == d and [int(x) for x in lb[i, :f]] == clb
+        assert [bool(x) for x in pr[i, :f]] == [bool(x) for x in prn]
+
+
+@pytest.mark.parametrize("key,scale", [("ta011@1582", 1000), ("gen:14:40:2024@3124", 700), ("ta061@5493", 100)])
+def test_wide_times_scaled_fixed_trees_match_reference(key, scale):
+    """Scaling every processing time by c scales every front, tail, bound and makespan by c and
+    keeps every comparison and MinMin tie, so the fixed tree of c*p under c*ub is the
+    reference's tree of p under ub: unique count, leaves and per-f histogram equal its golden
+    counts (m = 40 runs the M = 40 wide kernels, ta061 the n > 64 explorer pool)."""
+    g = golden_io.ref_counts()[key]
+    name, ub = key.split("@")
+    if name.startswith("gen:"):
+        n, m, seed = (int(x) for x in name[4:].split(":"))
+        base = pbb.generate_taillard(n, m, seed)
+    else:
+        base = pbb.taillard_named(name)
+    inst = pbb.Instance(base.n, base.m, base.p.astype(np.int64) * scale)
+    assert (inst.n + inst.m) * int(inst.p.max()) >= 1 << 16
+    cfg = pbb.PoolConfig(explorers=1024) if inst.n > 64 else pbb.PoolConfig()
+    res = pbb.pool_run(inst, int(ub) * scale, cfg=cfg)
+    assert res.stats.unique == g["decomposed"] and res.stats.leaves == g["leaves"]
+    assert res.best_value == int(ub) * scale
+    assert {str(k): v for k, v in res.hist.items()} == {str(k): v for k, v in g["hist"].items()}
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_wide_times_optimum_matches_brute_force(seed):
+    n, m = 8, 6
+    rng = np.random.default_rng(77 + seed)
+    inst = pbb.Instance(n, m, rng.integers(1, 200000, size=(n, m), dtype=np.int32))
+    best = min(pbb.makespan(inst, perm) for perm in itertools.permutations(range(n)))
+    res = pbb.pool_run(inst, 10 ** 9, cfg=pbb.PoolConfig(explorers=128))
+    assert res.best_value == best and pbb.makespan(inst, res.best.perm) == best
+
+
+def test_wide_times_limits():
+    """LB2's pair tables stay 16-bit; LB1 takes n*(n+m)*max p < 2^31; a narrow pool refuses a
+    wide instance in load_instance (its explorer tables are 16-bit)."""
+    wide = pbb.Instance(10, 5, np.full((10, 5), 10000, dtype=np.int32))
+    with pytest.raises(ValueError):
+        pbb.GpuPool(wide, bound="lb2")
+    with pytest.raises(ValueError):
+        pbb.GpuPool(pbb.Instance(10, 5, np.full((10, 5), 20_000_000, dtype=np.int32)), bound="lb1")
+    with pbb.GpuPool(pbb.generate_taillard(10, 5, 3), bound="lb1") as pool:
+        with pytest.raises(RuntimeError):
+            pool.load_instance(wide)
+    with pbb.GpuPool(wide, bound="lb1") as pool:  # a wide pool takes narrow instances too
+        pool.load_instance(pbb.generate_taillard(10, 5, 3))
+
+
 @pytest.mark.parametrize("workers", [1, 2])
 def test_product_worker_speaks_the_reference_protocol_over_tcp(workers):
     """libpbbgpu's own worker role and wire codec (pbbgpu_worker_run) connected over TCP to the
