@@ -106,12 +106,20 @@ __host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound, int lan
   o += L.mp * 4;
   L.o_rm = o;
   o += L.mp * 4;
-  L.o_rt = o;
-  o += L.mp * 4;
-  L.o_frm = o;
-  o += L.mp * 4;
-  // lbf / lbb live right after frm: two int32 [n] arrays
-  o += round_up(2 * n * 4, 16);
+  if (bound == kLB1) {  // remain + tail, front + remain: LB1's children only
+    L.o_rt = o;
+    o += L.mp * 4;
+    L.o_frm = o;
+    o += L.mp * 4;
+  } else {
+    L.o_rt = L.o_frm = -1;
+  }
+  if (bound == kLB2 && lanes == 32 && n <= 32) {
+    L.o_lbf = -1;  // children bounds stay in registers (decompose_branch)
+  } else {
+    L.o_lbf = o;  // lbf / lbb: two int32 [n] arrays
+    o += round_up(2 * n * 4, 16);
+  }
   L.o_free = o;
   o += round_up(n, 16);
   if (bound == kLB2) {
@@ -130,8 +138,14 @@ __host__ __device__ inline IvmLayout ivm_layout(int n, int m, int bound, int lan
       L.o_pos = o;
       o += round_up(n, 16);
     }
+    L.o_msk = 0;
+    if (lanes == 32 && n <= 32) {  // RowMask: [round][32] uint32 per explorer
+      o = round_up(o, 16);
+      L.o_msk = o;
+      o += ((m * (m - 1) / 2 + 31) / 32) * 32 * 4;
+    }
   } else {
-    L.o_heads = L.o_tails = L.o_lst = L.o_pos = 0;
+    L.o_heads = L.o_tails = L.o_lst = L.o_pos = L.o_msk = 0;
   }
   o = round_up(o, 16);
   // stride == 16 (mod 128): the groups of one warp hit distinct bank quads on LDS.128
@@ -209,9 +223,9 @@ struct IvmView {
     fr = reinterpret_cast<int*>(b + L.o_fr);
     tl = reinterpret_cast<int*>(b + L.o_tl);
     rm = reinterpret_cast<int*>(b + L.o_rm);
-    rt = reinterpret_cast<int*>(b + L.o_rt);
+    rt = reinterpret_cast<int*>(b + L.o_rt);    // LB1 only
     frm = reinterpret_cast<int*>(b + L.o_frm);
-    lbf = reinterpret_cast<int*>(b + L.o_frm + L.mp * 4);
+    lbf = reinterpret_cast<int*>(b + L.o_lbf);
     lbb = lbf + L.n;
     freej = b + L.o_free;
     heads = reinterpret_cast<uint16_t*>(b + L.o_heads);
@@ -421,38 +435,45 @@ __device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
 // a pair (32 pairs per round, the last round's spare lanes repeat pair P-1); per child the
 // 32 pair bounds are combined with REDUX.MAX.
 // Per-lane free-position masks of the current IVM row, one 32-bit word per pair round
-// (n <= 32, warp-per-explorer LB2): bit t of word r is set when the job at position t of pair
-// (32 r + lane)'s Johnson order is in the row. A node's free set is its row minus the selected
-// job, so the masks follow the explorer incrementally -- branch: the node's masks become the
-// next row's; backtrack: the job selected one level up is added back -- instead of being rebuilt
-// from the free jobs (f inverse-order lookups per pair round and node).
+// (n <= 32, warp-per-explorer LB2), kept in the explorer's shared scratch ([round][lane],
+// IvmLayout::o_msk): bit t of word r is set when the job at position t of pair (32 r + lane)'s
+// Johnson order is in the row. A node's free set is its row minus the selected job, so the
+// masks follow the explorer incrementally -- branch: the node's masks become the next row's;
+// backtrack: the job selected one level up is added back -- instead of being rebuilt from the
+// free jobs at every node (f inverse-order lookups per pair round). Rebuilt from the row at
+// every launch (the steal / split / exchange kernels only touch the persistent block).
 template <int M, bool ON>
 struct RowMask {
-  static constexpr int P = M * (M - 1) / 2;
-  static constexpr int R = ON ? (P + 31) / 32 : 1;
-  uint32_t w[R];
+  uint32_t* w = nullptr;  // this lane's words, stride 32
+  int R = 0, P = 0;
+  __device__ __forceinline__ void bind(const IvmView& iv, const IvmLayout& L, int npairs) {
+    if constexpr (ON) {
+      w = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(iv.hdr) + L.o_msk) + (threadIdx.x & 31);
+      P = npairs;
+      R = (npairs + 31) >> 5;
+    }
+  }
   __device__ __forceinline__ uint32_t bit(const InstView& in, int job, int r) const {
     const int q = min(32 * r + static_cast<int>(threadIdx.x & 31), P - 1);
     return 1u << in.invord[job * P + q];
   }
   __device__ __forceinline__ void build(const IvmView& iv, const InstView& in, int n, int level) {
     if constexpr (ON) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) w[r] = 0;
       if (level < 0) return;
       const int8_t* row = iv.cells + tri_off(level, n);
-      for (int c = 0; c < n - level; ++c) {
-        const int x = row[c];
-        const int job = (x < 0 ? -x : x) - 1;
-#pragma unroll
-        for (int r = 0; r < R; ++r) w[r] |= bit(in, job, r);
+      for (int r = 0; r < R; ++r) {
+        uint32_t acc = 0;
+        for (int c = 0; c < n - level; ++c) {
+          const int x = row[c];
+          acc |= bit(in, (x < 0 ? -x : x) - 1, r);
+        }
+        w[r * 32] = acc;
       }
     }
   }
   __device__ __forceinline__ void add(const InstView& in, int job) {
     if constexpr (ON) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) w[r] |= bit(in, job, r);
+      for (int r = 0; r < R; ++r) w[r * 32] |= bit(in, job, r);
     }
   }
 };
@@ -607,8 +628,10 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
 // path) the node's free-position masks come from the explorer's row masks (RowMask) minus the
 // selected job, and become the next row's masks (the caller branches); otherwise they are built
 // from the free jobs through the static inverse order.
+// n <= 32: returns lane c's child bounds (lbf | lbb << 16; lbf / lbb are not written),
+// otherwise writes lbf / lbb.
 template <int M, bool SMALLN, bool RM = false>
-__device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView& in, int n, int mp, int f,
+__device__ __forceinline__ uint32_t children_lb2_w(const IvmView& iv, const InstView& in, int n, int mp, int f,
                                                unsigned long long fmask, RowMask<M, RM>* rowmask = nullptr,
                                                int seljob = 0) {
   const int lane = threadIdx.x & 31;
@@ -637,10 +660,9 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
   uint32_t acc0 = 0, acc1 = 0;
   const int P = in.npairs;
   if constexpr (RM) {
-#pragma unroll
-    for (int r = 0; r < RowMask<M, RM>::R; ++r) {
-      const uint32_t Fr = rowmask->w[r] & ~rowmask->bit(in, seljob, r);
-      rowmask->w[r] = Fr;  // the caller branches: the node's free set is the next row
+    for (int r = 0; r < rowmask->R; ++r) {
+      const uint32_t Fr = rowmask->w[r * 32] & ~rowmask->bit(in, seljob, r);
+      rowmask->w[r * 32] = Fr;  // the caller branches: the node's free set is the next row
       lb2_round<M, SMALLN>(iv, in, f, 32 * r, Fr, 0, acc0, acc1);
     }
   } else {
@@ -671,14 +693,17 @@ __device__ __forceinline__ void children_lb2_w(const IvmView& iv, const InstView
     acc1 = static_cast<uint32_t>(a1) | static_cast<uint32_t>(b1) << 16;
     __syncwarp();
   }
-  if (lane < f) {
-    iv.lbf[lane] = static_cast<int>(acc0 & 0xffffu);
-    iv.lbb[lane] = static_cast<int>(acc0 >> 16);
+  if constexpr (!SMALLN) {
+    if (lane < f) {
+      iv.lbf[lane] = static_cast<int>(acc0 & 0xffffu);
+      iv.lbb[lane] = static_cast<int>(acc0 >> 16);
+    }
+    if (lane + 32 < f) {
+      iv.lbf[lane + 32] = static_cast<int>(acc1 & 0xffffu);
+      iv.lbb[lane + 32] = static_cast<int>(acc1 >> 16);
+    }
   }
-  if (!SMALLN && lane + 32 < f) {
-    iv.lbf[lane + 32] = static_cast<int>(acc1 & 0xffffu);
-    iv.lbb[lane + 32] = static_cast<int>(acc1 >> 16);
-  }
+  return acc0;
 }
 
 // MinMin (src/bound.cpp:109-131): lo over the union, fewer occurrences of lo wins, then the
@@ -719,9 +744,22 @@ __device__ __forceinline__ int minmin(const Group<G>& grp, const IvmView& iv, in
   return kFwd;
 }
 
+// MinMin over a warp whose lane c holds child c's bounds (a = forward, b = backward).
+__device__ __forceinline__ int minmin_lane(bool valid, int a, int b) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int glo = __reduce_min_sync(FULL, valid ? min(a, b) : INT_MAX);
+  const int cd = valid ? static_cast<int>(a == glo) - static_cast<int>(b == glo) : 0;
+  const int v = __reduce_add_sync(FULL, (cd << 24) + (valid ? a - b : 0));
+  const int c = (v + (1 << 23)) >> 24;
+  if (c) return c < 0 ? kFwd : kBwd;
+  if (v) return v > 0 ? kFwd : kBwd;
+  return kFwd;
+}
+
 // Node tables from the incremental stacks: node at `level` with selected job `job` placed
 // by dir[level]; d1/d2 include it.
-template <int M, int G, bool W = false>
+// RTF: also write remain + tail / front + remain (LB1's children; not LB2, not leaves)
+template <int M, int G, bool W = false, bool RTF = true>
 __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& iv,
                                             const InstView& in, int n, int mp, int job, int dI,
                                             int d1, int d2) {
@@ -792,8 +830,10 @@ __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& 
       iv.rm[k] = rmk;
       iv.fr[k] = frk;
       iv.tl[k] = tlk;
-      iv.rt[k] = rmk + tlk;
-      iv.frm[k] = frk + rmk;
+      if (RTF) {
+        iv.rt[k] = rmk + tlk;
+        iv.frm[k] = frk + rmk;
+      }
     }
   }
 }
@@ -899,25 +939,38 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
   const int x = row[sel];
   const int job = (x < 0 ? -x : x) - 1;
   const int dI = iv.dir[I];
-  node_tables<M, G, W>(grp, iv, in, n, mp, job, dI, d1, d2);
+  node_tables<M, G, W, BOUND == kLB1>(grp, iv, in, n, mp, job, dI, d1, d2);
   const unsigned long long fm0 = gather_free<G>(grp, iv, row, sel, f);
   unsigned long long fm = 0;
   if constexpr (BOUND == kLB2) fm = grp.ror64(fm0);  // LB1 does not use the free set mask
   grp.sync();
-  if constexpr (BOUND == kLB1) {
-    children_lb1<M, G>(grp, iv, in, mp, f);
-  } else if constexpr (G == 32) {
-    children_lb2_w<M, SMALLN, RM>(iv, in, n, mp, f, fm, &rowmask, job);
-  } else {
-    children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
-  }
-  grp.sync();
-  const int dir = minmin<G, W>(grp, iv, f);
   int8_t* nrow = iv.cells + tri_off(I + 1, n);
-  for (int c = grp.g; c < f; c += G) {
-    const int lb = dir == kFwd ? iv.lbf[c] : iv.lbb[c];
-    const int j1 = iv.freej[c] + 1;
-    nrow[c] = static_cast<int8_t>(lb >= prune ? -j1 : j1);
+  int dir;
+  if constexpr (BOUND == kLB2 && G == 32 && SMALLN) {
+    // lane c holds child c's two bounds in registers (no lbf / lbb round trip)
+    const uint32_t acc = children_lb2_w<M, SMALLN, RM>(iv, in, n, mp, f, fm, &rowmask, job);
+    const int a = static_cast<int>(acc & 0xffffu), b = static_cast<int>(acc >> 16);
+    dir = minmin_lane(grp.g < f, a, b);
+    if (grp.g < f) {
+      const int lb = dir == kFwd ? a : b;
+      const int j1 = iv.freej[grp.g] + 1;
+      nrow[grp.g] = static_cast<int8_t>(lb >= prune ? -j1 : j1);
+    }
+  } else {
+    if constexpr (BOUND == kLB1) {
+      children_lb1<M, G>(grp, iv, in, mp, f);
+    } else if constexpr (G == 32) {
+      children_lb2_w<M, SMALLN, RM>(iv, in, n, mp, f, fm, &rowmask, job);
+    } else {
+      children_lb2<M, G>(grp, iv, in, n, mp, f, fm);
+    }
+    grp.sync();
+    dir = minmin<G, W>(grp, iv, f);
+    for (int c = grp.g; c < f; c += G) {
+      const int lb = dir == kFwd ? iv.lbf[c] : iv.lbb[c];
+      const int j1 = iv.freej[c] + 1;
+      nrow[c] = static_cast<int8_t>(lb >= prune ? -j1 : j1);
+    }
   }
   FtT<W>* ft = iv.ftw<W>();
   for (int k = grp.g; k < M; k += G) {
@@ -948,7 +1001,7 @@ __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, con
   const int x = row[sel];
   const int job = (x < 0 ? -x : x) - 1;
   const int dI = iv.dir[level];
-  node_tables<M, G, W>(grp, iv, in, n, mp, job, dI, d1, d2);
+  node_tables<M, G, W, false>(grp, iv, in, n, mp, job, dI, d1, d2);
   grp.sync();
   if (grp.g == 0) {
     const int len = n - level;
@@ -1102,14 +1155,13 @@ __device__ __forceinline__ void stage_prefix_sums(unsigned char* smem, const Ins
   }
 }
 
-// incremental row masks (RowMask) for the warp-per-explorer LB2 path with n <= 32: 6 more
-// persistent registers per lane, hence at most 28 warps (explorers) per CTA. Measured on the
-// ta021 LB2 proof: 249 ms with, 227 ms without (the lost warps and a register spill cost more
-// than the f inverse-order lookups per pair round it saves), so it is compiled out.
+// incremental row masks (RowMask, shared memory) for the warp-per-explorer LB2 path with
+// n <= 32. (Held in registers instead -- 6 more per lane -- they cost warps and spilled: 249 ms
+// vs 227 ms on the ta021 LB2 proof.)
 template <int BOUND, int G, bool SMALLN>
-constexpr bool kRowMask = false;
+constexpr bool kRowMask = BOUND == kLB2 && G == 32 && SMALLN;
 template <int BOUND, int G, bool SMALLN>
-constexpr int kExploreThreads = (BOUND == kLB1 && G == 8) ? 768 : (kRowMask<BOUND, G, SMALLN> ? 896 : 1024);
+constexpr int kExploreThreads = (BOUND == kLB1 && G == 8) ? 768 : 1024;
 
 // W: wide (32-bit) FT / R / prefix sums, LB1 only (pool_init)
 template <int M, int G, int BOUND, bool SMALLN = false, bool W = false>
@@ -1188,6 +1240,7 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
     int rlev = iv.hdr->rlev, nrep = iv.hdr->nrep;
     const bool has_end = iv.hdr->has_end != 0;
     RowMask<M, RM> rowmask;
+    rowmask.bind(iv, L, in.npairs);
     if (state != kEmpty) rowmask.build(iv, in, n, level);
     if (grp.g == 0 && state != kEmpty) atomicAdd(reinterpret_cast<unsigned*>(smem + IL.o_cnt) + 6, 1u);
     int best = grp.bcast(grp.g == 0 ? *reinterpret_cast<volatile int*>(&P.ctr->best) : 0, 0);
@@ -1396,9 +1449,11 @@ __global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams
         const int* pr = in.p32 + perm[i] * mp;
         for (int k = 0; k < M; ++k) iv.rm[k] += pr[k];
       }
-      for (int k = 0; k < M; ++k) {
-        iv.rt[k] = iv.rm[k] + iv.tl[k];
-        iv.frm[k] = iv.fr[k] + iv.rm[k];
+      if constexpr (BOUND == kLB1) {
+        for (int k = 0; k < M; ++k) {
+          iv.rt[k] = iv.rm[k] + iv.tl[k];
+          iv.frm[k] = iv.fr[k] + iv.rm[k];
+        }
       }
     }
     unsigned long long fm = 0;
@@ -1409,6 +1464,22 @@ __global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams
     }
     fm = grp.ror64(fm);
     grp.sync();
+    if constexpr (BOUND == kLB2 && G == 32 && SMALLN) {  // lane c: child c's bounds in registers
+      const uint32_t acc = children_lb2_w<M, SMALLN>(iv, in, n, mp, f, fm);
+      const int a = static_cast<int>(acc & 0xffffu), b = static_cast<int>(acc >> 16);
+      const int dir = minmin_lane(grp.g < f, a, b);
+      if (grp.g < f) {
+        const size_t o = static_cast<size_t>(node) * n + grp.g;
+        const int lb = dir == kFwd ? a : b;
+        B.child_lb[o] = lb;
+        B.lb_fwd[o] = a;
+        B.lb_bwd[o] = b;
+        B.pruned[o] = lb >= B.incumbent;
+      }
+      if (grp.g == 0) B.dir[node] = static_cast<uint8_t>(dir);
+      grp.sync();
+      continue;
+    }
     if constexpr (BOUND == kLB1) children_lb1<M, G>(grp, iv, in, mp, f);
     else if constexpr (G == 32) children_lb2_w<M, SMALLN>(iv, in, n, mp, f, fm);
     else children_lb2<M, G>(grp, iv, in, n, mp, f, fm);

@@ -36,11 +36,13 @@ struct IvmLayout {
   int ftb;             // bytes per FT / R entry: 2, or 4 for wide times ((n+m)*max p >= 2^16, LB1)
   int gstride;         // persistent bytes per explorer (multiple of 16)
   // shared-memory scratch (per explorer)
-  int o_fr, o_tl, o_rm, o_rt, o_frm;  // int32 [m]: front, tail, remain, remain+tail, front+remain
+  int o_fr, o_tl, o_rm, o_rt, o_frm;  // int32 [m]: front, tail, remain, remain+tail, front+remain (rt, frm: LB1)
+  int o_lbf;           // int32 [n] lbf then int32 [n] lbb
   int o_free;          // uint8 [kMaxN]: free jobs of the node in decode order
   int o_heads, o_tails;  // uint16 [kMaxN*m] LB2 child heads / tails
   int o_lst;           // int4 [kMaxN] LB2 per-pair compacted Johnson sequence
   int o_pos;           // uint8 [kMaxN] LB2 job -> position in the compacted sequence
+  int o_msk;           // uint32 [rounds][32] LB2 row masks (warp explorers, n <= 32; 0 = none)
   int sstride;         // shared bytes per explorer (== 16 mod 128: conflict-free LDS.128)
 };
 
