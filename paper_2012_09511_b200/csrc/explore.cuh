@@ -1121,6 +1121,60 @@ __device__ __forceinline__ float remaining_log2_pos(const int* pos, const T* E, 
   return lgfact[n - 1 - lead] + __log2f(d);
 }
 
+// ---- remaining work of one explorer for the steal phase: log2 of its leaves, -2 busy /
+// unsplittable, -3 idle (lens_kernel, and the explore kernel's write-back, which evaluates it
+// on the shared-memory copy of the block). mode 0: the live siblings of the shallowest level
+// holding any (pool.cu live_siblings), (cnt + 1) (n-1-l*)!; mode 1: the exact factoradic
+// length of [effective position, end).
+__device__ __forceinline__ int live_count(const unsigned char* vb, const IvmLayout& L, int& lstar) {
+  const int n = L.n;
+  const IvmHdr* h = reinterpret_cast<const IvmHdr*>(vb);
+  const int8_t* V = reinterpret_cast<const int8_t*>(vb + L.o_v);
+  const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
+  const int8_t* C = reinterpret_cast<const int8_t*>(vb + L.o_cells);
+  const bool he = h->has_end != 0;
+  const int level = h->level;
+  int l = 0;
+  if (he) {
+    while (l <= level && V[l] == E[l]) ++l;
+    if (l <= level && V[l] > E[l]) return 0;
+  }
+  const int d = he ? l : -1;
+  for (; l <= level; ++l) {
+    const int8_t* row = C + tri_off(l, n);
+    const int lim = l == d ? E[l] : n - l;
+    int cnt = 0;
+    for (int c = V[l] + 1; c < lim; ++c) cnt += row[c] > 0;
+    if (cnt) {
+      lstar = l;
+      return cnt;
+    }
+  }
+  return 0;
+}
+
+__device__ __noinline__ float explorer_lens(const unsigned char* blk, const IvmLayout& L, const float* lgfact, int mode) {
+  const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
+  if (h->state == kInit) return -2.f;
+  if (h->state != kActive) return -3.f;
+  float lg = -2.f;
+  int cnt = 0;
+  if (mode != 1) {
+    int lstar = 0;
+    cnt = live_count(blk, L, lstar);
+    if (cnt > 0) lg = log2f(static_cast<float>(cnt + 1)) + lgfact[L.n - 1 - lstar];
+  }
+  if (mode == 1 || (mode == 0 && cnt == 0)) {
+    int pos[kMaxN];
+    if (effective_pos(reinterpret_cast<const int8_t*>(blk + L.o_v), h->level,
+                      reinterpret_cast<const int8_t*>(blk + L.o_cells), L.n, pos)) {
+      const float r = remaining_log2_pos(pos, reinterpret_cast<const int8_t*>(blk + L.o_end), h->has_end != 0, L.n, lgfact);
+      if (r >= 0.f) lg = r;
+    }
+  }
+  return lg;
+}
+
 // Prefix / suffix sums of every job's row (node_tables' max-plus scans), built from the
 // global p32 table while the CTA stages the instance.
 __device__ __forceinline__ void stage_prefix_sums(unsigned char* smem, const InstLayout& IL, const int* p32, int n,
@@ -1306,13 +1360,14 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
       ++sc.decomposed;
     }
     if (grp.g == 0) {
-      // remaining work of this explorer for the steal phase (read by steal_kernel)
       iv.hdr->level = static_cast<int16_t>(level);
       iv.hdr->state = static_cast<uint8_t>(state);
       iv.hdr->d1 = static_cast<uint8_t>(d1);
       iv.hdr->d2 = static_cast<uint8_t>(d2);
       iv.hdr->rlev = static_cast<uint8_t>(rlev);
       iv.hdr->nrep = static_cast<uint8_t>(nrep);
+      // remaining work of this explorer for the steal phase (read by steal_kernel)
+      if (P.lens) P.lens[first + gi] = explorer_lens(reinterpret_cast<const unsigned char*>(iv.hdr), L, P.lgfact, P.lens_mode);
       unsigned* cnt = reinterpret_cast<unsigned*>(smem + IL.o_cnt);
       atomicAdd(&cnt[0], sc.decomposed);
       atomicAdd(&cnt[1], sc.leaves);

@@ -432,30 +432,7 @@ __device__ __forceinline__ void live_point(const int8_t* V, int lstar, int cell,
 __global__ void lens_kernel(IvmLayout L, const unsigned char* state, int K, const float* lgfact, float* lens, int mode) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= K) return;
-  const unsigned char* blk = state + static_cast<size_t>(i) * L.gstride;
-  const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
-  float lg = -3.f;
-  if (h->state == kInit) {
-    lg = -2.f;
-  } else if (h->state == kActive) {
-    lg = -2.f;
-    int cnt = 0;
-    if (mode != 1) {
-      int cells[kMaxN];
-      int lstar = 0;
-      cnt = live_siblings(blk, L, lstar, cells);
-      if (cnt > 0) lg = log2f(static_cast<float>(cnt + 1)) + lgfact[L.n - 1 - lstar];
-    }
-    if (mode == 1 || (mode == 0 && cnt == 0)) {
-      int pos[kMaxN];
-      if (effective_pos(reinterpret_cast<const int8_t*>(blk + L.o_v), h->level,
-                        reinterpret_cast<const int8_t*>(blk + L.o_cells), L.n, pos)) {
-        const float r = remaining_log2_pos(pos, reinterpret_cast<const int8_t*>(blk + L.o_end), h->has_end != 0, L.n, lgfact);
-        if (r >= 0.f) lg = r;
-      }
-    }
-  }
-  lens[i] = lg;
+  lens[i] = explorer_lens(state + static_cast<size_t>(i) * L.gstride, L, lgfact, mode);
 }
 
 // ---- multi-way interval splitting (exact mixed-radix arithmetic, no big integers)
@@ -535,90 +512,71 @@ __device__ int split_setup(const unsigned char* vb, const IvmLayout& L, int r, i
   return r;
 }
 
-// Thief seating of a steal phase, one thread per (victim, part): part i (1..r) of the victim's
-// [pos, end) cut into r + 1 equal parts goes to thief i - 1. Reads the victims only; their
-// ends are cut afterwards by split_victims_kernel (stream order).
-__global__ void split_thieves_kernel(IvmLayout L, unsigned char* state, const int* ptot, const int* thief,
-                                     const int* victim, const int* plan, DevCounters* ctr, int mode) {
+// Splits of a steal phase, one warp per victim: the victim's block is staged in shared memory
+// with one coalesced read (the digit walks below then run on shared memory instead of
+// serialized global loads); lane i in 1..r seats thief i - 1 with part i of the victim's work
+// [pos, end) cut into r + 1 parts, and lane 0 cuts the victim's own end to the start of part 1
+// (the thieves read the old end from the staged copy).
+constexpr int kSplitWarps = 4;
+__global__ void __launch_bounds__(kSplitWarps * 32) split_kernel(IvmLayout L, unsigned char* state, const int* ptot,
+                                                                 const int* thief, const int* victim, const int* plan,
+                                                                 DevCounters* ctr, int mode) {
+  extern __shared__ __align__(16) unsigned char sbuf[];
   const int nv = plan[0], rs = plan[1];
-  const int g0 = blockIdx.x * blockDim.x + threadIdx.x;
-  int ok = 0;
-  if (g0 < nv * rs) {
-    const int v = g0 / rs, i = g0 % rs + 1;
-    const unsigned char* vb = state + static_cast<size_t>(victim[v]) * L.gstride;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int n = L.n;
+  unsigned char* vb = sbuf + static_cast<size_t>(wi) * L.gstride;
+  unsigned seated = 0;
+  for (int v = blockIdx.x * kSplitWarps + wi; v < nv; v += gridDim.x * kSplitWarps) {
+    unsigned char* gv = state + static_cast<size_t>(victim[v]) * L.gstride;
+    for (int i = lane; i < L.gstride / 16; i += 32) reinterpret_cast<uint4*>(vb)[i] = reinterpret_cast<const uint4*>(gv)[i];
+    __syncwarp();
     const IvmHdr* vh = reinterpret_cast<const IvmHdr*>(vb);
-    const int n = L.n;
-    int b0[kMaxN], b1[kMaxN];
-    int cells[kMaxN];
-    int lstar = 0;
-    const int cnt = mode == 1 ? 0 : live_siblings(vb, L, lstar, cells);
-    if (cnt > 0 || mode == 2) {
-      const int g = min(rs, cnt);
-      if (i <= g) {
-        const int8_t* V = reinterpret_cast<const int8_t*>(vb + L.o_v);
-        const bool last = i == g;
-        live_point(V, lstar, live_group_start(cells, cnt, g, i), n, b0);
-        if (last) {
-          const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
-          for (int l = 0; l < n; ++l) b1[l] = E[l];
-        } else {
-          live_point(V, lstar, live_group_start(cells, cnt, g, i + 1), n, b1);
-        }
-        seat_explorer(state + static_cast<size_t>(thief[v * rs + i - 1]) * L.gstride, L, ptot, b0, b1,
-                      last ? vh->has_end != 0 : true);
-        ok = 1;
-      }
-    } else {
+    const int8_t* V = reinterpret_cast<const int8_t*>(vb + L.o_v);
+    const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
+    int ok = 0;
+    if (lane <= rs) {
+      int b0[kMaxN], b1[kMaxN];
+      int cells[kMaxN];
+      int lstar = 0;
+      int parts = 0;  // thieves this victim feeds
+      const int cnt = mode == 1 ? 0 : live_siblings(vb, L, lstar, cells);
+      const bool live = cnt > 0 || mode == 2;
       int pos[kMaxN], D[kMaxN];
       int top = 0;
-      const int r = split_setup(vb, L, rs, pos, D, top);
-      if (i <= r) {
-        const bool last = i == r;
-        split_point(pos, D, top, i, r + 1, n, b0);
-        if (last) {
-          const int8_t* E = reinterpret_cast<const int8_t*>(vb + L.o_end);
-          for (int l = 0; l < n; ++l) b1[l] = E[l];
+      if (live) parts = min(rs, cnt);
+      else parts = split_setup(vb, L, rs, pos, D, top);
+      if (parts >= 1 && lane <= parts) {
+        const int i = lane;
+        if (live) live_point(V, lstar, live_group_start(cells, cnt, parts, max(i, 1)), n, b0);
+        else split_point(pos, D, top, max(i, 1), parts + 1, n, b0);
+        if (i == 0) {  // the victim keeps part 0: end <- start of part 1
+          int8_t* gE = reinterpret_cast<int8_t*>(gv + L.o_end);
+          for (int l = 0; l < n; ++l) gE[l] = static_cast<int8_t>(b0[l]);
+          reinterpret_cast<IvmHdr*>(gv)->has_end = 1;
         } else {
-          split_point(pos, D, top, i + 1, r + 1, n, b1);
+          const bool last = i == parts;
+          if (last) {
+            for (int l = 0; l < n; ++l) b1[l] = E[l];
+          } else if (live) {
+            live_point(V, lstar, live_group_start(cells, cnt, parts, i + 1), n, b1);
+          } else {
+            split_point(pos, D, top, i + 1, parts + 1, n, b1);
+          }
+          seat_explorer(state + static_cast<size_t>(thief[v * rs + i - 1]) * L.gstride, L, ptot, b0, b1,
+                        last ? vh->has_end != 0 : true);
+          ok = 1;
         }
-        seat_explorer(state + static_cast<size_t>(thief[v * rs + i - 1]) * L.gstride, L, ptot, b0, b1,
-                      last ? vh->has_end != 0 : true);
-        ok = 1;
       }
     }
+    seated += __popc(__ballot_sync(0xffffffffu, ok));
+    __syncwarp();
   }
-  const unsigned cnt = __popc(__ballot_sync(0xffffffffu, ok));
-  if ((threadIdx.x & 31) == 0 && cnt) {
-    atomicAdd(&ctr->active, static_cast<int>(cnt));
-    atomicAdd(&ctr->steals, static_cast<unsigned long long>(cnt));
-    atomicAdd(&ctr->inits, static_cast<unsigned long long>(cnt));
+  if (lane == 0 && seated) {
+    atomicAdd(&ctr->active, static_cast<int>(seated));
+    atomicAdd(&ctr->steals, static_cast<unsigned long long>(seated));
+    atomicAdd(&ctr->inits, static_cast<unsigned long long>(seated));
   }
-}
-
-// The victims keep the first part: end <- pos + D / (r + 1) (one thread per victim).
-__global__ void split_victims_kernel(IvmLayout L, unsigned char* state, const int* victim, const int* plan, int mode) {
-  const int nv = plan[0], rs = plan[1];
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nv) return;
-  unsigned char* vb = state + static_cast<size_t>(victim[v]) * L.gstride;
-  int8_t* E = reinterpret_cast<int8_t*>(vb + L.o_end);
-  int b[kMaxN];
-  int cells[kMaxN];
-  int lstar = 0;
-  const int cnt = mode == 1 ? 0 : live_siblings(vb, L, lstar, cells);
-  if (cnt > 0 || mode == 2) {
-    const int g = min(rs, cnt);
-    if (g < 1) return;
-    live_point(reinterpret_cast<const int8_t*>(vb + L.o_v), lstar, live_group_start(cells, cnt, g, 1), L.n, b);
-  } else {
-    int pos[kMaxN], D[kMaxN];
-    int top = 0;
-    const int r = split_setup(vb, L, rs, pos, D, top);
-    if (r < 1) return;
-    split_point(pos, D, top, 1, r + 1, L.n, b);
-  }
-  for (int l = 0; l < L.n; ++l) E[l] = static_cast<int8_t>(b[l]);
-  reinterpret_cast<IvmHdr*>(vb)->has_end = 1;
 }
 
 #include "steal_ref.cuh"
@@ -1218,6 +1176,7 @@ struct pbbgpu_pool {
   int big2w_grid = 0, big2w_warps = 0;
   size_t smem_optin = 0;               // cudaDevAttrMaxSharedMemoryPerBlockOptin
   int num_sms = 148;                   // cudaDeviceProp::multiProcessorCount
+  int split_grid = 0;                  // split_kernel blocks (kSplitWarps victims each per pass)
   uint16_t* d_inv16 = nullptr;
   int* d_big_scratch = nullptr;
   int big_grid = 0;
@@ -1756,6 +1715,9 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
   ck(cudaMalloc(&P->d_state, static_cast<size_t>(P->K) * P->L.gstride), "malloc state");
   ck(cudaMalloc(&P->d_wrk, (static_cast<size_t>(P->K) * 2 + 4) * sizeof(int)), "malloc");
   ck(cudaMalloc(&P->d_lens, static_cast<size_t>(P->K) * sizeof(float)), "malloc");
+  P->split_grid = std::max(1, std::min((P->K + kSplitWarps - 1) / kSplitWarps, 4 * P->num_sms));
+  ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(split_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kSplitWarps * P->L.gstride), "smem attr");
   ck(cudaMalloc(&P->d_ctr, sizeof(DevCounters)), "malloc");
   ck(cudaMallocHost(&P->h_ctr, sizeof(DevCounters)), "malloc host");
   ck(cudaMalloc(&P->d_hist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
@@ -2240,6 +2202,11 @@ int run_round(pbbgpu_pool* P) {
   S.lens = P->d_lens;
   S.max_split = P->cfg.max_split > 0 ? std::min(P->cfg.max_split, 63) : 4;
   S.split_mode = split_kind(P->cfg.split_mode);
+  if (P->cfg.steal_policy != 1) {  // the explore kernel leaves each explorer's steal length
+    E.lens = P->d_lens;
+    E.lgfact = P->d_lgfact;
+    E.lens_mode = S.split_mode;
+  }
   // several (explore, steal) rounds back to back per host synchronization: the rounds are
   // device-timed, and a round after exhaustion costs only the state copy of an empty launch
   const int R = P->rounds_per_sync;
@@ -2268,15 +2235,12 @@ int run_round(pbbgpu_pool* P) {
       P->launches += 2;
       continue;
     }
-    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, S.split_mode);
-    ck(cudaGetLastError(), "lens_kernel launch");
+    // lens: written by the explore kernel's write-back (E.lens)
     steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
     ck(cudaGetLastError(), "steal_kernel launch");
-    split_thieves_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, S.thief, S.victim,
-                                                                     S.plan, P->d_ctr, S.split_mode);
-    ck(cudaGetLastError(), "split_thieves_kernel launch");
-    split_victims_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, S.victim, S.plan, S.split_mode);
-    ck(cudaGetLastError(), "split_victims_kernel launch");
+    split_kernel<<<P->split_grid, kSplitWarps * 32, kSplitWarps * P->L.gstride, P->stream>>>(
+        P->L, P->d_state, P->d_ptot, S.thief, S.victim, S.plan, P->d_ctr, S.split_mode);
+    ck(cudaGetLastError(), "split_kernel launch");
     if (P->g_open) {  // inter-GPU exchange over peer memory (no host involvement)
       ck(cudaEventRecord(P->gev[r], P->stream), "event");
       const GroupParams G = group_params(P);
@@ -2289,7 +2253,7 @@ int run_round(pbbgpu_pool* P) {
       P->launches += 3;
     }
     ck(cudaEventRecord(P->evs[3 * r + 2], P->stream), "event");
-    P->launches += 5;
+    P->launches += 3;
   }
   read_counters(P);
   for (int r = 0; r < R; ++r) {
