@@ -756,13 +756,46 @@ __device__ __forceinline__ int minmin_lane(bool valid, int a, int b) {
   return kFwd;
 }
 
+// R (per-machine sum of the jobs of the current row) in registers, machine-chunked like
+// node_tables (lane g holds machines g*C .. g*C+C-1): set from the node's remain on branch,
+// + p of the job one level up on backtrack; the block's R is only read at entry and written
+// at the write-back.
+template <int M, int G>
+struct RowSum {
+  static constexpr int C = (M + G - 1) / G;
+  int v[C];
+  template <bool W>
+  __device__ __forceinline__ void load(const Group<G>& grp, const IvmView& iv) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int k = grp.g * C + c;
+      v[c] = k < M ? static_cast<int>(iv.Rw<W>()[k]) : 0;
+    }
+  }
+  template <bool W>
+  __device__ __forceinline__ void store(const Group<G>& grp, const IvmView& iv) const {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int k = grp.g * C + c;
+      if (k < M) iv.Rw<W>()[k] = static_cast<FtT<W>>(v[c]);
+    }
+  }
+  __device__ __forceinline__ void add(const Group<G>& grp, const int* pr) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const int k = grp.g * C + c;
+      if (k < M) v[c] += pr[k];
+    }
+  }
+};
+
 // Node tables from the incremental stacks: node at `level` with selected job `job` placed
-// by dir[level]; d1/d2 include it.
+// by dir[level]; d1/d2 include it. SET: the node's remain becomes the row sum (branch).
 // RTF: also write remain + tail / front + remain (LB1's children; not LB2, not leaves)
-template <int M, int G, bool W = false, bool RTF = true>
+template <int M, int G, bool W = false, bool RTF = true, bool SET = false>
 __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& iv,
                                             const InstView& in, int n, int mp, int job, int dI,
-                                            int d1, int d2) {
+                                            int d1, int d2, RowSum<M, G>& rs) {
   // The extended table (front of sigma1.job, or tail of job.sigma2) is the max-plus
   // recurrence e[k] = max(e[k-1], src[k]) + p[k] (e[M] = 0 backward). Unrolled with the
   // prefix sums of p it is a prefix max: e[k] = Sin[k] + max_{i<=k} (src[i] - Sex[i])
@@ -824,7 +857,8 @@ __device__ __forceinline__ void node_tables(const Group<G>& grp, const IvmView& 
     const int k = k0 + c;
     if (k < M) {
       const int e = inc[c] + loc[c];
-      const int rmk = static_cast<int>(iv.Rw<W>()[k]) - pr[k];
+      const int rmk = rs.v[c] - pr[k];
+      if (SET) rs.v[c] = rmk;
       const int frk = dI == kFwd ? e : static_cast<int>(fsrc[k]);
       const int tlk = dI == kFwd ? static_cast<int>(tsrc[k]) : e;
       iv.rm[k] = rmk;
@@ -879,7 +913,8 @@ __device__ __forceinline__ bool reached_end(const Group<G>& grp, const IvmView& 
 template <int M, int G, bool RM, bool W = false>
 __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& iv,
                                            const InstView& in, int n, int mp, bool has_end,
-                                           int& level, int& d1, int& d2, RowMask<M, RM>& rowmask) {
+                                           int& level, int& d1, int& d2, RowMask<M, RM>& rowmask,
+                                           RowSum<M, G>& rs) {
   for (;;) {
     if (level < 0) return -1;
     const int len = n - level;
@@ -905,9 +940,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
         const int psel = iv.V[level];
         const int x = iv.cells[tri_off(level, n) + psel];
         const int job = (x < 0 ? -x : x) - 1;
-        const int* pr = in.p32 + job * mp;
-        FtT<W>* R = iv.Rw<W>();
-        for (int k = grp.g; k < M; k += G) R[k] = static_cast<FtT<W>>(R[k] + pr[k]);
+        rs.add(grp, in.p32 + job * mp);
         rowmask.add(in, job);  // the row one level up holds the job selected there
         grp.sync();
         if (grp.g == 0) iv.V[level] = static_cast<int8_t>(psel + 1);
@@ -932,14 +965,14 @@ template <int M, int G, int BOUND, bool SMALLN, bool RM, bool W = false>
 __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmView& iv,
                                                  const InstView& in, int n, int mp, int sel,
                                                  int prune, int& level, int& d1, int& d2,
-                                                 unsigned* shist, RowMask<M, RM>& rowmask) {
+                                                 unsigned* shist, RowMask<M, RM>& rowmask, RowSum<M, G>& rs) {
   const int I = level;
   const int f = n - 1 - I;
   int8_t* row = iv.cells + tri_off(I, n);
   const int x = row[sel];
   const int job = (x < 0 ? -x : x) - 1;
   const int dI = iv.dir[I];
-  node_tables<M, G, W, BOUND == kLB1>(grp, iv, in, n, mp, job, dI, d1, d2);
+  node_tables<M, G, W, BOUND == kLB1, true>(grp, iv, in, n, mp, job, dI, d1, d2, rs);
   const unsigned long long fm0 = gather_free<G>(grp, iv, row, sel, f);
   unsigned long long fm = 0;
   if constexpr (BOUND == kLB2) fm = grp.ror64(fm0);  // LB1 does not use the free set mask
@@ -976,7 +1009,6 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
   for (int k = grp.g; k < M; k += G) {
     if (dI == kFwd) ft[d1 * M + k] = static_cast<FtT<W>>(iv.fr[k]);
     else ft[(n - d2) * M + k] = static_cast<FtT<W>>(iv.tl[k]);
-    iv.Rw<W>()[k] = static_cast<FtT<W>>(iv.rm[k]);
   }
   if (grp.g == 0) {
     iv.dir[I + 1] = static_cast<uint8_t>(dir);
@@ -992,7 +1024,7 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
 // Leaf: one free job (explorer.cpp:42-57). Makespan of sigma1.j.sigma2 from the node
 // tables: C = max_k (front_{sigma1.j}[k] + tail_{sigma2}[k]).
 template <int M, int G, bool W = false>
-__device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, const InstView& in,
+__device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, const InstView& in, RowSum<M, G>& rs,
                                      int n, int mp, int sel, int level, int d1, int d2,
                                      int improve, DevCounters* ctr, ImpRecord* imp,
                                      StepCounters& sc, unsigned long long* census = nullptr,
@@ -1001,7 +1033,7 @@ __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, con
   const int x = row[sel];
   const int job = (x < 0 ? -x : x) - 1;
   const int dI = iv.dir[level];
-  node_tables<M, G, W, false>(grp, iv, in, n, mp, job, dI, d1, d2);
+  node_tables<M, G, W, false>(grp, iv, in, n, mp, job, dI, d1, d2, rs);
   grp.sync();
   if (grp.g == 0) {
     const int len = n - level;
@@ -1215,7 +1247,7 @@ __device__ __forceinline__ void stage_prefix_sums(unsigned char* smem, const Ins
 template <int BOUND, int G, bool SMALLN>
 constexpr bool kRowMask = BOUND == kLB2 && G == 32 && SMALLN;
 template <int BOUND, int G, bool SMALLN>
-constexpr int kExploreThreads = (BOUND == kLB1 && G == 8) ? 768 : 1024;
+constexpr int kExploreThreads = 1024;
 
 // W: wide (32-bit) FT / R / prefix sums, LB1 only (pool_init)
 template <int M, int G, int BOUND, bool SMALLN = false, bool W = false>
@@ -1296,6 +1328,8 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
     RowMask<M, RM> rowmask;
     rowmask.bind(iv, L, in.npairs);
     if (state != kEmpty) rowmask.build(iv, in, n, level);
+    RowSum<M, G> rs;
+    rs.template load<W>(grp, iv);
     if (grp.g == 0 && state != kEmpty) atomicAdd(reinterpret_cast<unsigned*>(smem + IL.o_cnt) + 6, 1u);
     int best = grp.bcast(grp.g == 0 ? *reinterpret_cast<volatile int*>(&P.ctr->best) : 0, 0);
     int step = 0;
@@ -1341,24 +1375,25 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
           state = kActive;
           continue;
         }
-        decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist, rowmask);
+        decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist, rowmask, rs);
         ++sc.decomposed;
         ++nrep;
         rlev = level;
         continue;
       }
-      const int sel = select_next<M, G, RM, W>(grp, iv, in, n, mp, has_end, level, d1, d2, rowmask);
+      const int sel = select_next<M, G, RM, W>(grp, iv, in, n, mp, has_end, level, d1, d2, rowmask, rs);
       if (sel < 0) {
         state = kEmpty;
         break;
       }
       if (n - 1 - level <= 1) {
-        leaf<M, G, W>(grp, iv, in, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc, P.census, P.census_cap);
+        leaf<M, G, W>(grp, iv, in, rs, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc, P.census, P.census_cap);
         continue;
       }
-      decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist, rowmask);
+      decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist, rowmask, rs);
       ++sc.decomposed;
     }
+    rs.template store<W>(grp, iv);
     if (grp.g == 0) {
       iv.hdr->level = static_cast<int16_t>(level);
       iv.hdr->state = static_cast<uint8_t>(state);
