@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpbbgpu.so")
 SOURCES = [os.path.join(CSRC, "pool.cu"), os.path.join(CSRC, "wire.cpp")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("explore.cuh", "bound_big.cuh", "pbb_layout.h", "steal_ref.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("explore.cuh", "explore_big.cuh", "bound_big.cuh", "pbb_layout.h", "steal_ref.cuh")] + [
     os.path.join(ROOT, "include", "pbbgpu.h")]
 
 NVCC_FLAGS = [

@@ -572,17 +572,24 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
       pm = max(pm, E + static_cast<int>((e >> 13) & 0x7ffu));
       E += static_cast<int>(e) >> 24;
     };
+    // every lane's mask has exactly f set bits, but split differently over the two words: one
+    // loop of f iterations that switches words when the first runs dry keeps the warp converged
+    // (two loops per word would run max(lo bits) + max(hi bits) divergent iterations)
     const uint32_t lo32 = static_cast<uint32_t>(Fq), hi32 = static_cast<uint32_t>(Fq >> 32);
-    for (uint32_t w = __brev(lo32); w;) {  // ascending: positions 31 - u, then 63 - u
-      const int u = bfind_u32(w);
-      w ^= 1u << u;
-      fwd(31 - u);
+    {
+      uint32_t w = __brev(lo32), w2 = __brev(hi32);  // ascending: positions 31 - u, then 63 - u
+      int top = 31;
+      for (int i = 0; i < f; ++i) {
+        if (w == 0) {
+          w = w2;
+          top = 63;
+        }
+        const int u = bfind_u32(w);
+        w ^= 1u << u;
+        fwd(top - u);
+      }
     }
-    for (uint32_t w = __brev(hi32); w;) {
-      const int u = bfind_u32(w);
-      w ^= 1u << u;
-      fwd(63 - u);
-    }
+    __syncwarp();
     int G = Atot, sm = NEG;
     auto bwd = [&](int t) {
       const unsigned e = *reinterpret_cast<const unsigned*>(pq + t * strideB);
@@ -594,16 +601,20 @@ __device__ __forceinline__ void lb2_round(const IvmView& iv, const InstView& in,
       G -= v;
       sm = max(sm, G + static_cast<int>((e >> 13) & 0x7ffu));
     };
-    for (uint32_t w = hi32; w;) {  // descending
-      const int t = bfind_u32(w);
-      w ^= 1u << t;
-      bwd(32 + t);
+    {
+      uint32_t w = hi32;  // descending: positions 32 + t, then t
+      int base = 32;
+      for (int i = 0; i < f; ++i) {
+        if (w == 0) {
+          w = lo32;
+          base = 0;
+        }
+        const int t = bfind_u32(w);
+        w ^= 1u << t;
+        bwd(base + t);
+      }
     }
-    for (uint32_t w = lo32; w;) {
-      const int t = bfind_u32(w);
-      w ^= 1u << t;
-      bwd(t);
-    }
+    __syncwarp();
   }
   if constexpr (kFusedCombine<SMALLN>) return;
   const uint32_t* Hl = H + l;
@@ -888,45 +899,75 @@ __device__ __forceinline__ unsigned long long gather_free(const Group<G>& grp, c
 
 // ------------------------------------------------------------------ explorer steps
 
-// position_reached_end (src/ivm.cpp:90-97): padded V >= end.
-template <int G>
-__device__ __forceinline__ bool reached_end(const Group<G>& grp, const IvmView& iv, int n,
-                                            int level) {
-  for (int b0 = 0; b0 < n; b0 += G) {
-    const int l = b0 + grp.g;
-    int pv = 0, ev = 0;
-    if (l < n) {
-      pv = l <= level ? iv.V[l] : 0;
-      ev = iv.endd[l];
+
+// The end test kept incrementally (register state, uniform over the group) instead of a
+// digit-by-digit comparison of padded V and end at every select: eq = length of the common
+// prefix of V[0..level-1] and end (levels above the current row), lt = V[eq] < end[eq] when
+// eq < level, enz = the last non-zero end digit. V only changes at the current row, so a
+// descent extends or fixes the prefix and a backtrack truncates it.
+struct EndTrack {
+  int eq = 0, enz = -1;
+  bool lt = false;
+  template <int G>
+  __device__ __forceinline__ void init(const Group<G>& grp, const IvmView& iv, int n, int level) {
+    int d = level, z = -1;
+    for (int b0 = 0; b0 < n; b0 += G) {
+      const int l = b0 + grp.g;
+      const bool in = l < n;
+      const int e = in ? iv.endd[l] : 0;
+      if (in && l < level && iv.V[l] != e) d = min(d, l);
+      if (in && e != 0) z = l;
     }
-    const unsigned b = grp.ballot(pv != ev);
-    if (b) {
-      const int src = __ffs(b) - 1;
-      return grp.bcast(pv, src) > grp.bcast(ev, src);
+    eq = grp.rmin(d);
+    enz = grp.rmax(z);
+    lt = eq < level ? iv.V[eq] < iv.endd[eq] : false;
+  }
+  // position_reached_end (src/ivm.cpp:90-97) for V[level] = found: padded V >= end
+  __device__ __forceinline__ bool reached(const IvmView& iv, int level, int found) const {
+    if (eq < level) return !lt;
+    const int e = iv.endd[level];
+    if (found != e) return found > e;
+    return level >= enz;
+  }
+  __device__ __forceinline__ void descend(const IvmView& iv, int level, int sel) {
+    if (eq == level) {
+      const int e = iv.endd[level];
+      if (sel == e) eq = level + 1;
+      else lt = sel < e;
     }
   }
-  return true;
-}
+  __device__ __forceinline__ void up(int level) { eq = min(eq, level); }
+};
+
+constexpr int kNoHint = -2;
 
 // select_next (src/ivm.cpp:99-122) with the incremental R / d1 / d2 bookkeeping.
-// Returns the selected cell, or -1 when the explorer is exhausted.
+// Returns the selected cell, or -1 when the explorer is exhausted. hint: the first unpruned
+// cell of the current row when decompose_branch has just written it (-1: every child pruned,
+// backtrack at once), so the row is not scanned again; the IVM state stays the reference's.
 template <int M, int G, bool RM, bool W = false>
 __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& iv,
                                            const InstView& in, int n, int mp, bool has_end,
                                            int& level, int& d1, int& d2, RowMask<M, RM>& rowmask,
-                                           RowSum<M, G>& rs) {
+                                           RowSum<M, G>& rs, EndTrack& et, int hint = kNoHint) {
   for (;;) {
     if (level < 0) return -1;
     const int len = n - level;
     const int8_t* row = iv.cells + tri_off(level, n);
-    const int c0 = iv.V[level];
     int found = -1;
-    for (int b0 = c0; b0 < len; b0 += G) {
-      const int c = b0 + grp.g;
-      const unsigned b = grp.ballot(c < len && row[c] > 0);
-      if (b) {
-        found = b0 + __ffs(b) - 1;
-        break;
+    if (hint != kNoHint) {
+      // the row was just written by decompose_branch (V = 0): its first unpruned cell is known
+      found = hint;
+      hint = kNoHint;
+    } else {
+      const int c0 = iv.V[level];
+      for (int b0 = c0; b0 < len; b0 += G) {
+        const int c = b0 + grp.g;
+        const unsigned b = grp.ballot(c < len && row[c] > 0);
+        if (b) {
+          found = b0 + __ffs(b) - 1;
+          break;
+        }
       }
     }
     if (found < 0) {  // row exhausted: backtrack
@@ -936,6 +977,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
       grp.sync();
       if (grp.g == 0) iv.V[level] = 0;
       --level;
+      et.up(level);
       if (level >= 0) {
         const int psel = iv.V[level];
         const int x = iv.cells[tri_off(level, n) + psel];
@@ -951,7 +993,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
     grp.sync();
     if (grp.g == 0) iv.V[level] = static_cast<int8_t>(found);
     grp.sync();
-    if (has_end && reached_end(grp, iv, n, level)) return -1;
+    if (has_end && et.reached(iv, level, found)) return -1;
     return found;
   }
 }
@@ -962,7 +1004,7 @@ struct StepCounters {
 
 // Decompose the node at (level, sel) and branch (bound.cpp:98-139 + ivm.cpp:124-145).
 template <int M, int G, int BOUND, bool SMALLN, bool RM, bool W = false>
-__device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmView& iv,
+__device__ __forceinline__ int decompose_branch(const Group<G>& grp, const IvmView& iv,
                                                  const InstView& in, int n, int mp, int sel,
                                                  int prune, int& level, int& d1, int& d2,
                                                  unsigned* shist, RowMask<M, RM>& rowmask, RowSum<M, G>& rs) {
@@ -978,17 +1020,18 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
   if constexpr (BOUND == kLB2) fm = grp.ror64(fm0);  // LB1 does not use the free set mask
   grp.sync();
   int8_t* nrow = iv.cells + tri_off(I + 1, n);
-  int dir;
+  int dir, first;
   if constexpr (BOUND == kLB2 && G == 32 && SMALLN) {
     // lane c holds child c's two bounds in registers (no lbf / lbb round trip)
     const uint32_t acc = children_lb2_w<M, SMALLN, RM>(iv, in, n, mp, f, fm, &rowmask, job);
     const int a = static_cast<int>(acc & 0xffffu), b = static_cast<int>(acc >> 16);
     dir = minmin_lane(grp.g < f, a, b);
+    const int lb = dir == kFwd ? a : b;
     if (grp.g < f) {
-      const int lb = dir == kFwd ? a : b;
       const int j1 = iv.freej[grp.g] + 1;
       nrow[grp.g] = static_cast<int8_t>(lb >= prune ? -j1 : j1);
     }
+    first = __ffs(__ballot_sync(0xffffffffu, grp.g < f && lb < prune)) - 1;
   } else {
     if constexpr (BOUND == kLB1) {
       children_lb1<M, G>(grp, iv, in, mp, f);
@@ -999,11 +1042,15 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
     }
     grp.sync();
     dir = minmin<G, W>(grp, iv, f);
+    first = f;
     for (int c = grp.g; c < f; c += G) {
       const int lb = dir == kFwd ? iv.lbf[c] : iv.lbb[c];
       const int j1 = iv.freej[c] + 1;
       nrow[c] = static_cast<int8_t>(lb >= prune ? -j1 : j1);
+      if (lb < prune) first = min(first, c);
     }
+    first = grp.rmin(first);
+    if (first == f) first = -1;
   }
   FtT<W>* ft = iv.ftw<W>();
   for (int k = grp.g; k < M; k += G) {
@@ -1019,6 +1066,7 @@ __device__ __forceinline__ void decompose_branch(const Group<G>& grp, const IvmV
   level = I + 1;
   d1 += dir == kFwd;
   d2 += dir == kBwd;
+  return first;
 }
 
 // Leaf: one free job (explorer.cpp:42-57). Makespan of sigma1.j.sigma2 from the node
@@ -1185,7 +1233,7 @@ __device__ __forceinline__ int live_count(const unsigned char* vb, const IvmLayo
   return 0;
 }
 
-__device__ __noinline__ float explorer_lens(const unsigned char* blk, const IvmLayout& L, const float* lgfact, int mode) {
+__device__ __forceinline__ float explorer_lens(const unsigned char* blk, const IvmLayout& L, const float* lgfact, int mode) {
   const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
   if (h->state == kInit) return -2.f;
   if (h->state != kActive) return -3.f;
@@ -1332,7 +1380,9 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
     rs.template load<W>(grp, iv);
     if (grp.g == 0 && state != kEmpty) atomicAdd(reinterpret_cast<unsigned*>(smem + IL.o_cnt) + 6, 1u);
     int best = grp.bcast(grp.g == 0 ? *reinterpret_cast<volatile int*>(&P.ctr->best) : 0, 0);
-    int step = 0;
+    int step = 0, hint = kNoHint;
+    EndTrack et;
+    if (has_end && state == kActive) et.init(grp, iv, n, level);
     unsigned long long t_end = ~0ull;
     if (P.budget_ns) t_end = globaltimer_ns() + P.budget_ns;
     while (step < P.steps) {
@@ -1373,6 +1423,7 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
             for (int t = 0; t < dup; ++t) atomicAdd(&sdhist[n - 1 - t], 1u);
           }
           state = kActive;
+          if (has_end) et.init(grp, iv, n, level);
           continue;
         }
         decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist, rowmask, rs);
@@ -1381,7 +1432,8 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
         rlev = level;
         continue;
       }
-      const int sel = select_next<M, G, RM, W>(grp, iv, in, n, mp, has_end, level, d1, d2, rowmask, rs);
+      const int sel = select_next<M, G, RM, W>(grp, iv, in, n, mp, has_end, level, d1, d2, rowmask, rs, et, hint);
+      hint = kNoHint;
       if (sel < 0) {
         state = kEmpty;
         break;
@@ -1390,7 +1442,8 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
         leaf<M, G, W>(grp, iv, in, rs, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc, P.census, P.census_cap);
         continue;
       }
-      decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist, rowmask, rs);
+      if (has_end) et.descend(iv, level, sel);
+      hint = decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist, rowmask, rs);
       ++sc.decomposed;
     }
     rs.template store<W>(grp, iv);

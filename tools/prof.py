@@ -139,12 +139,17 @@ def cmd_src(rep, top=30):
             inst = int(r[hdr.index("Instructions Executed")])
         except (ValueError, IndexError):
             continue
-        res.append((samp, inst, fname, r[0], r[1].strip()[:110]))
+        try:
+            thr = int(r[hdr.index("Thread Instructions Executed")])
+        except (ValueError, IndexError):
+            thr = 0
+        res.append((samp, inst, thr, fname, r[0], r[1].strip()[:100]))
     tot = sum(x[0] for x in res) or 1
     toti = sum(x[1] for x in res) or 1
     res.sort(reverse=True)
-    for samp, inst, f, ln, src in res[:int(top)]:
-        print(f"{100 * samp / tot:5.1f}% {100 * inst / toti:5.1f}%i {f}:{ln:5s} {src}")
+    # stall share, instruction share, active threads per executed instruction, line
+    for samp, inst, thr, f, ln, src in res[:int(top)]:
+        print(f"{100 * samp / tot:5.1f}% {100 * inst / toti:5.1f}%i {thr / inst if inst else 0:4.1f}t {f}:{ln:5s} {src}")
 
 
 def cmd_launches(path, command="?"):
