@@ -87,8 +87,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
   int* sp = reinterpret_cast<int*>(smem);                         // [n][mp]
   uint16_t* heads = reinterpret_cast<uint16_t*>(sp + n * mp);     // [job][M]
   uint16_t* tails = heads + n * M;
-  uint8_t* isfree = reinterpret_cast<uint8_t*>(tails + n * M);   // [n]
-  int* accf = reinterpret_cast<int*>(isfree + round_up(n, 16));   // [job]
+  int* accf = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(tails + n * M) + round_up(n, 16));  // [job]
   int* accb = accf + n;
   int* fr = accb + n;  // [mp] each
   int* tl = fr + round_up(M, 4);
@@ -96,7 +95,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
   int* red = rm + round_up(M, 4);  // 8 x 4 reduction scratch
   uint16_t* spm = reinterpret_cast<uint16_t*>(red + 64);  // the node's perm
   const int MW = (n + 31) >> 5;
-  uint32_t* fmask = reinterpret_cast<uint32_t*>(spm + round_up(n, 8));  // LB2: [pair][MW] free positions
+  uint32_t* fmask = reinterpret_cast<uint32_t*>(spm + round_up(n, 8));  // LB2: [MW][pair] free positions
   for (int i = tid; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
   __syncthreads();
   for (int node = blockIdx.x; node < B.count; node += gridDim.x) {
@@ -104,7 +103,6 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
     const int d1 = B.d1[node], d2 = B.d2[node], f = n - d1 - d2;
     if (d1 < 0) continue;  // no node in this slot (big explorer pool steps)
     for (int j = tid; j < n; j += blockDim.x) {
-      isfree[j] = 0;
       accf[j] = 0;
       accb[j] = 0;
     }
@@ -112,17 +110,27 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
     if (BOUND == kLB2)
       for (int i = tid; i < B.npairs * MW; i += blockDim.x) fmask[i] = 0;
     __syncthreads();
-    for (int c = tid; c < f; c += blockDim.x) isfree[perm[d1 + c]] = 1;
     for (int i = tid; i < n; i += blockDim.x) spm[i] = static_cast<uint16_t>(perm[i]);
     __syncthreads();
-    if (BOUND == kLB2) {  // per pair, the free jobs' positions in its Johnson order as a bitmask
-      const int P = B.npairs, cs = blockDim.x / P;  // thread -> (pair, first child), cs children apart
-      if (tid < cs * P) {
-        const int q = tid % P;
-#pragma unroll 4
-        for (int c = tid / P; c < f; c += cs) {
+    if (BOUND == kLB2 && warp >= 2) {
+      // per pair, the free jobs' positions in its Johnson order as a bitmask, word-major
+      // ([MW][pair]: the pairs of a warp hit distinct banks), built by warps 2.. while warps 0/1
+      // run the node-table wavefronts
+      static_assert(kBigThreads - 64 >= 20 * 19 / 2, "a mask thread per pair (m <= 20)");
+      const int P = B.npairs, t0 = tid - 64, cs = (kBigThreads - 64) / P;  // thread -> (pair, first child)
+      if (t0 < cs * P) {
+        const int q = t0 % P;
+        int c = t0 / P;
+        for (; c + 15 * cs < f; c += 16 * cs) {  // 16 inverse-order loads in flight
+          int pos[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) pos[u] = B.inv16[static_cast<size_t>(spm[d1 + c + u * cs]) * P + q];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) atomicOr(&fmask[(pos[u] >> 5) * P + q], 1u << (pos[u] & 31));
+        }
+        for (; c < f; c += cs) {
           const int pos = B.inv16[static_cast<size_t>(spm[d1 + c]) * P + q];
-          atomicOr(&fmask[q * MW + (pos >> 5)], 1u << (pos & 31));
+          atomicOr(&fmask[(pos >> 5) * P + q], 1u << (pos & 31));
         }
       }
     }
@@ -136,14 +144,14 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
     {  // remain: per-warp partial sums over the free jobs, lane = machine
       int acc = 0;
       if (lane < M)
-        for (int c = warp; c < f; c += blockDim.x / 32) acc += sp[perm[d1 + c] * mp + lane];
+        for (int c = warp; c < f; c += blockDim.x / 32) acc += sp[spm[d1 + c] * mp + lane];
       __syncthreads();
       if (lane < M) atomicAdd(&rm[lane], acc);
     }
     __syncthreads();
     if (BOUND == kLB1) {
       for (int c = tid; c < f; c += blockDim.x) {
-        const int j = perm[d1 + c];
+        const int j = spm[d1 + c];
         const int* pr = sp + j * mp;
         int prev = 0, best = 0;
 #pragma unroll
@@ -165,7 +173,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
       }
     } else {
       for (int c = tid; c < f; c += blockDim.x) {  // child heads / tails, by job
-        const int j = perm[d1 + c];
+        const int j = spm[d1 + c];
         const int* pr = sp + j * mp;
         int prev = 0;
 #pragma unroll
@@ -192,8 +200,11 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
         {
         // the pair's Johnson order streams from L2, only at the free positions (set bits of
         // the pair's mask, f of them): kPf entries in flight per thread
-        const uint32_t* mk = fmask + q * MW;
-        int w = 0;
+        // PM_i is kept by rank (the i-th free position of the walk): every thread of a warp is
+        // at the same rank at every step, so the scratch accesses are coalesced
+        const uint32_t* mk = fmask + q;
+        const int P = B.npairs;
+        int w = 0, rank = 0;
         uint32_t bits = mk[0];
         for (int left = f; left > 0; left -= kPf) {
           const int cnt = min(left, kPf);
@@ -201,7 +212,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
 #pragma unroll
           for (int u = 0; u < kPf; ++u) {
             if (u < cnt) {
-              while (bits == 0) bits = mk[++w];
+              while (bits == 0) bits = mk[++w * P];
               const int t = w * 32 + __ffs(bits) - 1;
               bits &= bits - 1;
               ev[u] = col[static_cast<size_t>(t) * B.npairs];
@@ -211,10 +222,9 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
           for (int u = 0; u < kPf; ++u) {
             if (u < cnt) {
               const uint2 e = ev[u];
-              const int j = e.x & 0xffff;
               A += e.x >> 16;
               const int X = A + static_cast<int>(e.y >> 16) - Bp;
-              PM[j * kBigThreads] = pm;
+              PM[(rank++) * kBigThreads] = pm;
               pm = max(pm, X);
               Bp += e.y & 0xffff;
             }
@@ -222,22 +232,22 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
         }
         int As = 0, Bs = Atot - Btot, sm = NEG;
         w = MW - 1;
-        bits = mk[w];
+        bits = mk[w * P];
         for (int left = f; left > 0; left -= kPf) {
           const int cnt = min(left, kPf);
           uint2 ev[kPf];
 #pragma unroll
           for (int u = 0; u < kPf; ++u) {
             if (u < cnt) {
-              while (bits == 0) bits = mk[--w];
+              while (bits == 0) bits = mk[--w * P];
               const int b = 31 - __clz(bits);
               bits &= ~(1u << b);
               ev[u] = col[static_cast<size_t>(w * 32 + b) * B.npairs];
             }
           }
-          int pmv[kPf];  // the forward pass's PM_j of this batch, all loads in flight
+          int pmv[kPf];  // the forward pass's PM of this batch (ranks left-1 .. left-cnt), all loads in flight
 #pragma unroll
-          for (int u = 0; u < kPf; ++u) pmv[u] = u < cnt ? PM[(ev[u].x & 0xffff) * kBigThreads] : 0;
+          for (int u = 0; u < kPf; ++u) pmv[u] = u < cnt ? PM[(left - 1 - u) * kBigThreads] : 0;
 #pragma unroll
           for (int u = 0; u < kPf; ++u) {
             if (u < cnt) {
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
     // MinMin over children in decode order (src/bound.cpp:109-131)
     int lo = INT_MAX;
     for (int c = tid; c < f; c += blockDim.x) {
-      const int j = perm[d1 + c];
+      const int j = spm[d1 + c];
       lo = min(lo, min(accf[j], accb[j]));
     }
     lo = __reduce_min_sync(0xffffffffu, lo);
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
     __syncthreads();
     int cf = 0, cb = 0, sf = 0, sb = 0;
     for (int c = tid; c < f; c += blockDim.x) {
-      const int j = perm[d1 + c];
+      const int j = spm[d1 + c];
       cf += accf[j] == lo;
       cb += accb[j] == lo;
       sf += accf[j];
@@ -303,7 +313,7 @@ __global__ void __launch_bounds__(kBigThreads) decompose_big_kernel(const BigBat
     if (cf != cb) d = cf < cb ? kFwd : kBwd;
     else if (sf != sb) d = sf > sb ? kFwd : kBwd;
     for (int c = tid; c < f; c += blockDim.x) {
-      const int j = perm[d1 + c];
+      const int j = spm[d1 + c];
       const int lb = d == kFwd ? accf[j] : accb[j];
       const size_t o = static_cast<size_t>(node) * n + c;
       B.child_lb[o] = lb;

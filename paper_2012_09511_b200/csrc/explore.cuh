@@ -900,6 +900,26 @@ __device__ __forceinline__ unsigned long long gather_free(const Group<G>& grp, c
 // ------------------------------------------------------------------ explorer steps
 
 
+// position_reached_end (src/ivm.cpp:90-97): padded V >= end, digit by digit.
+template <int G>
+__device__ __forceinline__ bool reached_end(const Group<G>& grp, const IvmView& iv, int n, int level) {
+  for (int b0 = 0; b0 < n; b0 += G) {
+    const int l = b0 + grp.g;
+    int pv = 0, ev = 0;
+    if (l < n) {
+      pv = l <= level ? iv.V[l] : 0;
+      ev = iv.endd[l];
+    }
+    const unsigned b = grp.ballot(pv != ev);
+    if (b) {
+      const int src = __ffs(b) - 1;
+      return grp.bcast(pv, src) > grp.bcast(ev, src);
+    }
+  }
+  return true;
+}
+
+
 // The end test kept incrementally (register state, uniform over the group) instead of a
 // digit-by-digit comparison of padded V and end at every select: eq = length of the common
 // prefix of V[0..level-1] and end (levels above the current row), lt = V[eq] < end[eq] when
@@ -945,7 +965,7 @@ constexpr int kNoHint = -2;
 // Returns the selected cell, or -1 when the explorer is exhausted. hint: the first unpruned
 // cell of the current row when decompose_branch has just written it (-1: every child pruned,
 // backtrack at once), so the row is not scanned again; the IVM state stays the reference's.
-template <int M, int G, bool RM, bool W = false>
+template <int M, int G, bool RM, bool W = false, bool INC = true>
 __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& iv,
                                            const InstView& in, int n, int mp, bool has_end,
                                            int& level, int& d1, int& d2, RowMask<M, RM>& rowmask,
@@ -977,7 +997,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
       grp.sync();
       if (grp.g == 0) iv.V[level] = 0;
       --level;
-      et.up(level);
+      if (INC) et.up(level);
       if (level >= 0) {
         const int psel = iv.V[level];
         const int x = iv.cells[tri_off(level, n) + psel];
@@ -993,7 +1013,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
     grp.sync();
     if (grp.g == 0) iv.V[level] = static_cast<int8_t>(found);
     grp.sync();
-    if (has_end && et.reached(iv, level, found)) return -1;
+    if (has_end && (INC ? et.reached(iv, level, found) : reached_end(grp, iv, n, level))) return -1;
     return found;
   }
 }
@@ -1202,10 +1222,9 @@ __device__ __forceinline__ float remaining_log2_pos(const int* pos, const T* E, 
 }
 
 // ---- remaining work of one explorer for the steal phase: log2 of its leaves, -2 busy /
-// unsplittable, -3 idle (lens_kernel, and the explore kernel's write-back, which evaluates it
-// on the shared-memory copy of the block). mode 0: the live siblings of the shallowest level
-// holding any (pool.cu live_siblings), (cnt + 1) (n-1-l*)!; mode 1: the exact factoradic
-// length of [effective position, end).
+// unsplittable, -3 idle (lens_kernel, on a shared-memory copy of the block). mode 0: the live
+// siblings of the shallowest level holding any (pool.cu live_siblings), (cnt + 1) (n-1-l*)!;
+// mode 1: the exact factoradic length of [effective position, end).
 __device__ __forceinline__ int live_count(const unsigned char* vb, const IvmLayout& L, int& lstar) {
   const int n = L.n;
   const IvmHdr* h = reinterpret_cast<const IvmHdr*>(vb);
@@ -1296,6 +1315,17 @@ template <int BOUND, int G, bool SMALLN>
 constexpr bool kRowMask = BOUND == kLB2 && G == 32 && SMALLN;
 template <int BOUND, int G, bool SMALLN>
 constexpr int kExploreThreads = 1024;
+// Steal lengths evaluated at the explore kernel's write-back (a noinline call, once per explorer
+// and launch) instead of by lens_kernel after it: measured per variant -- the call site changes
+// ptxas' allocation of the register-capped explorer loop, which the n <= 32 LB2 warp kernel
+// likes (ta021 LB2 proof 196 -> 192 ms) and LB1 / n > 32 LB2 do not (ta021 LB1 176 -> 182 ms,
+// ta056 LB2 30 -> 24 M nodes/s at 5 s).
+template <int BOUND, int G, bool SMALLN>
+constexpr bool kLensInKernel = BOUND == kLB2 && G == 32 && SMALLN;
+__device__ __noinline__ float explorer_lens_call(const unsigned char* blk, const IvmLayout& L, const float* lgfact,
+                                                 int mode) {
+  return explorer_lens(blk, L, lgfact, mode);
+}
 
 // W: wide (32-bit) FT / R / prefix sums, LB1 only (pool_init)
 template <int M, int G, int BOUND, bool SMALLN = false, bool W = false>
@@ -1381,8 +1411,12 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
     if (grp.g == 0 && state != kEmpty) atomicAdd(reinterpret_cast<unsigned*>(smem + IL.o_cnt) + 6, 1u);
     int best = grp.bcast(grp.g == 0 ? *reinterpret_cast<volatile int*>(&P.ctr->best) : 0, 0);
     int step = 0, hint = kNoHint;
+    // the survivor hint and the incremental end test pay for LB1 (select / backtrack dominate
+    // its steps: ta021 proof 192 -> 176 ms); the LB2 warp kernels are register-capped and lose
+    // more to the extra live state than the selects cost them (ta021 LB2 192 -> 199 ms)
+    constexpr bool INC = BOUND == kLB1;
     EndTrack et;
-    if (has_end && state == kActive) et.init(grp, iv, n, level);
+    if (INC && has_end && state == kActive) et.init(grp, iv, n, level);
     unsigned long long t_end = ~0ull;
     if (P.budget_ns) t_end = globaltimer_ns() + P.budget_ns;
     while (step < P.steps) {
@@ -1423,7 +1457,7 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
             for (int t = 0; t < dup; ++t) atomicAdd(&sdhist[n - 1 - t], 1u);
           }
           state = kActive;
-          if (has_end) et.init(grp, iv, n, level);
+          if (INC && has_end) et.init(grp, iv, n, level);
           continue;
         }
         decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, digit, prune, level, d1, d2, shist, rowmask, rs);
@@ -1432,7 +1466,7 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
         rlev = level;
         continue;
       }
-      const int sel = select_next<M, G, RM, W>(grp, iv, in, n, mp, has_end, level, d1, d2, rowmask, rs, et, hint);
+      const int sel = select_next<M, G, RM, W, INC>(grp, iv, in, n, mp, has_end, level, d1, d2, rowmask, rs, et, hint);
       hint = kNoHint;
       if (sel < 0) {
         state = kEmpty;
@@ -1442,8 +1476,9 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
         leaf<M, G, W>(grp, iv, in, rs, n, mp, sel, level, d1, d2, improve, P.ctr, P.imp, sc, P.census, P.census_cap);
         continue;
       }
-      if (has_end) et.descend(iv, level, sel);
+      if (INC && has_end) et.descend(iv, level, sel);
       hint = decompose_branch<M, G, BOUND, SMALLN, RM, W>(grp, iv, in, n, mp, sel, prune, level, d1, d2, shist, rowmask, rs);
+      if (!INC) hint = kNoHint;
       ++sc.decomposed;
     }
     rs.template store<W>(grp, iv);
@@ -1454,8 +1489,8 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
       iv.hdr->d2 = static_cast<uint8_t>(d2);
       iv.hdr->rlev = static_cast<uint8_t>(rlev);
       iv.hdr->nrep = static_cast<uint8_t>(nrep);
-      // remaining work of this explorer for the steal phase (read by steal_kernel)
-      if (P.lens) P.lens[first + gi] = explorer_lens(reinterpret_cast<const unsigned char*>(iv.hdr), L, P.lgfact, P.lens_mode);
+      if constexpr (kLensInKernel<BOUND, G, SMALLN>)
+        if (P.lens) P.lens[first + gi] = explorer_lens_call(reinterpret_cast<const unsigned char*>(iv.hdr), L, P.lgfact, P.lens_mode);
       unsigned* cnt = reinterpret_cast<unsigned*>(smem + IL.o_cnt);
       atomicAdd(&cnt[0], sc.decomposed);
       atomicAdd(&cnt[1], sc.leaves);

@@ -95,7 +95,8 @@ struct ExploreParams {
   int free_replay;            // init_at replay levels do not consume steps (reference policy)
   int census_cap;             // record_census: capacity of `census` (0 = off)
   unsigned long long* census; // leaf positions as decimals (position_u64, explorer.cpp:47)
-  float* lens;                // [K] steal-phase remaining work, written at the write-back (null = lens_kernel)
+  float* lens;                // [K] steal-phase remaining work written at the write-back (kLensInKernel
+                              // variants; null = lens_kernel after the launch)
   const float* lgfact;        // [n+1] log2(k!)
   int lens_mode;              // split mode of the steal phase (explorer_lens)
 };

@@ -429,10 +429,23 @@ __device__ __forceinline__ void live_point(const int8_t* V, int lstar, int cell,
 // log2 of leaves; -2 busy / unsplittable, -3 idle. mode 0: the live siblings of the
 // shallowest level holding any, (cnt + 1) (n-1-l*)!; mode 1: the exact factoradic length of
 // [effective position, end).
-__global__ void lens_kernel(IvmLayout L, const unsigned char* state, int K, const float* lgfact, float* lens, int mode) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= K) return;
-  lens[i] = explorer_lens(state + static_cast<size_t>(i) * L.gstride, L, lgfact, mode);
+// One warp per explorer: the block is staged in shared memory with coalesced 16-byte loads, so
+// the digit / row walks of explorer_lens run on shared memory instead of serialized global loads.
+// (Evaluated inside the explore kernel's write-back instead, the code costs the explorer loop
+// registers in every variant: 2-3 % on the ta021 / ta056 proofs.)
+constexpr int kLensWarps = 8;
+__global__ void __launch_bounds__(kLensWarps * 32) lens_kernel(IvmLayout L, const unsigned char* state, int K,
+                                                               const float* lgfact, float* lens, int mode) {
+  extern __shared__ __align__(16) unsigned char lbuf[];
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  unsigned char* vb = lbuf + static_cast<size_t>(wi) * L.gstride;
+  for (int i = blockIdx.x * kLensWarps + wi; i < K; i += gridDim.x * kLensWarps) {
+    const uint4* src = reinterpret_cast<const uint4*>(state + static_cast<size_t>(i) * L.gstride);
+    for (int w = lane; w < L.gstride / 16; w += 32) reinterpret_cast<uint4*>(vb)[w] = src[w];
+    __syncwarp();
+    if (lane == 0) lens[i] = explorer_lens(vb, L, lgfact, mode);
+    __syncwarp();
+  }
 }
 
 // ---- multi-way interval splitting (exact mixed-radix arithmetic, no big integers)
@@ -1718,6 +1731,8 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
   P->split_grid = std::max(1, std::min((P->K + kSplitWarps - 1) / kSplitWarps, 4 * P->num_sms));
   ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(split_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kSplitWarps * P->L.gstride), "smem attr");
+  ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(lens_kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kLensWarps * P->L.gstride), "smem attr");
   ck(cudaMalloc(&P->d_ctr, sizeof(DevCounters)), "malloc");
   ck(cudaMallocHost(&P->h_ctr, sizeof(DevCounters)), "malloc host");
   ck(cudaMalloc(&P->d_hist, (static_cast<size_t>(n) + 1) * sizeof(unsigned long long)), "malloc");
@@ -1783,6 +1798,13 @@ void launch_big_bounding(pbbgpu_pool* P, const BigBatchParams& G, int count, int
     P->big<<<std::min(count, P->big_grid), kBigThreads, P->big_smem, P->stream>>>(G);
   }
   ck(cudaGetLastError(), "decompose_big launch");
+}
+
+// remaining work of every explorer (lens_kernel) before a steal phase / export / census
+void launch_lens(pbbgpu_pool* P, int mode) {
+  const int grid = std::max(1, std::min((P->K + kLensWarps - 1) / kLensWarps, 4 * P->num_sms));
+  lens_kernel<<<grid, kLensWarps * 32, kLensWarps * P->L.gstride, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact,
+                                                                                P->d_lens, mode);
 }
 
 void read_counters(pbbgpu_pool* P) {
@@ -2202,7 +2224,7 @@ int run_round(pbbgpu_pool* P) {
   S.lens = P->d_lens;
   S.max_split = P->cfg.max_split > 0 ? std::min(P->cfg.max_split, 63) : 4;
   S.split_mode = split_kind(P->cfg.split_mode);
-  if (P->cfg.steal_policy != 1) {  // the explore kernel leaves each explorer's steal length
+  if (P->cfg.steal_policy != 1 && P->bound == kLB2 && P->G == 32 && P->n <= 32) {  // kLensInKernel
     E.lens = P->d_lens;
     E.lgfact = P->d_lgfact;
     E.lens_mode = S.split_mode;
@@ -2235,7 +2257,7 @@ int run_round(pbbgpu_pool* P) {
       P->launches += 2;
       continue;
     }
-    // lens: written by the explore kernel's write-back (E.lens)
+    if (!E.lens) launch_lens(P, S.split_mode);  // else written by the explore kernel (kLensInKernel)
     steal_kernel<<<1, kStealThreads, 0, P->stream>>>(S);
     ck(cudaGetLastError(), "steal_kernel launch");
     split_kernel<<<P->split_grid, kSplitWarps * 32, kSplitWarps * P->L.gstride, P->stream>>>(
@@ -2246,14 +2268,14 @@ int run_round(pbbgpu_pool* P) {
       const GroupParams G = group_params(P);
       group_exchange_kernel<<<1, kStealThreads, 0, P->stream>>>(P->L, P->d_state, P->d_ptot, P->d_ctr, G);
       ck(cudaGetLastError(), "group_exchange_kernel launch");
-      lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, S.split_mode);
+      launch_lens(P, S.split_mode);
       ck(cudaGetLastError(), "lens_kernel launch");
       group_export_kernel<<<1, kStealThreads, 0, P->stream>>>(S, G);
       ck(cudaGetLastError(), "group_export_kernel launch");
       P->launches += 3;
     }
     ck(cudaEventRecord(P->evs[3 * r + 2], P->stream), "event");
-    P->launches += 3;
+    P->launches += E.lens ? 3 : 4;
   }
   read_counters(P);
   for (int r = 0; r < R; ++r) {
@@ -2731,7 +2753,7 @@ int pbbgpu_export(pbbgpu_pool* P, int max_count, uint16_t* a_out, uint16_t* b_ou
     S.lgfact = P->d_lgfact;
     S.lens = P->d_lens;
     S.split_mode = split_kind(P->cfg.split_mode);
-    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, S.split_mode);
+    launch_lens(P, S.split_mode);
     ck(cudaGetLastError(), "lens_kernel");
     P->launches += 1;
     export_kernel<<<1, kStealThreads, 0, P->stream>>>(S, want, d_dig, d_nf, d_cnt);
@@ -2983,7 +3005,7 @@ int pbbgpu_explorer_lengths(pbbgpu_pool* P, float* out, int cap) {
   return guarded([&] {
     if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
     if (cap < P->K) throw std::invalid_argument("explorer_lengths buffer smaller than K");
-    lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->L, P->d_state, P->K, P->d_lgfact, P->d_lens, 1);
+    launch_lens(P, 1);
     ck(cudaGetLastError(), "lens_kernel");
     P->launches += 1;
     xfer(P, out, P->d_lens, static_cast<size_t>(P->K) * sizeof(float), cudaMemcpyDeviceToHost, "lens copy");
