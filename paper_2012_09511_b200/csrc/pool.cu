@@ -1961,37 +1961,67 @@ GroupParams group_params(const pbbgpu_pool* P) {
 
 // ---- host views of explorer blocks (snapshot, timeline, work updates)
 std::vector<unsigned char> download_state(pbbgpu_pool* P) {
-  std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
+  std::vector<unsigned char> st(static_cast<size_t>(P->K) * state_stride(P));
   xfer(P, st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost, "state copy");
   return st;
+}
+
+// Host view of one explorer block of either layout (n <= 64: IvmHdr, int8 digits and cells;
+// n > 64: BigHdr, int16) -- the IVM semantics are the same, so snapshot / work update / timeline
+// code reads both through this.
+struct BlockRef {
+  const pbbgpu_pool* P;
+  unsigned char* b;
+  bool big() const { return P->big_explore; }
+  template <typename T>
+  T* at(int off) const { return reinterpret_cast<T*>(b + off); }
+  int state() const { return big() ? at<BigHdr>(0)->state : at<IvmHdr>(0)->state; }
+  int level() const { return big() ? at<BigHdr>(0)->level : at<IvmHdr>(0)->level; }
+  int nrep() const { return big() ? at<BigHdr>(0)->nrep : at<IvmHdr>(0)->nrep; }
+  bool has_end() const { return big() ? at<BigHdr>(0)->has_end != 0 : at<IvmHdr>(0)->has_end != 0; }
+  void set_empty() const {
+    if (big()) at<BigHdr>(0)->state = kEmpty, at<BigHdr>(0)->level = -1;
+    else at<IvmHdr>(0)->state = kEmpty, at<IvmHdr>(0)->level = -1;
+  }
+  int digit(int o_big, int o_small, int l) const { return big() ? at<int16_t>(o_big)[l] : at<int8_t>(o_small)[l]; }
+  int V(int l) const { return digit(P->BL.o_v, P->L.o_v, l); }
+  int E(int l) const { return digit(P->BL.o_end, P->L.o_end, l); }
+  int T(int l) const { return digit(P->BL.o_tgt, P->L.o_tgt, l); }
+  int cell(int l, int c) const { return digit(P->BL.o_cells, P->L.o_cells, tri_off(l, P->n) + c); }
+  void set_end(const std::vector<int>& e) const {
+    for (int l = 0; l < P->n; ++l) {
+      if (big()) at<int16_t>(P->BL.o_end)[l] = static_cast<int16_t>(e[static_cast<size_t>(l)]);
+      else at<int8_t>(P->L.o_end)[l] = static_cast<int8_t>(e[static_cast<size_t>(l)]);
+    }
+    if (big()) at<BigHdr>(0)->has_end = 1;
+    else at<IvmHdr>(0)->has_end = 1;
+  }
+};
+BlockRef block_ref(const pbbgpu_pool* P, std::vector<unsigned char>& st, int i) {
+  return BlockRef{P, st.data() + static_cast<size_t>(i) * state_stride(P)};
 }
 
 // Remaining work of an explorer block: [pos, end), pos the effective position (a parked
 // explorer's consumed cell excluded, as pbbgpu_snapshot reports it; kInit: the replay target).
 // False when nothing remains.
 // raw = the reference's position() (zero-padded V, ivm.cpp:180-184) instead of the effective one.
-bool block_span(const pbbgpu_pool* P, const unsigned char* blk, std::vector<int>& pos, std::vector<int>& end,
-                bool& end_nf, bool raw = false) {
-  const int n = P->n;
-  const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
-  if (h->state == kEmpty) return false;
-  const int8_t* V = reinterpret_cast<const int8_t*>(blk + P->L.o_v);
-  const int8_t* E = reinterpret_cast<const int8_t*>(blk + P->L.o_end);
-  const int8_t* T = reinterpret_cast<const int8_t*>(blk + P->L.o_tgt);
-  const int8_t* C = reinterpret_cast<const int8_t*>(blk + P->L.o_cells);
+bool block_span(const BlockRef& h, std::vector<int>& pos, std::vector<int>& end, bool& end_nf, bool raw = false) {
+  const int n = h.P->n;
+  if (h.state() == kEmpty) return false;
+  const int state = h.state(), level = h.level();
   pos.assign(static_cast<size_t>(n), 0);
   end.assign(static_cast<size_t>(n), 0);
-  for (int l = 0; l < n; ++l) pos[static_cast<size_t>(l)] = h->state == kInit ? T[l] : (l <= h->level ? V[l] : 0);
-  if (!raw && h->state == kActive && h->level >= 0 && C[tri_off(h->level, n) + V[h->level]] <= 0) {
-    int l = h->level;
+  for (int l = 0; l < n; ++l) pos[static_cast<size_t>(l)] = state == kInit ? h.T(l) : (l <= level ? h.V(l) : 0);
+  if (!raw && state == kActive && level >= 0 && h.cell(level, h.V(level)) <= 0) {
+    int l = level;
     for (; l >= 0; --l) {
       if (++pos[static_cast<size_t>(l)] <= n - 1 - l) break;
       pos[static_cast<size_t>(l)] = 0;
     }
     if (l < 0) return false;
   }
-  end_nf = !h->has_end;
-  for (int l = 0; l < n; ++l) end[static_cast<size_t>(l)] = h->has_end ? E[l] : 0;
+  end_nf = !h.has_end();
+  for (int l = 0; l < n; ++l) end[static_cast<size_t>(l)] = end_nf ? 0 : h.E(l);
   if (!end_nf) {
     int cmp = 0;
     for (int l = 0; l < n && !cmp; ++l) cmp = pos[static_cast<size_t>(l)] < end[static_cast<size_t>(l)] ? -1 : (pos[static_cast<size_t>(l)] > end[static_cast<size_t>(l)] ? 1 : 0);
@@ -2044,14 +2074,14 @@ void sample_timeline(pbbgpu_pool* P, bool force) {
   P->sampled = true;
   P->t_last_sample = now;
   const long long ts = std::chrono::duration_cast<std::chrono::milliseconds>(now - P->t_start).count();
-  const std::vector<unsigned char> st = download_state(P);
+  std::vector<unsigned char> st = download_state(P);
   std::vector<int> pos, end;
   for (int i = 0; i < P->K; ++i) {
-    const unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
-    const bool active = reinterpret_cast<const IvmHdr*>(blk)->state != kEmpty;
+    const BlockRef h = block_ref(P, st, i);
+    const bool active = h.state() != kEmpty;
     bool nf = false;
     long lg = -1;
-    if (active && block_span(P, blk, pos, end, nf, true)) lg = exact_log2_len(pos, end, nf, P->n);
+    if (active && block_span(h, pos, end, nf, true)) lg = exact_log2_len(pos, end, nf, P->n);
     std::fprintf(P->timeline, "%lld,%d,%d,%ld\n", ts, i, active ? 1 : 0, lg);
   }
 }
@@ -2805,56 +2835,35 @@ int pbbgpu_snapshot(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_n
 int pbbgpu_snapshot_ex(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* end_nf, int cap, int* count,
                        uint64_t* resume_recount) {
   return guarded([&] {
-    if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
+    if (P->batch_only && !P->big_explore) throw StateError("pbbgpu: bounding-only pool has no explorers");
     const int n = P->n;
     uint64_t recount = 0;
-    std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
-    xfer(P, st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost, "state copy");
+    std::vector<unsigned char> st = download_state(P);  // either layout (BlockRef)
+    std::vector<int> pv, ev;
     int c = 0;
     for (int i = 0; i < P->K; ++i) {
-      const unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
-      const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
-      if (h->state == kEmpty) continue;
-      const int8_t* V = reinterpret_cast<const int8_t*>(blk + P->L.o_v);
-      const int8_t* E = reinterpret_cast<const int8_t*>(blk + P->L.o_end);
-      const int8_t* T = reinterpret_cast<const int8_t*>(blk + P->L.o_tgt);
-      const int8_t* C = reinterpret_cast<const int8_t*>(blk + P->L.o_cells);
-      std::vector<int> pv(static_cast<size_t>(n));
-      for (int l = 0; l < n; ++l) pv[static_cast<size_t>(l)] = h->state == kInit ? T[l] : (l <= h->level ? V[l] : 0);
+      const BlockRef h = block_ref(P, st, i);
+      if (h.state() == kEmpty) continue;
+      bool nf = false;
       // an explorer parked on a pruned/consumed cell (evaluated leaf, replay into a pruned
-      // subtree) has covered that cell's whole subtree: the remaining work starts after it
-      // (effective_pos in explore.cuh)
-      bool past_end = false;
-      bool parked = false;
-      if (h->state == kActive && h->level >= 0 && C[tri_off(h->level, n) + V[h->level]] <= 0) {
-        parked = true;
-        int l = h->level;
-        for (; l >= 0; --l) {
-          if (++pv[static_cast<size_t>(l)] <= n - 1 - l) break;
-          pv[static_cast<size_t>(l)] = 0;
-        }
-        past_end = l < 0;
-      }
-      if (!past_end && h->has_end) {
-        int cmp = 0;
-        for (int l = 0; l < n && !cmp; ++l) cmp = pv[static_cast<size_t>(l)] < E[l] ? -1 : (pv[static_cast<size_t>(l)] > E[l] ? 1 : 0);
-        past_end = cmp >= 0;
-      }
-      if (past_end) continue;
+      // subtree) has covered that cell's whole subtree: its remaining work starts after it
+      // (block_span's effective position, effective_pos in explore.cuh)
+      if (!block_span(h, pv, ev, nf)) continue;
       if (c >= cap) throw CapacityError("snapshot buffer too small");
-      if (h->state == kInit) {
-        recount += h->nrep;
+      const bool parked = h.state() == kActive && h.level() >= 0 && h.cell(h.level(), h.V(h.level())) <= 0;
+      if (h.state() == kInit) {
+        recount += static_cast<uint64_t>(h.nrep());
       } else if (!parked) {
         int lnz = 0;
         for (int l = 0; l < n; ++l)
           if (pv[static_cast<size_t>(l)] != 0) lnz = l;
-        recount += static_cast<uint64_t>(std::max(0, h->level - lnz));
+        recount += static_cast<uint64_t>(std::max(0, h.level() - lnz));
       }
       for (int l = 0; l < n; ++l) {
         pos[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(pv[static_cast<size_t>(l)]);
-        end[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(h->has_end ? E[l] : 0);
+        end[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(ev[static_cast<size_t>(l)]);
       }
-      end_nf[c] = h->has_end ? 0 : 1;
+      end_nf[c] = nf ? 1 : 0;
       ++c;
     }
     *count = c;
@@ -3250,7 +3259,7 @@ std::vector<DInterval> dsubtract(const std::vector<DInterval>& A, const std::vec
 
 int pbbgpu_apply_work_update(pbbgpu_pool* P, const uint16_t* a, const uint16_t* b, const uint8_t* nf, int count) {
   return guarded([&] {
-    if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
+    if (P->batch_only && !P->big_explore) throw StateError("pbbgpu: bounding-only pool has no explorers");
     if (count < 0) throw std::invalid_argument("negative interval count");
     if (count > P->K) throw std::invalid_argument("work update holds more intervals than explorers");
     const int n = P->n;
@@ -3281,38 +3290,30 @@ int pbbgpu_apply_work_update(pbbgpu_pool* P, const uint16_t* a, const uint16_t* 
     std::vector<Reset> resets;
     std::vector<int> pos, end;
     for (int i = 0; i < P->K; ++i) {
-      unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
-      IvmHdr* h = reinterpret_cast<IvmHdr*>(blk);
-      if (h->state == kEmpty) {
+      const BlockRef h = block_ref(P, st, i);
+      if (h.state() == kEmpty) {
         idle.push_back(i);
         continue;
       }
       bool end_nf = false;
       std::vector<DInterval> mine;
-      const bool has_span = block_span(P, blk, pos, end, end_nf);
+      const bool has_span = block_span(h, pos, end, end_nf);
       if (has_span) mine = dintersect(incoming, {{pos, end, end_nf}});
       if (mine.size() == 1 && dcmp(mine[0].a, pos) == 0) {
-        if (pcmp(mine[0].b, mine[0].b_nf, end, end_nf) < 0) {  // shrink_end (ivm.cpp:186-189)
-          int8_t* E = reinterpret_cast<int8_t*>(blk + P->L.o_end);
-          for (int l = 0; l < n; ++l) E[l] = static_cast<int8_t>(mine[0].b[static_cast<size_t>(l)]);
-          h->has_end = 1;
-        }
+        if (pcmp(mine[0].b, mine[0].b_nf, end, end_nf) < 0) h.set_end(mine[0].b);  // shrink_end (ivm.cpp:186-189)
         kept.push_back(std::move(mine[0]));
       } else {
         if (has_span) {
-          const int8_t* V = reinterpret_cast<const int8_t*>(blk + P->L.o_v);
-          const int8_t* C = reinterpret_cast<const int8_t*>(blk + P->L.o_cells);
           int lnz = 0;
           for (int l = 0; l < n; ++l)
             if (pos[static_cast<size_t>(l)] != 0) lnz = l;
-          if (h->state == kInit) {
-            resets.push_back({pos, 0, h->nrep, std::min<int>(h->nrep, lnz)});
-          } else if (C[tri_off(h->level, n) + V[h->level]] > 0) {  // not parked
-            resets.push_back({pos, lnz, std::max<int>(lnz, h->level), 0});
+          if (h.state() == kInit) {
+            resets.push_back({pos, 0, h.nrep(), std::min<int>(h.nrep(), lnz)});
+          } else if (h.cell(h.level(), h.V(h.level())) > 0) {  // not parked
+            resets.push_back({pos, lnz, std::max<int>(lnz, h.level()), 0});
           }
         }
-        h->state = kEmpty;
-        h->level = -1;
+        h.set_empty();
         idle.push_back(i);
       }
     }

@@ -905,6 +905,79 @@ def test_large_n_explorer_pool_fixed_trees(key, bound, K):
     assert {str(k): v for k, v in res.hist.items()} == {str(k): v for k, v in gold["hist"].items()}
 
 
+@pytest.mark.parametrize("key,bound,rounds", [("ta081@6070", "lb1", 2), ("ta081@6070", "lb1", 5),
+                                              ("ta081@6070", "lb2", 3), ("ta101@11150", "lb1", 3)])
+def test_large_n_snapshot_resume_preserves_count(key, bound, rounds):
+    """snapshot_intervals on the n > 64 explorer pool (int16 IVMs): the remaining work after a
+    few rounds, resumed in a fresh pool, completes the fixed tree with exact node accounting
+    (nodes before - resume recount + nodes after == the reference's / the oracle's count)."""
+    gold = golden_io.ref_counts()[key] if bound == "lb1" else golden_io.lb2_counts()[key]
+    want = gold["decomposed"] if bound == "lb1" else gold["unique"]
+    name, ub = key.split("@")
+    inst = pbb.taillard_named(name)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=1024, rounds_per_sync=1), bound=bound) as pool:
+        pool.set_initial_bound(int(ub))
+        pool.assign_split(1024)
+        for _ in range(rounds):
+            pool.run_round()
+        snap, recount = pool.snapshot()
+        done = pool.stats()
+    assert snap and not done.completed
+    res = pbb.pool_run(inst, int(ub), intervals=snap, cfg=pbb.PoolConfig(explorers=max(1024, len(snap))), bound=bound)
+    assert done.unique - recount + res.stats.unique == want
+    assert done.leaves + res.stats.leaves == gold["leaves"]
+
+
+def test_large_n_apply_work_update_keeps_splits_and_reseats():
+    """apply_work_update on the n > 64 explorer pool: the echo keeps every explorer, halving
+    every interval shrinks ends and seats the right halves; the proof completes exactly."""
+    ref = golden_io.ref_counts()["ta081@6070"]
+    inst = pbb.taillard_named("ta081")
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=1024, rounds_per_sync=1)) as pool:
+        pool.set_initial_bound(6070)
+        pool.assign_split(200)
+        pool.run_round()
+        snap = pool.snapshot_intervals()
+        assert snap
+        act = pool.active_count()
+        pool.apply_work_update(snap)
+        assert pool.snapshot_intervals() == snap and pool.active_count() == act
+        halves = []
+        for a, b in snap:
+            mid = (a + b) // 2
+            halves += [(a, mid), (mid, b)] if b - a >= 2 else [(a, b)]
+        pool.apply_work_update(halves)
+        assert _merged(pool.snapshot_intervals()) == _merged(snap)
+        while pool.run_round():
+            pass
+        st = pool.stats()
+    assert st.unique == ref["decomposed"] and st.leaves == ref["leaves"]
+
+
+def test_large_n_checkpoint_restart_completes_the_proof(tmp_path):
+    """Checkpoint / restart (reference format) of an n > 64 explorer pool: totals exact."""
+    from paper_2012_09511_b200 import checkpoint as ck
+
+    ref = golden_io.ref_counts()["ta101@11150"]
+    inst = pbb.taillard_named("ta101")
+    path = str(tmp_path / "ta101.ckpt")
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=2048, rounds_per_sync=1)) as pool:
+        pool.set_initial_bound(11150)
+        pool.assign_split()
+        for _ in range(4):
+            pool.run_round()
+        first = pool.stats()
+        d = ck.save_pool(pool, path)
+    assert d.units[0].intervals and not first.completed
+    with ck.resume_pool(path, inst, pbb.PoolConfig(explorers=2048)) as pool2:
+        while pool2.run_round():
+            pass
+        rest = pool2.stats()
+        assert pool2.best_value() == 11150
+    assert first.leaves + rest.leaves == ref["leaves"]
+    assert d.total_nodes + rest.unique == ref["decomposed"]
+
+
 def test_large_n_explorer_pool_finds_optimum_and_partitions():
     """An improving run from NEH on ta061 (100 x 5) proves the optimum 5493 with a verified
     schedule; a user partition of [0, n!) gives the same fixed-tree count."""

@@ -60,17 +60,26 @@ def test_two_ranks_match_single_gpu_counts(name, ub, bound, split_mode, native):
     assert {str(k): v for k, v in r0[5].items()} == gold["hist"]
 
 
-@pytest.mark.timeout(600)
+@pytest.mark.timeout(1200)
 def test_two_ranks_native_ta021_lb2_exact_with_transfers():
     """The headline proof (ta021, LB2, UB 2297: 35,671,488 unique nodes) split over 2 ranks on the
     native peer-memory plane: exact count, and intervals did move between the ranks."""
     gold = golden_io.lb2_counts()["ta021@2297"]
     ctx = mp.get_context("spawn")
-    with ctx.Manager() as mgr:
-        out = mgr.dict()
-        mp.start_processes(_worker, args=(2, _port(), "ta021", 2297, "lb2", 0, out, True, 0), nprocs=2,
-                           start_method="spawn", join=True)
-        r0, r1 = out[0], out[1]
-    assert r0[0] == r1[0] == gold["unique"]
-    assert r0[2] == r1[2] == 2297
-    assert r0[3] == r1[3] > 0
+    moved = []
+    # whether a rank runs dry while the other is still busy depends on how the two processes'
+    # kernels interleave (on a 1-GPU box both ranks share the device): the count must be exact on
+    # every attempt, and intervals must have moved on at least one of three
+    for _ in range(3):
+        with ctx.Manager() as mgr:
+            out = mgr.dict()
+            mp.start_processes(_worker, args=(2, _port(), "ta021", 2297, "lb2", 0, out, True, 0), nprocs=2,
+                               start_method="spawn", join=True)
+            r0, r1 = out[0], out[1]
+        assert r0[0] == r1[0] == gold["unique"]
+        assert r0[2] == r1[2] == 2297
+        assert r0[3] == r1[3]
+        moved.append(r0[3])
+        if r0[3] > 0:
+            break
+    assert max(moved) > 0, moved
