@@ -209,8 +209,8 @@ int pbbgpu_histogram(pbbgpu_pool* pool, uint64_t* hist_out, int len);
 /* n > 64 (up to 512, e.g. ta111): created with explorers == 0 the pool is bounding-only
  * (decompose_batch; exploration entry points return PBBGPU_ERR_STATE); with explorers > 0 it
  * explores with int16 IVMs in HBM (assign / run_round / solve / stats / best / offer /
- * snapshot_ex / apply_work_update), while promote, explorer_lengths, census and the
- * peer-memory group stay n <= 64 (PBBGPU_ERR_STATE). */
+ * snapshot_ex / apply_work_update / promote / explorer_lengths / timeline), while census and
+ * the peer-memory group stay n <= 64 (PBBGPU_ERR_STATE). */
 int pbbgpu_decompose_batch(pbbgpu_pool* pool, const int32_t* perms, const int32_t* d1,
                            const int32_t* d2, int count, int64_t incumbent, int64_t* child_lb,
                            uint8_t* direction, uint8_t* pruned, int64_t* lb_fwd_or_null,

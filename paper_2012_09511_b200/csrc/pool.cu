@@ -1528,6 +1528,8 @@ void reset_search(pbbgpu_pool* P) {
   P->host_improvements = 0;
 }
 
+void open_timeline(pbbgpu_pool* P);
+
 void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bound, const pbbgpu_config_t* cfg) {
   if (n < 2 || n > kBigMaxN) throw std::invalid_argument("pbbgpu: n must be in [2, 512]");
   if (bound != kLB1 && bound != kLB2) throw std::invalid_argument("pbbgpu: bound must be PBBGPU_LB1 or PBBGPU_LB2");
@@ -1612,8 +1614,8 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
     }
     P->K = 0;
     if (P->cfg.explorers > 0) {  // explorer pool (explore_big.cuh)
-      if (P->cfg.steal_policy == 1 || P->cfg.record_census || (P->cfg.timeline_path && *P->cfg.timeline_path))
-        throw std::invalid_argument("pbbgpu: steal_policy 1, census and timeline need n <= 64");
+      if (P->cfg.steal_policy == 1 || P->cfg.record_census)
+        throw std::invalid_argument("pbbgpu: steal_policy 1 and census need n <= 64");
       P->big_explore = true;
       P->K = P->cfg.explorers;
       P->BL = big_ivm_layout(n);
@@ -1642,7 +1644,9 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
       for (int k = 2; k <= n; ++k) lgf[static_cast<size_t>(k)] = lgf[static_cast<size_t>(k - 1)] + std::log2(static_cast<float>(k));
       put(P, P->d_lgfact, lgf);
       reset_search(P);
+      open_timeline(P);
     }
+    P->cfg.timeline_path = nullptr;
     return;
   }
   P->G = P->cfg.group > 0 ? P->cfg.group : pick_group(n, bound);
@@ -1754,13 +1758,8 @@ void pool_init(pbbgpu_pool* P, int n, int m_real, const int32_t* p_real, int bou
     P->census_cap = P->cfg.census_cap > 0 ? P->cfg.census_cap : (1 << 20);
     ck(cudaMalloc(&P->d_census, static_cast<size_t>(P->census_cap) * sizeof(unsigned long long)), "malloc census");
   }
-  if (P->cfg.timeline_path && *P->cfg.timeline_path) {
-    P->timeline = std::fopen(P->cfg.timeline_path, "w");
-    if (!P->timeline) throw std::runtime_error(std::string("cannot open timeline file: ") + P->cfg.timeline_path);
-    std::fputs("timestamp_ms,explorer_id,active,interval_length_log2\n", P->timeline);
-  }
+  open_timeline(P);
   P->cfg.timeline_path = nullptr;  // the caller's string is not kept
-  P->t_start = std::chrono::steady_clock::now();
   put(P, P->d_lgfact, lgf);
   upload_tables(P, T);
   reset_search(P);
@@ -1898,6 +1897,16 @@ void clear_explorers(pbbgpu_pool* P) {
   ck(cudaGetLastError(), "clear_kernel");
 }
 
+// activity timeline (PoolConfig.timeline_path, explorer.cpp:71-85): header row, clock start
+void open_timeline(pbbgpu_pool* P) {
+  if (P->cfg.timeline_path && *P->cfg.timeline_path) {
+    P->timeline = std::fopen(P->cfg.timeline_path, "w");
+    if (!P->timeline) throw std::runtime_error(std::string("cannot open timeline file: ") + P->cfg.timeline_path);
+    std::fputs("timestamp_ms,explorer_id,active,interval_length_log2\n", P->timeline);
+  }
+  P->t_start = std::chrono::steady_clock::now();
+}
+
 size_t state_stride(const pbbgpu_pool* P) { return P->big_explore ? static_cast<size_t>(P->BL.stride) : static_cast<size_t>(P->L.gstride); }
 int state_off(const pbbgpu_pool* P) { return P->big_explore ? static_cast<int>(offsetof(BigHdr, state)) : static_cast<int>(offsetof(IvmHdr, state)); }
 
@@ -1988,6 +1997,7 @@ struct BlockRef {
   int E(int l) const { return digit(P->BL.o_end, P->L.o_end, l); }
   int T(int l) const { return digit(P->BL.o_tgt, P->L.o_tgt, l); }
   int cell(int l, int c) const { return digit(P->BL.o_cells, P->L.o_cells, tri_off(l, P->n) + c); }
+  int dir(int l) const { return at<uint8_t>(big() ? P->BL.o_dir : P->L.o_dir)[l]; }
   void set_end(const std::vector<int>& e) const {
     for (int l = 0; l < P->n; ++l) {
       if (big()) at<int16_t>(P->BL.o_end)[l] = static_cast<int16_t>(e[static_cast<size_t>(l)]);
@@ -2218,6 +2228,7 @@ int big_run_round(pbbgpu_pool* P) {
   P->rounds += static_cast<uint64_t>(P->rounds_per_sync);
   harvest_big(P);
   P->last_active = P->h_ctr->active;
+  if (P->timeline) sample_timeline(P, P->h_ctr->active == 0);
   return P->h_ctr->active;
 }
 
@@ -2964,34 +2975,29 @@ int pbbgpu_promote(pbbgpu_pool* P, int capacity, int32_t* perms_out, int64_t* cm
       std::scoped_lock lk(P->best_mu);
       inc = P->best_sched;
     }
-    if (inc.empty() || capacity <= 0 || P->batch_only) return;
+    if (inc.empty() || capacity <= 0 || (P->batch_only && !P->big_explore)) return;
     const int n = P->n;
     std::vector<int> rank(static_cast<size_t>(n));
     for (int i = 0; i < n; ++i) rank[static_cast<size_t>(inc[static_cast<size_t>(i)])] = i;
-    std::vector<unsigned char> st(static_cast<size_t>(P->K) * P->L.gstride);
-    xfer(P, st.data(), P->d_state, st.size(), cudaMemcpyDeviceToHost, "state copy");
+    std::vector<unsigned char> st = download_state(P);  // either layout (BlockRef)
     std::vector<std::pair<int64_t, std::vector<int32_t>>> cands;
     std::vector<int32_t> perm(static_cast<size_t>(n));
     for (int i = 0; i < P->K; ++i) {
-      const unsigned char* blk = st.data() + static_cast<size_t>(i) * P->L.gstride;
-      const IvmHdr* h = reinterpret_cast<const IvmHdr*>(blk);
-      if (h->state != kActive || h->level < 0) continue;
-      const int8_t* C = reinterpret_cast<const int8_t*>(blk + P->L.o_cells);
-      const int8_t* V = reinterpret_cast<const int8_t*>(blk + P->L.o_v);
-      const uint8_t* dir = blk + P->L.o_dir;
-      const int level = h->level;
-      if (V[level] >= n - level) continue;
+      const BlockRef h = block_ref(P, st, i);
+      if (h.state() != kActive || h.level() < 0) continue;
+      const int level = h.level();
+      if (h.V(level) >= n - level) continue;
       int d1 = 0, d2 = 0;  // decode (src/ivm.cpp:152-172)
       for (int l = 0; l <= level; ++l) {
-        const int x = C[tri_off(l, n) + V[l]];
+        const int x = h.cell(l, h.V(l));
         const int job = (x < 0 ? -x : x) - 1;
-        if (dir[l] == kFwd) perm[static_cast<size_t>(d1++)] = job;
+        if (h.dir(l) == kFwd) perm[static_cast<size_t>(d1++)] = job;
         else perm[static_cast<size_t>(n - 1 - d2++)] = job;
       }
       int pos = d1;
       for (int c = 0; c < n - level; ++c) {
-        if (c == V[level]) continue;
-        const int x = C[tri_off(level, n) + c];
+        if (c == h.V(level)) continue;
+        const int x = h.cell(level, c);
         perm[static_cast<size_t>(pos++)] = (x < 0 ? -x : x) - 1;
       }
       std::sort(perm.begin() + d1, perm.end() - d2, [&](int a, int b) { return rank[static_cast<size_t>(a)] < rank[static_cast<size_t>(b)]; });
@@ -3012,9 +3018,10 @@ int pbbgpu_promote(pbbgpu_pool* P, int capacity, int32_t* perms_out, int64_t* cm
 // not tracked), -3 = idle.
 int pbbgpu_explorer_lengths(pbbgpu_pool* P, float* out, int cap) {
   return guarded([&] {
-    if (P->batch_only) throw StateError("pbbgpu: bounding-only pool has no explorers");
+    if (P->batch_only && !P->big_explore) throw StateError("pbbgpu: bounding-only pool has no explorers");
     if (cap < P->K) throw std::invalid_argument("explorer_lengths buffer smaller than K");
-    launch_lens(P, 1);
+    if (P->big_explore) big_lens_kernel<<<(P->K + 127) / 128, 128, 0, P->stream>>>(P->BL, P->d_state, P->K, P->d_lgfact, P->d_lens);
+    else launch_lens(P, 1);
     ck(cudaGetLastError(), "lens_kernel");
     P->launches += 1;
     xfer(P, out, P->d_lens, static_cast<size_t>(P->K) * sizeof(float), cudaMemcpyDeviceToHost, "lens copy");

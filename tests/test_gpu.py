@@ -978,6 +978,53 @@ def test_large_n_checkpoint_restart_completes_the_proof(tmp_path):
     assert d.total_nodes + rest.unique == ref["decomposed"]
 
 
+def test_large_n_timeline_and_explorer_lengths(tmp_path):
+    """The pool-written activity timeline (PoolConfig.timeline_path) and explorer_lengths on an
+    n > 64 explorer pool: reference CSV rows, work tracked while active, all idle at the end."""
+    import csv
+
+    inst = pbb.taillard_named("ta081")
+    path = tmp_path / "tl_big.csv"
+    K = 512
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=K, rounds_per_sync=1, timeline_path=str(path))) as pool:
+        pool.set_initial_bound(6070)
+        pool.assign_split()
+        pool.run_round()
+        lens = pool.explorer_lengths()
+        assert len(lens) == K and max(lens) > 0
+        while pool.run_round():
+            pass
+        pool.flush_timeline()
+        assert max(pool.explorer_lengths()) == -3.0   # every explorer idle
+    rows = list(csv.reader(open(path)))
+    assert rows[0] == ["timestamp_ms", "explorer_id", "active", "interval_length_log2"]
+    body = rows[1:]
+    assert len(body) >= 2 * K and len(body) % K == 0
+    assert all(r[2] == "0" and r[3] == "-1" for r in body[-K:])
+    assert any(r[2] == "1" and int(r[3]) > 0 for r in body[:-K])
+
+
+def test_large_n_promote_and_offer_schedule():
+    """promote_solutions on an n > 64 explorer pool: valid complete schedules (the explorers'
+    paths completed in the incumbent's order), sorted by makespan; offers are taken."""
+    inst = pbb.taillard_named("ta081")
+    start = pbb.neh(inst)
+    with pbb.GpuPool(inst, pbb.PoolConfig(explorers=512), bound="lb1") as pool:
+        pool.set_initial_bound(start.cmax, start.perm)
+        pool.assign_split()
+        pool.run_round()
+        proms = pool.promote_solutions(5)
+        assert 0 < len(proms) <= 5
+        assert [p.cmax for p in proms] == sorted(p.cmax for p in proms)
+        for p in proms:
+            assert sorted(p.perm) == list(range(inst.n)) and pbb.makespan(inst, p.perm) == p.cmax
+        better = pbb.insertion_local_search(inst, start, max_iterations=200, rng_seed=1)
+        if better.cmax < start.cmax:
+            assert pool.offer_schedule(better)
+            pool.run_round()
+            assert pool.best_value() <= better.cmax
+
+
 def test_large_n_explorer_pool_finds_optimum_and_partitions():
     """An improving run from NEH on ta061 (100 x 5) proves the optimum 5493 with a verified
     schedule; a user partition of [0, n!) gives the same fixed-tree count."""
