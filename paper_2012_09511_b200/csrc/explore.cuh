@@ -38,7 +38,7 @@ __host__ __device__ inline int round_up(int x, int a) { return (x + a - 1) / a *
 
 // Per-CTA shared instance region (identical computation on host and device).
 struct InstLayout {
-  int o_p32, o_psf, o_psb, o_pk, o_pl, o_ord, o_lag, o_pk32, o_inv, o_cnt, o_cta, o_hist, o_dhist, bytes;
+  int o_p32, o_psf, o_psb, o_pk, o_pl, o_ord, o_lag, o_pk32, o_inv, o_cnt, o_cta, o_hist, o_dhist, o_roff, bytes;
 };
 
 // packed = warp-per-explorer LB2 (children_lb2_w): one uint32 per (position, pair),
@@ -72,6 +72,8 @@ __host__ __device__ inline InstLayout inst_layout(int n, int mp, int npairs, boo
   o += round_up((n + 1) * 4, 16);
   s.o_dhist = o;
   o += round_up((n + 1) * 4, 16);
+  s.o_roff = o;  // [n + 1] uint16: tri_off(l, n), the IVM row offsets
+  o += round_up((n + 1) * 2, 16);
   s.bytes = round_up(o, 128);
   return s;
 }
@@ -251,8 +253,18 @@ struct InstView {
   const uint16_t* lag;
   const uint32_t* packed;  // [n][npairs]: a | job << 7 | b << 13 | lag << 20
   const uint8_t* invord;   // [n][npairs]: position of job j in pair q's order
+  const uint16_t* roff;    // [n + 1]: IVM row offsets tri_off(l, n)
   int npairs;
 };
+
+// Row offset of IVM level l: a shared-memory table for the lane-group kernels (LB1: their steps
+// are issue-bound and select / branch / backtrack each need one), the arithmetic for the
+// warp-per-explorer LB2 kernels (left as compiled: their register allocation is tight).
+template <int G>
+__device__ __forceinline__ int row_off(const InstView& in, int l, int n) {
+  if constexpr (G < 32) return in.roff[l];
+  else return tri_off(l, n);
+}
 
 // ------------------------------------------------------------------ bounding
 //
@@ -973,7 +985,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
   for (;;) {
     if (level < 0) return -1;
     const int len = n - level;
-    const int8_t* row = iv.cells + tri_off(level, n);
+    const int8_t* row = iv.cells + row_off<G>(in, level, n);
     int found = -1;
     if (hint != kNoHint) {
       // the row was just written by decompose_branch (V = 0): its first unpruned cell is known
@@ -1000,7 +1012,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
       if (INC) et.up(level);
       if (level >= 0) {
         const int psel = iv.V[level];
-        const int x = iv.cells[tri_off(level, n) + psel];
+        const int x = iv.cells[row_off<G>(in, level, n) + psel];
         const int job = (x < 0 ? -x : x) - 1;
         rs.add(grp, in.p32 + job * mp);
         rowmask.add(in, job);  // the row one level up holds the job selected there
@@ -1030,7 +1042,7 @@ __device__ __forceinline__ int decompose_branch(const Group<G>& grp, const IvmVi
                                                  unsigned* shist, RowMask<M, RM>& rowmask, RowSum<M, G>& rs) {
   const int I = level;
   const int f = n - 1 - I;
-  int8_t* row = iv.cells + tri_off(I, n);
+  int8_t* row = iv.cells + row_off<G>(in, I, n);
   const int x = row[sel];
   const int job = (x < 0 ? -x : x) - 1;
   const int dI = iv.dir[I];
@@ -1039,7 +1051,7 @@ __device__ __forceinline__ int decompose_branch(const Group<G>& grp, const IvmVi
   unsigned long long fm = 0;
   if constexpr (BOUND == kLB2) fm = grp.ror64(fm0);  // LB1 does not use the free set mask
   grp.sync();
-  int8_t* nrow = iv.cells + tri_off(I + 1, n);
+  int8_t* nrow = iv.cells + row_off<G>(in, I + 1, n);
   int dir, first;
   if constexpr (BOUND == kLB2 && G == 32 && SMALLN) {
     // lane c holds child c's two bounds in registers (no lbf / lbb round trip)
@@ -1097,7 +1109,7 @@ __device__ __forceinline__ void leaf(const Group<G>& grp, const IvmView& iv, con
                                      int improve, DevCounters* ctr, ImpRecord* imp,
                                      StepCounters& sc, unsigned long long* census = nullptr,
                                      int census_cap = 0) {
-  int8_t* row = iv.cells + tri_off(level, n);
+  int8_t* row = iv.cells + row_off<G>(in, level, n);
   const int x = row[sel];
   const int job = (x < 0 ? -x : x) - 1;
   const int dI = iv.dir[level];
@@ -1343,6 +1355,7 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
     int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = P.p32[i];
     stage_prefix_sums(smem, IL, P.p32, n, mp, W);
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) reinterpret_cast<uint16_t*>(smem + IL.o_roff)[i] = static_cast<uint16_t>(tri_off(i, n));
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
       for (int i = threadIdx.x; i < round_up(P.npairs, 32) * n; i += blockDim.x) sk[i] = P.packed[i];
@@ -1391,6 +1404,7 @@ __global__ void __launch_bounds__(kExploreThreads<BOUND, G, SMALLN>) explore_ker
   in.lag = reinterpret_cast<const uint16_t*>(smem + IL.o_lag);
   in.packed = reinterpret_cast<const uint32_t*>(smem + IL.o_pk32);
   in.invord = smem + IL.o_inv;
+  in.roff = reinterpret_cast<const uint16_t*>(smem + IL.o_roff);
   in.npairs = P.npairs;
   unsigned* shist = reinterpret_cast<unsigned*>(smem + IL.o_hist);
   unsigned* sdhist = reinterpret_cast<unsigned*>(smem + IL.o_dhist);
@@ -1566,6 +1580,7 @@ __global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams
     int* sp = reinterpret_cast<int*>(smem + IL.o_p32);
     for (int i = threadIdx.x; i < n * mp; i += blockDim.x) sp[i] = B.p32[i];
     stage_prefix_sums(smem, IL, B.p32, n, mp, W);
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) reinterpret_cast<uint16_t*>(smem + IL.o_roff)[i] = static_cast<uint16_t>(tri_off(i, n));
     if (PACKED) {
       uint32_t* sk = reinterpret_cast<uint32_t*>(smem + IL.o_pk32);
       for (int i = threadIdx.x; i < round_up(B.npairs, 32) * n; i += blockDim.x) sk[i] = B.packed[i];
@@ -1597,6 +1612,7 @@ __global__ void __launch_bounds__(1024) decompose_batch_kernel(const BatchParams
   in.lag = reinterpret_cast<const uint16_t*>(smem + IL.o_lag);
   in.packed = reinterpret_cast<const uint32_t*>(smem + IL.o_pk32);
   in.invord = smem + IL.o_inv;
+  in.roff = reinterpret_cast<const uint16_t*>(smem + IL.o_roff);
   in.npairs = B.npairs;
   Group<G> grp;
   const int gi = threadIdx.x / G;
