@@ -982,6 +982,10 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
                                            const InstView& in, int n, int mp, bool has_end,
                                            int& level, int& d1, int& d2, RowMask<M, RM>& rowmask,
                                            RowSum<M, G>& rs, EndTrack& et, int hint = kNoHint) {
+  // INC (LB1): the scan start of the row one level up comes back from a backtrack in a register
+  // (lane 0's V read broadcast by a shuffle), so V is only ever written by lane 0 and read by
+  // the group before a ballot or shuffle that orders it: no group barriers on this path.
+  int cnext = -1;
   for (;;) {
     if (level < 0) return -1;
     const int len = n - level;
@@ -992,7 +996,7 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
       found = hint;
       hint = kNoHint;
     } else {
-      const int c0 = iv.V[level];
+      const int c0 = (INC && cnext >= 0) ? cnext : iv.V[level];
       for (int b0 = c0; b0 < len; b0 += G) {
         const int c = b0 + grp.g;
         const unsigned b = grp.ballot(c < len && row[c] > 0);
@@ -1002,29 +1006,31 @@ __device__ __forceinline__ int select_next(const Group<G>& grp, const IvmView& i
         }
       }
     }
+    cnext = -1;
     if (found < 0) {  // row exhausted: backtrack
       const int dl = iv.dir[level];
       d1 -= dl == kFwd;
       d2 -= dl == kBwd;
-      grp.sync();
+      if (!INC) grp.sync();
       if (grp.g == 0) iv.V[level] = 0;
       --level;
       if (INC) et.up(level);
       if (level >= 0) {
-        const int psel = iv.V[level];
+        const int psel = INC ? grp.bcast(grp.g == 0 ? iv.V[level] : 0, 0) : iv.V[level];
         const int x = iv.cells[row_off<G>(in, level, n) + psel];
         const int job = (x < 0 ? -x : x) - 1;
         rs.add(grp, in.p32 + job * mp);
         rowmask.add(in, job);  // the row one level up holds the job selected there
-        grp.sync();
+        if (!INC) grp.sync();
         if (grp.g == 0) iv.V[level] = static_cast<int8_t>(psel + 1);
+        cnext = psel + 1;
       }
-      grp.sync();
+      if (!INC) grp.sync();
       continue;
     }
-    grp.sync();
+    if (!INC) grp.sync();
     if (grp.g == 0) iv.V[level] = static_cast<int8_t>(found);
-    grp.sync();
+    if (!INC) grp.sync();
     if (has_end && (INC ? et.reached(iv, level, found) : reached_end(grp, iv, n, level))) return -1;
     return found;
   }
