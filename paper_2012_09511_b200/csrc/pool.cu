@@ -2077,6 +2077,34 @@ long exact_log2_len(const std::vector<int>& pos, const std::vector<int>& end, bo
   return -1;
 }
 
+// Factoradic midpoint of [pos, end) (end = n! when end_nf): pos + floor((end - pos) / 2), digit
+// l of radix n - l, exact mixed-radix arithmetic (the host counterpart of split_point).
+std::vector<int> factoradic_mid(const std::vector<int>& pos, const std::vector<int>& end, bool end_nf, int n) {
+  std::vector<int> d(static_cast<size_t>(n));
+  int borrow = 0;
+  for (int l = n - 1; l >= 0; --l) {  // end - pos
+    int x = (end_nf ? 0 : end[static_cast<size_t>(l)]) - pos[static_cast<size_t>(l)] - borrow;
+    borrow = x < 0;
+    if (borrow) x += n - l;
+    d[static_cast<size_t>(l)] = x;
+  }
+  int rem = end_nf ? 1 - borrow : 0;  // the n! unit above digit 0
+  for (int l = 0; l < n; ++l) {  // halve, most significant digit first
+    const int cur = rem * (n - l) + d[static_cast<size_t>(l)];
+    d[static_cast<size_t>(l)] = cur / 2;
+    rem = cur % 2;
+  }
+  std::vector<int> m(static_cast<size_t>(n));
+  int carry = 0;
+  for (int l = n - 1; l >= 0; --l) {  // pos + half
+    int x = pos[static_cast<size_t>(l)] + d[static_cast<size_t>(l)] + carry;
+    carry = x >= n - l;
+    if (carry) x -= n - l;
+    m[static_cast<size_t>(l)] = x;
+  }
+  return m;
+}
+
 // sample_timeline (src/explorer.cpp:448-464): one row per explorer, >= 50 ms apart unless forced.
 void sample_timeline(pbbgpu_pool* P, bool force) {
   const auto now = std::chrono::steady_clock::now();
@@ -2777,8 +2805,48 @@ int pbbgpu_export(pbbgpu_pool* P, int max_count, uint16_t* a_out, uint16_t* b_ou
   return guarded([&] {
     *count = 0;
     if (max_count <= 0) return;
+    if (P->batch_only && !P->big_explore) throw StateError("pbbgpu: bounding-only pool has no explorers");
     const int n = P->n;
     const int want = std::min(max_count, P->K);
+    if (P->big_explore) {
+      // n > 64 explorers (int16 IVMs in HBM): on the host through BlockRef -- the longest
+      // remaining intervals (exact log2 lengths) are halved at their factoradic midpoint, the
+      // explorer keeps [pos, mid) (shrink_end) and [mid, end) is exported
+      std::vector<unsigned char> st = download_state(P);
+      struct Cand {
+        long lg;
+        int i;
+      };
+      std::vector<Cand> cands;
+      std::vector<int> pos, end;
+      bool nf = false;
+      for (int i = 0; i < P->K; ++i) {
+        const BlockRef h = block_ref(P, st, i);
+        if (h.state() != kActive) continue;  // replaying explorers are not split
+        if (!block_span(h, pos, end, nf)) continue;
+        const long lg = exact_log2_len(pos, end, nf, n);
+        if (lg >= 1) cands.push_back({lg, i});
+      }
+      std::stable_sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) { return x.lg > y.lg; });
+      int c = 0;
+      for (const Cand& cd : cands) {
+        if (c >= want) break;
+        const BlockRef h = block_ref(P, st, cd.i);
+        block_span(h, pos, end, nf);
+        const std::vector<int> mid = factoradic_mid(pos, end, nf, n);
+        if (mid == pos) continue;  // a single leaf left: nothing to give
+        for (int l = 0; l < n; ++l) {
+          a_out[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(mid[static_cast<size_t>(l)]);
+          b_out[static_cast<size_t>(c) * n + l] = static_cast<uint16_t>(nf ? 0 : end[static_cast<size_t>(l)]);
+        }
+        nf_out[c] = nf ? 1 : 0;
+        h.set_end(mid);
+        ++c;
+      }
+      if (c) xfer(P, P->d_state, st.data(), st.size(), cudaMemcpyHostToDevice, "state copy");
+      *count = c;
+      return;
+    }
     int* d_dig = scratch<int>(P, 0, static_cast<size_t>(want + 64) * 2 * n);
     uint8_t* d_nf = scratch<uint8_t>(P, 1, static_cast<size_t>(want + 64));
     int* d_cnt = scratch<int>(P, 2, 1);

@@ -83,3 +83,23 @@ def test_two_ranks_native_ta021_lb2_exact_with_transfers():
         if r0[3] > 0:
             break
     assert max(moved) > 0, moved
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("name,ub,bound", [("ta081", 6070, "lb1"), ("ta081", 6070, "lb2")])
+def test_two_ranks_large_n_host_staged(name, ub, bound):
+    """n > 64 explorer pools (int16 IVMs in HBM) on 2 ranks over the host-staged plane: the
+    exported right halves (factoradic midpoints on the host) and the imports keep the
+    fixed-tree count exact."""
+    gold = golden_io.ref_counts()[f"{name}@{ub}"] if bound == "lb1" else golden_io.lb2_counts()[f"{name}@{ub}"]
+    want = gold["decomposed"] if bound == "lb1" else gold["unique"]
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        out = mgr.dict()
+        mp.start_processes(_worker, args=(2, _port(), name, ub, bound, 0, out, False, 1024), nprocs=2,
+                           start_method="spawn", join=True)
+        r0, r1 = out[0], out[1]
+    assert r0[0] == r1[0] == want
+    assert r0[1] == r1[1] == gold["leaves"]
+    assert r0[2] == r1[2] == ub
+    assert r0[4] and r1[4]
