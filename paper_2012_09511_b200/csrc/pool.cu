@@ -2952,6 +2952,7 @@ int pbbgpu_snapshot_ex(pbbgpu_pool* P, uint16_t* pos, uint16_t* end, uint8_t* en
 
 int pbbgpu_debug_state(pbbgpu_pool* P, uint8_t* out, int64_t cap, int* gstride, int* offsets) {
   return guarded([&] {
+    if (P->batch_only) throw StateError("pbbgpu_debug_state: the n <= 64 block layout only");
     const size_t bytes = static_cast<size_t>(P->K) * P->L.gstride;
     if (static_cast<int64_t>(bytes) > cap) throw std::invalid_argument("debug_state buffer too small");
     xfer(P, out, P->d_state, bytes, cudaMemcpyDeviceToHost, "state copy");
